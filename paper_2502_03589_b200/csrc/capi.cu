@@ -1,0 +1,294 @@
+// capi.cu -- the C ABI of libhack.so (include/hack.h): validation, status codes,
+// dispatch to the sm_100a kernels.  No CPU fallback exists: without an sm_100
+// device every compute entry point returns HACK_ERR_CUDA.
+#include <cuda_runtime.h>
+
+#include <cstdarg>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <string>
+
+#include "capi_util.h"
+#include "internal.h"
+
+namespace hack {
+
+thread_local std::string g_last_error;
+
+hack_status_t fail(hack_status_t st, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_last_error = buf;
+  return st;
+}
+
+hack_status_t cuda_status(cudaError_t e, const char* where) {
+  if (e == cudaSuccess) return HACK_OK;
+  return fail(HACK_ERR_CUDA, "%s: %s", where, cudaGetErrorString(e));
+}
+
+hack_status_t check_device() {
+  int dev = -1;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return fail(HACK_ERR_CUDA, "no CUDA device: %s", cudaGetErrorString(e));
+  int major = 0, minor = 0;
+  cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev);
+  cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, dev);
+  if (major != 10 || minor != 0)
+    return fail(HACK_ERR_CUDA, "libhack is built for sm_100a (B200); device %d is sm_%d%d", dev, major, minor);
+  return HACK_OK;
+}
+
+hack_status_t make_kernel_cfg(const hack_config_t* c, KernelCfg* kc) {
+  hack_status_t st = hack_config_validate(c);
+  if (st != HACK_OK) return st;
+  kc->Hq = c->num_q_heads;
+  kc->Hkv = c->num_kv_heads;
+  kc->G = c->num_q_heads / c->num_kv_heads;
+  kc->d = c->head_dim;
+  kc->Pi = c->partition;
+  kc->bits = c->kv_bits;
+  kc->kv_round = c->kv_round;
+  kc->q_round = c->q_round;
+  kc->p_round = c->p_round;
+  kc->seed = c->seed;
+  kc->layer = c->layer;
+  kc->head_base = c->head_base;
+  kc->out_fp32 = c->out_dtype == 1;
+  kc->pl = page_layout(c->head_dim, c->partition, c->kv_bits);
+  return HACK_OK;
+}
+
+hack_status_t make_cache_view(const KernelCfg& kc, const hack_kv_cache_t* c, CacheView* cv) {
+  if (!c) return fail(HACK_ERR_INVALID_ARG, "cache is NULL");
+  if (!c->pages || !c->v_tail || !c->block_table || !c->seq_lens || !c->rng_ids)
+    return fail(HACK_ERR_INVALID_ARG, "cache has a NULL device pointer");
+  if (c->page_bytes != kc.pl.page_bytes)
+    return fail(HACK_ERR_SHAPE, "cache page_bytes %d != layout %d", c->page_bytes, kc.pl.page_bytes);
+  if (c->num_pages <= 0 || c->max_reqs <= 0 || c->max_pages_per_req <= 0)
+    return fail(HACK_ERR_SHAPE, "cache dims must be positive");
+  cv->pages = c->pages;
+  cv->v_tail = c->v_tail;
+  cv->block_table = c->block_table;
+  cv->seq_lens = c->seq_lens;
+  cv->rng_ids = c->rng_ids;
+  cv->num_pages = c->num_pages;
+  cv->max_reqs = c->max_reqs;
+  cv->max_pages_per_req = c->max_pages_per_req;
+  cv->page_bytes = c->page_bytes;
+  cv->num_kv_heads = kc.Hkv;
+  return HACK_OK;
+}
+
+}  // namespace hack
+
+using namespace hack;
+
+extern "C" {
+
+void hack_config_default(hack_config_t* c) {
+  if (!c) return;
+  memset(c, 0, sizeof(*c));
+  c->num_q_heads = 1;
+  c->num_kv_heads = 1;
+  c->head_dim = 128;
+  c->partition = 64;
+  c->kv_bits = 2;
+  c->kv_round = HACK_ROUND_STOCHASTIC;
+  c->q_round = HACK_ROUND_STOCHASTIC;
+  c->p_round = HACK_ROUND_NEAREST_EVEN;
+  c->seed = 0x48414BULL;
+  c->layer = 0;
+  c->head_base = 0;
+  c->out_dtype = 0;
+}
+
+hack_status_t hack_config_validate(const hack_config_t* c) {
+  if (!c) return fail(HACK_ERR_INVALID_ARG, "config is NULL");
+  if (c->kv_bits != 2 && c->kv_bits != 4) return fail(HACK_ERR_INVALID_ARG, "kv_bits must be 2 or 4 (got %d)", c->kv_bits);
+  if (c->num_q_heads <= 0 || c->num_kv_heads <= 0) return fail(HACK_ERR_INVALID_ARG, "head counts must be positive");
+  if (c->num_q_heads % c->num_kv_heads) return fail(HACK_ERR_SHAPE, "H_q %% H_kv != 0");
+  if (c->num_q_heads / c->num_kv_heads > 16) return fail(HACK_ERR_UNSUPPORTED, "GQA group > 16");
+  if (c->head_dim != 128) return fail(HACK_ERR_UNSUPPORTED, "head_dim must be 128 (got %d)", c->head_dim);
+  if (c->partition != 32 && c->partition != 64 && c->partition != 128)
+    return fail(HACK_ERR_UNSUPPORTED, "partition must be 32, 64 or 128 (got %d)", c->partition);
+  if (c->head_dim % c->partition) return fail(HACK_ERR_UNSUPPORTED, "head_dim %% partition != 0");
+  if ((c->kv_round != 0 && c->kv_round != 1) || (c->q_round != 0 && c->q_round != 1))
+    return fail(HACK_ERR_INVALID_ARG, "bad rounding mode");
+  if (c->p_round != HACK_ROUND_NEAREST_EVEN) return fail(HACK_ERR_UNSUPPORTED, "P rounding must be NEAREST_EVEN (R6)");
+  if (c->out_dtype != 0 && c->out_dtype != 1) return fail(HACK_ERR_INVALID_ARG, "out_dtype must be 0 or 1");
+  if (c->layer < 0 || c->layer > 0xFFFF || c->head_base < 0 || c->head_base > 0xFFF)
+    return fail(HACK_ERR_INVALID_ARG, "layer/head_base out of counter range");
+  return HACK_OK;
+}
+
+int64_t hack_page_bytes(const hack_config_t* c) {
+  if (hack_config_validate(c) != HACK_OK) return -1;
+  return page_layout(c->head_dim, c->partition, c->kv_bits).page_bytes;
+}
+
+hack_status_t hack_page_layout(const hack_config_t* c, int64_t off[12]) {
+  hack_status_t st = hack_config_validate(c);
+  if (st != HACK_OK) return st;
+  if (!off) return fail(HACK_ERR_INVALID_ARG, "offsets_out is NULL");
+  const PageLayout L = page_layout(c->head_dim, c->partition, c->kv_bits);
+  const int d = c->head_dim, Pi = c->partition, b = c->kv_bits, nb = d / Pi;
+  const int64_t v[12] = {L.k_codes, (int64_t)Pi * d * b / 8, L.k_meta, (int64_t)Pi * nb * 4,
+                         L.k_sums, (int64_t)Pi * nb * L.sum_bytes, L.v_codes, (int64_t)d * Pi * b / 8,
+                         L.v_meta, (int64_t)d * 4, L.v_sums, (int64_t)d * L.sum_bytes};
+  memcpy(off, v, sizeof(v));
+  return HACK_OK;
+}
+
+const char* hack_last_error(void) { return g_last_error.c_str(); }
+const char* hack_version(void) { return "libhack 0.1 (sm_100a)"; }
+int32_t hack_abi_version(void) { return HACK_ABI_VERSION; }
+
+hack_status_t hack_quantize_pack(const hack_config_t* cfg, int32_t mode, const void* x, int64_t rows,
+                                 int32_t heads, int64_t pos0, int32_t head0, uint32_t rng_id, uint8_t* codes,
+                                 void* meta, void* sums, void* stream) {
+  KernelCfg kc;
+  hack_status_t st = make_kernel_cfg(cfg, &kc);
+  if (st != HACK_OK) return st;
+  if (!x || !codes || !meta || !sums) return fail(HACK_ERR_INVALID_ARG, "quantize_pack: NULL pointer");
+  if (mode != HACK_QMODE_K && mode != HACK_QMODE_V && mode != HACK_QMODE_Q)
+    return fail(HACK_ERR_INVALID_ARG, "quantize_pack: bad mode %d", mode);
+  if (rows <= 0 || heads <= 0) return fail(HACK_ERR_INVALID_ARG, "quantize_pack: empty input (S:45)");
+  if (pos0 < 0 || head0 < 0) return fail(HACK_ERR_INVALID_ARG, "quantize_pack: negative position/head");
+  if (mode == HACK_QMODE_V && (rows % kc.Pi || pos0 % 4))
+    return fail(HACK_ERR_SHAPE, "quantize_pack V: rows must be a multiple of Pi and pos0 of 4");
+  if ((st = check_device()) != HACK_OK) return st;
+  return cuda_status(launch_quantize_pack(kc, mode, x, rows, heads, pos0, head0, rng_id, codes, meta, sums,
+                                          (cudaStream_t)stream),
+                     "quantize_pack");
+}
+
+hack_status_t hack_cache_ingest(const hack_config_t* cfg, const void* k, const void* v, const int32_t* cu,
+                                const int32_t* slots, int32_t batch, int32_t max_seqlen,
+                                const hack_kv_cache_t* cache, void* stream) {
+  KernelCfg kc;
+  CacheView cv;
+  hack_status_t st = make_kernel_cfg(cfg, &kc);
+  if (st != HACK_OK) return st;
+  if ((st = make_cache_view(kc, cache, &cv)) != HACK_OK) return st;
+  if (!k || !v || !cu || !slots) return fail(HACK_ERR_INVALID_ARG, "ingest: NULL pointer");
+  if (batch <= 0 || max_seqlen <= 0) return fail(HACK_ERR_INVALID_ARG, "ingest: empty batch/prompt (S:303)");
+  if ((max_seqlen + kc.Pi - 1) / kc.Pi > cache->max_pages_per_req)
+    return fail(HACK_ERR_CAPACITY, "ingest: max_seqlen needs more pages than max_pages_per_req");
+  if (batch > cache->max_reqs) return fail(HACK_ERR_CAPACITY, "ingest: batch > max_reqs");
+  if ((st = check_device()) != HACK_OK) return st;
+  return cuda_status(launch_ingest(kc, k, v, cu, slots, batch, max_seqlen, cv, (cudaStream_t)stream), "ingest");
+}
+
+size_t hack_prefill_workspace_size(const hack_config_t* cfg, int32_t batch, int32_t max_seqlen) {
+  KernelCfg kc;
+  if (make_kernel_cfg(cfg, &kc) != HACK_OK) return 0;
+  return prefill_workspace_bytes(kc, batch, max_seqlen);
+}
+
+hack_status_t hack_prefill_attention_cached(const hack_config_t* cfg, const void* q, const int32_t* cu,
+                                            const int32_t* slots, int32_t batch, int32_t max_seqlen,
+                                            const hack_kv_cache_t* cache, void* out, void* ws, size_t ws_bytes,
+                                            const hack_debug_t* dbg, void* stream) {
+  KernelCfg kc;
+  CacheView cv;
+  hack_status_t st = make_kernel_cfg(cfg, &kc);
+  if (st != HACK_OK) return st;
+  if ((st = make_cache_view(kc, cache, &cv)) != HACK_OK) return st;
+  if (!q || !cu || !slots || !out) return fail(HACK_ERR_INVALID_ARG, "prefill: NULL pointer");
+  if (batch <= 0 || max_seqlen <= 0) return fail(HACK_ERR_INVALID_ARG, "prefill: empty batch/prompt (S:303)");
+  if ((max_seqlen + kc.Pi - 1) / kc.Pi > cache->max_pages_per_req)
+    return fail(HACK_ERR_CAPACITY, "prefill: max_seqlen needs more pages than max_pages_per_req");
+  const size_t need = prefill_workspace_bytes(kc, batch, max_seqlen);
+  if (ws_bytes < need || (need && !ws)) return fail(HACK_ERR_CAPACITY, "prefill: workspace %zu < %zu", ws_bytes, need);
+  if (dbg && dbg->pcodes && dbg->pcodes_stride < max_seqlen)
+    return fail(HACK_ERR_SHAPE, "prefill: debug pcodes_stride < max_seqlen");
+  if ((st = check_device()) != HACK_OK) return st;
+  return cuda_status(launch_prefill_attention(kc, q, cu, slots, batch, max_seqlen, cv, out, ws, dbg,
+                                              (cudaStream_t)stream),
+                     "prefill_attention");
+}
+
+hack_status_t hack_prefill_attention(const hack_config_t* cfg, const void* q, const void* k, const void* v,
+                                     const int32_t* cu, const int32_t* slots, int32_t batch, int32_t max_seqlen,
+                                     const hack_kv_cache_t* cache, void* out, void* ws, size_t ws_bytes,
+                                     const hack_debug_t* dbg, void* stream) {
+  hack_status_t st = hack_cache_ingest(cfg, k, v, cu, slots, batch, max_seqlen, cache, stream);
+  if (st != HACK_OK) return st;
+  return hack_prefill_attention_cached(cfg, q, cu, slots, batch, max_seqlen, cache, out, ws, ws_bytes, dbg, stream);
+}
+
+hack_status_t hack_decode_append(const hack_config_t* cfg, const void* k_new, const void* v_new,
+                                 const int32_t* slots, int32_t batch, const hack_kv_cache_t* cache, void* stream) {
+  KernelCfg kc;
+  CacheView cv;
+  hack_status_t st = make_kernel_cfg(cfg, &kc);
+  if (st != HACK_OK) return st;
+  if ((st = make_cache_view(kc, cache, &cv)) != HACK_OK) return st;
+  if (!k_new || !v_new || !slots) return fail(HACK_ERR_INVALID_ARG, "decode_append: NULL pointer");
+  if (batch <= 0) return fail(HACK_ERR_INVALID_ARG, "decode_append: empty batch");
+  if (batch > cache->max_reqs) return fail(HACK_ERR_CAPACITY, "decode_append: batch > max_reqs");
+  if ((st = check_device()) != HACK_OK) return st;
+  return cuda_status(launch_append(kc, k_new, v_new, slots, batch, cv, (cudaStream_t)stream), "decode_append");
+}
+
+size_t hack_decode_workspace_size(const hack_config_t* cfg, int32_t batch, int32_t max_seqlen) {
+  KernelCfg kc;
+  if (make_kernel_cfg(cfg, &kc) != HACK_OK) return 0;
+  return decode_workspace_bytes(kc, batch, max_seqlen);
+}
+
+hack_status_t hack_decode_attention_cached(const hack_config_t* cfg, const void* q_new, const int32_t* slots,
+                                           int32_t batch, int32_t max_seqlen, const hack_kv_cache_t* cache,
+                                           void* out, void* ws, size_t ws_bytes, const hack_debug_t* dbg,
+                                           void* stream) {
+  KernelCfg kc;
+  CacheView cv;
+  hack_status_t st = make_kernel_cfg(cfg, &kc);
+  if (st != HACK_OK) return st;
+  if ((st = make_cache_view(kc, cache, &cv)) != HACK_OK) return st;
+  if (!q_new || !slots || !out) return fail(HACK_ERR_INVALID_ARG, "decode: NULL pointer");
+  if (batch <= 0 || max_seqlen <= 0) return fail(HACK_ERR_INVALID_ARG, "decode: empty batch");
+  if ((max_seqlen + kc.Pi - 1) / kc.Pi > cache->max_pages_per_req)
+    return fail(HACK_ERR_CAPACITY, "decode: max_seqlen needs more pages than max_pages_per_req");
+  const size_t need = decode_workspace_bytes(kc, batch, max_seqlen);
+  if (ws_bytes < need || (need && !ws)) return fail(HACK_ERR_CAPACITY, "decode: workspace %zu < %zu", ws_bytes, need);
+  if (dbg && dbg->pcodes && dbg->pcodes_stride < max_seqlen)
+    return fail(HACK_ERR_SHAPE, "decode: debug pcodes_stride < max_seqlen");
+  if ((st = check_device()) != HACK_OK) return st;
+  return cuda_status(launch_decode_attention(kc, q_new, slots, batch, max_seqlen, cv, out, ws, dbg,
+                                             (cudaStream_t)stream),
+                     "decode_attention");
+}
+
+hack_status_t hack_decode_attention(const hack_config_t* cfg, const void* q_new, const void* k_new,
+                                    const void* v_new, const int32_t* slots, int32_t batch, int32_t max_seqlen,
+                                    const hack_kv_cache_t* cache, void* out, void* ws, size_t ws_bytes,
+                                    const hack_debug_t* dbg, void* stream) {
+  hack_status_t st = hack_decode_append(cfg, k_new, v_new, slots, batch, cache, stream);
+  if (st != HACK_OK) return st;
+  return hack_decode_attention_cached(cfg, q_new, slots, batch, max_seqlen, cache, out, ws, ws_bytes, dbg, stream);
+}
+
+hack_status_t hack_homomorphic_matmul(const hack_config_t* cfg, const uint8_t* a_codes, const float* a_meta,
+                                      const uint16_t* a_sums, const uint8_t* b_packed, const void* b_meta,
+                                      const void* b_sums, int32_t M, int32_t N, int32_t Z, int32_t* d_blocks,
+                                      float* c, void* stream) {
+  KernelCfg kc;
+  hack_status_t st = make_kernel_cfg(cfg, &kc);
+  if (st != HACK_OK) return st;
+  if (!a_codes || !a_meta || !a_sums || !b_packed || !b_meta || !b_sums || !c)
+    return fail(HACK_ERR_INVALID_ARG, "homomorphic_matmul: NULL pointer");
+  if (M <= 0 || N <= 0 || Z <= 0) return fail(HACK_ERR_INVALID_ARG, "homomorphic_matmul: empty shape");
+  if (Z % kc.Pi) return fail(HACK_ERR_SHAPE, "homomorphic_matmul: Z %% Pi != 0 (S:143)");
+  if ((st = check_device()) != HACK_OK) return st;
+  return cuda_status(launch_homomorphic_matmul(kc, a_codes, a_meta, a_sums, b_packed, b_meta, b_sums, M, N, Z,
+                                               d_blocks, c, (cudaStream_t)stream),
+                     "homomorphic_matmul");
+}
+
+}  // extern "C"

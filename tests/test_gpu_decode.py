@@ -1,0 +1,87 @@
+"""GPU parity: decode append/flush (a8) and decode attention (a9) vs the oracle.
+
+Summation elimination: the GPU never re-sums codes (it reads the cached sums).
+Requantization elimination: the tail is FP16 until it reaches Pi, then flushed once;
+committed pages are bit-stable.  Outputs within 1e-3 row-relative (R18)."""
+import numpy as np
+import pytest
+import torch
+
+import hack_inputs
+from oracle import attention as att
+
+from .gpu_util import ROW_TOL, check_pcodes, compare_pages, gpu_cfg, hk, make_cache, row_rel_err
+
+pytestmark = pytest.mark.gpu
+
+
+def run_decode(ocfg, prompts, steps, seed=21, check_every=1, check_pages_at=()):
+    h = hk()
+    cfg = gpu_cfg(ocfg)
+    B = len(prompts)
+    maxL = max(prompts) + steps
+    cache = make_cache(cfg, max_reqs=B + 2, max_len=maxL, seed=seed)
+    slots = (np.arange(B, dtype=np.int32) + 1)
+    rid = np.array([7000 + 13 * i for i in range(B)], np.uint32)
+    cache.rng_ids[torch.from_numpy(slots).long()] = torch.from_numpy(rid.view(np.int32)).cuda()
+    states = []
+    # prefill each request (the ingest path), oracle state alongside
+    for i, L in enumerate(prompts):
+        q, k, v = hack_inputs.qkv(seed + i, L, ocfg.Hq, ocfg.Hkv)
+        cu = torch.tensor([0, L], dtype=torch.int32, device="cuda")
+        sl = torch.tensor([slots[i]], dtype=torch.int32, device="cuda")
+        out = torch.zeros((L, ocfg.Hq, 128), dtype=torch.float32, device="cuda")
+        h.prefill_attention(cfg, torch.from_numpy(q).cuda(), torch.from_numpy(k).cuda(),
+                            torch.from_numpy(v).cuda(), cu, sl, L, cache, out)
+        states.append(att.ingest_prompt(ocfg, k, v, rng_id=int(rid[i])))
+    qd, kd, vd = hack_inputs.decode_tokens(seed, steps, B, ocfg.Hq, ocfg.Hkv)
+    sl = torch.from_numpy(slots).cuda()
+    stride = (maxL + 63) // 64 * 64
+    worst, flips = 0.0, 0
+    for s in range(steps):
+        out = torch.zeros((B, ocfg.Hq, 128), dtype=torch.float32, device="cuda")
+        pc = torch.zeros((B, ocfg.Hq, stride), dtype=torch.uint8, device="cuda")
+        h.decode_attention(cfg, torch.from_numpy(qd[s]).cuda(), torch.from_numpy(kd[s]).cuda(),
+                           torch.from_numpy(vd[s]).cuda(), sl, maxL, cache, out, debug_pcodes=pc)
+        torch.cuda.synchronize()
+        og, pcn = out.cpu().numpy(), pc.cpu().numpy()
+        for i in range(B):
+            O, diag = att.decode_step(states[i], qd[s, i], kd[s, i], vd[s, i], keep_diag=True)
+            if s % check_every == 0 or s == steps - 1:
+                nf = states[i].nblocks * ocfg.Pi
+                for hq in range(ocfg.Hq):
+                    if nf:
+                        flips += check_pcodes(pcn[i, hq, :nf][None], diag[hq]["pcodes"], diag[hq]["py"])
+                err = row_rel_err(og[i], O).max()
+                worst = max(worst, float(err))
+                assert err <= ROW_TOL, f"step {s} req {i}: row error {err:.3g}"
+            assert int(cache.seq_lens[int(slots[i])]) == states[i].length
+        if s in check_pages_at:
+            for i in range(B):
+                compare_pages(cache, int(slots[i]), states[i])
+    for i in range(B):
+        compare_pages(cache, int(slots[i]), states[i])
+    return worst, flips
+
+
+def test_c1_decode_512_plus_16():
+    run_decode(att.Config(Hq=1, Hkv=1, Pi=64, bits=2), [512], 16)
+
+
+@pytest.mark.parametrize("L", [1, 63, 64, 65, 127, 500])
+def test_decode_crosses_flush(L):
+    # 70 steps: every prompt crosses at least one Pi boundary (RQE flush)
+    run_decode(att.Config(Hq=4, Hkv=1, Pi=64, bits=2), [L], 70, check_every=7, check_pages_at=(5, 40))
+
+
+def test_decode_batch_gqa_mixed_lengths():
+    run_decode(att.Config(Hq=8, Hkv=2, Pi=64, bits=2, seed=99, layer=1), [100, 1, 64, 255], 40, check_every=5)
+
+
+@pytest.mark.parametrize("Pi,bits", [(32, 2), (128, 2), (64, 4), (128, 4)])
+def test_decode_partition_and_bits(Pi, bits):
+    run_decode(att.Config(Hq=4, Hkv=2, Pi=Pi, bits=bits), [150, 129], 2 * Pi + 3, check_every=11)
+
+
+def test_decode_group_16():
+    run_decode(att.Config(Hq=16, Hkv=1, Pi=64, bits=2), [70], 10, check_every=3)

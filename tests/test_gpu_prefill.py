@@ -1,0 +1,111 @@
+"""GPU parity: homomorphic prefill (a1-a7) through the C ABI vs the oracle.
+
+Bit-exact: page bytes (K/V codes, fp16 meta, sums), FP16 tail, seq_lens.
+Outputs: row-relative error <= 1e-3 (north star, R18) with every P-code mismatch a
+near-tie."""
+import numpy as np
+import pytest
+import torch
+
+import hack_inputs
+from oracle import attention as att
+
+from .gpu_util import ROW_TOL, check_pcodes, compare_pages, gpu_cfg, hk, make_cache, row_rel_err
+
+pytestmark = pytest.mark.gpu
+
+
+def run_prefill(ocfg, prompts, dist="normal", seed=11, rng_ids=None, debug=True):
+    """prompts: list of lengths (one request each).  Returns GPU out [T,Hq,d],
+    pcodes, cache, and per-request inputs."""
+    h = hk()
+    cfg = gpu_cfg(ocfg)
+    reqs = [hack_inputs.qkv(seed + i, L, ocfg.Hq, ocfg.Hkv, dist=dist, partition=ocfg.Pi, kv_bits=ocfg.bits)
+            for i, L in enumerate(prompts)]
+    q = np.concatenate([r[0] for r in reqs]); k = np.concatenate([r[1] for r in reqs])
+    v = np.concatenate([r[2] for r in reqs])
+    cu = np.concatenate([[0], np.cumsum(prompts)]).astype(np.int32)
+    maxL = max(prompts)
+    B = len(prompts)
+    cache = make_cache(cfg, max_reqs=B + 1, max_len=maxL, seed=seed)
+    slots = np.arange(B, dtype=np.int32)[::-1].copy()          # non-trivial slot mapping
+    rid = np.array(rng_ids if rng_ids is not None else [1000 + i for i in range(B)], np.uint32)
+    cache.rng_ids[torch.from_numpy(slots).long()] = torch.from_numpy(rid.view(np.int32)).cuda()
+    out = torch.zeros((q.shape[0], ocfg.Hq, 128), dtype=torch.float32, device="cuda")
+    stride = (maxL + 63) // 64 * 64
+    pc = torch.zeros((q.shape[0], ocfg.Hq, stride), dtype=torch.uint8, device="cuda") if debug else None
+    h.prefill_attention(cfg, torch.from_numpy(q).cuda(), torch.from_numpy(k).cuda(), torch.from_numpy(v).cuda(),
+                        torch.from_numpy(cu).cuda(), torch.from_numpy(slots).cuda(), maxL, cache, out,
+                        debug_pcodes=pc)
+    torch.cuda.synchronize()
+    return out.cpu().numpy(), (pc.cpu().numpy() if debug else None), cache, reqs, cu, slots, rid
+
+
+def check_request(ocfg, i, out, pc, cache, reqs, cu, slots, rid, rows=None):
+    q, k, v = reqs[i]
+    O, state, diag = att.prefill(ocfg, q, k, v, rng_id=int(rid[i]), rows=rows, keep_diag=True)
+    compare_pages(cache, int(slots[i]), state)
+    assert int(cache.seq_lens[int(slots[i])]) == q.shape[0]
+    rows = np.arange(q.shape[0]) if rows is None else np.asarray(rows)
+    Og = out[cu[i]:cu[i + 1]]
+    worst = 0.0
+    flips = 0
+    nfull = q.shape[0] // ocfg.Pi
+    for hq in diag:
+        if pc is not None and nfull:
+            flips += check_pcodes(pc[cu[i] + rows, hq, :nfull * ocfg.Pi], diag[hq]["pcodes"], diag[hq]["py"])
+        err = row_rel_err(Og[rows, hq], O[rows, hq])
+        worst = max(worst, float(err.max()))
+    assert worst <= ROW_TOL, f"max row-relative error {worst:.3g} (P flips {flips})"
+    return worst, flips
+
+
+@pytest.mark.parametrize("L", [512, 1, 63, 64, 65, 127, 500])
+def test_c1_prefill_single_head(L):
+    ocfg = att.Config(Hq=1, Hkv=1, Pi=64, bits=2)
+    res = run_prefill(ocfg, [L])
+    check_request(ocfg, 0, *res)
+
+
+@pytest.mark.parametrize("Pi,bits", [(32, 2), (128, 2), (64, 4), (32, 4), (128, 4)])
+def test_prefill_partition_and_bits(Pi, bits):
+    ocfg = att.Config(Hq=4, Hkv=2, Pi=Pi, bits=bits)
+    res = run_prefill(ocfg, [300])
+    check_request(ocfg, 0, *res)
+
+
+def test_prefill_gqa_varlen_batch():
+    ocfg = att.Config(Hq=8, Hkv=2, Pi=64, bits=2, seed=12345, layer=3, head_base=1)
+    res = run_prefill(ocfg, [200, 64, 333, 17])
+    for i in range(4):
+        check_request(ocfg, i, *res)
+
+
+@pytest.mark.parametrize("dist", ["outlier", "constant", "grid"])
+def test_prefill_adversarial_inputs(dist):
+    ocfg = att.Config(Hq=2, Hkv=1, Pi=64, bits=2, kv_round="rn" if dist == "grid" else "sr")
+    res = run_prefill(ocfg, [257], dist=dist)
+    check_request(ocfg, 0, *res)
+
+
+def test_prefill_rn_rounding():
+    ocfg = att.Config(Hq=2, Hkv=2, Pi=64, bits=2, kv_round="rn", q_round="rn")
+    res = run_prefill(ocfg, [190])
+    check_request(ocfg, 0, *res)
+
+
+def test_c2_full_size_sampled_rows():
+    """Mistral-7B shape (32 Q / 8 KV heads, 4K tokens) at BASELINE size: all page bytes
+    bit-exact, sampled query rows of sampled heads within tolerance."""
+    ocfg = att.Config(Hq=32, Hkv=8, Pi=64, bits=2)
+    res = run_prefill(ocfg, [4096], debug=True)
+    out, pc, cache, reqs, cu, slots, rid = res
+    q, k, v = reqs[0]
+    rows = np.array([0, 1, 63, 64, 777, 2048, 3000, 4031, 4095])
+    O, state, diag = att.prefill(ocfg, q, k, v, rng_id=int(rid[0]), rows=rows, heads=[0, 5, 17, 31],
+                                 keep_diag=True)
+    compare_pages(cache, int(slots[0]), state)
+    for hq in (0, 5, 17, 31):
+        check_pcodes(pc[rows, hq, :4096], diag[hq]["pcodes"], diag[hq]["py"])
+        assert row_rel_err(out[rows, hq], O[rows, hq]).max() <= ROW_TOL
+    assert np.isfinite(out).all()
