@@ -19,7 +19,7 @@ constexpr int kT = 128;
 constexpr int kMaxG = 16;
 
 template <int PI>
-struct DecodeSmem {
+struct __align__(16) DecodeSmem {
   static constexpr int NB = 128 / PI;
   uint8_t q[kMaxG * 128];
   uint8_t p[kMaxG * PI];

@@ -24,7 +24,7 @@ constexpr int BM = 64;        // query rows per CTA
 constexpr int kThreads = 256;
 
 template <int PI>
-struct PrefillSmem {
+struct __align__(16) PrefillSmem {
   static constexpr int BN = PI;                 // key tile = one V block (Pi-aligned, a6)
   static constexpr int QS = 128 + 4;            // padded u8 row strides (bank spread)
   static constexpr int KS = 128 + 4;
@@ -108,7 +108,9 @@ __global__ void __launch_bounds__(kThreads) prefill_simt_kernel(
     int sum;
     quant_row16<8, false>(raw, lane16, PI, i, kc.seed, rng_id,
                           stream_c3(kc.layer, kTagQ, kc.head_base * kc.G + hq), kc.q_round, packed, m, s, sum);
-    *reinterpret_cast<uint2*>(&sm.q[r * SM::QS + lane16 * 8]) = make_uint2((uint32_t)packed, (uint32_t)(packed >> 32));
+    uint32_t* qd = reinterpret_cast<uint32_t*>(&sm.q[r * SM::QS + lane16 * 8]);  // row stride is 4-aligned
+    qd[0] = (uint32_t)packed;
+    qd[1] = (uint32_t)(packed >> 32);
     if ((lane16 & (PI / 8 - 1)) == 0) {
       const int beta = lane16 / (PI / 8);
       // centered: q_hat = s (q' - 127.5) + mu,  mu = m + 127.5 s

@@ -41,22 +41,33 @@ def run_prefill(ocfg, prompts, dist="normal", seed=11, rng_ids=None, debug=True)
     return out.cpu().numpy(), (pc.cpu().numpy() if debug else None), cache, reqs, cu, slots, rid
 
 
-def check_request(ocfg, i, out, pc, cache, reqs, cu, slots, rid, rows=None):
+def check_request(ocfg, i, out, pc, cache, reqs, cu, slots, rid, rows=None, heads=None):
+    """Parity protocol (DESIGN.md): pages bit-exact; every P-code mismatch a near-tie;
+    plain row error <= 1e-3, else the oracle re-run with the GPU's P codes (which differ
+    from its own only at near-ties) must be within 1e-3."""
     q, k, v = reqs[i]
-    O, state, diag = att.prefill(ocfg, q, k, v, rng_id=int(rid[i]), rows=rows, keep_diag=True)
+    O, state, diag = att.prefill(ocfg, q, k, v, rng_id=int(rid[i]), rows=rows, heads=heads, keep_diag=True)
     compare_pages(cache, int(slots[i]), state)
     assert int(cache.seq_lens[int(slots[i])]) == q.shape[0]
     rows = np.arange(q.shape[0]) if rows is None else np.asarray(rows)
     Og = out[cu[i]:cu[i + 1]]
-    worst = 0.0
-    flips = 0
     nfull = q.shape[0] // ocfg.Pi
+    flips, worst_plain, override = 0, 0.0, {}
     for hq in diag:
-        if pc is not None and nfull:
-            flips += check_pcodes(pc[cu[i] + rows, hq, :nfull * ocfg.Pi], diag[hq]["pcodes"], diag[hq]["py"])
         err = row_rel_err(Og[rows, hq], O[rows, hq])
-        worst = max(worst, float(err.max()))
-    assert worst <= ROW_TOL, f"max row-relative error {worst:.3g} (P flips {flips})"
+        worst_plain = max(worst_plain, float(err.max()))
+        if pc is not None and nfull:
+            g = pc[cu[i] + rows, hq, :nfull * ocfg.Pi]
+            flips += check_pcodes(g, diag[hq]["pcodes"], diag[hq]["py"])
+            override[hq] = g          # rows of `rows`, the order att.prefill computes them
+    worst = worst_plain
+    if worst_plain > ROW_TOL:
+        assert pc is not None and flips > 0, f"row error {worst_plain:.3g} without any P-code flip"
+        O2, _, _ = att.prefill(ocfg, q, k, v, rng_id=int(rid[i]), rows=rows, heads=list(override),
+                               pcodes_override=override)
+        worst = max(float(row_rel_err(Og[rows, hq], O2[rows, hq]).max()) for hq in override)
+    print(f"req {i}: plain {worst_plain:.3g}, with GPU P codes {worst:.3g}, near-tie flips {flips}")
+    assert worst <= ROW_TOL, f"max row-relative error {worst:.3g} (plain {worst_plain:.3g}, P flips {flips})"
     return worst, flips
 
 
@@ -100,12 +111,6 @@ def test_c2_full_size_sampled_rows():
     ocfg = att.Config(Hq=32, Hkv=8, Pi=64, bits=2)
     res = run_prefill(ocfg, [4096], debug=True)
     out, pc, cache, reqs, cu, slots, rid = res
-    q, k, v = reqs[0]
     rows = np.array([0, 1, 63, 64, 777, 2048, 3000, 4031, 4095])
-    O, state, diag = att.prefill(ocfg, q, k, v, rng_id=int(rid[0]), rows=rows, heads=[0, 5, 17, 31],
-                                 keep_diag=True)
-    compare_pages(cache, int(slots[0]), state)
-    for hq in (0, 5, 17, 31):
-        check_pcodes(pc[rows, hq, :4096], diag[hq]["pcodes"], diag[hq]["py"])
-        assert row_rel_err(out[rows, hq], O[rows, hq]).max() <= ROW_TOL
+    check_request(ocfg, 0, out, pc, cache, reqs, cu, slots, rid, rows=rows, heads=[0, 5, 17, 31])
     assert np.isfinite(out).all()
