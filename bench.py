@@ -1,0 +1,458 @@
+#!/usr/bin/env python3
+"""HACK hot-path benchmark on B200 (contract: see DESIGN.md "Measurement").
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl hack|reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...    (one rank per GPU)
+
+Workload (BASELINE.json configs[1], "C2"): Mistral-7B-shaped homomorphic prefill --
+32 Q / 8 KV heads, d=128, one 4096-token prompt, 2-bit K/V, Pi=64.  One step =
+hack_cache_ingest (a1, a2: quantize K/V into pages + FP16 tail) +
+hack_prefill_attention_cached (a3-a7: Q quant, Eq. 4 Q'K'^T, online softmax, P quant,
+Eq. 4 P'V' + FP tail).  The decode rows (a8, a9) are timed in the same run on
+configs[2] ("C3": Llama-3.1-8B-shaped decode, batch 64, context 8192) and reported
+under "decode".  Headline: algorithmic int8 ops (2 matmuls x 2*d*L(L+1)/2 x H_q,
+causal triangle) / step time, in TOPS.  Multi-GPU: weak scaling, every rank runs its
+own independent requests (no data-path collective; SURVEY e).
+
+Timing: W warm-up steps, then K steps between barrier + synchronize, per-step CUDA
+events on the launching stream, L2 flushed (512 MB write) before every prefill step
+(outside the events); the C3 cache (352 MB) exceeds L2.  Max over ranks.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+C2 = dict(Hq=32, Hkv=8, L=4096, Pi=64, bits=2)
+C3 = dict(Hq=32, Hkv=8, B=64, ctx=8192, Pi=64, bits=2)
+WORKLOAD = ("C2: Mistral-7B-shaped homomorphic prefill attention (32 Q / 8 KV heads, d=128), "
+            "one 4096-token causal prompt, 2-bit K/V, Pi=64, Q/P 8-bit")
+DECODE_WORKLOAD = ("C3: Llama-3.1-8B-shaped decode attention (32 Q / 8 KV heads, d=128), batch 64, "
+                   "context 8192, 2-bit K/V + summation cache + FP16 last-V block, Pi=64")
+METRIC = "prefill attn int8 TOPS"
+BASELINE_METRIC = "decode attn tokens/s & effective KV GB/s; prefill attn int8 TOPS vs peak"
+
+
+def prefill_ops(L, Hq, d=128):
+    """Algorithmic int8 ops of one causal prefill: 2 matmuls x 2*d*L(L+1)/2 x H_q."""
+    return 2 * 2 * d * (L * (L + 1) // 2) * Hq
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        j = json.load(open(p))
+        return dict(hbm=j["hbm_gbs"], bf16=j["bf16_tflops"], bf16_sus=j.get("bf16_tflops_sustained"),
+                    src="MEASURED_PEAKS.json (measured)", sm_max=j.get("sm_max_mhz"))
+    return dict(hbm=6650.0, bf16=1590.0, bf16_sus=1400.0, src="B200_PROFILING.md fallback", sm_max=1965.0)
+
+
+def load_traffic():
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(p):
+        return json.load(open(p))
+    return {}
+
+
+# ----------------------------------------------------------------------------- clocks
+
+class ClockSampler:
+    """Samples SM clock + throttle reasons with NVML every ~10 ms (own thread)."""
+
+    REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+               0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
+               0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting"}
+
+    def __init__(self, index):
+        self.samples, self.reasons, self.ok = [], 0, False
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception:
+            self.max = None
+        self._stop = threading.Event()
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                self.reasons |= self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+            except Exception:
+                pass
+            time.sleep(0.01)
+
+    def __enter__(self):
+        if self.ok:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        if self.ok:
+            self._stop.set()
+            self.t.join()
+
+    def summary(self):
+        if not self.ok or not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max, "reasons": ["nvml unavailable"]}
+        names = [n for b, n in self.REASONS.items() if self.reasons & b and n != "gpu_idle"]
+        return {"sm_mhz": float(statistics.median(self.samples)), "sm_max_mhz": self.max, "reasons": names,
+                "samples": len(self.samples)}
+
+
+# ----------------------------------------------------------------------------- helpers
+
+def dev_normal(shape, seed, device):
+    """Seeded synthetic fp16 N(0,1) generated on the device (values never affect speed)."""
+    import torch
+    g = torch.Generator(device=device)
+    g.manual_seed(int(seed))
+    return torch.randn(shape, generator=g, device=device, dtype=torch.float32).to(torch.float16)
+
+
+def max_over_ranks(x, world):
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def barrier(world):
+    import torch
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+    torch.cuda.synchronize()
+
+
+# ----------------------------------------------------------------------------- CPU oracle (baseline)
+
+def oracle_sample(seconds_hint=False, L=4096, heads=1):
+    """Time the oracle (as it stands) on a bounded sample of the C2 workload: one KV
+    head group's first `heads` query heads over the full 4096-token prompt.  Returns
+    (TOPS, seconds, ops, description)."""
+    import hack_inputs
+    from oracle import attention as att
+    q, k, v = hack_inputs.qkv(hack_inputs.DATA_SEED, L, 4, 1)
+    cfg = att.Config(Hq=4, Hkv=1, Pi=C2["Pi"], bits=C2["bits"])
+    t0 = time.perf_counter()
+    att.prefill(cfg, q, k, v, heads=list(range(heads)))
+    dt = time.perf_counter() - t0
+    ops = prefill_ops(L, heads)
+    desc = (f"oracle prefill of {heads} of 32 query heads (1 KV head group) of the C2 4096-token prompt, "
+            f"incl. K/V quantization of that KV head")
+    return ops / dt / 1e12, dt, ops, desc
+
+
+def cpu_threads():
+    try:
+        import threadpoolctl
+        info = threadpoolctl.threadpool_info()
+        return max([i.get("num_threads", 1) for i in info] + [1])
+    except Exception:
+        return os.cpu_count()
+
+
+# ----------------------------------------------------------------------------- reference arm
+
+def run_reference(args, rank):
+    if rank != 0:
+        return
+    for _ in range(args.warmup):
+        oracle_sample(heads=1)
+    vals, secs = [], []
+    for _ in range(args.steps):
+        v, dt, ops, desc = oracle_sample(heads=1)
+        vals.append(v)
+        secs.append(dt)
+    value = sum(prefill_ops(C2["L"], 1) for _ in secs) / sum(secs) / 1e12
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "TOPS", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * statistics.mean(secs),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": {"workload": WORKLOAD, "batch": 1, "seq_len": C2["L"],
+                                            "parallelism": "cpu oracle, rank 0 only"},
+            "cpu_baseline": {"value": value, "unit": "TOPS", "cores": cpu_threads(), "kind": "oracle",
+                             "sample": desc + " per step"},
+            "e2e": {"value": value, "unit": "TOPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------------------- HACK arm
+
+def run_hack(args, rank, local_rank, world):
+    import torch
+
+    from paper_2502_03589_b200 import hack as h
+
+    dev = torch.device("cuda", local_rank)
+    torch.cuda.set_device(dev)
+    peaks = load_peaks()
+    traffic = load_traffic()
+    seed = 20250205 + 1000 * rank
+    stream = torch.cuda.current_stream()
+
+    # ---------------- C2 prefill setup
+    L, Hq, Hkv = C2["L"], C2["Hq"], C2["Hkv"]
+    cfg = h.config(num_q_heads=Hq, num_kv_heads=Hkv, partition=C2["Pi"], kv_bits=C2["bits"], out_fp32=False)
+    q = dev_normal((L, Hq, 128), seed + 1, dev)
+    k = dev_normal((L, Hkv, 128), seed + 2, dev)
+    v = dev_normal((L, Hkv, 128), seed + 3, dev)
+    cu = torch.tensor([0, L], dtype=torch.int32, device=dev)
+    slots = torch.tensor([0], dtype=torch.int32, device=dev)
+    cache = h.KVCache.allocate(cfg, max_reqs=1, max_pages_per_req=L // C2["Pi"], device=dev)
+    cache.rng_ids.fill_(rank)
+    out = torch.empty((L, Hq, 128), dtype=torch.float16, device=dev)
+    ws_bytes = h.prefill_workspace_size(cfg, 1, L)
+    ws = torch.empty(max(ws_bytes, 1), dtype=torch.uint8, device=dev)
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
+    ops = prefill_ops(L, Hq)
+
+    def prefill_step(evs=None):
+        if evs:
+            evs[0].record(stream)
+        h.cache_ingest(cfg, k, v, cu, slots, L, cache)
+        if evs:
+            evs[1].record(stream)
+        h.prefill_attention_cached(cfg, q, cu, slots, L, cache, out, workspace=ws)
+        if evs:
+            evs[2].record(stream)
+
+    for _ in range(args.warmup):
+        flush.fill_(1)
+        prefill_step()
+    barrier(world)
+    n0 = h.kernel_launches()
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
+    with ClockSampler(local_rank) as clk:
+        barrier(world)
+        for i in range(args.steps):
+            flush.fill_(1)                      # L2 flush, outside the events
+            prefill_step(evs[i])
+        barrier(world)
+    launches = h.kernel_launches() - n0
+    step_ms = [e[0].elapsed_time(e[2]) for e in evs]
+    attn_ms = [e[1].elapsed_time(e[2]) for e in evs]
+    ms = max_over_ranks(sum(step_ms) / len(step_ms), world)
+    attn_avg = max_over_ranks(sum(attn_ms) / len(attn_ms), world)
+    value = ops * world / (ms * 1e-3) / 1e12
+    int8_peak = 2.0 * peaks["bf16"]
+    achieved = ops / (attn_avg * 1e-3) / 1e12
+    tr = traffic.get("prefill_attention", {}).get("dram_bytes_per_launch")
+
+    # ---------------- e2e through the C ABI with host buffers
+    qh = q.cpu().pin_memory(); kh = k.cpu().pin_memory(); vh = v.cpu().pin_memory()
+    outh = torch.empty(out.shape, dtype=out.dtype).pin_memory()
+    qd = torch.empty_like(q); kd = torch.empty_like(k); vd = torch.empty_like(v)
+
+    def e2e_step():
+        qd.copy_(qh, non_blocking=True); kd.copy_(kh, non_blocking=True); vd.copy_(vh, non_blocking=True)
+        h.prefill_attention(cfg, qd, kd, vd, cu, slots, L, cache, out, workspace=ws)
+        outh.copy_(out, non_blocking=True)
+
+    for _ in range(args.warmup):
+        e2e_step()
+    barrier(world)
+    e_ms = []
+    for _ in range(args.steps):
+        flush.fill_(1)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        e2e_step()
+        b.record(stream)
+        b.synchronize()
+        e_ms.append(a.elapsed_time(b))
+    barrier(world)
+    e2e_ms = max_over_ranks(sum(e_ms) / len(e_ms), world)
+    e2e_val = ops * world / (e2e_ms * 1e-3) / 1e12
+    del qd, kd, vd
+
+    # ---------------- C3 decode (a8, a9)
+    dec = run_decode(args, h, dev, rank, world, peaks, traffic, seed, flush)
+
+    # ---------------- CPU oracle baseline (rank 0, N = 1)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        v_c, dt, ops_s, desc = oracle_sample(heads=2)
+        cpu = {"value": v_c, "unit": "TOPS", "cores": cpu_threads(), "kind": "oracle",
+               "sample": f"{desc}; {dt:.1f} s wall"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "TOPS", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "u8", "data": "synthetic",
+            "config": {"workload": WORKLOAD, "batch": 1, "seq_len": L, "num_q_heads": Hq, "num_kv_heads": Hkv,
+                       "partition": C2["Pi"], "kv_bits": C2["bits"],
+                       "parallelism": f"replicas x{world} (independent requests per GPU)",
+                       "l2": "flushed (512 MB write) before every step, outside the events",
+                       "baseline_metric": BASELINE_METRIC},
+            "roofline": {"bound": "tensor", "achieved": achieved, "peak": int8_peak, "unit": "TFLOP/s",
+                         "frac": achieved / int8_peak, "traffic": tr,
+                         "kernel": "prefill attention (hack_prefill_attention_cached)",
+                         "peak_src": f"{peaks['src']} bf16 burst {peaks['bf16']} x 2 (nominal int8:bf16 4.5:2.25)",
+                         "ops_per_launch": ops, "ms_per_launch": attn_avg},
+            "cpu_baseline": cpu,
+            "e2e": {"value": e2e_val, "unit": "TOPS", "h2d_bytes_per_step": q.nbytes + k.nbytes + v.nbytes,
+                    "d2h_bytes_per_step": out.nbytes, "ms_per_step": e2e_ms,
+                    "path": "pinned host q/k/v -> hack_prefill_attention (ingest + attention) -> host out"},
+            "gpu_launches": launches,
+            "clocks": clk.summary(),
+            "decode": dec,
+        }
+        print(json.dumps(line), flush=True)
+
+
+def run_decode(args, h, dev, rank, world, peaks, traffic, seed, flush):
+    import torch
+    B, ctx, Hq, Hkv, Pi = C3["B"], C3["ctx"], C3["Hq"], C3["Hkv"], C3["Pi"]
+    cfg = h.config(num_q_heads=Hq, num_kv_heads=Hkv, partition=Pi, kv_bits=C3["bits"], out_fp32=False, layer=1)
+    nsteps = args.warmup * 2 + args.steps * 2 + 2
+    max_len = ctx + nsteps
+    mp = (max_len + Pi - 1) // Pi
+    cache = h.KVCache.allocate(cfg, max_reqs=B, max_pages_per_req=mp, device=dev)
+    cache.rng_ids.copy_(torch.arange(B, dtype=torch.int32, device=dev) + 1000 * rank)
+    # fill every request with an 8192-token prompt through the ingest path (chunks of 8 requests)
+    slots_all = torch.arange(B, dtype=torch.int32, device=dev)
+    for c0 in range(0, B, 8):
+        kk = dev_normal((8 * ctx, Hkv, 128), seed + 100 + c0, dev)
+        vv = dev_normal((8 * ctx, Hkv, 128), seed + 200 + c0, dev)
+        cu = torch.arange(0, 9, dtype=torch.int32, device=dev) * ctx
+        h.cache_ingest(cfg, kk, vv, cu, slots_all[c0:c0 + 8].contiguous(), ctx, cache)
+        del kk, vv
+    torch.cuda.synchronize()
+    qn = dev_normal((nsteps, B, Hq, 128), seed + 300, dev)
+    kn = dev_normal((nsteps, B, Hkv, 128), seed + 301, dev)
+    vn = dev_normal((nsteps, B, Hkv, 128), seed + 302, dev)
+    out = torch.empty((B, Hq, 128), dtype=torch.float16, device=dev)
+    ws_bytes = h.decode_workspace_size(cfg, B, max_len)
+    ws = torch.empty(max(ws_bytes, 1), dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream()
+    it = [0]
+
+    def step(evs=None):
+        i = it[0]
+        it[0] += 1
+        if evs:
+            evs[0].record(stream)
+        h.decode_append(cfg, kn[i], vn[i], slots_all, cache)
+        if evs:
+            evs[1].record(stream)
+        h.decode_attention_cached(cfg, qn[i], slots_all, max_len, cache, out, workspace=ws)
+        if evs:
+            evs[2].record(stream)
+
+    for _ in range(args.warmup):
+        step()
+    barrier(world)
+    n_before = int(cache.seq_lens[0].item())
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
+    n0 = h.kernel_launches()
+    barrier(world)
+    for i in range(args.steps):
+        step(evs[i])
+    barrier(world)
+    launches = h.kernel_launches() - n0
+    step_ms = [e[0].elapsed_time(e[2]) for e in evs]
+    attn_ms = [e[1].elapsed_time(e[2]) for e in evs]
+    ms = max_over_ranks(sum(step_ms) / len(step_ms), world)
+    attn_avg = max_over_ranks(sum(attn_ms) / len(attn_ms), world)
+    # algorithmic bytes of one attention launch (context n after the append): committed
+    # tokens at 84 B/token/head (packed K+V, meta, sums), tail tokens at K-row bytes +
+    # fp16 V, plus q in and out.
+    lay = h.page_layout(cfg)
+    pb = h.page_bytes(cfg)
+    krow = sum(lay[x][1] for x in ("k_codes", "k_meta", "k_sums")) // Pi
+    nbytes = []
+    for i in range(args.steps):
+        n = n_before + i + 1
+        C = (n // Pi) * Pi
+        T = n - C
+        nbytes.append(B * Hkv * (C * pb / Pi + T * (krow + 256)) + B * Hq * 128 * 2 * 2)
+    avg_bytes = sum(nbytes) / len(nbytes)
+    gbs = avg_bytes / (attn_avg * 1e-3) / 1e9
+    tok_s = B * world / (ms * 1e-3)
+    # e2e: host q/k/v in, host out back, through hack_decode_attention (append + attend)
+    qh = torch.empty((B, Hq, 128), dtype=torch.float16).pin_memory()
+    kh = torch.empty((B, Hkv, 128), dtype=torch.float16).pin_memory()
+    vh = torch.empty((B, Hkv, 128), dtype=torch.float16).pin_memory()
+    oh = torch.empty((B, Hq, 128), dtype=torch.float16).pin_memory()
+    qd, kd, vd = torch.empty_like(qn[0]), torch.empty_like(kn[0]), torch.empty_like(vn[0])
+    e_ms = []
+    for i in range(args.steps + args.warmup):
+        qh.copy_(qn[it[0] % nsteps]); kh.copy_(kn[it[0] % nsteps]); vh.copy_(vn[it[0] % nsteps])
+        it[0] += 1
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        qd.copy_(qh, non_blocking=True); kd.copy_(kh, non_blocking=True); vd.copy_(vh, non_blocking=True)
+        h.decode_attention(cfg, qd, kd, vd, slots_all, max_len, cache, out, workspace=ws)
+        oh.copy_(out, non_blocking=True)
+        b.record(stream)
+        b.synchronize()
+        if i >= args.warmup:
+            e_ms.append(a.elapsed_time(b))
+    e2e_ms = max_over_ranks(sum(e_ms) / len(e_ms), world)
+    tr = traffic.get("decode_attention", {}).get("dram_bytes_per_launch")
+    return {
+        "metric": "decode attn tokens/s", "value": tok_s, "unit": "tokens/s (per layer)",
+        "kv_gbs": gbs, "ms_per_step": ms, "attn_ms": attn_avg, "steps": args.steps,
+        "config": {"workload": DECODE_WORKLOAD, "batch": B, "context": ctx, "num_q_heads": Hq,
+                   "num_kv_heads": Hkv, "partition": Pi, "kv_bits": C3["bits"],
+                   "step": "hack_decode_append (a8) + hack_decode_attention_cached (a9)",
+                   "l2": "cache 352 MB > L2"},
+        "roofline": {"bound": "hbm", "achieved": gbs, "peak": peaks["hbm"], "unit": "GB/s",
+                     "frac": gbs / peaks["hbm"], "traffic": tr, "bytes_per_launch": avg_bytes,
+                     "kernel": "decode attention (hack_decode_attention_cached)", "peak_src": peaks["src"]},
+        "e2e": {"value": B * world / (e2e_ms * 1e-3), "unit": "tokens/s (per layer)",
+                "h2d_bytes_per_step": qh.nbytes + kh.nbytes + vh.nbytes, "d2h_bytes_per_step": oh.nbytes,
+                "ms_per_step": e2e_ms},
+        "gpu_launches": launches,
+    }
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["hack", "reference"], default="hack")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3) if args.impl == "hack" else args.warmup
+    rank = int(os.environ.get("RANK", 0))
+    local_rank = int(os.environ.get("LOCAL_RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    if args.impl == "reference":
+        run_reference(args, rank)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    try:
+        run_hack(args, rank, local_rank, world)
+    finally:
+        if world > 1:
+            import torch.distributed as dist
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -121,6 +121,8 @@ hack_status_t hack_page_layout(const hack_config_t* cfg, int64_t offsets_out[12]
 const char* hack_last_error(void);
 const char* hack_version(void);
 int32_t hack_abi_version(void);
+/* Total kernels this library has launched in this process (bench launch accounting). */
+int64_t hack_kernel_launches(void);
 
 /* ---- (a1-a3) quantize_pack ---------------------------------------------- */
 /* Quantize x (device fp16, dense [rows][heads][d]) per partition.

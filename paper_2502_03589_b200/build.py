@@ -1,7 +1,8 @@
 """Build libhack.so in-tree with nvcc for sm_100a (B200).
 
-    python -m paper_2502_03589_b200.build          # incremental
-    python -m paper_2502_03589_b200.build --force  # rebuild everything
+    python paper_2502_03589_b200/build.py          # incremental
+    python paper_2502_03589_b200/build.py --force  # rebuild everything
+(run by path: importing the package needs the library it builds)
 
 Objects go to paper_2502_03589_b200/build/, the library to
 paper_2502_03589_b200/libhack.so (git-ignored, travels with gpurun snapshots).

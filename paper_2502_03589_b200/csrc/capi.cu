@@ -3,6 +3,7 @@
 // device every compute entry point returns HACK_ERR_CUDA.
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <cstdarg>
 #include <cstdio>
 #include <cstdlib>
@@ -15,6 +16,8 @@
 namespace hack {
 
 thread_local std::string g_last_error;
+static std::atomic<int64_t> g_launches{0};
+void note_launch(int n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 
 hack_status_t fail(hack_status_t st, const char* fmt, ...) {
   char buf[512];
@@ -147,6 +150,7 @@ hack_status_t hack_page_layout(const hack_config_t* c, int64_t off[12]) {
 const char* hack_last_error(void) { return g_last_error.c_str(); }
 const char* hack_version(void) { return "libhack 0.1 (sm_100a)"; }
 int32_t hack_abi_version(void) { return HACK_ABI_VERSION; }
+int64_t hack_kernel_launches(void) { return g_launches.load(std::memory_order_relaxed); }
 
 hack_status_t hack_quantize_pack(const hack_config_t* cfg, int32_t mode, const void* x, int64_t rows,
                                  int32_t heads, int64_t pos0, int32_t head0, uint32_t rng_id, uint8_t* codes,

@@ -227,6 +227,7 @@ hack_status_t hack_kv_pack(const hack_config_t* cfg, const hack_kv_cache_t* cach
   if ((st = check_device()) != HACK_OK) return st;
   gather_kernel<<<dim3(g.npages + 1, num_layers), 256, 0, (cudaStream_t)stream>>>(
       lp, caches[0].block_table, caches[0].max_pages_per_req, slot, g, hdr, (uint8_t*)staging);
+  note_launch();
   return cuda_status(cudaGetLastError(), "kv_pack gather");
 }
 
@@ -244,6 +245,7 @@ hack_status_t hack_kv_unpack(const hack_config_t* cfg, const hack_kv_cache_t* ca
   scatter_kernel<<<dim3(g.npages + 1, num_layers), 256, 0, (cudaStream_t)stream>>>(
       lp, caches[0].block_table, caches[0].max_pages_per_req, caches[0].seq_lens, caches[0].rng_ids, slot, g, hdr,
       (const uint8_t*)staging, status_dev);
+  note_launch();
   return cuda_status(cudaGetLastError(), "kv_unpack scatter");
 }
 

@@ -231,7 +231,7 @@ cudaError_t launch_decode_simt(const KernelCfg& kc, const void* q_new, const int
   const int64_t ds = dbg ? dbg->pcodes_stride : 0;
   const __half* qh = reinterpret_cast<const __half*>(q_new);
 #define HACK_DC(P, B) \
-  if (kc.Pi == P && kc.bits == B) { decode_simt_kernel<P, B><<<grid, kT, 0, st>>>(qh, slots, cv, kc, out, dp, ds); return cudaGetLastError(); }
+  if (kc.Pi == P && kc.bits == B) { decode_simt_kernel<P, B><<<grid, kT, 0, st>>>(qh, slots, cv, kc, out, dp, ds); note_launch(); return cudaGetLastError(); }
   HACK_DC(32, 2) HACK_DC(64, 2) HACK_DC(128, 2) HACK_DC(32, 4) HACK_DC(64, 4) HACK_DC(128, 4)
 #undef HACK_DC
   return cudaErrorInvalidValue;

@@ -67,6 +67,7 @@ cudaError_t launch_homomorphic_matmul(const KernelCfg& kc, const uint8_t* a_code
   else
     homomm_kernel<4><<<grid, blk, 0, st>>>(a_codes, (const float2*)a_meta, a_sums, b_packed, (const __half2*)b_meta,
                                            (const uint8_t*)b_sums, sb, M, N, Z, kc.Pi, d_blocks, c);
+  note_launch();
   return cudaGetLastError();
 }
 

@@ -8,6 +8,9 @@
 
 namespace hack {
 
+// Counts every kernel this library launches (hack_kernel_launches()).
+void note_launch(int n = 1);
+
 // Validated, kernel-friendly copy of hack_config_t.
 struct KernelCfg {
   int Hq, Hkv, G, d, Pi, bits;

@@ -385,6 +385,7 @@ cudaError_t launch_t(const KernelCfg& kc, const void* q, const int32_t* cu, cons
   dim3 grid((max_seqlen + BM - 1) / BM, kc.Hq, batch);
   kern<<<grid, kThreads, smem, st>>>(reinterpret_cast<const __half*>(q), cu, slots, cv, kc, out,
                                      dbg ? dbg->pcodes : nullptr, dbg ? dbg->pcodes_stride : 0);
+  note_launch();
   return cudaGetLastError();
 }
 

@@ -221,6 +221,7 @@ cudaError_t launch_quantize_pack(const KernelCfg& kc, int mode, const void* x, i
       quant_v_flat_kernel<4><<<grid, 128, 0, st>>>(xh, nblk, heads, pos0, head0, kc.seed, rng_id, kc.layer,
                                                    kc.Pi, kc.kv_round, codes, (__half2*)meta, sums,
                                                    kc.pl.sum_bytes);
+    note_launch();
     return cudaGetLastError();
   }
   const int64_t n = rows * heads;
@@ -237,6 +238,7 @@ cudaError_t launch_quantize_pack(const KernelCfg& kc, int mode, const void* x, i
     quant_rows_flat_kernel<4, true><<<grid, 256, 0, st>>>(xh, rows, heads, pos0, head0, kc.seed, rng_id,
                                                           kc.layer, kTagK, kc.Pi, kc.kv_round, codes, meta,
                                                           sums, kc.pl.sum_bytes);
+  note_launch();
   return cudaGetLastError();
 }
 
@@ -254,6 +256,7 @@ cudaError_t launch_ingest(const KernelCfg& kc, const void* k, const void* v, con
     ingest_k_kernel<4><<<gk, 256, 0, st>>>(kh, cu_seqlens, slots, cv, kc);
     ingest_v_kernel<4><<<gv, 128, 0, st>>>(vh, cu_seqlens, slots, cv, kc);
   }
+  note_launch(2);
   return cudaGetLastError();
 }
 
@@ -265,6 +268,7 @@ cudaError_t launch_append(const KernelCfg& kc, const void* k_new, const void* v_
     append_kernel<2><<<batch, 128, 0, st>>>(kh, vh, slots, cv, kc);
   else
     append_kernel<4><<<batch, 128, 0, st>>>(kh, vh, slots, cv, kc);
+  note_launch();
   return cudaGetLastError();
 }
 

@@ -19,7 +19,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libhack.so")
 
 if not os.path.exists(LIB_PATH):
-    raise ImportError(f"{LIB_PATH} is missing: build it with `python -m paper_2502_03589_b200.build` "
+    raise ImportError(f"{LIB_PATH} is missing: build it with `python paper_2502_03589_b200/build.py` "
                       "(there is no CPU fallback)")
 _lib = C.CDLL(LIB_PATH)
 
@@ -59,6 +59,7 @@ _P = C.c_void_p
 _lib.hack_last_error.restype = C.c_char_p
 _lib.hack_version.restype = C.c_char_p
 _lib.hack_abi_version.restype = C.c_int32
+_lib.hack_kernel_launches.restype = C.c_int64
 _lib.hack_page_bytes.restype = C.c_int64
 _lib.hack_kv_transfer_bytes.restype = C.c_int64
 _lib.hack_prefill_workspace_size.restype = C.c_size_t
@@ -132,6 +133,11 @@ def version() -> str:
 
 def abi_version() -> int:
     return int(_lib.hack_abi_version())
+
+
+def kernel_launches() -> int:
+    """Kernels libhack has launched in this process."""
+    return int(_lib.hack_kernel_launches())
 
 
 def library():
