@@ -5,6 +5,8 @@
 // bit-exact comparison.  A: 8-bit codes (Q-like, fp32 meta); B: kv_bits codes packed
 // per column (K-like, fp16 meta).  Uses the same centered evaluation as the attention
 // kernels.
+#include <cstdlib>
+
 #include "common.cuh"
 #include "internal.h"
 
@@ -55,10 +57,18 @@ __global__ void homomm_kernel(const uint8_t* __restrict__ a, const float2* __res
 
 }  // namespace
 
+cudaError_t launch_homomm_tc(const KernelCfg& kc, const uint8_t* a_codes, const float* a_meta, const uint16_t* a_sums,
+                             const uint8_t* b_packed, const void* b_meta, const void* b_sums, int M, int N, int Z,
+                             int32_t* d_blocks, float* c, cudaStream_t st);
+
 cudaError_t launch_homomorphic_matmul(const KernelCfg& kc, const uint8_t* a_codes, const float* a_meta,
                                       const uint16_t* a_sums, const uint8_t* b_packed, const void* b_meta,
                                       const void* b_sums, int M, int N, int Z, int32_t* d_blocks, float* c,
                                       cudaStream_t st) {
+  // tcgen05 path (the prefill kernel's MMA core) unless HACK_HOMOMM_IMPL=simt
+  const char* impl = getenv("HACK_HOMOMM_IMPL");
+  if (Z <= 512 && !(impl && impl[0] == 's'))
+    return launch_homomm_tc(kc, a_codes, a_meta, a_sums, b_packed, b_meta, b_sums, M, N, Z, d_blocks, c, st);
   dim3 blk(32, 8), grid((N + 31) / 32, (M + 7) / 8);
   const int sb = sum_bytes_for(kc.bits, kc.Pi);
   if (kc.bits == 2)
