@@ -14,6 +14,10 @@ namespace hack {
 cudaError_t launch_prefill_simt(const KernelCfg& kc, const void* q, const int32_t* cu, const int32_t* slots,
                                 int batch, int max_seqlen, const CacheView& cv, void* out,
                                 const hack_debug_t* dbg, cudaStream_t st);
+bool prefill_tc_supported(const KernelCfg& kc);
+cudaError_t launch_prefill_tc(const KernelCfg& kc, const void* q, const int32_t* cu, const int32_t* slots, int batch,
+                              int max_seqlen, const CacheView& cv, void* out, const hack_debug_t* dbg,
+                              cudaStream_t st);
 cudaError_t launch_decode_simt(const KernelCfg& kc, const void* q_new, const int32_t* slots, int batch,
                                const CacheView& cv, void* out, const hack_debug_t* dbg, cudaStream_t st);
 
@@ -31,7 +35,8 @@ cudaError_t launch_prefill_attention(const KernelCfg& kc, const void* q, const i
                                      const int32_t* slots, int batch, int max_seqlen, const CacheView& cv,
                                      void* out, void* workspace, const hack_debug_t* dbg, cudaStream_t st) {
   (void)workspace;
-  (void)env_is;
+  if (prefill_tc_supported(kc) && !env_is("HACK_PREFILL_IMPL", "simt"))
+    return launch_prefill_tc(kc, q, cu_seqlens, slots, batch, max_seqlen, cv, out, dbg, st);
   return launch_prefill_simt(kc, q, cu_seqlens, slots, batch, max_seqlen, cv, out, dbg, st);
 }
 
