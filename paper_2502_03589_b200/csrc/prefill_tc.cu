@@ -42,8 +42,8 @@ struct TcSmem {
   alignas(128) uint8_t k[2][BN * 128];    // K' K-major, SBO 1024
   alignas(128) uint8_t v[2][128 * BN];    // V' K-major (keys = K), SBO 512
   alignas(128) uint8_t p[2][BM * BN];     // P' K-major, SBO 512
-  float4 kconst[2][BN * 2];               // per (key, beta): sk, mu_k, y_k, r_k
-  float4 vconst[2][128];                  // per channel: sv, mu_v, y_v, r_v
+  alignas(16) float kcf[2][2][4][BN];     // [buf][beta][field][key]: sk, mu_k, y_k, -r_k
+  alignas(16) float vcf[2][4][128];       // [buf][field][channel]: sv, mu_v, y_v, -r_v
   float4 qconst[2][BM];                   // per (beta, row): aq, xq, mu_q, r_q
   float4 rowmeta[2][BM];                  // per row: alpha, ap, mup, -
   int sp_part[2][2][BM];                  // per (buffer, softmax WG, row): partial P-code sums
@@ -190,17 +190,23 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_tc_kernel(
           }
         }
 #pragma unroll
-        for (int e2 = 0; e2 < 2; ++e2) {  // (key, beta) coefficients
-          const int e = ut + 64 * e2, key = e >> 1;
-          float4 c4 = make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int beta = 0; beta < 2; ++beta) {  // per-(key, beta) Eq. 4 coefficients
+          const int key = ut, e = 2 * key + beta;
+          float c0 = 0.f, c1 = 0.f, c2 = 0.f, c3 = 0.f;
           if (key < nk) {
             const __half2 mh = reinterpret_cast<const __half2*>(pg + PL.k_meta)[e];
             const float m = __low2float(mh), s2 = __high2float(mh);
             const int sum = load_sum(pg + PL.k_sums, e, PL.sum_bytes);  // cached sum (SE)
             const float mu = m + 0.5f * qkm * s2;
-            c4 = make_float4(s2, mu, s2 * ((float)sum - 0.5f * qkm * PI) + PI * mu, (float)(510 * sum));
+            c0 = s2;
+            c1 = mu;
+            c2 = s2 * ((float)sum - 0.5f * qkm * PI) + PI * mu;
+            c3 = -(float)(510 * sum);
           }
-          sm.kconst[bj][e] = c4;
+          sm.kcf[bj][beta][0][key] = c0;
+          sm.kcf[bj][beta][1][key] = c1;
+          sm.kcf[bj][beta][2][key] = c2;
+          sm.kcf[bj][beta][3][key] = c3;
         }
         if (j < nfull) {
 #pragma unroll
@@ -224,7 +230,10 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_tc_kernel(
             const float m = __low2float(mh), s2 = __high2float(mh);
             const int sum = load_sum(pg + PL.v_sums, ch, PL.sum_bytes);  // cached sum (SE)
             const float mu = m + 0.5f * qkm * s2;
-            sm.vconst[bj][ch] = make_float4(s2, mu, s2 * ((float)sum - 0.5f * qkm * PI) + PI * mu, (float)(510 * sum));
+            sm.vcf[bj][0][ch] = s2;
+            sm.vcf[bj][1][ch] = mu;
+            sm.vcf[bj][2][ch] = s2 * ((float)sum - 0.5f * qkm * PI) + PI * mu;
+            sm.vcf[bj][3][ch] = -(float)(510 * sum);
           }
         }
         ptx::fence_proxy_async_smem();
@@ -303,6 +312,10 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_tc_kernel(
       ptx::named_bar_sync(2, 256);  // both halves of the Q row constants visible
     }
     const float4 qc0 = sm.qconst[0][r], qc1 = sm.qconst[1][r];
+    const float2 qa0 = make_float2(qc0.x, qc0.x), qx0 = make_float2(qc0.y, qc0.y), qm0 = make_float2(qc0.z, qc0.z),
+                 qn0 = make_float2(-qc0.w, -qc0.w);
+    const float2 qa1 = make_float2(qc1.x, qc1.x), qx1 = make_float2(qc1.y, qc1.y), qm1 = make_float2(qc1.z, qc1.z),
+                 qn1 = make_float2(-qc1.w, -qc1.w);
     float m_run = -INFINITY, l_run = 0.f;
     const uint32_t lane_base = (uint32_t)(32 * (warp & 3)) << 16;
     const int kb = 32 * w;
@@ -311,6 +324,8 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_tc_kernel(
       const int bj = j & 1, t0 = j * BN;
       ptx::mbar_wait(&sm.s_full, j & 1);
       ptx::tc_fence_after();
+      // a tile is "full" when every key is visible to every row of this CTA (no causal mask)
+      const bool full = (t0 + BN - 1) <= i0;
       float s[32];
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
@@ -319,63 +334,112 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_tc_kernel(
         ptx::tmem_ld16(tS + lane_base + 64 + kb + 16 * h, d1);
         ptx::tmem_wait_ld();
 #pragma unroll
-        for (int t = 0; t < 16; ++t) {
-          const int kk = kb + 16 * h + t;
-          const float4 k0 = sm.kconst[bj][2 * kk], k1 = sm.kconst[bj][2 * kk + 1];
-          const float e0 = fmaf(4.f, u2f(d0[t]), -(qc0.w + k0.w));  // 4 x centered int dot (exact)
-          const float e1 = fmaf(4.f, u2f(d1[t]), -(qc1.w + k1.w));
-          float acc = fmaf(qc0.x, k0.x * e0, fmaf(qc0.y, k0.y, qc0.z * k0.z));
-          acc += fmaf(qc1.x, k1.x * e1, fmaf(qc1.y, k1.y, qc1.z * k1.z));
-          s[16 * h + t] = (t0 + kk <= i) ? acc : -INFINITY;  // causal mask (R8)
+        for (int g4 = 0; g4 < 4; ++g4) {
+          const int kl = kb + 16 * h + 4 * g4;  // first of 4 keys
+          float2 acc[2];
+#pragma unroll
+          for (int beta = 0; beta < 2; ++beta) {
+            const float4 sk4 = *reinterpret_cast<const float4*>(&sm.kcf[bj][beta][0][kl]);
+            const float4 mu4 = *reinterpret_cast<const float4*>(&sm.kcf[bj][beta][1][kl]);
+            const float4 y4 = *reinterpret_cast<const float4*>(&sm.kcf[bj][beta][2][kl]);
+            const float4 nr4 = *reinterpret_cast<const float4*>(&sm.kcf[bj][beta][3][kl]);
+            const uint32_t* d = beta ? d1 : d0;
+            const float2 A = beta ? qa1 : qa0, X = beta ? qx1 : qx0, M = beta ? qm1 : qm0, NR = beta ? qn1 : qn0;
+#pragma unroll
+            for (int pr = 0; pr < 2; ++pr) {
+              const float2 df = make_float2(u2f(d[4 * g4 + 2 * pr]), u2f(d[4 * g4 + 2 * pr + 1]));
+              const float2 skp = pr ? make_float2(sk4.z, sk4.w) : make_float2(sk4.x, sk4.y);
+              const float2 mup = pr ? make_float2(mu4.z, mu4.w) : make_float2(mu4.x, mu4.y);
+              const float2 yp = pr ? make_float2(y4.z, y4.w) : make_float2(y4.x, y4.y);
+              const float2 nrp = pr ? make_float2(nr4.z, nr4.w) : make_float2(nr4.x, nr4.y);
+              // e = 4 D - r_q - r_k: the centered integer dot x 4, exact in fp32
+              const float2 e = ptx::ffma2(make_float2(4.f, 4.f), df, ptx::fadd2(nrp, NR));
+              const float2 g = ptx::fmul2(skp, e);
+              const float2 base = beta ? ptx::ffma2(M, yp, acc[pr]) : ptx::fmul2(M, yp);
+              acc[pr] = ptx::ffma2(A, g, ptx::ffma2(X, mup, base));
+            }
+          }
+          s[16 * h + 4 * g4 + 0] = acc[0].x;
+          s[16 * h + 4 * g4 + 1] = acc[0].y;
+          s[16 * h + 4 * g4 + 2] = acc[1].x;
+          s[16 * h + 4 * g4 + 3] = acc[1].y;
         }
       }
       ptx::tc_fence_before();
       ptx::mbar_arrive(&sm.s_free);  // S columns may now be overwritten by QK(j+1)
-      float mx = -INFINITY, mn = INFINITY;
       bool masked = false;
+      if (!full) {
 #pragma unroll
-      for (int kk = 0; kk < 32; ++kk) {
+        for (int kk = 0; kk < 32; ++kk) {
+          const bool vis = (t0 + kb + kk) <= i;  // causal mask (R8)
+          masked |= !vis;
+          s[kk] = vis ? s[kk] : -INFINITY;
+        }
+      }
+      float mx = s[0], mn = s[0];
+#pragma unroll
+      for (int kk = 1; kk < 32; ++kk) {
         mx = fmaxf(mx, s[kk]);
-        masked |= (s[kk] == -INFINITY);
-        mn = fminf(mn, s[kk] == -INFINITY ? INFINITY : s[kk]);
+        mn = fminf(mn, s[kk]);
+      }
+      if (masked) {  // min over the visible keys only
+        mn = INFINITY;
+#pragma unroll
+        for (int kk = 0; kk < 32; ++kk) mn = fminf(mn, s[kk] == -INFINITY ? INFINITY : s[kk]);
       }
       sm.xch[j & 1][w][r] = make_float2(mx, masked ? -INFINITY : mn);
       ptx::named_bar_sync(2, 256);
       const float2 other = sm.xch[j & 1][w ^ 1][r];
       mx = fmaxf(mx, other.x);
-      masked = masked || (other.y == -INFINITY);
+      const bool any_masked = masked || (other.y == -INFINITY);
       mn = fminf(mn, other.y == -INFINITY ? INFINITY : other.y);
       const float m_new = fmaxf(m_run, mx);
       const float al = (m_run == -INFINITY) ? 0.f : ex2(m_run - m_new);
-      float lsum = 0.f;
+      float2 ls2 = make_float2(0.f, 0.f);
+      const float2 mneg = make_float2(-m_new, -m_new);
 #pragma unroll
-      for (int kk = 0; kk < 32; ++kk) {
-        s[kk] = (s[kk] == -INFINITY) ? 0.f : ex2(s[kk] - m_new);  // p~ (unnormalised)
-        lsum += s[kk];
+      for (int kk = 0; kk < 32; kk += 2) {
+        const float2 a2 = ptx::fadd2(make_float2(s[kk], s[kk + 1]), mneg);
+        s[kk] = ex2(a2.x);  // ex2(-inf) = +0 for masked keys
+        s[kk + 1] = ex2(a2.y);
+        ls2 = ptx::fadd2(ls2, make_float2(s[kk], s[kk + 1]));
       }
-      l_run = l_run * al + lsum;
+      l_run = l_run * al + (ls2.x + ls2.y);
       m_run = m_new;
       if (j < nfull) {
-        // (a6) P' per (row, V block): 8-bit RN on p~ (codes invariant to the row scale)
-        const float plo = masked ? 0.f : ex2(mn - m_new);
+        // (a6) P' per (row, V block): 8-bit RN on p~ (codes invariant to the row scale);
+        // y = (p - lo) / s rounded with the 1.5*2^23 magic number (y in [0, 255])
+        const float plo = any_masked ? 0.f : ex2(mn - m_new);
         const float phi = ex2(mx - m_new);
         QMeta pm = meta_fp32(plo, phi, 255);
-        if (!(pm.s > 1e-30f)) pm.s = 0.f;
+        if (!(pm.s > 1e-30f)) {
+          pm.s = 0.f;
+          pm.inv = 0.f;
+        }
+        const float2 inv2 = make_float2(pm.inv, pm.inv), nlo2 = make_float2(-plo * pm.inv, -plo * pm.inv);
+        const float2 magic = make_float2(12582912.f, 12582912.f);
+        uint32_t bits[32];
+#pragma unroll
+        for (int kk = 0; kk < 32; kk += 2) {
+          const float2 y = ptx::fadd2(ptx::ffma2(make_float2(s[kk], s[kk + 1]), inv2, nlo2), magic);
+          bits[kk] = __float_as_uint(y.x);
+          bits[kk + 1] = __float_as_uint(y.y);
+        }
         ptx::mbar_wait(&sm.p_free[bj], ((j >> 1) & 1) ^ 1);
-        int sum = 0;
         uint32_t cw[8];
+        uint32_t sum = 0;
 #pragma unroll
         for (int x4 = 0; x4 < 8; ++x4) {
-          uint32_t wd = 0;
-#pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            const int pos = 4 * x4 + e;                                   // byte position (own 32)
-            const int key = 16 * (pos >> 4) + perm_src<BITS>(pos & 15);   // local key it holds
-            const int code = quant_rn(s[key], pm, 255);
-            sum += code;
-            wd |= (uint32_t)code << (8 * e);
-          }
-          cw[x4] = wd;
+          // byte position pos holds local key 16 (pos >> 4) + perm_src(pos & 15)
+          const int p0 = 4 * x4;
+          const int k0 = 16 * (p0 >> 4) + perm_src<BITS>((p0 + 0) & 15);
+          const int k1 = 16 * (p0 >> 4) + perm_src<BITS>((p0 + 1) & 15);
+          const int k2 = 16 * (p0 >> 4) + perm_src<BITS>((p0 + 2) & 15);
+          const int k3 = 16 * (p0 >> 4) + perm_src<BITS>((p0 + 3) & 15);
+          const uint32_t lo2 = ptx::prmt(bits[k0], bits[k1], 0x0040u);
+          const uint32_t hi2 = ptx::prmt(bits[k2], bits[k3], 0x0040u);
+          cw[x4] = ptx::prmt(lo2, hi2, 0x5410u);
+          sum = __dp4a(cw[x4], 0x01010101u, sum);
         }
 #pragma unroll
         for (int g = 0; g < 2; ++g)
@@ -387,7 +451,7 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_tc_kernel(
           for (int pos = 0; pos < 32; ++pos)
             dp[16 * (pos >> 4) + perm_src<BITS>(pos & 15)] = (uint8_t)((cw[pos >> 2] >> (8 * (pos & 3))) & 0xFF);
         }
-        sm.sp_part[bj][w][r] = sum;
+        sm.sp_part[bj][w][r] = (int)sum;
         if (w == 0) sm.rowmeta[bj][r] = make_float4(al, pm.s * 0.25f, pm.m + 127.5f * pm.s, pm.s);
         ptx::fence_proxy_async_smem();
       } else {
@@ -407,9 +471,9 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_tc_kernel(
     const int r = (tid - 384) & (BM - 1);
     const int cb = 64 * c;
     const uint32_t lane_base = (uint32_t)(32 * (warp & 3)) << 16;
-    float o[64];
+    float2 o2[32];  // channels cb + 2x, cb + 2x + 1
 #pragma unroll
-    for (int x = 0; x < 64; ++x) o[x] = 0.f;
+    for (int x = 0; x < 32; ++x) o2[x] = make_float2(0.f, 0.f);
     const int T = L - nfull * PI;
 #pragma unroll 1
     for (int j = 0; j < nkt; ++j) {
@@ -423,16 +487,32 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_tc_kernel(
         ptx::mbar_wait(&sm.d_full[bj], (j >> 1) & 1);
         ptx::mbar_wait(&sm.kv_ready[bj], (j >> 1) & 1);
         ptx::tc_fence_after();
+        const float2 al2 = make_float2(rm.x, rm.x), ap2 = make_float2(rm.y, rm.y), mp2 = make_float2(rm.z, rm.z);
+        const float2 xp2 = make_float2(xp, xp), nrp2 = make_float2(-rp, -rp), four = make_float2(4.f, 4.f);
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
           uint32_t d[32];
           ptx::tmem_ld32(tD0 + 128 * bj + lane_base + cb + 32 * h, d);
           ptx::tmem_wait_ld();
 #pragma unroll
-          for (int x = 0; x < 32; ++x) {
-            const float4 v4 = sm.vconst[bj][cb + 32 * h + x];
-            const float e = fmaf(4.f, u2f(d[x]), -(rp + v4.w));  // 4 x centered int dot (exact)
-            o[32 * h + x] = fmaf(rm.x, o[32 * h + x], fmaf(rm.y, v4.x * e, fmaf(xp, v4.y, rm.z * v4.z)));
+          for (int x4 = 0; x4 < 8; ++x4) {
+            const int c0 = cb + 32 * h + 4 * x4;
+            const float4 sv4 = *reinterpret_cast<const float4*>(&sm.vcf[bj][0][c0]);
+            const float4 mu4 = *reinterpret_cast<const float4*>(&sm.vcf[bj][1][c0]);
+            const float4 y4 = *reinterpret_cast<const float4*>(&sm.vcf[bj][2][c0]);
+            const float4 nr4 = *reinterpret_cast<const float4*>(&sm.vcf[bj][3][c0]);
+#pragma unroll
+            for (int pr = 0; pr < 2; ++pr) {
+              const int xo = 4 * x4 + 2 * pr;
+              const float2 df = make_float2(u2f(d[xo]), u2f(d[xo + 1]));
+              const float2 svp = pr ? make_float2(sv4.z, sv4.w) : make_float2(sv4.x, sv4.y);
+              const float2 mup = pr ? make_float2(mu4.z, mu4.w) : make_float2(mu4.x, mu4.y);
+              const float2 yp = pr ? make_float2(y4.z, y4.w) : make_float2(y4.x, y4.y);
+              const float2 nrp = pr ? make_float2(nr4.z, nr4.w) : make_float2(nr4.x, nr4.y);
+              const float2 e = ptx::ffma2(four, df, ptx::fadd2(nrp, nrp2));  // 4 x centered int dot (exact)
+              const float2 t = ptx::ffma2(ap2, ptx::fmul2(svp, e), ptx::ffma2(xp2, mup, ptx::fmul2(mp2, yp)));
+              o2[16 * h + 2 * x4 + pr] = ptx::ffma2(al2, o2[16 * h + 2 * x4 + pr], t);
+            }
           }
         }
         ptx::tc_fence_before();
@@ -442,7 +522,7 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_tc_kernel(
         const __half* tail =
             reinterpret_cast<const __half*>(cv.v_tail) + ((int64_t)slot * kc.Hkv + hk) * PI * 128 + cb;
 #pragma unroll
-        for (int x = 0; x < 64; ++x) o[x] *= rm.x;
+        for (int x = 0; x < 32; ++x) o2[x] = ptx::fmul2(o2[x], make_float2(rm.x, rm.x));
 #pragma unroll 1
         for (int t = 0; t < T; ++t) {
           const float pt = sm.ptail[r][t];
@@ -453,9 +533,7 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_tc_kernel(
             const __half2* h2 = reinterpret_cast<const __half2*>(&raw);
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
-              const float2 f = __half22float2(h2[e]);
-              o[c8 * 8 + 2 * e] = fmaf(pt, f.x, o[c8 * 8 + 2 * e]);
-              o[c8 * 8 + 2 * e + 1] = fmaf(pt, f.y, o[c8 * 8 + 2 * e + 1]);
+              o2[c8 * 4 + e] = ptx::ffma2(make_float2(pt, pt), __half22float2(h2[e]), o2[c8 * 4 + e]);
             }
           }
         }
@@ -470,14 +548,15 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_tc_kernel(
         float4* op = reinterpret_cast<float4*>(reinterpret_cast<float*>(out) + base);
 #pragma unroll
         for (int c4 = 0; c4 < 16; ++c4)
-          op[c4] = make_float4(o[4 * c4] * inv_l, o[4 * c4 + 1] * inv_l, o[4 * c4 + 2] * inv_l, o[4 * c4 + 3] * inv_l);
+          op[c4] = make_float4(o2[2 * c4].x * inv_l, o2[2 * c4].y * inv_l, o2[2 * c4 + 1].x * inv_l,
+                               o2[2 * c4 + 1].y * inv_l);
       } else {
         uint4* op = reinterpret_cast<uint4*>(reinterpret_cast<__half*>(out) + base);
 #pragma unroll
         for (int c8 = 0; c8 < 8; ++c8) {
           __half2 hh[4];
 #pragma unroll
-          for (int e = 0; e < 4; ++e) hh[e] = __floats2half2_rn(o[8 * c8 + 2 * e] * inv_l, o[8 * c8 + 2 * e + 1] * inv_l);
+          for (int e = 0; e < 4; ++e) hh[e] = __floats2half2_rn(o2[4 * c8 + e].x * inv_l, o2[4 * c8 + e].y * inv_l);
           op[c8] = *reinterpret_cast<uint4*>(hh);
         }
       }
