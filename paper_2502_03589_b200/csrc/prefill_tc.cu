@@ -32,6 +32,7 @@ constexpr int PI = 64;
 constexpr int BM = 128;
 constexpr int BN = 64;
 constexpr int NS = 4;           // page stages
+constexpr int NB = 3;           // K/V/P tile buffer sets (softmax may run NB-1 tiles ahead of correction)
 constexpr int kThreads = 640;   // 20 warps: 4 (producer, MMA, 2 unpack) + 2 softmax WGs + 2 correction WGs
 
 template <int BITS>
@@ -39,19 +40,19 @@ struct TcSmem {
   static constexpr int PB = BITS == 2 ? 5376 : 9728;  // page bytes (d=128, Pi=64)
   uint8_t stage[NS][PB];
   alignas(128) uint8_t q[BM * 128];       // Q' K-major, SBO 1024
-  alignas(128) uint8_t k[2][BN * 128];    // K' K-major, SBO 1024
-  alignas(128) uint8_t v[2][128 * BN];    // V' K-major (keys = K), SBO 512
-  alignas(128) uint8_t p[2][BM * BN];     // P' K-major, SBO 512
-  alignas(16) float kcf[2][2][4][BN];     // [buf][beta][field][key]: sk, mu_k, y_k, -r_k
-  alignas(16) float vcf[2][4][128];       // [buf][field][channel]: sv, mu_v, y_v, -r_v
+  alignas(128) uint8_t k[NB][BN * 128];   // K' K-major, SBO 1024
+  alignas(128) uint8_t v[NB][128 * BN];   // V' K-major (keys = K), SBO 512
+  alignas(128) uint8_t p[NB][BM * BN];    // P' K-major, SBO 512
+  alignas(16) float kcf[NB][2][4][BN];    // [buf][beta][field][key]: sk, mu_k, y_k, -r_k
+  alignas(16) float vcf[NB][4][128];      // [buf][field][channel]: sv, mu_v, y_v, -r_v
   float4 qconst[2][BM];                   // per (beta, row): aq, xq, mu_q, r_q
-  float4 rowmeta[2][BM];                  // per row: alpha, ap, mup, -
-  int sp_part[2][2][BM];                  // per (buffer, softmax WG, row): partial P-code sums
+  float4 rowmeta[NB][BM];                 // per row: alpha, ap, mup, s_p
+  int sp_part[NB][2][BM];                 // per (buffer, softmax WG, row): partial P-code sums
   float2 xch[2][2][BM];                   // per (parity, softmax WG, row): partial (max, min|-inf)
   float ptail[BM][BN + 1];                // p~ of the FP16 tail tile
   float lpart[2][BM];
-  uint64_t full[NS], empty[NS], kv_ready[2], kv_free[2], s_full, s_free, p_ready[2], p_free[2], d_full[2],
-      d_free[2], q_ready;
+  uint64_t full[NS], empty[NS], k_ready[NB], k_free[NB], v_ready[NB], v_free[NB], p_ready[NB], p_free[NB],
+      meta_free[NB], d_full[2], d_free[2], s_full, s_free, q_ready;
   uint32_t tmem_base;
 };
 
@@ -84,11 +85,16 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_tc_kernel(
       ptx::mbar_init(&sm.full[s], 1);
       ptx::mbar_init(&sm.empty[s], 64);
     }
-    for (int x = 0; x < 2; ++x) {
-      ptx::mbar_init(&sm.kv_ready[x], 64);
-      ptx::mbar_init(&sm.kv_free[x], 256);
+    for (int x = 0; x < NB; ++x) {
+      ptx::mbar_init(&sm.k_ready[x], 64);
+      ptx::mbar_init(&sm.k_free[x], 256);
+      ptx::mbar_init(&sm.v_ready[x], 64);
+      ptx::mbar_init(&sm.v_free[x], 256);
       ptx::mbar_init(&sm.p_ready[x], 256);
       ptx::mbar_init(&sm.p_free[x], 1);
+      ptx::mbar_init(&sm.meta_free[x], 256);
+    }
+    for (int x = 0; x < 2; ++x) {
       ptx::mbar_init(&sm.d_full[x], 1);
       ptx::mbar_init(&sm.d_free[x], 256);
     }
@@ -126,12 +132,12 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_tc_kernel(
       ptx::mbar_wait(&sm.q_ready, 0);
       for (int j = 0; j <= nkt; ++j) {
         if (j < nkt) {
-          const int bj = j & 1;
-          ptx::mbar_wait(&sm.kv_ready[bj], (j >> 1) & 1);
+          const int bq = j % NB;
+          ptx::mbar_wait(&sm.k_ready[bq], (j / NB) & 1);
           ptx::mbar_wait(&sm.s_free, (j & 1) ^ 1);
           ptx::tc_fence_after();
           if (lane == 0) {
-            const uint32_t ka = ptx::smem_u32(sm.k[bj]);
+            const uint32_t ka = ptx::smem_u32(sm.k[bq]);
 #pragma unroll
             for (int beta = 0; beta < 2; ++beta)
 #pragma unroll
@@ -146,18 +152,20 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_tc_kernel(
         }
         const int jj = j - 1;  // PV of the previous tile, after QK of this one (overlap)
         if (jj >= 0 && jj < nfull) {
-          const int bb = jj & 1;
-          ptx::mbar_wait(&sm.p_ready[bb], (jj >> 1) & 1);
+          const int bb = jj & 1, bq = jj % NB;
+          const uint32_t ph = (jj / NB) & 1;
+          ptx::mbar_wait(&sm.p_ready[bq], ph);
+          ptx::mbar_wait(&sm.v_ready[bq], ph);
           ptx::mbar_wait(&sm.d_free[bb], ((jj >> 1) & 1) ^ 1);
           ptx::tc_fence_after();
           if (lane == 0) {
-            const uint32_t pa = ptx::smem_u32(sm.p[bb]), va = ptx::smem_u32(sm.v[bb]);
+            const uint32_t pa = ptx::smem_u32(sm.p[bq]), va = ptx::smem_u32(sm.v[bq]);
 #pragma unroll
             for (int ks = 0; ks < BN / 32; ++ks)
               ptx::mma_u8(tD0 + 128 * bb, ptx::smem_desc_kmajor(pa + ks * 256, 128, 512),
                           ptx::smem_desc_kmajor(va + ks * 256, 128, 512), idesc_pv, ks > 0);
             ptx::mma_commit(&sm.d_full[bb]);
-            ptx::mma_commit(&sm.p_free[bb]);
+            ptx::mma_commit(&sm.p_free[bq]);
           }
           __syncwarp();
         }
@@ -167,9 +175,10 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_tc_kernel(
       const int ut = tid - 64;
 #pragma unroll 1
       for (int j = 0; j < nkt; ++j) {
-        const int s = j % NS, bj = j & 1;
+        const int s = j % NS, bj = j % NB;
+        const uint32_t ph = (j / NB) & 1;
         ptx::mbar_wait(&sm.full[s], (j / NS) & 1);
-        ptx::mbar_wait(&sm.kv_free[bj], ((j >> 1) & 1) ^ 1);
+        ptx::mbar_wait(&sm.k_free[bj], ph ^ 1);
         const uint8_t* pg = sm.stage[s];
         const int nk = min(BN, L - j * BN);
         {  // K' codes: thread = key; 8 consecutive keys fill one 128-byte core matrix per store
@@ -208,6 +217,9 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_tc_kernel(
           sm.kcf[bj][beta][2][key] = c2;
           sm.kcf[bj][beta][3][key] = c3;
         }
+        ptx::fence_proxy_async_smem();
+        ptx::mbar_arrive(&sm.k_ready[bj]);
+        ptx::mbar_wait(&sm.v_free[bj], ph ^ 1);
         if (j < nfull) {
 #pragma unroll
           for (int c2 = 0; c2 < 2; ++c2) {
@@ -237,7 +249,7 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_tc_kernel(
           }
         }
         ptx::fence_proxy_async_smem();
-        ptx::mbar_arrive(&sm.kv_ready[bj]);
+        ptx::mbar_arrive(&sm.v_ready[bj]);
         ptx::mbar_arrive(&sm.empty[s]);
       }
     }
@@ -321,7 +333,8 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_tc_kernel(
     const int kb = 32 * w;
 #pragma unroll 1
     for (int j = 0; j < nkt; ++j) {
-      const int bj = j & 1, t0 = j * BN;
+      const int bj = j % NB, t0 = j * BN;
+      const uint32_t ph = (j / NB) & 1;
       ptx::mbar_wait(&sm.s_full, j & 1);
       ptx::tc_fence_after();
       // a tile is "full" when every key is visible to every row of this CTA (no causal mask)
@@ -366,7 +379,8 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_tc_kernel(
         }
       }
       ptx::tc_fence_before();
-      ptx::mbar_arrive(&sm.s_free);  // S columns may now be overwritten by QK(j+1)
+      ptx::mbar_arrive(&sm.s_free);      // S columns may now be overwritten by QK(j+1)
+      ptx::mbar_arrive(&sm.k_free[bj]);  // K' tile + key coefficients may be refilled
       bool masked = false;
       if (!full) {
 #pragma unroll
@@ -425,7 +439,8 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_tc_kernel(
           bits[kk] = __float_as_uint(y.x);
           bits[kk + 1] = __float_as_uint(y.y);
         }
-        ptx::mbar_wait(&sm.p_free[bj], ((j >> 1) & 1) ^ 1);
+        ptx::mbar_wait(&sm.p_free[bj], ph ^ 1);
+        ptx::mbar_wait(&sm.meta_free[bj], ph ^ 1);
         uint32_t cw[8];
         uint32_t sum = 0;
 #pragma unroll
@@ -455,6 +470,7 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_tc_kernel(
         if (w == 0) sm.rowmeta[bj][r] = make_float4(al, pm.s * 0.25f, pm.m + 127.5f * pm.s, pm.s);
         ptx::fence_proxy_async_smem();
       } else {
+        ptx::mbar_wait(&sm.meta_free[bj], ph ^ 1);
 #pragma unroll
         for (int kk = 0; kk < 32; ++kk) sm.ptail[r][kb + kk] = s[kk];
         if (w == 0) sm.rowmeta[bj][r] = make_float4(al, 0.f, 0.f, 0.f);
@@ -477,22 +493,24 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_tc_kernel(
     const int T = L - nfull * PI;
 #pragma unroll 1
     for (int j = 0; j < nkt; ++j) {
-      const int bj = j & 1;
-      ptx::mbar_wait(&sm.p_ready[bj], (j >> 1) & 1);
+      const int bj = j % NB, bd = j & 1;
+      const uint32_t ph = (j / NB) & 1;
+      ptx::mbar_wait(&sm.p_ready[bj], ph);
       const float4 rm = sm.rowmeta[bj][r];
+      const int sp = sm.sp_part[bj][0][r] + sm.sp_part[bj][1][r];
+      ptx::mbar_arrive(&sm.meta_free[bj]);  // row meta consumed
       if (j < nfull) {
-        const int sp = sm.sp_part[bj][0][r] + sm.sp_part[bj][1][r];
         const float xp = rm.w * ((float)sp - 127.5f * PI);
         const float rp = (float)(2 * qkm * sp - PI * 255 * qkm);
-        ptx::mbar_wait(&sm.d_full[bj], (j >> 1) & 1);
-        ptx::mbar_wait(&sm.kv_ready[bj], (j >> 1) & 1);
+        ptx::mbar_wait(&sm.d_full[bd], (j >> 1) & 1);
+        ptx::mbar_wait(&sm.v_ready[bj], ph);
         ptx::tc_fence_after();
         const float2 al2 = make_float2(rm.x, rm.x), ap2 = make_float2(rm.y, rm.y), mp2 = make_float2(rm.z, rm.z);
         const float2 xp2 = make_float2(xp, xp), nrp2 = make_float2(-rp, -rp), four = make_float2(4.f, 4.f);
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
           uint32_t d[32];
-          ptx::tmem_ld32(tD0 + 128 * bj + lane_base + cb + 32 * h, d);
+          ptx::tmem_ld32(tD0 + 128 * bd + lane_base + cb + 32 * h, d);
           ptx::tmem_wait_ld();
 #pragma unroll
           for (int x4 = 0; x4 < 8; ++x4) {
@@ -516,7 +534,7 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_tc_kernel(
           }
         }
         ptx::tc_fence_before();
-        ptx::mbar_arrive(&sm.d_free[bj]);
+        ptx::mbar_arrive(&sm.d_free[bd]);
       } else {
         // FP16 last V block (RQE): O = alpha O + sum_t p~_t v_t in fp32
         const __half* tail =
@@ -538,7 +556,7 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_tc_kernel(
           }
         }
       }
-      ptx::mbar_arrive(&sm.kv_free[bj]);
+      ptx::mbar_arrive(&sm.v_free[bj]);
     }
     ptx::named_bar_sync(1, 512);
     if (i0 + r < L) {
