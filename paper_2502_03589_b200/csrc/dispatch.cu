@@ -21,6 +21,14 @@ cudaError_t launch_prefill_tc(const KernelCfg& kc, const void* q, const int32_t*
 cudaError_t launch_decode_simt(const KernelCfg& kc, const void* q_new, const int32_t* slots, int batch,
                                const CacheView& cv, void* out, const hack_debug_t* dbg, cudaStream_t st);
 
+bool decode_mma_supported(const KernelCfg& kc);
+size_t decode_mma_workspace(const KernelCfg& kc, int batch, int max_seqlen);
+cudaError_t launch_decode_mma(const KernelCfg& kc, const void* q_new, const int32_t* slots, int batch,
+                              int max_seqlen, const CacheView& cv, void* out, void* workspace,
+                              const hack_debug_t* dbg, cudaStream_t st);
+
+static bool use_decode_mma(const KernelCfg& kc);
+
 static bool env_is(const char* name, const char* val) {
   const char* e = getenv(name);
   return e && strcmp(e, val) == 0;
@@ -40,15 +48,19 @@ cudaError_t launch_prefill_attention(const KernelCfg& kc, const void* q, const i
   return launch_prefill_simt(kc, q, cu_seqlens, slots, batch, max_seqlen, cv, out, dbg, st);
 }
 
+static bool use_decode_mma(const KernelCfg& kc) {
+  return decode_mma_supported(kc) && !env_is("HACK_DECODE_IMPL", "simt");
+}
+
 size_t decode_workspace_bytes(const KernelCfg& kc, int batch, int max_seqlen) {
-  (void)kc; (void)batch; (void)max_seqlen;
-  return 0;
+  return use_decode_mma(kc) ? decode_mma_workspace(kc, batch, max_seqlen) : 0;
 }
 
 cudaError_t launch_decode_attention(const KernelCfg& kc, const void* q_new, const int32_t* slots, int batch,
                                     int max_seqlen, const CacheView& cv, void* out, void* workspace,
                                     const hack_debug_t* dbg, cudaStream_t st) {
-  (void)workspace; (void)max_seqlen;
+  if (use_decode_mma(kc))
+    return launch_decode_mma(kc, q_new, slots, batch, max_seqlen, cv, out, workspace, dbg, st);
   return launch_decode_simt(kc, q_new, slots, batch, cv, out, dbg, st);
 }
 
