@@ -29,6 +29,7 @@ constexpr int PI = 64;
 constexpr int NW = 4;        // compute warps per CTA
 constexpr int NSTG = 8;      // page stages per CTA
 constexpr int kThreads = (NW + 1) * 32;
+constexpr uint32_t kMagicI = 0x4B000000u;  // bits of 2^23
 
 template <int BITS>
 struct DecSmem {
@@ -38,8 +39,8 @@ struct DecSmem {
     float mrg_o[NW][8][128];  // after the page loop: per-warp partial O for the CTA merge
   };
   struct Warp {
-    alignas(16) float kc[2][4][PI];   // [beta][field][token]: sk, mu_k, y_k, -r_k
-    alignas(16) float vc[4][128];     // [field][channel]: sv, mu_v, y_v, -r_v
+    float4 kc[2][PI];                 // [beta][token]: sk, mu_k, y_k, -r_k
+    float4 vc[128];                   // [channel]: sv, mu_v, y_v, -r_v
     alignas(16) uint8_t pcode[8][PI]; // P' in B-fragment order
     float ptl[8][PI];                 // p~ of the FP16 tail page
   } w[NW];
@@ -191,10 +192,7 @@ __global__ void __launch_bounds__(kThreads, 3) decode_mma_kernel(const __half* _
           c2 = sk * ((float)sum - 0.5f * qkm * PI) + PI * mu;
           c3 = -(float)(510 * sum);
         }
-        ws.kc[beta][0][t] = c0;
-        ws.kc[beta][1][t] = c1;
-        ws.kc[beta][2][t] = c2;
-        ws.kc[beta][3][t] = c3;
+        ws.kc[beta][t] = make_float4(c0, c1, c2, c3);
       }
       if (committed) {
 #pragma unroll
@@ -204,10 +202,7 @@ __global__ void __launch_bounds__(kThreads, 3) decode_mma_kernel(const __half* _
           const float mv = __low2float(mh), sv = __high2float(mh);
           const int sum = load_sum(pg + PL.v_sums, c, PL.sum_bytes);  // cached (SE)
           const float mu = mv + 0.5f * qkm * sv;
-          ws.vc[0][c] = sv;
-          ws.vc[1][c] = mu;
-          ws.vc[2][c] = sv * ((float)sum - 0.5f * qkm * PI) + PI * mu;
-          ws.vc[3][c] = -(float)(510 * sum);
+          ws.vc[c] = make_float4(sv, mu, sv * ((float)sum - 0.5f * qkm * PI) + PI * mu, -(float)(510 * sum));
         }
       }
       __syncwarp();
@@ -226,7 +221,8 @@ __global__ void __launch_bounds__(kThreads, 3) decode_mma_kernel(const __half* _
           w0[4 * x] = a.x; w0[4 * x + 1] = a.y; w0[4 * x + 2] = a.z; w0[4 * x + 3] = a.w;
           w1[4 * x] = c.x; w1[4 * x + 1] = c.y; w1[4 * x + 2] = c.z; w1[4 * x + 3] = c.w;
         }
-        uint32_t acc[2][4] = {{0u, 0u, 0u, 0u}, {0u, 0u, 0u, 0u}};
+        // accumulate on top of 0x4B000000: asfloat(acc) = 2^23 + D exactly (D < 2^22)
+        uint32_t acc[2][4] = {{kMagicI, kMagicI, kMagicI, kMagicI}, {kMagicI, kMagicI, kMagicI, kMagicI}};
 #pragma unroll
         for (int ks = 0; ks < 4; ++ks) {
           uint32_t a[4];
@@ -252,16 +248,18 @@ __global__ void __launch_bounds__(kThreads, 3) decode_mma_kernel(const __half* _
           float2 accf = make_float2(0.f, 0.f);
 #pragma unroll
           for (int beta = 0; beta < 2; ++beta) {
-            const float sk = ws.kc[beta][0][t], mu = ws.kc[beta][1][t], yk = ws.kc[beta][2][t], nr = ws.kc[beta][3][t];
-            const float2 df = make_float2(u2f(acc[beta][2 * hh]), u2f(acc[beta][2 * hh + 1]));
+            const float4 k4 = ws.kc[beta][t];
+            const float sk = k4.x, mu = k4.y, yk = k4.z, nr = k4.w;
+            const float2 df = ptx::fadd2(make_float2(__uint_as_float(acc[beta][2 * hh]), __uint_as_float(acc[beta][2 * hh + 1])),
+                                         make_float2(-8388608.f, -8388608.f));
             const float2 e = ptx::ffma2(make_float2(4.f, 4.f), df, ptx::fadd2(QN[beta], make_float2(nr, nr)));
             const float2 base = ptx::ffma2(QM[beta], make_float2(yk, yk), accf);
             accf = ptx::ffma2(QA[beta], ptx::fmul2(make_float2(sk, sk), e), ptx::ffma2(QX[beta], make_float2(mu, mu), base));
           }
-          if (t >= nk) accf = make_float2(-INFINITY, -INFINITY);
+          if (!committed && t >= nk) accf = make_float2(-INFINITY, -INFINITY);  // beyond the cache (tail page)
           st[hh] = accf;
           mx2 = make_float2(fmaxf(mx2.x, accf.x), fmaxf(mx2.y, accf.y));
-          if (t < nk) mn2 = make_float2(fminf(mn2.x, accf.x), fminf(mn2.y, accf.y));
+          if (committed || t < nk) mn2 = make_float2(fminf(mn2.x, accf.x), fminf(mn2.y, accf.y));
         }
         sv2[mt][0] = st[0];
         sv2[mt][1] = st[1];
@@ -322,10 +320,6 @@ __global__ void __launch_bounds__(kThreads, 3) decode_mma_kernel(const __half* _
                                        : (t & ~15) + 4 * (((tp >> 3) << 1) | (tp & 1)) + ((tp >> 1) & 3);
             ws.pcode[n0][posn] = (uint8_t)c0;
             ws.pcode[n1][posn] = (uint8_t)c1;
-            if (dbg_pcodes != nullptr) {
-              if (n0 < G) dbg_pcodes[((int64_t)b * kc.Hq + hk * G + n0) * dbg_stride + jp * PI + t] = (uint8_t)c0;
-              if (n1 < G) dbg_pcodes[((int64_t)b * kc.Hq + hk * G + n1) * dbg_stride + jp * PI + t] = (uint8_t)c1;
-            }
           }
 #pragma unroll
         for (int o2 = 4; o2 < 32; o2 <<= 1) {
@@ -333,6 +327,14 @@ __global__ void __launch_bounds__(kThreads, 3) decode_mma_kernel(const __half* _
           sp1 += __shfl_xor_sync(0xffffffffu, sp1, o2);
         }
         __syncwarp();
+        if (dbg_pcodes != nullptr && g < G) {  // debug dump (natural token order) of row g
+          for (int t = tig; t < PI; t += 4) {
+            const int tp = t & 15;
+            const int posn = BITS == 2 ? (t & ~15) + 4 * (tp & 3) + (tp >> 2)
+                                       : (t & ~15) + 4 * (((tp >> 3) << 1) | (tp & 1)) + ((tp >> 1) & 3);
+            dbg_pcodes[((int64_t)b * kc.Hq + hk * G + g) * dbg_stride + jp * PI + t] = ws.pcode[g][posn];
+          }
+        }
         // P' B fragments (row n = g): positions 32ks + 4tig (b0) and 32ks + 16 + 4tig (b1)
         uint32_t pb[2][2];
 #pragma unroll
@@ -351,7 +353,7 @@ __global__ void __launch_bounds__(kThreads, 3) decode_mma_kernel(const __half* _
           const int c0 = 16 * mt + g, c1 = c0 + 8;
           const uint4 va = *reinterpret_cast<const uint4*>(pg + PL.v_codes + c0 * (PI * BITS / 8));
           const uint4 vb = *reinterpret_cast<const uint4*>(pg + PL.v_codes + c1 * (PI * BITS / 8));
-          uint32_t dacc[4] = {0u, 0u, 0u, 0u};
+          uint32_t dacc[4] = {kMagicI, kMagicI, kMagicI, kMagicI};
           if (BITS == 2) {
             const uint32_t wa[4] = {va.x, va.y, va.z, va.w}, wb[4] = {vb.x, vb.y, vb.z, vb.w};
 #pragma unroll
@@ -378,8 +380,10 @@ __global__ void __launch_bounds__(kThreads, 3) decode_mma_kernel(const __half* _
 #pragma unroll
           for (int hh = 0; hh < 2; ++hh) {
             const int c = hh ? c1 : c0;
-            const float svv = ws.vc[0][c], mu = ws.vc[1][c], yv = ws.vc[2][c], nr = ws.vc[3][c];
-            const float2 df = make_float2(u2f(dacc[2 * hh]), u2f(dacc[2 * hh + 1]));
+            const float4 v4 = ws.vc[c];
+            const float svv = v4.x, mu = v4.y, yv = v4.z, nr = v4.w;
+            const float2 df = ptx::fadd2(make_float2(__uint_as_float(dacc[2 * hh]), __uint_as_float(dacc[2 * hh + 1])),
+                                         make_float2(-8388608.f, -8388608.f));
             const float2 e = ptx::ffma2(make_float2(4.f, 4.f), df, ptx::fadd2(NRP, make_float2(nr, nr)));
             const float2 t2 = ptx::ffma2(AP, ptx::fmul2(make_float2(svv, svv), e),
                                          ptx::ffma2(XP, make_float2(mu, mu), ptx::fmul2(MP, make_float2(yv, yv))));
