@@ -1,25 +1,27 @@
 // prefill_tc.cu -- homomorphic prefill attention on the 5th-gen tensor cores (a3-a7).
 //
 // One CTA = 128 query rows of one query head, warp-specialised (20 warps):
-//   warp 0     producer: whole packed pages (K' + V' codes, fp16 meta, cached sums;
-//              DESIGN.md "HBM layout") -> smem ring via cp.async.bulk (TMA) + mbarrier
-//   warp 1     MMA issuer: tcgen05.mma kind::i8 (u8 x u8 -> s32, accumulators in TMEM)
-//                QK: per d-block beta D_beta[128 x 64] = Q'_beta K'_beta^T
-//                PV: D'[128 x 128] = P'_j V'_j^T per 64-token V block
-//   warps 2-3  unpack: 2/4-bit codes -> u8 K-major UMMA tiles (tc_common.cuh) + per-key /
-//              per-channel Eq. 4 coefficients from the page meta and CACHED sums
-//   warps 4-11 two softmax WGs (thread = query row = TMEM lane; WG w owns keys 32w..+31
-//              of each tile): in-kernel Q quantization (a3, 8-bit SR; WG w does
-//              d-block w); S = centered Eq. 4 (a4) x log2e/sqrt(d); causal online
-//              softmax (a5, row max/min exchanged through smem); P 8-bit RN per (row, V
-//              block) (a6)
-//   warps 12-19 two correction WGs (thread = row; WG c owns channels 64c..+63):
-//              O = alpha O + centered Eq. 4 on D' (a7); FP16 last V block (RQE) as
-//              fp32 FMAs; O / l; store.
-// TMEM (512 columns): S (2 x 64) | D'[2] (2 x 128) | spare.  The softmax WG pulls the
-// whole S tile into registers and frees TMEM immediately, so QK(j+1) overlaps
-// softmax(j); D' is double-buffered so PV(j+1) overlaps correction(j).
-// Pi = 64 (C2); other partitions use prefill_simt.cu.
+//   warp 0      producer: whole packed pages (K' + V' codes, fp16 meta, cached sums;
+//               DESIGN.md "HBM layout") -> 4-stage smem ring via cp.async.bulk (TMA)
+//   warp 1      MMA issuer: tcgen05.mma kind::i8, accumulators in TMEM
+//                 QK: per d-block beta D_beta[128 x 64] = (Q'-128)_beta K'_beta^T
+//                 PV: D'[128 x 128] = (P'-128) V'^T per 64-token V block
+//               (A operands are stored as signed s8 = code - 128, B as u8 codes)
+//   warps 2-3   unpack: 2/4-bit codes -> u8 K-major UMMA tiles (tc_common.cuh) + per-key /
+//               per-channel Eq. 4 coefficients from the page meta and CACHED sums (SE)
+//   warps 4-19  four symmetric compute warpgroups; thread = query row = TMEM lane.
+//               WG w owns keys 16w..16w+15 of every tile and output channels 32w..32w+31:
+//                 (a3) Q quantization, 8-bit SR (WG0: d-block 0, WG1: d-block 1)
+//                 (a4) S = centered Eq. 4 x log2e/sqrt(d)
+//                 (a5) causal online softmax, row max/min combined through smem
+//                 (a6) P' 8-bit RN per (row, V block)
+//                 (a7) O = alpha O + centered Eq. 4 on D' for the PREVIOUS tile (so the PV
+//                      MMA of tile j overlaps S of tile j+1); FP16 last V block (RQE)
+//                      in fp32; O / l.
+// Centering with s8 A codes: sum (q'-128)(k'-c) = D_s - c SQ_s, so 2 x that is the exact
+// integer 2 D_s - (2^b-1) SQ_s with only a per-row offset.
+// TMEM (512 columns): S (D_0 | D_1, 128) | D'[2] (2 x 128).  Pi = 64; other partitions
+// use prefill_simt.cu.
 #include "common.cuh"
 #include "internal.h"
 #include "tc_common.cuh"
@@ -31,28 +33,29 @@ namespace {
 constexpr int PI = 64;
 constexpr int BM = 128;
 constexpr int BN = 64;
-constexpr int NS = 4;           // page stages
-constexpr int NB = 3;           // K/V/P tile buffer sets (softmax may run NB-1 tiles ahead of correction)
-constexpr int kThreads = 640;   // 20 warps: 4 (producer, MMA, 2 unpack) + 2 softmax WGs + 2 correction WGs
+constexpr int NS = 4;          // page stages
+constexpr int NB = 3;          // K/V/P tile buffer sets
+constexpr int NWG = 4;         // compute warpgroups
+constexpr int kThreads = 128 + 128 * NWG;
+constexpr int NC = 128 * NWG;  // compute threads
 
 template <int BITS>
 struct TcSmem {
   static constexpr int PB = BITS == 2 ? 5376 : 9728;  // page bytes (d=128, Pi=64)
   uint8_t stage[NS][PB];
-  alignas(128) uint8_t q[BM * 128];       // Q' K-major, SBO 1024
-  alignas(128) uint8_t k[NB][BN * 128];   // K' K-major, SBO 1024
-  alignas(128) uint8_t v[NB][128 * BN];   // V' K-major (keys = K), SBO 512
-  alignas(128) uint8_t p[NB][BM * BN];    // P' K-major, SBO 512
-  alignas(16) float kcf[NB][2][4][BN];    // [buf][beta][field][key]: sk, mu_k, y_k, -r_k
-  alignas(16) float vcf[NB][4][128];      // [buf][field][channel]: sv, mu_v, y_v, -r_v
-  float4 qconst[2][BM];                   // per (beta, row): aq, xq, mu_q, r_q
-  float4 rowmeta[NB][BM];                 // per row: alpha, ap, mup, s_p
-  int sp_part[NB][2][BM];                 // per (buffer, softmax WG, row): partial P-code sums
-  float2 xch[2][2][BM];                   // per (parity, softmax WG, row): partial (max, min|-inf)
+  alignas(128) uint8_t q[BM * 128];       // Q' - 128 (s8), K-major, SBO 1024
+  alignas(128) uint8_t k[NB][BN * 128];   // K' (u8), K-major, SBO 1024
+  alignas(128) uint8_t v[NB][128 * BN];   // V' (u8), K-major (keys = K), SBO 512
+  alignas(128) uint8_t p[NB][BM * BN];    // P' - 128 (s8), K-major, SBO 512
+  alignas(16) float kcf[NB][2][3][BN];    // [buf][beta][field][key]: s_k, mu_k, y_k
+  alignas(16) float vcf[NB][3][128];      // [buf][field][channel]: s_v, mu_v, y_v
+  float4 qconst[2][BM];                   // per (beta, row): aq, xq, mu_q, -r_q
+  int sp_part[NB][NWG][BM];               // partial P-code sums
+  float2 xch[2][NWG][BM];                 // partial (max, min | -inf if masked)
   float ptail[BM][BN + 1];                // p~ of the FP16 tail tile
-  float lpart[2][BM];
+  float lpart[NWG][BM];
   uint64_t full[NS], empty[NS], k_ready[NB], k_free[NB], v_ready[NB], v_free[NB], p_ready[NB], p_free[NB],
-      meta_free[NB], d_full[2], d_free[2], s_full, s_free, q_ready;
+      d_full[2], d_free[2], s_full, s_free, q_ready;
   uint32_t tmem_base;
 };
 
@@ -64,6 +67,7 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_tc_kernel(
     CacheView cv, KernelCfg kc, void* __restrict__ out, uint8_t* __restrict__ dbg_pcodes, int64_t dbg_stride) {
   using SM = TcSmem<BITS>;
   constexpr int qkm = (1 << BITS) - 1;
+  constexpr float ck = 0.5f * qkm;  // K/V code centre
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   SM& sm = *reinterpret_cast<SM*>(smem_raw);
 
@@ -87,19 +91,18 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_tc_kernel(
     }
     for (int x = 0; x < NB; ++x) {
       ptx::mbar_init(&sm.k_ready[x], 64);
-      ptx::mbar_init(&sm.k_free[x], 256);
+      ptx::mbar_init(&sm.k_free[x], NC);
       ptx::mbar_init(&sm.v_ready[x], 64);
-      ptx::mbar_init(&sm.v_free[x], 256);
-      ptx::mbar_init(&sm.p_ready[x], 256);
+      ptx::mbar_init(&sm.v_free[x], NC);
+      ptx::mbar_init(&sm.p_ready[x], NC);
       ptx::mbar_init(&sm.p_free[x], 1);
-      ptx::mbar_init(&sm.meta_free[x], 256);
     }
     for (int x = 0; x < 2; ++x) {
       ptx::mbar_init(&sm.d_full[x], 1);
-      ptx::mbar_init(&sm.d_free[x], 256);
+      ptx::mbar_init(&sm.d_free[x], NC);
     }
     ptx::mbar_init(&sm.s_full, 1);
-    ptx::mbar_init(&sm.s_free, 256);
+    ptx::mbar_init(&sm.s_free, NC);
     ptx::mbar_init(&sm.q_ready, 256);
     ptx::fence_mbar_init();
   }
@@ -108,8 +111,8 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_tc_kernel(
   __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem = sm.tmem_base;
-  const uint32_t tS = tmem;            // columns 0..127: D_0 | D_1
-  const uint32_t tD0 = tmem + 128;     // D'[0] columns 128..255, D'[1] 256..383
+  const uint32_t tS = tmem;         // columns 0..127: D_0 | D_1
+  const uint32_t tD0 = tmem + 128;  // D'[0] columns 128..255, D'[1] 256..383
 
   if (warp < 4) {
     asm volatile("setmaxnreg.dec.sync.aligned.u32 40;");
@@ -127,7 +130,7 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_tc_kernel(
       }
     } else if (warp == 1) {
       // ---------------------------------------------------------------- MMA issuer
-      const uint32_t idesc_qk = ptx::idesc_u8(BM, BN), idesc_pv = ptx::idesc_u8(BM, 128);
+      const uint32_t idesc_qk = ptx::idesc_s8u8(BM, BN), idesc_pv = ptx::idesc_s8u8(BM, 128);
       const uint32_t qa = ptx::smem_u32(sm.q);
       ptx::mbar_wait(&sm.q_ready, 0);
       for (int j = 0; j <= nkt; ++j) {
@@ -152,19 +155,19 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_tc_kernel(
         }
         const int jj = j - 1;  // PV of the previous tile, after QK of this one (overlap)
         if (jj >= 0 && jj < nfull) {
-          const int bb = jj & 1, bq = jj % NB;
+          const int bd = jj & 1, bq = jj % NB;
           const uint32_t ph = (jj / NB) & 1;
           ptx::mbar_wait(&sm.p_ready[bq], ph);
           ptx::mbar_wait(&sm.v_ready[bq], ph);
-          ptx::mbar_wait(&sm.d_free[bb], ((jj >> 1) & 1) ^ 1);
+          ptx::mbar_wait(&sm.d_free[bd], ((jj >> 1) & 1) ^ 1);
           ptx::tc_fence_after();
           if (lane == 0) {
             const uint32_t pa = ptx::smem_u32(sm.p[bq]), va = ptx::smem_u32(sm.v[bq]);
 #pragma unroll
             for (int ks = 0; ks < BN / 32; ++ks)
-              ptx::mma_u8(tD0 + 128 * bb, ptx::smem_desc_kmajor(pa + ks * 256, 128, 512),
+              ptx::mma_u8(tD0 + 128 * bd, ptx::smem_desc_kmajor(pa + ks * 256, 128, 512),
                           ptx::smem_desc_kmajor(va + ks * 256, 128, 512), idesc_pv, ks > 0);
-            ptx::mma_commit(&sm.d_full[bb]);
+            ptx::mma_commit(&sm.d_full[bd]);
             ptx::mma_commit(&sm.p_free[bq]);
           }
           __syncwarp();
@@ -201,21 +204,19 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_tc_kernel(
 #pragma unroll
         for (int beta = 0; beta < 2; ++beta) {  // per-(key, beta) Eq. 4 coefficients
           const int key = ut, e = 2 * key + beta;
-          float c0 = 0.f, c1 = 0.f, c2 = 0.f, c3 = 0.f;
+          float c0 = 0.f, c1 = 0.f, c2 = 0.f;
           if (key < nk) {
             const __half2 mh = reinterpret_cast<const __half2*>(pg + PL.k_meta)[e];
             const float m = __low2float(mh), s2 = __high2float(mh);
             const int sum = load_sum(pg + PL.k_sums, e, PL.sum_bytes);  // cached sum (SE)
-            const float mu = m + 0.5f * qkm * s2;
+            const float mu = m + ck * s2;
             c0 = s2;
             c1 = mu;
-            c2 = s2 * ((float)sum - 0.5f * qkm * PI) + PI * mu;
-            c3 = -(float)(510 * sum);
+            c2 = s2 * ((float)sum - ck * PI) + PI * mu;
           }
           sm.kcf[bj][beta][0][key] = c0;
           sm.kcf[bj][beta][1][key] = c1;
           sm.kcf[bj][beta][2][key] = c2;
-          sm.kcf[bj][beta][3][key] = c3;
         }
         ptx::fence_proxy_async_smem();
         ptx::mbar_arrive(&sm.k_ready[bj]);
@@ -241,11 +242,10 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_tc_kernel(
             const __half2 mh = reinterpret_cast<const __half2*>(pg + PL.v_meta)[ch];
             const float m = __low2float(mh), s2 = __high2float(mh);
             const int sum = load_sum(pg + PL.v_sums, ch, PL.sum_bytes);  // cached sum (SE)
-            const float mu = m + 0.5f * qkm * s2;
+            const float mu = m + ck * s2;
             sm.vcf[bj][0][ch] = s2;
             sm.vcf[bj][1][ch] = mu;
-            sm.vcf[bj][2][ch] = s2 * ((float)sum - 0.5f * qkm * PI) + PI * mu;
-            sm.vcf[bj][3][ch] = -(float)(510 * sum);
+            sm.vcf[bj][2][ch] = s2 * ((float)sum - ck * PI) + PI * mu;
           }
         }
         ptx::fence_proxy_async_smem();
@@ -253,15 +253,15 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_tc_kernel(
         ptx::mbar_arrive(&sm.empty[s]);
       }
     }
-  } else if (warp < 12) {
-    // ------------------------------------------------------------------ softmax WGs
-    // WG w (0/1) owns keys 32w..32w+31 of every tile and d-block beta = w of Q.
-    // (register budget: 96 at launch; WG0 releases 56/thread, the correction WGs take 24)
+  } else {
+    // ------------------------------------------------------------------ compute WGs
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 104;");
     const int w = (warp - 4) >> 2;
     const int r = (tid - 128) & (BM - 1);
     const int i = min(i0 + r, L - 1);  // this thread's query position (padding rows clamp)
+    const uint32_t lane_base = (uint32_t)(32 * (warp & 3)) << 16;
     const float cscale = 1.4426950408889634f / sqrtf(128.f);
-    {
+    if (w < 2) {
       // (a3) quantize Q[i, 64w .. 64w+63]: 8-bit, fp32 meta, SR (op sequence of quant_row16)
       const uint4* qrow = reinterpret_cast<const uint4*>(q + ((int64_t)(start + i) * kc.Hq + hq) * 128 + 64 * w);
       float lo = INFINITY, hi = -INFINITY;
@@ -311,51 +311,123 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_tc_kernel(
           uint32_t wd = 0;
 #pragma unroll
           for (int e = 0; e < 4; ++e) wd |= (uint32_t)cc[perm_src<BITS>(4 * x4 + e)] << (8 * e);
-          wv[x4] = wd;
+          wv[x4] = wd ^ 0x80808080u;  // s8 operand: code - 128
         }
 #pragma unroll
         for (int e = 0; e < 16; ++e) sum += cc[e];
         *reinterpret_cast<uint4*>(sm.q + kmaj_off(r, 64 * w + 16 * g, 1024)) = make_uint4(wv[0], wv[1], wv[2], wv[3]);
       }
-      sm.qconst[w][r] = make_float4(cscale * qm.s * 0.25f, cscale * qm.s * ((float)sum - 127.5f * PI),
-                                    cscale * (qm.m + 127.5f * qm.s), (float)(2 * qkm * sum - PI * 255 * qkm));
+      const int sqs = sum - 128 * PI;  // sum (q' - 128)
+      sm.qconst[w][r] = make_float4(cscale * qm.s * 0.5f, cscale * qm.s * (float)sqs,
+                                    cscale * (qm.m + 128.f * qm.s), -(float)(qkm * sqs));
       ptx::fence_proxy_async_smem();
       ptx::mbar_arrive(&sm.q_ready);
-      ptx::named_bar_sync(2, 256);  // both halves of the Q row constants visible
     }
+    ptx::named_bar_sync(2, NC);  // both halves of the Q row constants visible
     const float4 qc0 = sm.qconst[0][r], qc1 = sm.qconst[1][r];
     const float2 qa0 = make_float2(qc0.x, qc0.x), qx0 = make_float2(qc0.y, qc0.y), qm0 = make_float2(qc0.z, qc0.z),
-                 qn0 = make_float2(-qc0.w, -qc0.w);
+                 qn0 = make_float2(qc0.w, qc0.w);
     const float2 qa1 = make_float2(qc1.x, qc1.x), qx1 = make_float2(qc1.y, qc1.y), qm1 = make_float2(qc1.z, qc1.z),
-                 qn1 = make_float2(-qc1.w, -qc1.w);
+                 qn1 = make_float2(qc1.w, qc1.w);
+    const float2 two = make_float2(2.f, 2.f);
+    const int kb = 16 * w;   // this WG's keys in a tile
+    const int cb = 32 * w;   // this WG's output channels
     float m_run = -INFINITY, l_run = 0.f;
-    const uint32_t lane_base = (uint32_t)(32 * (warp & 3)) << 16;
-    const int kb = 32 * w;
+    float2 o2[16];           // channels cb + 2x, cb + 2x + 1
+#pragma unroll
+    for (int x = 0; x < 16; ++x) o2[x] = make_float2(0.f, 0.f);
+    // state of the tile whose O update is pending (lags one tile)
+    float pend_al = 0.f, pend_s = 0.f, pend_m = 0.f;
+
+    // O = alpha O + Eq. 4 (centered) on D' of tile jj (a7)
+    auto o_update = [&](int jj) {
+      const int bq = jj % NB, bd = jj & 1;
+      const uint32_t ph = (jj / NB) & 1;
+      if (jj < nfull) {
+        int sp = 0;
+#pragma unroll
+        for (int x = 0; x < NWG; ++x) sp += sm.sp_part[bq][x][r];
+        const int sps = sp - 128 * PI;  // sum (p' - 128)
+        const float2 al2 = make_float2(pend_al, pend_al);
+        const float2 ap2 = make_float2(0.5f * pend_s, 0.5f * pend_s);
+        const float2 xp2 = make_float2(pend_s * (float)sps, pend_s * (float)sps);
+        const float2 mp2 = make_float2(pend_m + 128.f * pend_s, pend_m + 128.f * pend_s);
+        const float2 np2 = make_float2(-(float)(qkm * sps), -(float)(qkm * sps));
+        ptx::mbar_wait(&sm.d_full[bd], (jj >> 1) & 1);
+        ptx::mbar_wait(&sm.v_ready[bq], ph);
+        ptx::tc_fence_after();
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          uint32_t d[16];
+          ptx::tmem_ld16(tD0 + 128 * bd + lane_base + cb + 16 * h, d);
+          ptx::tmem_wait_ld();
+#pragma unroll
+          for (int x4 = 0; x4 < 4; ++x4) {
+            const int c0 = cb + 16 * h + 4 * x4;
+            const float4 sv4 = *reinterpret_cast<const float4*>(&sm.vcf[bq][0][c0]);
+            const float4 mu4 = *reinterpret_cast<const float4*>(&sm.vcf[bq][1][c0]);
+            const float4 y4 = *reinterpret_cast<const float4*>(&sm.vcf[bq][2][c0]);
+#pragma unroll
+            for (int pr = 0; pr < 2; ++pr) {
+              const int xo = 4 * x4 + 2 * pr;
+              const float2 df = make_float2(u2f(d[xo]), u2f(d[xo + 1]));
+              const float2 svp = pr ? make_float2(sv4.z, sv4.w) : make_float2(sv4.x, sv4.y);
+              const float2 mup = pr ? make_float2(mu4.z, mu4.w) : make_float2(mu4.x, mu4.y);
+              const float2 yp = pr ? make_float2(y4.z, y4.w) : make_float2(y4.x, y4.y);
+              const float2 e = ptx::ffma2(two, df, np2);  // 2 x centered int dot (exact)
+              const float2 t = ptx::ffma2(ap2, ptx::fmul2(svp, e), ptx::ffma2(xp2, mup, ptx::fmul2(mp2, yp)));
+              o2[8 * h + 2 * x4 + pr] = ptx::ffma2(al2, o2[8 * h + 2 * x4 + pr], t);
+            }
+          }
+        }
+        ptx::tc_fence_before();
+        ptx::mbar_arrive(&sm.d_free[bd]);
+      } else {
+        // FP16 last V block (RQE, P:722): O = alpha O + sum_t p~_t v_t in fp32
+        const int T = L - nfull * PI;
+        const __half* tail =
+            reinterpret_cast<const __half*>(cv.v_tail) + ((int64_t)slot * kc.Hkv + hk) * PI * 128 + cb;
+#pragma unroll
+        for (int x = 0; x < 16; ++x) o2[x] = ptx::fmul2(o2[x], make_float2(pend_al, pend_al));
+#pragma unroll 1
+        for (int t = 0; t < T; ++t) {
+          const float pt = sm.ptail[r][t];
+          const uint4* vr = reinterpret_cast<const uint4*>(tail + t * 128);
+#pragma unroll
+          for (int c8 = 0; c8 < 4; ++c8) {
+            const uint4 raw = vr[c8];
+            const __half2* h2 = reinterpret_cast<const __half2*>(&raw);
+#pragma unroll
+            for (int e = 0; e < 4; ++e)
+              o2[c8 * 4 + e] = ptx::ffma2(make_float2(pt, pt), __half22float2(h2[e]), o2[c8 * 4 + e]);
+          }
+        }
+      }
+      ptx::mbar_arrive(&sm.v_free[bq]);
+    };
+
 #pragma unroll 1
     for (int j = 0; j < nkt; ++j) {
       const int bj = j % NB, t0 = j * BN;
       const uint32_t ph = (j / NB) & 1;
+      const bool full = (t0 + BN - 1) <= i0;  // every key visible to every row of the CTA
       ptx::mbar_wait(&sm.s_full, j & 1);
       ptx::tc_fence_after();
-      // a tile is "full" when every key is visible to every row of this CTA (no causal mask)
-      const bool full = (t0 + BN - 1) <= i0;
-      float s[32];
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
+      float s[16];
+      {
         uint32_t d0[16], d1[16];
-        ptx::tmem_ld16(tS + lane_base + kb + 16 * h, d0);
-        ptx::tmem_ld16(tS + lane_base + 64 + kb + 16 * h, d1);
+        ptx::tmem_ld16(tS + lane_base + kb, d0);
+        ptx::tmem_ld16(tS + lane_base + 64 + kb, d1);
         ptx::tmem_wait_ld();
 #pragma unroll
         for (int g4 = 0; g4 < 4; ++g4) {
-          const int kl = kb + 16 * h + 4 * g4;  // first of 4 keys
+          const int kl = kb + 4 * g4;  // first of 4 keys
           float2 acc[2];
 #pragma unroll
           for (int beta = 0; beta < 2; ++beta) {
             const float4 sk4 = *reinterpret_cast<const float4*>(&sm.kcf[bj][beta][0][kl]);
             const float4 mu4 = *reinterpret_cast<const float4*>(&sm.kcf[bj][beta][1][kl]);
             const float4 y4 = *reinterpret_cast<const float4*>(&sm.kcf[bj][beta][2][kl]);
-            const float4 nr4 = *reinterpret_cast<const float4*>(&sm.kcf[bj][beta][3][kl]);
             const uint32_t* d = beta ? d1 : d0;
             const float2 A = beta ? qa1 : qa0, X = beta ? qx1 : qx0, M = beta ? qm1 : qm0, NR = beta ? qn1 : qn0;
 #pragma unroll
@@ -364,18 +436,15 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_tc_kernel(
               const float2 skp = pr ? make_float2(sk4.z, sk4.w) : make_float2(sk4.x, sk4.y);
               const float2 mup = pr ? make_float2(mu4.z, mu4.w) : make_float2(mu4.x, mu4.y);
               const float2 yp = pr ? make_float2(y4.z, y4.w) : make_float2(y4.x, y4.y);
-              const float2 nrp = pr ? make_float2(nr4.z, nr4.w) : make_float2(nr4.x, nr4.y);
-              // e = 4 D - r_q - r_k: the centered integer dot x 4, exact in fp32
-              const float2 e = ptx::ffma2(make_float2(4.f, 4.f), df, ptx::fadd2(nrp, NR));
-              const float2 g = ptx::fmul2(skp, e);
+              const float2 e = ptx::ffma2(two, df, NR);  // 2 x centered int dot (exact)
               const float2 base = beta ? ptx::ffma2(M, yp, acc[pr]) : ptx::fmul2(M, yp);
-              acc[pr] = ptx::ffma2(A, g, ptx::ffma2(X, mup, base));
+              acc[pr] = ptx::ffma2(A, ptx::fmul2(skp, e), ptx::ffma2(X, mup, base));
             }
           }
-          s[16 * h + 4 * g4 + 0] = acc[0].x;
-          s[16 * h + 4 * g4 + 1] = acc[0].y;
-          s[16 * h + 4 * g4 + 2] = acc[1].x;
-          s[16 * h + 4 * g4 + 3] = acc[1].y;
+          s[4 * g4 + 0] = acc[0].x;
+          s[4 * g4 + 1] = acc[0].y;
+          s[4 * g4 + 2] = acc[1].x;
+          s[4 * g4 + 3] = acc[1].y;
         }
       }
       ptx::tc_fence_before();
@@ -384,7 +453,7 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_tc_kernel(
       bool masked = false;
       if (!full) {
 #pragma unroll
-        for (int kk = 0; kk < 32; ++kk) {
+        for (int kk = 0; kk < 16; ++kk) {
           const bool vis = (t0 + kb + kk) <= i;  // causal mask (R8)
           masked |= !vis;
           s[kk] = vis ? s[kk] : -INFINITY;
@@ -392,27 +461,33 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_tc_kernel(
       }
       float mx = s[0], mn = s[0];
 #pragma unroll
-      for (int kk = 1; kk < 32; ++kk) {
+      for (int kk = 1; kk < 16; ++kk) {
         mx = fmaxf(mx, s[kk]);
         mn = fminf(mn, s[kk]);
       }
       if (masked) {  // min over the visible keys only
         mn = INFINITY;
 #pragma unroll
-        for (int kk = 0; kk < 32; ++kk) mn = fminf(mn, s[kk] == -INFINITY ? INFINITY : s[kk]);
+        for (int kk = 0; kk < 16; ++kk) mn = fminf(mn, s[kk] == -INFINITY ? INFINITY : s[kk]);
       }
       sm.xch[j & 1][w][r] = make_float2(mx, masked ? -INFINITY : mn);
-      ptx::named_bar_sync(2, 256);
-      const float2 other = sm.xch[j & 1][w ^ 1][r];
-      mx = fmaxf(mx, other.x);
-      const bool any_masked = masked || (other.y == -INFINITY);
-      mn = fminf(mn, other.y == -INFINITY ? INFINITY : other.y);
+      ptx::named_bar_sync(2, NC);
+      bool any_masked = false;
+      mn = INFINITY;
+      mx = -INFINITY;
+#pragma unroll
+      for (int x = 0; x < NWG; ++x) {
+        const float2 o = sm.xch[j & 1][x][r];
+        mx = fmaxf(mx, o.x);
+        any_masked |= (o.y == -INFINITY);
+        mn = fminf(mn, o.y == -INFINITY ? INFINITY : o.y);
+      }
       const float m_new = fmaxf(m_run, mx);
       const float al = (m_run == -INFINITY) ? 0.f : ex2(m_run - m_new);
       float2 ls2 = make_float2(0.f, 0.f);
       const float2 mneg = make_float2(-m_new, -m_new);
 #pragma unroll
-      for (int kk = 0; kk < 32; kk += 2) {
+      for (int kk = 0; kk < 16; kk += 2) {
         const float2 a2 = ptx::fadd2(make_float2(s[kk], s[kk + 1]), mneg);
         s[kk] = ex2(a2.x);  // ex2(-inf) = +0 for masked keys
         s[kk + 1] = ex2(a2.y);
@@ -420,6 +495,7 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_tc_kernel(
       }
       l_run = l_run * al + (ls2.x + ls2.y);
       m_run = m_new;
+      float pm_s = 0.f, pm_m = 0.f;
       if (j < nfull) {
         // (a6) P' per (row, V block): 8-bit RN on p~ (codes invariant to the row scale);
         // y = (p - lo) / s rounded with the 1.5*2^23 magic number (y in [0, 255])
@@ -430,148 +506,68 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_tc_kernel(
           pm.s = 0.f;
           pm.inv = 0.f;
         }
+        pm_s = pm.s;
+        pm_m = pm.m;
         const float2 inv2 = make_float2(pm.inv, pm.inv), nlo2 = make_float2(-plo * pm.inv, -plo * pm.inv);
         const float2 magic = make_float2(12582912.f, 12582912.f);
-        uint32_t bits[32];
+        uint32_t bits[16];
 #pragma unroll
-        for (int kk = 0; kk < 32; kk += 2) {
+        for (int kk = 0; kk < 16; kk += 2) {
           const float2 y = ptx::fadd2(ptx::ffma2(make_float2(s[kk], s[kk + 1]), inv2, nlo2), magic);
           bits[kk] = __float_as_uint(y.x);
           bits[kk + 1] = __float_as_uint(y.y);
         }
-        ptx::mbar_wait(&sm.p_free[bj], ph ^ 1);
-        ptx::mbar_wait(&sm.meta_free[bj], ph ^ 1);
-        uint32_t cw[8];
+        uint32_t cw[4];
         uint32_t sum = 0;
 #pragma unroll
-        for (int x4 = 0; x4 < 8; ++x4) {
-          // byte position pos holds local key 16 (pos >> 4) + perm_src(pos & 15)
-          const int p0 = 4 * x4;
-          const int k0 = 16 * (p0 >> 4) + perm_src<BITS>((p0 + 0) & 15);
-          const int k1 = 16 * (p0 >> 4) + perm_src<BITS>((p0 + 1) & 15);
-          const int k2 = 16 * (p0 >> 4) + perm_src<BITS>((p0 + 2) & 15);
-          const int k3 = 16 * (p0 >> 4) + perm_src<BITS>((p0 + 3) & 15);
-          const uint32_t lo2 = ptx::prmt(bits[k0], bits[k1], 0x0040u);
-          const uint32_t hi2 = ptx::prmt(bits[k2], bits[k3], 0x0040u);
+        for (int x4 = 0; x4 < 4; ++x4) {
+          // byte position p of this 16-key chunk holds local key perm_src(p)
+          const uint32_t lo2 = ptx::prmt(bits[perm_src<BITS>(4 * x4 + 0)], bits[perm_src<BITS>(4 * x4 + 1)], 0x0040u);
+          const uint32_t hi2 = ptx::prmt(bits[perm_src<BITS>(4 * x4 + 2)], bits[perm_src<BITS>(4 * x4 + 3)], 0x0040u);
           cw[x4] = ptx::prmt(lo2, hi2, 0x5410u);
           sum = __dp4a(cw[x4], 0x01010101u, sum);
         }
-#pragma unroll
-        for (int g = 0; g < 2; ++g)
-          *reinterpret_cast<uint4*>(sm.p[bj] + kmaj_off(r, kb + 16 * g, 512)) =
-              make_uint4(cw[4 * g], cw[4 * g + 1], cw[4 * g + 2], cw[4 * g + 3]);
+        ptx::mbar_wait(&sm.p_free[bj], ph ^ 1);
+        *reinterpret_cast<uint4*>(sm.p[bj] + kmaj_off(r, kb, 512)) =
+            make_uint4(cw[0] ^ 0x80808080u, cw[1] ^ 0x80808080u, cw[2] ^ 0x80808080u, cw[3] ^ 0x80808080u);
         if (dbg_pcodes != nullptr && i0 + r < L) {
           uint8_t* dp = dbg_pcodes + ((int64_t)(start + i0 + r) * kc.Hq + hq) * dbg_stride + t0 + kb;
 #pragma unroll
-          for (int pos = 0; pos < 32; ++pos)
-            dp[16 * (pos >> 4) + perm_src<BITS>(pos & 15)] = (uint8_t)((cw[pos >> 2] >> (8 * (pos & 3))) & 0xFF);
+          for (int pos = 0; pos < 16; ++pos)
+            dp[perm_src<BITS>(pos)] = (uint8_t)((cw[pos >> 2] >> (8 * (pos & 3))) & 0xFF);
         }
         sm.sp_part[bj][w][r] = (int)sum;
-        if (w == 0) sm.rowmeta[bj][r] = make_float4(al, pm.s * 0.25f, pm.m + 127.5f * pm.s, pm.s);
         ptx::fence_proxy_async_smem();
       } else {
-        ptx::mbar_wait(&sm.meta_free[bj], ph ^ 1);
 #pragma unroll
-        for (int kk = 0; kk < 32; ++kk) sm.ptail[r][kb + kk] = s[kk];
-        if (w == 0) sm.rowmeta[bj][r] = make_float4(al, 0.f, 0.f, 0.f);
+        for (int kk = 0; kk < 16; ++kk) sm.ptail[r][kb + kk] = s[kk];
       }
       ptx::mbar_arrive(&sm.p_ready[bj]);
+      if (j >= 1) o_update(j - 1);  // overlaps the PV MMA of tile j with S of tile j+1
+      pend_al = al;
+      pend_s = pm_s;
+      pend_m = pm_m;
     }
+    ptx::named_bar_sync(2, NC);  // sp_part / ptail of the last tile complete
+    o_update(nkt - 1);
     sm.lpart[w][r] = l_run;
-    ptx::named_bar_sync(1, 512);
-  } else {
-    // ------------------------------------------------------------------ correction WGs
-    // WG c (0/1) owns output channels 64c .. 64c+63 of every row.
-    asm volatile("setmaxnreg.inc.sync.aligned.u32 120;");
-    const int c = (warp - 12) >> 2;
-    const int r = (tid - 384) & (BM - 1);
-    const int cb = 64 * c;
-    const uint32_t lane_base = (uint32_t)(32 * (warp & 3)) << 16;
-    float2 o2[32];  // channels cb + 2x, cb + 2x + 1
-#pragma unroll
-    for (int x = 0; x < 32; ++x) o2[x] = make_float2(0.f, 0.f);
-    const int T = L - nfull * PI;
-#pragma unroll 1
-    for (int j = 0; j < nkt; ++j) {
-      const int bj = j % NB, bd = j & 1;
-      const uint32_t ph = (j / NB) & 1;
-      ptx::mbar_wait(&sm.p_ready[bj], ph);
-      const float4 rm = sm.rowmeta[bj][r];
-      const int sp = sm.sp_part[bj][0][r] + sm.sp_part[bj][1][r];
-      ptx::mbar_arrive(&sm.meta_free[bj]);  // row meta consumed
-      if (j < nfull) {
-        const float xp = rm.w * ((float)sp - 127.5f * PI);
-        const float rp = (float)(2 * qkm * sp - PI * 255 * qkm);
-        ptx::mbar_wait(&sm.d_full[bd], (j >> 1) & 1);
-        ptx::mbar_wait(&sm.v_ready[bj], ph);
-        ptx::tc_fence_after();
-        const float2 al2 = make_float2(rm.x, rm.x), ap2 = make_float2(rm.y, rm.y), mp2 = make_float2(rm.z, rm.z);
-        const float2 xp2 = make_float2(xp, xp), nrp2 = make_float2(-rp, -rp), four = make_float2(4.f, 4.f);
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          uint32_t d[32];
-          ptx::tmem_ld32(tD0 + 128 * bd + lane_base + cb + 32 * h, d);
-          ptx::tmem_wait_ld();
-#pragma unroll
-          for (int x4 = 0; x4 < 8; ++x4) {
-            const int c0 = cb + 32 * h + 4 * x4;
-            const float4 sv4 = *reinterpret_cast<const float4*>(&sm.vcf[bj][0][c0]);
-            const float4 mu4 = *reinterpret_cast<const float4*>(&sm.vcf[bj][1][c0]);
-            const float4 y4 = *reinterpret_cast<const float4*>(&sm.vcf[bj][2][c0]);
-            const float4 nr4 = *reinterpret_cast<const float4*>(&sm.vcf[bj][3][c0]);
-#pragma unroll
-            for (int pr = 0; pr < 2; ++pr) {
-              const int xo = 4 * x4 + 2 * pr;
-              const float2 df = make_float2(u2f(d[xo]), u2f(d[xo + 1]));
-              const float2 svp = pr ? make_float2(sv4.z, sv4.w) : make_float2(sv4.x, sv4.y);
-              const float2 mup = pr ? make_float2(mu4.z, mu4.w) : make_float2(mu4.x, mu4.y);
-              const float2 yp = pr ? make_float2(y4.z, y4.w) : make_float2(y4.x, y4.y);
-              const float2 nrp = pr ? make_float2(nr4.z, nr4.w) : make_float2(nr4.x, nr4.y);
-              const float2 e = ptx::ffma2(four, df, ptx::fadd2(nrp, nrp2));  // 4 x centered int dot (exact)
-              const float2 t = ptx::ffma2(ap2, ptx::fmul2(svp, e), ptx::ffma2(xp2, mup, ptx::fmul2(mp2, yp)));
-              o2[16 * h + 2 * x4 + pr] = ptx::ffma2(al2, o2[16 * h + 2 * x4 + pr], t);
-            }
-          }
-        }
-        ptx::tc_fence_before();
-        ptx::mbar_arrive(&sm.d_free[bd]);
-      } else {
-        // FP16 last V block (RQE, P:722): O = alpha O + sum_t p~_t v_t in fp32
-        const __half* tail =
-            reinterpret_cast<const __half*>(cv.v_tail) + ((int64_t)slot * kc.Hkv + hk) * PI * 128 + cb;
-#pragma unroll
-        for (int x = 0; x < 32; ++x) o2[x] = ptx::fmul2(o2[x], make_float2(rm.x, rm.x));
-#pragma unroll 1
-        for (int t = 0; t < T; ++t) {
-          const float pt = sm.ptail[r][t];
-          const uint4* vr = reinterpret_cast<const uint4*>(tail + t * 128);
-#pragma unroll
-          for (int c8 = 0; c8 < 8; ++c8) {
-            const uint4 raw = vr[c8];
-            const __half2* h2 = reinterpret_cast<const __half2*>(&raw);
-#pragma unroll
-            for (int e = 0; e < 4; ++e) {
-              o2[c8 * 4 + e] = ptx::ffma2(make_float2(pt, pt), __half22float2(h2[e]), o2[c8 * 4 + e]);
-            }
-          }
-        }
-      }
-      ptx::mbar_arrive(&sm.v_free[bj]);
-    }
-    ptx::named_bar_sync(1, 512);
+    ptx::named_bar_sync(2, NC);
     if (i0 + r < L) {
-      const float inv_l = 1.f / (sm.lpart[0][r] + sm.lpart[1][r]);
+      float l = 0.f;
+#pragma unroll
+      for (int x = 0; x < NWG; ++x) l += sm.lpart[x][r];
+      const float inv_l = 1.f / l;
       const int64_t base = ((int64_t)(start + i0 + r) * kc.Hq + hq) * 128 + cb;
       if (kc.out_fp32) {
         float4* op = reinterpret_cast<float4*>(reinterpret_cast<float*>(out) + base);
 #pragma unroll
-        for (int c4 = 0; c4 < 16; ++c4)
+        for (int c4 = 0; c4 < 8; ++c4)
           op[c4] = make_float4(o2[2 * c4].x * inv_l, o2[2 * c4].y * inv_l, o2[2 * c4 + 1].x * inv_l,
                                o2[2 * c4 + 1].y * inv_l);
       } else {
         uint4* op = reinterpret_cast<uint4*>(reinterpret_cast<__half*>(out) + base);
 #pragma unroll
-        for (int c8 = 0; c8 < 8; ++c8) {
+        for (int c8 = 0; c8 < 4; ++c8) {
           __half2 hh[4];
 #pragma unroll
           for (int e = 0; e < 4; ++e) hh[e] = __floats2half2_rn(o2[4 * c8 + e].x * inv_l, o2[4 * c8 + e].y * inv_l);

@@ -121,6 +121,9 @@ HACK_DEV constexpr uint32_t idesc_u8(int M, int N) {
          | ((uint32_t)(M >> 4) << 24);  // M >> 4
 }
 
+// kind::i8 with a signed (s8) A operand and unsigned (u8) B operand.
+HACK_DEV constexpr uint32_t idesc_s8u8(int M, int N) { return idesc_u8(M, N) | (1u << 7); }
+
 // D[tmem] (+)= A[smem] . B[smem]^T, issued by ONE thread.
 HACK_DEV void mma_u8(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc, uint32_t accumulate) {
   asm volatile(
