@@ -504,6 +504,13 @@ cudaError_t launch_t(const KernelCfg& kc, const void* q_new, const int32_t* slot
 
 }  // namespace
 
+cudaError_t launch_decode_combine(const float* part, int nsplit, const KernelCfg& kc, int batch, void* out,
+                                  cudaStream_t st) {
+  decode_combine_kernel<<<dim3(batch, kc.Hq), 128, 0, st>>>(part, nsplit, kc, out);
+  note_launch();
+  return cudaGetLastError();
+}
+
 bool decode_mma_supported(const KernelCfg& kc) { return kc.Pi == 64 && kc.G <= 8; }
 
 int decode_nsplit(const KernelCfg& kc, int batch, int max_seqlen) {

@@ -46,8 +46,13 @@ HACK_DEV bool mbar_try_wait_sleep(uint64_t* bar, uint32_t parity) {
   return ok != 0;
 }
 HACK_DEV void mbar_wait(uint64_t* bar, uint32_t parity) {
+#ifdef HACK_WAIT_SLEEP
   while (!mbar_try_wait_sleep(bar, parity)) {
   }
+#else
+  while (!mbar_try_wait(bar, parity)) {
+  }
+#endif
 }
 
 // ---------------------------------------------------------------- bulk copy (TMA, 1D)
@@ -97,7 +102,40 @@ HACK_DEV void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
         "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
       : "r"(taddr));
 }
+HACK_DEV void tmem_ld8(uint32_t taddr, uint32_t (&r)[8]) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+               : "r"(taddr));
+}
 HACK_DEV void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+
+// registers -> TMEM (this thread's lane, consecutive columns)
+HACK_DEV void tmem_st16(uint32_t taddr, const uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(
+          taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]),
+      "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])
+      : "memory");
+}
+HACK_DEV void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+
+// warp-wide reductions (sm_100a CREDUX / REDUX)
+HACK_DEV float redux_max(float v) {
+  float r;
+  asm volatile("redux.sync.max.f32 %0, %1, 0xffffffff;" : "=f"(r) : "f"(v));
+  return r;
+}
+HACK_DEV float redux_min(float v) {
+  float r;
+  asm volatile("redux.sync.min.f32 %0, %1, 0xffffffff;" : "=f"(r) : "f"(v));
+  return r;
+}
+HACK_DEV uint32_t redux_add(uint32_t v) {
+  uint32_t r;
+  asm volatile("redux.sync.add.u32 %0, %1, 0xffffffff;" : "=r"(r) : "r"(v));
+  return r;
+}
 
 // ---------------------------------------------------------------- UMMA descriptors
 // K-major, no-swizzle ("interleaved") canonical layout: core matrices of 8 rows x 16 B
@@ -123,6 +161,8 @@ HACK_DEV constexpr uint32_t idesc_u8(int M, int N) {
 
 // kind::i8 with a signed (s8) A operand and unsigned (u8) B operand.
 HACK_DEV constexpr uint32_t idesc_s8u8(int M, int N) { return idesc_u8(M, N) | (1u << 7); }
+// u8 A (unsigned codes) x s8 B (code - 128).
+HACK_DEV constexpr uint32_t idesc_u8s8(int M, int N) { return idesc_u8(M, N) | (1u << 10); }
 
 // D[tmem] (+)= A[smem] . B[smem]^T, issued by ONE thread.
 HACK_DEV void mma_u8(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc, uint32_t accumulate) {
@@ -130,6 +170,15 @@ HACK_DEV void mma_u8(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t
       "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
       "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
       "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+
+// D[tmem] (+)= A[tmem] . B[smem]^T (A in tensor memory: lane = row, 4 K-bytes per column).
+HACK_DEV void mma_u8_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate)
       : "memory");
 }
 

@@ -114,3 +114,12 @@ def test_c2_full_size_sampled_rows():
     rows = np.array([0, 1, 63, 64, 777, 2048, 3000, 4031, 4095])
     check_request(ocfg, 0, out, pc, cache, reqs, cu, slots, rid, rows=rows, heads=[0, 5, 17, 31])
     assert np.isfinite(out).all()
+
+
+def test_prefill_simt_baseline_kernel(monkeypatch):
+    # the CUDA-core baseline (used for Pi != 64) meets the same bar at Pi = 64
+    monkeypatch.setenv("HACK_PREFILL_IMPL", "simt")
+    ocfg = att.Config(Hq=4, Hkv=2, Pi=64, bits=2)
+    res = run_prefill(ocfg, [300, 77])
+    for i in range(2):
+        check_request(ocfg, i, *res)
