@@ -2,9 +2,10 @@
 //
 // Prefill: the tcgen05 kernel (prefill_tc.cu) for Pi = 64, else the CUDA-core kernel
 // (prefill_simt.cu).  Decode: the split-KV mma.sync kernel (decode_mma.cu) for Pi = 64,
-// G <= 8, else decode_simt.cu; HACK_DECODE_IMPL=tc selects the experimental tcgen05
-// TMEM-operand kernel (decode_tc.cu).  HACK_PREFILL_IMPL / HACK_DECODE_IMPL = "simt"
-// force the baseline kernels (parity cross-checks).
+// G <= 8, else decode_simt.cu.  HACK_PREFILL_IMPL / HACK_DECODE_IMPL = "simt" force the
+// baseline kernels (parity cross-checks).  csrc/experimental/decode_tc.cu (a tcgen05
+// decode with K/V operands unpacked into TMEM) is not built: it was slower than the
+// mma.sync kernel and hangs in some configurations (round-2 work).
 #include <cstdlib>
 #include <cstring>
 
@@ -29,9 +30,7 @@ cudaError_t launch_decode_mma(const KernelCfg& kc, const void* q_new, const int3
                               const hack_debug_t* dbg, cudaStream_t st);
 
 static bool use_decode_mma(const KernelCfg& kc);
-cudaError_t launch_decode_tc(const KernelCfg& kc, const void* q_new, const int32_t* slots, int batch,
-                             int max_seqlen, const CacheView& cv, void* out, void* workspace,
-                             const hack_debug_t* dbg, cudaStream_t st);
+
 
 static bool env_is(const char* name, const char* val) {
   const char* e = getenv(name);
@@ -63,8 +62,6 @@ size_t decode_workspace_bytes(const KernelCfg& kc, int batch, int max_seqlen) {
 cudaError_t launch_decode_attention(const KernelCfg& kc, const void* q_new, const int32_t* slots, int batch,
                                     int max_seqlen, const CacheView& cv, void* out, void* workspace,
                                     const hack_debug_t* dbg, cudaStream_t st) {
-  if (use_decode_mma(kc) && env_is("HACK_DECODE_IMPL", "tc"))  // experimental TMEM-operand kernel
-    return launch_decode_tc(kc, q_new, slots, batch, max_seqlen, cv, out, workspace, dbg, st);
   if (use_decode_mma(kc))
     return launch_decode_mma(kc, q_new, slots, batch, max_seqlen, cv, out, workspace, dbg, st);
   return launch_decode_simt(kc, q_new, slots, batch, cv, out, dbg, st);

@@ -214,8 +214,7 @@ __global__ void __launch_bounds__(kThreads, 2) decode_tc_kernel(const __half* __
       l_run[n] = 0.f;
     }
     // stage pair u: unpack this token's K row straight into TMEM (A operand, 4 codes per
-    // column) and compute its Eq. 4 coefficients (cached sums, SE).  Software-pipelined:
-    // pair u+1 is staged before the softmax of pair u so QK(u+1) overlaps it.
+    // column) and compute its Eq. 4 coefficients (cached sums, SE).
     auto stage_k = [&](int u, float (&sk)[2], float (&mu)[2], float (&yk)[2]) {
       const int s = u % NST, bu = u & 1;
       const int jp = p_beg + 2 * u + x;
@@ -266,8 +265,7 @@ __global__ void __launch_bounds__(kThreads, 2) decode_tc_kernel(const __half* __
       ptx::mbar_arrive(&sm.ka_ready[bu]);
       ptx::mbar_arrive(&sm.empty[s]);  // this warpgroup is done with the stage
     };
-    float sk[2], mu[2], yk[2], nsk[2], nmu[2], nyk[2];
-    if (npair > 0) stage_k(0, sk, mu, yk);
+    float sk[2], mu[2], yk[2];
 #pragma unroll 1
     for (int u = 0; u < npair; ++u) {
       const int bu = u & 1;
@@ -276,7 +274,7 @@ __global__ void __launch_bounds__(kThreads, 2) decode_tc_kernel(const __half* __
       const int tok = jp * PI + row;
       const bool valid = present && tok < len;
       const bool committed = present && jp < nfull;
-      if (u + 1 < npair) stage_k(u + 1, nsk, nmu, nyk);
+      stage_k(u, sk, mu, yk);
       // -- S for this token, all rows
       ptx::mbar_wait(&sm.s_full[bu], (u >> 1) & 1);
       ptx::tc_fence_after();
@@ -369,12 +367,6 @@ __global__ void __launch_bounds__(kThreads, 2) decode_tc_kernel(const __half* __
         for (int n = 0; n < 8; ++n) sm.ptl[n][row] = p[n];  // FP16 tail page (RQE)
       }
       ptx::mbar_arrive(&sm.p_ready[bu]);
-#pragma unroll
-      for (int beta = 0; beta < 2; ++beta) {
-        sk[beta] = nsk[beta];
-        mu[beta] = nmu[beta];
-        yk[beta] = nyk[beta];
-      }
     }
     // -- final l per row: sum over the 128 token slots
 #pragma unroll
@@ -398,7 +390,7 @@ __global__ void __launch_bounds__(kThreads, 2) decode_tc_kernel(const __half* __
 #pragma unroll
     for (int n = 0; n < 8; ++n) o[n] = 0.f;
     // stage pair u: unpack this channel's V rows (both pages) into TMEM and compute the
-    // per-channel Eq. 4 coefficients; software-pipelined one pair ahead of the O update.
+    // per-channel Eq. 4 coefficients.
     auto stage_v = [&](int u, bool (&comm)[2], float (&svv)[2], float (&mu)[2], float (&yv)[2]) {
       const int s = u % NST, bu = u & 1;
       ptx::mbar_wait(&sm.full[s], (u / NST) & 1);
@@ -444,13 +436,12 @@ __global__ void __launch_bounds__(kThreads, 2) decode_tc_kernel(const __half* __
       ptx::mbar_arrive(&sm.va_ready[bu]);
       ptx::mbar_arrive(&sm.empty[s]);
     };
-    bool comm[2], ncomm[2];
-    float svv[2], mu[2], yv[2], nsvv[2], nmu[2], nyv[2];
-    if (npair > 0) stage_v(0, comm, svv, mu, yv);
+    bool comm[2];
+    float svv[2], mu[2], yv[2];
 #pragma unroll 1
     for (int u = 0; u < npair; ++u) {
       const int bu = u & 1;
-      if (u + 1 < npair) stage_v(u + 1, ncomm, nsvv, nmu, nyv);
+      stage_v(u, comm, svv, mu, yv);
       // -- O update for this pair
       ptx::mbar_wait(&sm.p_ready[bu], (u >> 1) & 1);
       const bool anyc = comm[0] || comm[1];
@@ -490,13 +481,6 @@ __global__ void __launch_bounds__(kThreads, 2) decode_tc_kernel(const __half* __
         }
       }
       ptx::mbar_arrive(&sm.m_free[bu]);  // alpha / rmeta / xs of this pair consumed
-#pragma unroll
-      for (int x = 0; x < 2; ++x) {
-        comm[x] = ncomm[x];
-        svv[x] = nsvv[x];
-        mu[x] = nmu[x];
-        yv[x] = nyv[x];
-      }
     }
     for (int n = 0; n < G; ++n)
       part[((((int64_t)b * kc.Hkv + hk) * nsplit + split) * G + n) * 130 + 2 + c] = o[n];

@@ -87,8 +87,7 @@ def test_decode_group_16():
     run_decode(att.Config(Hq=16, Hkv=1, Pi=64, bits=2), [70], 10, check_every=3)
 
 
-@pytest.mark.parametrize("impl", ["tc", "simt"])
-def test_decode_alternative_kernels(impl, monkeypatch):
-    # the experimental tcgen05 TMEM-operand kernel and the CUDA-core baseline meet the same bar
-    monkeypatch.setenv("HACK_DECODE_IMPL", impl)
+def test_decode_simt_baseline_kernel(monkeypatch):
+    # the CUDA-core baseline (used for Pi != 64 or G > 8) meets the same bar at Pi = 64
+    monkeypatch.setenv("HACK_DECODE_IMPL", "simt")
     run_decode(att.Config(Hq=4, Hkv=2, Pi=64, bits=2), [130, 64, 5], 70, check_every=9)
