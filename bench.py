@@ -67,7 +67,7 @@ def load_traffic():
 # ----------------------------------------------------------------------------- clocks
 
 class ClockSampler:
-    """Samples SM clock + throttle reasons with NVML every ~10 ms (own thread)."""
+    """Samples SM clock + throttle reasons with NVML every ~2 ms (own thread)."""
 
     REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
                0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
@@ -93,7 +93,7 @@ class ClockSampler:
                 self.reasons |= self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
             except Exception:
                 pass
-            time.sleep(0.01)
+            time.sleep(0.002)
 
     def __enter__(self):
         if self.ok:
@@ -364,10 +364,11 @@ def run_decode(args, h, dev, rank, world, peaks, traffic, seed, flush):
     n_before = int(cache.seq_lens[0].item())
     evs = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
     n0 = h.kernel_launches()
-    barrier(world)
-    for i in range(args.steps):
-        step(evs[i])
-    barrier(world)
+    with ClockSampler(dev.index if dev.index is not None else 0) as clk:
+        barrier(world)
+        for i in range(args.steps):
+            step(evs[i])
+        barrier(world)
     launches = h.kernel_launches() - n0
     step_ms = [e[0].elapsed_time(e[2]) for e in evs]
     attn_ms = [e[1].elapsed_time(e[2]) for e in evs]
@@ -423,13 +424,14 @@ def run_decode(args, h, dev, rank, world, peaks, traffic, seed, flush):
                 "h2d_bytes_per_step": qh.nbytes + kh.nbytes + vh.nbytes, "d2h_bytes_per_step": oh.nbytes,
                 "ms_per_step": e2e_ms},
         "gpu_launches": launches,
+        "clocks": clk.summary(),
     }
 
 
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["hack", "reference"], default="hack")
     ap.add_argument("--no-cpu-baseline", action="store_true")
