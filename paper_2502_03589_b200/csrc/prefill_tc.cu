@@ -7,8 +7,9 @@
 //                 QK: per d-block beta D_beta[128 x 64] = (Q'-128)_beta K'_beta^T
 //                 PV: D'[128 x 128] = (P'-128) V'^T per 64-token V block
 //               (A operands are stored as signed s8 = code - 128, B as u8 codes)
-//   warps 2-3   unpack: 2/4-bit codes -> u8 K-major UMMA tiles (tc_common.cuh) + per-key /
-//               per-channel Eq. 4 coefficients from the page meta and CACHED sums (SE)
+//   warps 2-3   unpack: 2/4-bit codes c -> doubled codes 2c (u8) in K-major UMMA tiles
+//               (tc_common.cuh) + per-key / per-channel Eq. 4 coefficients from the page
+//               meta and CACHED sums (SE)
 //   warps 4-19  four symmetric compute warpgroups; thread = query row = TMEM lane.
 //               WG w owns keys 16w..16w+15 of every tile and output channels 32w..32w+31:
 //                 (a3) Q quantization, 8-bit SR (WG0: d-block 0, WG1: d-block 1)
@@ -18,8 +19,15 @@
 //                 (a7) O = alpha O + centered Eq. 4 on D' for the PREVIOUS tile (so the PV
 //                      MMA of tile j overlaps S of tile j+1); FP16 last V block (RQE)
 //                      in fp32; O / l.
-// Centering with s8 A codes: sum (q'-128)(k'-c) = D_s - c SQ_s, so 2 x that is the exact
-// integer 2 D_s - (2^b-1) SQ_s with only a per-row offset.
+// Centering: with s8 A codes a' - 128 and B = 2c the MMA gives
+// E = 2 D_s = 2 sum (a'-128) c exactly (|E| < 2^18, so its fp32 conversion is exact).  The
+// remaining Eq. 4 terms are a rank-2 update per block:
+//   S  = cs [ (s_q/2) s_k 2D_s + s_q SQ_s m_k + mu_q y_k ],  y_k = s_k SK + Pi m_k
+//   O += (s_p/2) s_v 2D_s + s_p SP_s m_v + mu_p y_v,         y_v = s_v SV + Pi m_v
+// (mu = m + 128 s for the 8-bit side; m_k, m_v the stored fp16 minima).
+// Online softmax with lazy rescaling: the running max only moves when a row's tile max
+// exceeds it by more than 8 (log2 units; p~ <= 256), warp-uniformly, so most tiles skip the
+// O *= alpha pass.  P' codes are invariant to the row scale (R13).
 // TMEM (512 columns): S (D_0 | D_1, 128) | D'[2] (2 x 128).  Pi = 64; other partitions
 // use prefill_simt.cu.
 #include "common.cuh"
@@ -38,6 +46,8 @@ constexpr int NB = 3;          // K/V/P tile buffer sets
 constexpr int NWG = 4;         // compute warpgroups
 constexpr int kThreads = 128 + 128 * NWG;
 constexpr int NC = 128 * NWG;  // compute threads
+constexpr float kMagic = 12582912.f;           // 1.5 * 2^23 (P' rounding)
+constexpr float kRescaleTh = 8.f;             // lazy-rescale threshold (log2 units)
 
 template <int BITS>
 struct TcSmem {
@@ -47,9 +57,9 @@ struct TcSmem {
   alignas(128) uint8_t k[NB][BN * 128];   // K' (u8), K-major, SBO 1024
   alignas(128) uint8_t v[NB][128 * BN];   // V' (u8), K-major (keys = K), SBO 512
   alignas(128) uint8_t p[NB][BM * BN];    // P' - 128 (s8), K-major, SBO 512
-  alignas(16) float kcf[NB][2][3][BN];    // [buf][beta][field][key]: s_k, mu_k, y_k
-  alignas(16) float vcf[NB][3][128];      // [buf][field][channel]: s_v, mu_v, y_v
-  float4 qconst[2][BM];                   // per (beta, row): aq, xq, mu_q, -r_q
+  alignas(16) float kcf[NB][2][3][BN];    // [buf][beta][field][key]: s_k, m_k, y_k
+  alignas(16) float vcf[NB][3][128];      // [buf][field][channel]: s_v, m_v, y_v
+  float4 qconst[2][BM];                   // per (beta, row): cs s_q / 2, cs s_q SQ_s, cs mu_q
   int sp_part[NB][NWG][BM];               // partial P-code sums
   float2 xch[2][NWG][BM];                 // partial (max, min | -inf if masked)
   float ptail[BM][BN + 1];                // p~ of the FP16 tail tile
@@ -66,8 +76,6 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_tc_kernel(
     const __half* __restrict__ q, const int32_t* __restrict__ cu_seqlens, const int32_t* __restrict__ slots,
     CacheView cv, KernelCfg kc, void* __restrict__ out, uint8_t* __restrict__ dbg_pcodes, int64_t dbg_stride) {
   using SM = TcSmem<BITS>;
-  constexpr int qkm = (1 << BITS) - 1;
-  constexpr float ck = 0.5f * qkm;  // K/V code centre
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   SM& sm = *reinterpret_cast<SM*>(smem_raw);
 
@@ -103,7 +111,7 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_tc_kernel(
     }
     ptx::mbar_init(&sm.s_full, 1);
     ptx::mbar_init(&sm.s_free, NC);
-    ptx::mbar_init(&sm.q_ready, 256);
+    ptx::mbar_init(&sm.q_ready, NC);
     ptx::fence_mbar_init();
   }
   if (warp == 1) ptx::tmem_alloc(&sm.tmem_base, 512);
@@ -115,7 +123,7 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_tc_kernel(
   const uint32_t tD0 = tmem + 128;  // D'[0] columns 128..255, D'[1] 256..383
 
   if (warp < 4) {
-    asm volatile("setmaxnreg.dec.sync.aligned.u32 40;");
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 40;");  // frees registers for the compute WGs
     if (warp == 0) {
       // ---------------------------------------------------------------- producer
       if (lane == 0) {
@@ -195,9 +203,9 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_tc_kernel(
             for (int x = 0; x < 4; ++x) {
               const int wi = 4 * h + x;
               if (BITS == 2)
-                *reinterpret_cast<uint4*>(sm.k[bj] + kmaj_off(key, 16 * wi, 1024)) = unpack16_2b(w4[x]);
+                *reinterpret_cast<uint4*>(sm.k[bj] + kmaj_off(key, 16 * wi, 1024)) = unpack16_2b_x2(w4[x]);
               else
-                *reinterpret_cast<uint2*>(sm.k[bj] + kmaj_off(key, 8 * wi, 1024)) = unpack8_4b(w4[x]);
+                *reinterpret_cast<uint2*>(sm.k[bj] + kmaj_off(key, 8 * wi, 1024)) = unpack8_4b_x2(w4[x]);
             }
           }
         }
@@ -209,10 +217,9 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_tc_kernel(
             const __half2 mh = reinterpret_cast<const __half2*>(pg + PL.k_meta)[e];
             const float m = __low2float(mh), s2 = __high2float(mh);
             const int sum = load_sum(pg + PL.k_sums, e, PL.sum_bytes);  // cached sum (SE)
-            const float mu = m + ck * s2;
             c0 = s2;
-            c1 = mu;
-            c2 = s2 * ((float)sum - ck * PI) + PI * mu;
+            c1 = m;
+            c2 = fmaf(s2, (float)sum, PI * m);  // y_k = s_k SK + Pi m_k
           }
           sm.kcf[bj][beta][0][key] = c0;
           sm.kcf[bj][beta][1][key] = c1;
@@ -234,18 +241,17 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_tc_kernel(
               for (int x = 0; x < 4; ++x) {
                 const int wi = 4 * h + x;
                 if (BITS == 2)
-                  *reinterpret_cast<uint4*>(sm.v[bj] + kmaj_off(ch, 16 * wi, 512)) = unpack16_2b(w4[x]);
+                  *reinterpret_cast<uint4*>(sm.v[bj] + kmaj_off(ch, 16 * wi, 512)) = unpack16_2b_x2(w4[x]);
                 else
-                  *reinterpret_cast<uint2*>(sm.v[bj] + kmaj_off(ch, 8 * wi, 512)) = unpack8_4b(w4[x]);
+                  *reinterpret_cast<uint2*>(sm.v[bj] + kmaj_off(ch, 8 * wi, 512)) = unpack8_4b_x2(w4[x]);
               }
             }
             const __half2 mh = reinterpret_cast<const __half2*>(pg + PL.v_meta)[ch];
             const float m = __low2float(mh), s2 = __high2float(mh);
             const int sum = load_sum(pg + PL.v_sums, ch, PL.sum_bytes);  // cached sum (SE)
-            const float mu = m + ck * s2;
             sm.vcf[bj][0][ch] = s2;
-            sm.vcf[bj][1][ch] = mu;
-            sm.vcf[bj][2][ch] = s2 * ((float)sum - ck * PI) + PI * mu;
+            sm.vcf[bj][1][ch] = m;
+            sm.vcf[bj][2][ch] = fmaf(s2, (float)sum, PI * m);  // y_v = s_v SV + Pi m_v
           }
         }
         ptx::fence_proxy_async_smem();
@@ -255,12 +261,15 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_tc_kernel(
     }
   } else {
     // ------------------------------------------------------------------ compute WGs
-    asm volatile("setmaxnreg.inc.sync.aligned.u32 104;");
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 104;  // (96 - 40) x 128 freed >= (104 - 96) x 512");
     const int w = (warp - 4) >> 2;
     const int r = (tid - 128) & (BM - 1);
     const int i = min(i0 + r, L - 1);  // this thread's query position (padding rows clamp)
     const uint32_t lane_base = (uint32_t)(32 * (warp & 3)) << 16;
+    const uint32_t qbar = 3 + (warp & 3);  // the 4 warps (one per WG) sharing these 32 rows
     const float cscale = 1.4426950408889634f / sqrtf(128.f);
+    const int kb = 16 * w;  // this WG's keys in a tile
+    const int cb = 32 * w;  // this WG's output channels
     if (w < 2) {
       // (a3) quantize Q[i, 64w .. 64w+63]: 8-bit, fp32 meta, SR (op sequence of quant_row16)
       const uint4* qrow = reinterpret_cast<const uint4*>(q + ((int64_t)(start + i) * kc.Hq + hq) * 128 + 64 * w);
@@ -318,77 +327,76 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_tc_kernel(
         *reinterpret_cast<uint4*>(sm.q + kmaj_off(r, 64 * w + 16 * g, 1024)) = make_uint4(wv[0], wv[1], wv[2], wv[3]);
       }
       const int sqs = sum - 128 * PI;  // sum (q' - 128)
-      sm.qconst[w][r] = make_float4(cscale * qm.s * 0.5f, cscale * qm.s * (float)sqs,
-                                    cscale * (qm.m + 128.f * qm.s), -(float)(qkm * sqs));
+      sm.qconst[w][r] = make_float4(cscale * qm.s * 0.5f, cscale * qm.s * (float)sqs, cscale * (qm.m + 128.f * qm.s), 0.f);
       ptx::fence_proxy_async_smem();
-      ptx::mbar_arrive(&sm.q_ready);
     }
-    ptx::named_bar_sync(2, NC);  // both halves of the Q row constants visible
+    ptx::mbar_arrive(&sm.q_ready);
+    ptx::named_bar_sync(qbar, 128);  // both halves of the Q row constants visible
     const float4 qc0 = sm.qconst[0][r], qc1 = sm.qconst[1][r];
-    const float2 qa0 = make_float2(qc0.x, qc0.x), qx0 = make_float2(qc0.y, qc0.y), qm0 = make_float2(qc0.z, qc0.z),
-                 qn0 = make_float2(qc0.w, qc0.w);
-    const float2 qa1 = make_float2(qc1.x, qc1.x), qx1 = make_float2(qc1.y, qc1.y), qm1 = make_float2(qc1.z, qc1.z),
-                 qn1 = make_float2(qc1.w, qc1.w);
-    const float2 two = make_float2(2.f, 2.f);
-    const int kb = 16 * w;   // this WG's keys in a tile
-    const int cb = 32 * w;   // this WG's output channels
+    const float2 qa0 = make_float2(qc0.x, qc0.x), qx0 = make_float2(qc0.y, qc0.y), qm0 = make_float2(qc0.z, qc0.z);
+    const float2 qa1 = make_float2(qc1.x, qc1.x), qx1 = make_float2(qc1.y, qc1.y), qm1 = make_float2(qc1.z, qc1.z);
     float m_run = -INFINITY, l_run = 0.f;
-    float2 o2[16];           // channels cb + 2x, cb + 2x + 1
+    float2 o2[16];  // channels cb + 2x, cb + 2x + 1
 #pragma unroll
     for (int x = 0; x < 16; ++x) o2[x] = make_float2(0.f, 0.f);
     // state of the tile whose O update is pending (lags one tile)
-    float pend_al = 0.f, pend_s = 0.f, pend_m = 0.f;
+    float pend_al = 1.f, pend_s = 0.f, pend_m = 0.f;
+    bool pend_resc = false;
 
     // O = alpha O + Eq. 4 (centered) on D' of tile jj (a7)
     auto o_update = [&](int jj) {
       const int bq = jj % NB, bd = jj & 1;
       const uint32_t ph = (jj / NB) & 1;
+      if (pend_resc) {  // warp-uniform (lazy rescaling)
+        const float2 al2 = make_float2(pend_al, pend_al);
+#pragma unroll
+        for (int x = 0; x < 16; ++x) o2[x] = ptx::fmul2(o2[x], al2);
+      }
       if (jj < nfull) {
         int sp = 0;
 #pragma unroll
         for (int x = 0; x < NWG; ++x) sp += sm.sp_part[bq][x][r];
         const int sps = sp - 128 * PI;  // sum (p' - 128)
-        const float2 al2 = make_float2(pend_al, pend_al);
         const float2 ap2 = make_float2(0.5f * pend_s, 0.5f * pend_s);
         const float2 xp2 = make_float2(pend_s * (float)sps, pend_s * (float)sps);
         const float2 mp2 = make_float2(pend_m + 128.f * pend_s, pend_m + 128.f * pend_s);
-        const float2 np2 = make_float2(-(float)(qkm * sps), -(float)(qkm * sps));
         ptx::mbar_wait(&sm.d_full[bd], (jj >> 1) & 1);
         ptx::mbar_wait(&sm.v_ready[bq], ph);
         ptx::tc_fence_after();
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
           uint32_t d[16];
-          ptx::tmem_ld16(tD0 + 128 * bd + lane_base + cb + 16 * h, d);
+          const uint32_t ta = tD0 + 128 * bd + lane_base + cb + 16 * h;
+          ptx::tmem_ld16(ta, d);
           ptx::tmem_wait_ld();
 #pragma unroll
           for (int x4 = 0; x4 < 4; ++x4) {
             const int c0 = cb + 16 * h + 4 * x4;
             const float4 sv4 = *reinterpret_cast<const float4*>(&sm.vcf[bq][0][c0]);
-            const float4 mu4 = *reinterpret_cast<const float4*>(&sm.vcf[bq][1][c0]);
+            const float4 mv4 = *reinterpret_cast<const float4*>(&sm.vcf[bq][1][c0]);
             const float4 y4 = *reinterpret_cast<const float4*>(&sm.vcf[bq][2][c0]);
 #pragma unroll
             for (int pr = 0; pr < 2; ++pr) {
               const int xo = 4 * x4 + 2 * pr;
-              const float2 df = make_float2(u2f(d[xo]), u2f(d[xo + 1]));
+              const int oi = 8 * h + 2 * x4 + pr;
+              const float2 E = make_float2(u2f(d[xo]), u2f(d[xo + 1]));
               const float2 svp = pr ? make_float2(sv4.z, sv4.w) : make_float2(sv4.x, sv4.y);
-              const float2 mup = pr ? make_float2(mu4.z, mu4.w) : make_float2(mu4.x, mu4.y);
+              const float2 mvp = pr ? make_float2(mv4.z, mv4.w) : make_float2(mv4.x, mv4.y);
               const float2 yp = pr ? make_float2(y4.z, y4.w) : make_float2(y4.x, y4.y);
-              const float2 e = ptx::ffma2(two, df, np2);  // 2 x centered int dot (exact)
-              const float2 t = ptx::ffma2(ap2, ptx::fmul2(svp, e), ptx::ffma2(xp2, mup, ptx::fmul2(mp2, yp)));
-              o2[8 * h + 2 * x4 + pr] = ptx::ffma2(al2, o2[8 * h + 2 * x4 + pr], t);
+              const float2 t = ptx::fmul2(svp, E);  // s_v 2D_s
+              float2 o = ptx::ffma2(ap2, t, o2[oi]);
+              o = ptx::ffma2(xp2, mvp, o);
+              o2[oi] = ptx::ffma2(mp2, yp, o);
             }
           }
         }
         ptx::tc_fence_before();
         ptx::mbar_arrive(&sm.d_free[bd]);
       } else {
-        // FP16 last V block (RQE): O = alpha O + sum_t p~_t v_t in fp32
+        // FP16 last V block (RQE): O += sum_t p~_t v_t in fp32
         const int T = L - nfull * PI;
         const __half* tail =
             reinterpret_cast<const __half*>(cv.v_tail) + ((int64_t)slot * kc.Hkv + hk) * PI * 128 + cb;
-#pragma unroll
-        for (int x = 0; x < 16; ++x) o2[x] = ptx::fmul2(o2[x], make_float2(pend_al, pend_al));
 #pragma unroll 1
         for (int t = 0; t < T; ++t) {
           const float pt = sm.ptail[r][t];
@@ -414,37 +422,33 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_tc_kernel(
       ptx::mbar_wait(&sm.s_full, j & 1);
       ptx::tc_fence_after();
       float s[16];
-      {
-        uint32_t d0[16], d1[16];
-        ptx::tmem_ld16(tS + lane_base + kb, d0);
-        ptx::tmem_ld16(tS + lane_base + 64 + kb, d1);
+#pragma unroll
+      for (int beta = 0; beta < 2; ++beta) {  // one d-block at a time (register pressure)
+        uint32_t d[16];
+        const uint32_t ta = tS + lane_base + 64 * beta + kb;
+        ptx::tmem_ld16(ta, d);
         ptx::tmem_wait_ld();
+        const float2 A = beta ? qa1 : qa0, X = beta ? qx1 : qx0, M = beta ? qm1 : qm0;
 #pragma unroll
         for (int g4 = 0; g4 < 4; ++g4) {
           const int kl = kb + 4 * g4;  // first of 4 keys
-          float2 acc[2];
+          const float4 sk4 = *reinterpret_cast<const float4*>(&sm.kcf[bj][beta][0][kl]);
+          const float4 mk4 = *reinterpret_cast<const float4*>(&sm.kcf[bj][beta][1][kl]);
+          const float4 y4 = *reinterpret_cast<const float4*>(&sm.kcf[bj][beta][2][kl]);
 #pragma unroll
-          for (int beta = 0; beta < 2; ++beta) {
-            const float4 sk4 = *reinterpret_cast<const float4*>(&sm.kcf[bj][beta][0][kl]);
-            const float4 mu4 = *reinterpret_cast<const float4*>(&sm.kcf[bj][beta][1][kl]);
-            const float4 y4 = *reinterpret_cast<const float4*>(&sm.kcf[bj][beta][2][kl]);
-            const uint32_t* d = beta ? d1 : d0;
-            const float2 A = beta ? qa1 : qa0, X = beta ? qx1 : qx0, M = beta ? qm1 : qm0, NR = beta ? qn1 : qn0;
-#pragma unroll
-            for (int pr = 0; pr < 2; ++pr) {
-              const float2 df = make_float2(u2f(d[4 * g4 + 2 * pr]), u2f(d[4 * g4 + 2 * pr + 1]));
-              const float2 skp = pr ? make_float2(sk4.z, sk4.w) : make_float2(sk4.x, sk4.y);
-              const float2 mup = pr ? make_float2(mu4.z, mu4.w) : make_float2(mu4.x, mu4.y);
-              const float2 yp = pr ? make_float2(y4.z, y4.w) : make_float2(y4.x, y4.y);
-              const float2 e = ptx::ffma2(two, df, NR);  // 2 x centered int dot (exact)
-              const float2 base = beta ? ptx::ffma2(M, yp, acc[pr]) : ptx::fmul2(M, yp);
-              acc[pr] = ptx::ffma2(A, ptx::fmul2(skp, e), ptx::ffma2(X, mup, base));
-            }
+          for (int pr = 0; pr < 2; ++pr) {
+            const int k2 = 4 * g4 + 2 * pr;
+            const float2 E = make_float2(u2f(d[k2]), u2f(d[k2 + 1]));
+            const float2 skp = pr ? make_float2(sk4.z, sk4.w) : make_float2(sk4.x, sk4.y);
+            const float2 mkp = pr ? make_float2(mk4.z, mk4.w) : make_float2(mk4.x, mk4.y);
+            const float2 yp = pr ? make_float2(y4.z, y4.w) : make_float2(y4.x, y4.y);
+            const float2 t = ptx::fmul2(skp, E);  // s_k 2D_s
+            float2 a = beta ? ptx::ffma2(X, mkp, make_float2(s[k2], s[k2 + 1])) : ptx::fmul2(X, mkp);
+            a = ptx::ffma2(M, yp, a);
+            a = ptx::ffma2(A, t, a);
+            s[k2] = a.x;
+            s[k2 + 1] = a.y;
           }
-          s[4 * g4 + 0] = acc[0].x;
-          s[4 * g4 + 1] = acc[0].y;
-          s[4 * g4 + 2] = acc[1].x;
-          s[4 * g4 + 3] = acc[1].y;
         }
       }
       ptx::tc_fence_before();
@@ -471,7 +475,7 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_tc_kernel(
         for (int kk = 0; kk < 16; ++kk) mn = fminf(mn, s[kk] == -INFINITY ? INFINITY : s[kk]);
       }
       sm.xch[j & 1][w][r] = make_float2(mx, masked ? -INFINITY : mn);
-      ptx::named_bar_sync(2, NC);
+      ptx::named_bar_sync(qbar, 128);
       bool any_masked = false;
       mn = INFINITY;
       mx = -INFINITY;
@@ -482,10 +486,17 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_tc_kernel(
         any_masked |= (o.y == -INFINITY);
         mn = fminf(mn, o.y == -INFINITY ? INFINITY : o.y);
       }
-      const float m_new = fmaxf(m_run, mx);
-      const float al = (m_run == -INFINITY) ? 0.f : ex2(m_run - m_new);
+      // lazy rescaling: move the running max only when some row of this warp outgrew it by
+      // more than kRescaleTh (identical decision in the 4 warps sharing these rows)
+      float al = 1.f;
+      const bool resc = __any_sync(0xffffffffu, mx > m_run + kRescaleTh);
+      if (resc) {
+        const float m_new = fmaxf(m_run, mx);
+        al = (m_run == -INFINITY) ? 0.f : ex2(m_run - m_new);
+        m_run = m_new;
+      }
       float2 ls2 = make_float2(0.f, 0.f);
-      const float2 mneg = make_float2(-m_new, -m_new);
+      const float2 mneg = make_float2(-m_run, -m_run);
 #pragma unroll
       for (int kk = 0; kk < 16; kk += 2) {
         const float2 a2 = ptx::fadd2(make_float2(s[kk], s[kk + 1]), mneg);
@@ -494,13 +505,12 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_tc_kernel(
         ls2 = ptx::fadd2(ls2, make_float2(s[kk], s[kk + 1]));
       }
       l_run = l_run * al + (ls2.x + ls2.y);
-      m_run = m_new;
       float pm_s = 0.f, pm_m = 0.f;
       if (j < nfull) {
         // (a6) P' per (row, V block): 8-bit RN on p~ (codes invariant to the row scale);
         // y = (p - lo) / s rounded with the 1.5*2^23 magic number (y in [0, 255])
-        const float plo = any_masked ? 0.f : ex2(mn - m_new);
-        const float phi = ex2(mx - m_new);
+        const float plo = any_masked ? 0.f : ex2(mn - m_run);
+        const float phi = ex2(mx - m_run);
         QMeta pm = meta_fp32(plo, phi, 255);
         if (!(pm.s > 1e-30f)) {
           pm.s = 0.f;
@@ -509,7 +519,7 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_tc_kernel(
         pm_s = pm.s;
         pm_m = pm.m;
         const float2 inv2 = make_float2(pm.inv, pm.inv), nlo2 = make_float2(-plo * pm.inv, -plo * pm.inv);
-        const float2 magic = make_float2(12582912.f, 12582912.f);
+        const float2 magic = make_float2(kMagic, kMagic);
         uint32_t bits[16];
 #pragma unroll
         for (int kk = 0; kk < 16; kk += 2) {
@@ -545,13 +555,14 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_tc_kernel(
       ptx::mbar_arrive(&sm.p_ready[bj]);
       if (j >= 1) o_update(j - 1);  // overlaps the PV MMA of tile j with S of tile j+1
       pend_al = al;
+      pend_resc = resc;
       pend_s = pm_s;
       pend_m = pm_m;
     }
-    ptx::named_bar_sync(2, NC);  // sp_part / ptail of the last tile complete
+    ptx::named_bar_sync(qbar, 128);  // sp_part / ptail of the last tile complete
     o_update(nkt - 1);
     sm.lpart[w][r] = l_run;
-    ptx::named_bar_sync(2, NC);
+    ptx::named_bar_sync(qbar, 128);
     if (i0 + r < L) {
       float l = 0.f;
 #pragma unroll

@@ -28,6 +28,13 @@ HACK_DEV uint4 unpack16_2b(uint32_t w) {
 // 8 codes (4-bit) -> 8 bytes in pi4 order.
 HACK_DEV uint2 unpack8_4b(uint32_t w) { return make_uint2(w & 0x0F0F0F0Fu, (w >> 4) & 0x0F0F0F0Fu); }
 
+// Doubled codes 2c (u8) in the same orders: the B operand of the centered kernels, so that
+// sum (a - 128)(2c) + offsets gives the exact integer 2 x sum (a - 128)(c - (2^b - 1)/2).
+HACK_DEV uint4 unpack16_2b_x2(uint32_t w) {
+  return make_uint4((w << 1) & 0x06060606u, (w >> 1) & 0x06060606u, (w >> 3) & 0x06060606u, (w >> 5) & 0x06060606u);
+}
+HACK_DEV uint2 unpack8_4b_x2(uint32_t w) { return make_uint2((w << 1) & 0x1E1E1E1Eu, (w >> 3) & 0x1E1E1E1Eu); }
+
 // Offset of (row, k-byte) in a K-major no-swizzle tile: [row/8][k/16][row%8][16 B].
 HACK_DEV uint32_t kmaj_off(int row, int kbyte, int sbo) {
   return (uint32_t)((row >> 3) * sbo + (kbyte >> 4) * 128 + (row & 7) * 16 + (kbyte & 15));
