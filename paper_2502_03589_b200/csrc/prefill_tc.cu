@@ -10,14 +10,15 @@
 //   warps 2-3   unpack: 2/4-bit codes c -> doubled codes 2c (u8) in K-major UMMA tiles
 //               (tc_common.cuh) + per-key / per-channel Eq. 4 coefficients from the page
 //               meta and CACHED sums (SE)
-//   warps 4-19  four symmetric compute warpgroups; thread = query row = TMEM lane.
-//               WG w owns keys 16w..16w+15 of every tile and output channels 32w..32w+31:
-//                 (a3) Q quantization, 8-bit SR (WG0: d-block 0, WG1: d-block 1)
+//   warps 4-11  two S warpgroups; thread = query row = TMEM lane; SW s owns keys
+//               32s..32s+31 of every tile:
+//                 (a3) Q quantization, 8-bit SR (SW s: d-block s)
 //                 (a4) S = centered Eq. 4 x log2e/sqrt(d)
-//                 (a5) causal online softmax, row max/min combined through smem
-//                 (a6) P' 8-bit RN per (row, V block)
-//                 (a7) O = alpha O + centered Eq. 4 on D' for the PREVIOUS tile (so the PV
-//                      MMA of tile j overlaps S of tile j+1); FP16 last V block (RQE)
+//                 (a5) causal online softmax, row max/min combined through smem (2 warps)
+//                 (a6) P' 8-bit RN per (row, V block) -> smem A tile + row info
+//   warps 12-19 two O warpgroups; thread = row; OW o owns output channels 64o..64o+63:
+//                 (a7) O = alpha O + centered Eq. 4 on D' (TMEM, double-buffered, so the
+//                      S warps run up to NB tiles ahead); FP16 last V block (RQE)
 //                      in fp32; O / l.
 // Centering: with s8 A codes a' - 128 and B = 2c the MMA gives
 // E = 2 D_s = 2 sum (a'-128) c exactly (|E| < 2^18, so its fp32 conversion is exact).  The
@@ -43,9 +44,9 @@ constexpr int BM = 128;
 constexpr int BN = 64;
 constexpr int NS = 4;          // page stages
 constexpr int NB = 3;          // K/V/P tile buffer sets
-constexpr int NWG = 4;         // compute warpgroups
-constexpr int kThreads = 128 + 128 * NWG;
-constexpr int NC = 128 * NWG;  // compute threads
+constexpr int kThreads = 640;  // 4 service warps + 2 S warpgroups + 2 O warpgroups
+constexpr int NSW = 256;       // S-warpgroup threads
+constexpr int NOW = 256;       // O-warpgroup threads
 constexpr float kMagic = 12582912.f;           // 1.5 * 2^23 (P' rounding)
 constexpr float kRescaleTh = 8.f;             // lazy-rescale threshold (log2 units)
 
@@ -60,12 +61,13 @@ struct TcSmem {
   alignas(16) float kcf[NB][2][3][BN];    // [buf][beta][field][key]: s_k, m_k, y_k
   alignas(16) float vcf[NB][3][128];      // [buf][field][channel]: s_v, m_v, y_v
   float4 qconst[2][BM];                   // per (beta, row): cs s_q / 2, cs s_q SQ_s, cs mu_q
-  int sp_part[NB][NWG][BM];               // partial P-code sums
-  float2 xch[2][NWG][BM];                 // partial (max, min | -inf if masked)
+  int sp_part[NB][2][BM];                 // partial P-code sums (per S warpgroup)
+  float4 pinfo[NB][BM];                   // per (tile, row): alpha, rescaled?, s_p, m_p
+  float2 xch[2][2][BM];                   // partial (max, min | -inf if masked)
   float ptail[BM][BN + 1];                // p~ of the FP16 tail tile
-  float lpart[NWG][BM];
-  uint64_t full[NS], empty[NS], k_ready[NB], k_free[NB], v_ready[NB], v_free[NB], p_ready[NB], p_free[NB],
-      d_full[2], d_free[2], s_full, s_free, q_ready;
+  float lpart[2][BM];
+  uint64_t full[NS], empty[NS], k_ready[NB], k_free[NB], v_ready[NB], o_done[NB], p_ready[NB], p_free[NB],
+      d_full[2], d_free[2], s_full, s_free, q_ready, l_ready;
   uint32_t tmem_base;
 };
 
@@ -99,19 +101,20 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_tc_kernel(
     }
     for (int x = 0; x < NB; ++x) {
       ptx::mbar_init(&sm.k_ready[x], 64);
-      ptx::mbar_init(&sm.k_free[x], NC);
+      ptx::mbar_init(&sm.k_free[x], NSW);
       ptx::mbar_init(&sm.v_ready[x], 64);
-      ptx::mbar_init(&sm.v_free[x], NC);
-      ptx::mbar_init(&sm.p_ready[x], NC);
+      ptx::mbar_init(&sm.o_done[x], NOW);
+      ptx::mbar_init(&sm.p_ready[x], NSW);
       ptx::mbar_init(&sm.p_free[x], 1);
     }
     for (int x = 0; x < 2; ++x) {
       ptx::mbar_init(&sm.d_full[x], 1);
-      ptx::mbar_init(&sm.d_free[x], NC);
+      ptx::mbar_init(&sm.d_free[x], NOW);
     }
     ptx::mbar_init(&sm.s_full, 1);
-    ptx::mbar_init(&sm.s_free, NC);
-    ptx::mbar_init(&sm.q_ready, NC);
+    ptx::mbar_init(&sm.s_free, NSW);
+    ptx::mbar_init(&sm.q_ready, NSW);
+    ptx::mbar_init(&sm.l_ready, NSW);
     ptx::fence_mbar_init();
   }
   if (warp == 1) ptx::tmem_alloc(&sm.tmem_base, 512);
@@ -123,7 +126,8 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_tc_kernel(
   const uint32_t tD0 = tmem + 128;  // D'[0] columns 128..255, D'[1] 256..383
 
   if (warp < 4) {
-    asm volatile("setmaxnreg.dec.sync.aligned.u32 40;");  // frees registers for the compute WGs
+    // register budget (launch: 96 x 640): service 40, S 88, O 128 -> 9216 freed >= 8192 taken
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 40;");
     if (warp == 0) {
       // ---------------------------------------------------------------- producer
       if (lane == 0) {
@@ -227,7 +231,7 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_tc_kernel(
         }
         ptx::fence_proxy_async_smem();
         ptx::mbar_arrive(&sm.k_ready[bj]);
-        ptx::mbar_wait(&sm.v_free[bj], ph ^ 1);
+        ptx::mbar_wait(&sm.o_done[bj], ph ^ 1);  // O warps done with tile j - NB
         if (j < nfull) {
 #pragma unroll
           for (int c2 = 0; c2 < 2; ++c2) {
@@ -259,20 +263,20 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_tc_kernel(
         ptx::mbar_arrive(&sm.empty[s]);
       }
     }
-  } else {
-    // ------------------------------------------------------------------ compute WGs
-    asm volatile("setmaxnreg.inc.sync.aligned.u32 104;  // (96 - 40) x 128 freed >= (104 - 96) x 512");
-    const int w = (warp - 4) >> 2;
+  } else if (warp < 12) {
+    // ------------------------------------------------------------------ S warpgroups (2)
+    // thread = query row r = TMEM lane; SW s owns keys 32s..32s+31 of every tile
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 88;");
+    const int sw = (warp - 4) >> 2;
     const int r = (tid - 128) & (BM - 1);
     const int i = min(i0 + r, L - 1);  // this thread's query position (padding rows clamp)
     const uint32_t lane_base = (uint32_t)(32 * (warp & 3)) << 16;
-    const uint32_t qbar = 3 + (warp & 3);  // the 4 warps (one per WG) sharing these 32 rows
+    const uint32_t qbar = 3 + (warp & 3);  // the 2 S warps sharing these 32 rows
     const float cscale = 1.4426950408889634f / sqrtf(128.f);
-    const int kb = 16 * w;  // this WG's keys in a tile
-    const int cb = 32 * w;  // this WG's output channels
-    if (w < 2) {
-      // (a3) quantize Q[i, 64w .. 64w+63]: 8-bit, fp32 meta, SR (op sequence of quant_row16)
-      const uint4* qrow = reinterpret_cast<const uint4*>(q + ((int64_t)(start + i) * kc.Hq + hq) * 128 + 64 * w);
+    const int kb = 32 * sw;
+    {
+      // (a3) quantize Q[i, 64 sw .. 64 sw + 63] (d-block beta = sw): 8-bit, fp32 meta, SR
+      const uint4* qrow = reinterpret_cast<const uint4*>(q + ((int64_t)(start + i) * kc.Hq + hq) * 128 + 64 * sw);
       float lo = INFINITY, hi = -INFINITY;
 #pragma unroll 1
       for (int v8 = 0; v8 < 8; ++v8) {
@@ -303,7 +307,7 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_tc_kernel(
         if (kc.q_round == HACK_ROUND_STOCHASTIC) {
 #pragma unroll
           for (int k4 = 0; k4 < 4; ++k4) {
-            const uint64_t n = ((uint64_t)i * 128u + (uint64_t)(64 * w + 16 * g + 4 * k4)) >> 2;
+            const uint64_t n = ((uint64_t)i * 128u + (uint64_t)(64 * sw + 16 * g + 4 * k4)) >> 2;
             const Philox4 rr = philox_block(kc.seed, rng_id, c3, n);
             cc[4 * k4 + 0] = quant_sr(x[4 * k4 + 0], qm, u24(rr.x), 255);
             cc[4 * k4 + 1] = quant_sr(x[4 * k4 + 1], qm, u24(rr.y), 255);
@@ -324,57 +328,206 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_tc_kernel(
         }
 #pragma unroll
         for (int e = 0; e < 16; ++e) sum += cc[e];
-        *reinterpret_cast<uint4*>(sm.q + kmaj_off(r, 64 * w + 16 * g, 1024)) = make_uint4(wv[0], wv[1], wv[2], wv[3]);
+        *reinterpret_cast<uint4*>(sm.q + kmaj_off(r, 64 * sw + 16 * g, 1024)) = make_uint4(wv[0], wv[1], wv[2], wv[3]);
       }
       const int sqs = sum - 128 * PI;  // sum (q' - 128)
-      sm.qconst[w][r] = make_float4(cscale * qm.s * 0.5f, cscale * qm.s * (float)sqs, cscale * (qm.m + 128.f * qm.s), 0.f);
+      sm.qconst[sw][r] =
+          make_float4(cscale * qm.s * 0.5f, cscale * qm.s * (float)sqs, cscale * (qm.m + 128.f * qm.s), 0.f);
       ptx::fence_proxy_async_smem();
+      ptx::mbar_arrive(&sm.q_ready);
     }
-    ptx::mbar_arrive(&sm.q_ready);
-    ptx::named_bar_sync(qbar, 128);  // both halves of the Q row constants visible
+    ptx::named_bar_sync(qbar, 64);  // both halves of the Q row constants visible
     const float4 qc0 = sm.qconst[0][r], qc1 = sm.qconst[1][r];
     const float2 qa0 = make_float2(qc0.x, qc0.x), qx0 = make_float2(qc0.y, qc0.y), qm0 = make_float2(qc0.z, qc0.z);
     const float2 qa1 = make_float2(qc1.x, qc1.x), qx1 = make_float2(qc1.y, qc1.y), qm1 = make_float2(qc1.z, qc1.z);
     float m_run = -INFINITY, l_run = 0.f;
-    float2 o2[16];  // channels cb + 2x, cb + 2x + 1
-#pragma unroll
-    for (int x = 0; x < 16; ++x) o2[x] = make_float2(0.f, 0.f);
-    // state of the tile whose O update is pending (lags one tile)
-    float pend_al = 1.f, pend_s = 0.f, pend_m = 0.f;
-    bool pend_resc = false;
 
-    // O = alpha O + Eq. 4 (centered) on D' of tile jj (a7)
-    auto o_update = [&](int jj) {
-      const int bq = jj % NB, bd = jj & 1;
-      const uint32_t ph = (jj / NB) & 1;
-      if (pend_resc) {  // warp-uniform (lazy rescaling)
-        const float2 al2 = make_float2(pend_al, pend_al);
+#pragma unroll 1
+    for (int j = 0; j < nkt; ++j) {
+      const int bj = j % NB, t0 = j * BN;
+      const uint32_t ph = (j / NB) & 1;
+      const bool full = (t0 + BN - 1) <= i0;  // every key visible to every row of the CTA
+      ptx::mbar_wait(&sm.s_full, j & 1);
+      ptx::tc_fence_after();
+      float s[32];
 #pragma unroll
-        for (int x = 0; x < 16; ++x) o2[x] = ptx::fmul2(o2[x], al2);
+      for (int beta = 0; beta < 2; ++beta) {
+        const float2 A = beta ? qa1 : qa0, X = beta ? qx1 : qx0, M = beta ? qm1 : qm0;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {  // 16 keys per TMEM load (register pressure)
+          uint32_t d[16];
+          ptx::tmem_ld16(tS + lane_base + 64 * beta + kb + 16 * h, d);
+          ptx::tmem_wait_ld();
+#pragma unroll
+          for (int g4 = 0; g4 < 4; ++g4) {
+            const int kl = kb + 16 * h + 4 * g4;  // first of 4 keys
+            const float4 sk4 = *reinterpret_cast<const float4*>(&sm.kcf[bj][beta][0][kl]);
+            const float4 mk4 = *reinterpret_cast<const float4*>(&sm.kcf[bj][beta][1][kl]);
+            const float4 y4 = *reinterpret_cast<const float4*>(&sm.kcf[bj][beta][2][kl]);
+#pragma unroll
+            for (int pr = 0; pr < 2; ++pr) {
+              const int k2 = 4 * g4 + 2 * pr, ks = 16 * h + k2;
+              const float2 E = make_float2(u2f(d[k2]), u2f(d[k2 + 1]));
+              const float2 skp = pr ? make_float2(sk4.z, sk4.w) : make_float2(sk4.x, sk4.y);
+              const float2 mkp = pr ? make_float2(mk4.z, mk4.w) : make_float2(mk4.x, mk4.y);
+              const float2 yp = pr ? make_float2(y4.z, y4.w) : make_float2(y4.x, y4.y);
+              const float2 t = ptx::fmul2(skp, E);  // s_k 2D_s
+              float2 a = beta ? ptx::ffma2(X, mkp, make_float2(s[ks], s[ks + 1])) : ptx::fmul2(X, mkp);
+              a = ptx::ffma2(M, yp, a);
+              a = ptx::ffma2(A, t, a);
+              s[ks] = a.x;
+              s[ks + 1] = a.y;
+            }
+          }
+        }
       }
-      if (jj < nfull) {
-        int sp = 0;
+      ptx::tc_fence_before();
+      ptx::mbar_arrive(&sm.s_free);      // S columns may now be overwritten by QK(j+1)
+      ptx::mbar_arrive(&sm.k_free[bj]);  // K' tile + key coefficients may be refilled
+      bool masked = false;
+      if (!full) {
 #pragma unroll
-        for (int x = 0; x < NWG; ++x) sp += sm.sp_part[bq][x][r];
-        const int sps = sp - 128 * PI;  // sum (p' - 128)
-        const float2 ap2 = make_float2(0.5f * pend_s, 0.5f * pend_s);
-        const float2 xp2 = make_float2(pend_s * (float)sps, pend_s * (float)sps);
-        const float2 mp2 = make_float2(pend_m + 128.f * pend_s, pend_m + 128.f * pend_s);
-        ptx::mbar_wait(&sm.d_full[bd], (jj >> 1) & 1);
-        ptx::mbar_wait(&sm.v_ready[bq], ph);
+        for (int kk = 0; kk < 32; ++kk) {
+          const bool vis = (t0 + kb + kk) <= i;  // causal mask (R8)
+          masked |= !vis;
+          s[kk] = vis ? s[kk] : -INFINITY;
+        }
+      }
+      float mx = s[0], mn = s[0];
+#pragma unroll
+      for (int kk = 1; kk < 32; ++kk) {
+        mx = fmaxf(mx, s[kk]);
+        mn = fminf(mn, s[kk]);
+      }
+      if (masked) {  // min over the visible keys only
+        mn = INFINITY;
+#pragma unroll
+        for (int kk = 0; kk < 32; ++kk) mn = fminf(mn, s[kk] == -INFINITY ? INFINITY : s[kk]);
+      }
+      sm.xch[j & 1][sw][r] = make_float2(mx, masked ? -INFINITY : mn);
+      ptx::named_bar_sync(qbar, 64);
+      const float2 o = sm.xch[j & 1][sw ^ 1][r];
+      mx = fmaxf(mx, o.x);
+      const bool any_masked = masked || (o.y == -INFINITY);
+      mn = fminf(masked ? INFINITY : mn, o.y == -INFINITY ? INFINITY : o.y);
+      // lazy rescaling: move the running max only when some row of this warp outgrew it by
+      // more than kRescaleTh (identical decision in both S warps sharing these rows)
+      float al = 1.f;
+      const bool resc = __any_sync(0xffffffffu, mx > m_run + kRescaleTh);
+      if (resc) {
+        const float m_new = fmaxf(m_run, mx);
+        al = (m_run == -INFINITY) ? 0.f : ex2(m_run - m_new);
+        m_run = m_new;
+      }
+      float2 ls2 = make_float2(0.f, 0.f);
+      const float2 mneg = make_float2(-m_run, -m_run);
+#pragma unroll
+      for (int kk = 0; kk < 32; kk += 2) {
+        const float2 a2 = ptx::fadd2(make_float2(s[kk], s[kk + 1]), mneg);
+        s[kk] = ex2(a2.x);  // ex2(-inf) = +0 for masked keys
+        s[kk + 1] = ex2(a2.y);
+        ls2 = ptx::fadd2(ls2, make_float2(s[kk], s[kk + 1]));
+      }
+      l_run = l_run * al + (ls2.x + ls2.y);
+      // tile j-NB must be fully consumed by the O warps before its P / info slots are reused
+      ptx::mbar_wait(&sm.o_done[bj], ph ^ 1);
+      if (j < nfull) {
+        // (a6) P' per (row, V block): 8-bit RN on p~ (codes invariant to the row scale);
+        // y = (p - lo) / s rounded with the 1.5*2^23 magic number (y in [0, 255])
+        const float plo = any_masked ? 0.f : ex2(mn - m_run);
+        const float phi = ex2(mx - m_run);
+        QMeta pm = meta_fp32(plo, phi, 255);
+        if (!(pm.s > 1e-30f)) {
+          pm.s = 0.f;
+          pm.inv = 0.f;
+        }
+        const float2 inv2 = make_float2(pm.inv, pm.inv), nlo2 = make_float2(-plo * pm.inv, -plo * pm.inv);
+        const float2 magic = make_float2(kMagic, kMagic);
+        uint32_t sum = 0;
+#pragma unroll
+        for (int c16 = 0; c16 < 2; ++c16) {
+          uint32_t bits[16];
+#pragma unroll
+          for (int kk = 0; kk < 16; kk += 2) {
+            const float2 y =
+                ptx::fadd2(ptx::ffma2(make_float2(s[16 * c16 + kk], s[16 * c16 + kk + 1]), inv2, nlo2), magic);
+            bits[kk] = __float_as_uint(y.x);
+            bits[kk + 1] = __float_as_uint(y.y);
+          }
+          uint32_t cw[4];
+#pragma unroll
+          for (int x4 = 0; x4 < 4; ++x4) {
+            // byte position p of this 16-key chunk holds local key perm_src(p)
+            const uint32_t lo2 =
+                ptx::prmt(bits[perm_src<BITS>(4 * x4 + 0)], bits[perm_src<BITS>(4 * x4 + 1)], 0x0040u);
+            const uint32_t hi2 =
+                ptx::prmt(bits[perm_src<BITS>(4 * x4 + 2)], bits[perm_src<BITS>(4 * x4 + 3)], 0x0040u);
+            cw[x4] = ptx::prmt(lo2, hi2, 0x5410u);
+            sum = __dp4a(cw[x4], 0x01010101u, sum);
+          }
+          *reinterpret_cast<uint4*>(sm.p[bj] + kmaj_off(r, kb + 16 * c16, 512)) =
+              make_uint4(cw[0] ^ 0x80808080u, cw[1] ^ 0x80808080u, cw[2] ^ 0x80808080u, cw[3] ^ 0x80808080u);
+          if (dbg_pcodes != nullptr && i0 + r < L) {
+            uint8_t* dp = dbg_pcodes + ((int64_t)(start + i0 + r) * kc.Hq + hq) * dbg_stride + t0 + kb + 16 * c16;
+#pragma unroll
+            for (int pos = 0; pos < 16; ++pos)
+              dp[perm_src<BITS>(pos)] = (uint8_t)((cw[pos >> 2] >> (8 * (pos & 3))) & 0xFF);
+          }
+        }
+        sm.sp_part[bj][sw][r] = (int)sum;
+        if (sw == 0) sm.pinfo[bj][r] = make_float4(al, resc ? 1.f : 0.f, pm.s, pm.m);
+        ptx::fence_proxy_async_smem();
+      } else {
+#pragma unroll
+        for (int kk = 0; kk < 32; ++kk) sm.ptail[r][kb + kk] = s[kk];
+        if (sw == 0) sm.pinfo[bj][r] = make_float4(al, resc ? 1.f : 0.f, 0.f, 0.f);
+      }
+      ptx::mbar_arrive(&sm.p_ready[bj]);
+    }
+    sm.lpart[sw][r] = l_run;
+    ptx::mbar_arrive(&sm.l_ready);
+  } else {
+    // ------------------------------------------------------------------ O warpgroups (2)
+    // thread = query row r = TMEM lane; OW o owns output channels 64o..64o+63
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 128;");
+    const int ow = (warp - 12) >> 2;
+    const int r = (tid - 384) & (BM - 1);
+    const uint32_t lane_base = (uint32_t)(32 * (warp & 3)) << 16;
+    const int cb = 64 * ow;
+    float2 o2[32];  // channels cb + 2x, cb + 2x + 1
+#pragma unroll
+    for (int x = 0; x < 32; ++x) o2[x] = make_float2(0.f, 0.f);
+#pragma unroll 1
+    for (int j = 0; j < nkt; ++j) {
+      const int bj = j % NB, bd = j & 1;
+      const uint32_t ph = (j / NB) & 1;
+      ptx::mbar_wait(&sm.p_ready[bj], ph);
+      const float4 pi4 = sm.pinfo[bj][r];
+      if (pi4.y != 0.f) {  // warp-uniform (lazy rescaling decided per S warp = same 32 rows)
+        const float2 al2 = make_float2(pi4.x, pi4.x);
+#pragma unroll
+        for (int x = 0; x < 32; ++x) o2[x] = ptx::fmul2(o2[x], al2);
+      }
+      if (j < nfull) {
+        // (a7) O += (s_p/2) s_v E + s_p SP_s m_v + mu_p y_v on D' of this tile
+        const int sps = sm.sp_part[bj][0][r] + sm.sp_part[bj][1][r] - 128 * PI;  // sum (p' - 128)
+        const float2 ap2 = make_float2(0.5f * pi4.z, 0.5f * pi4.z);
+        const float2 xp2 = make_float2(pi4.z * (float)sps, pi4.z * (float)sps);
+        const float2 mp2 = make_float2(pi4.w + 128.f * pi4.z, pi4.w + 128.f * pi4.z);
+        ptx::mbar_wait(&sm.v_ready[bj], ph);
+        ptx::mbar_wait(&sm.d_full[bd], (j >> 1) & 1);
         ptx::tc_fence_after();
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
+        for (int h = 0; h < 4; ++h) {
           uint32_t d[16];
-          const uint32_t ta = tD0 + 128 * bd + lane_base + cb + 16 * h;
-          ptx::tmem_ld16(ta, d);
+          ptx::tmem_ld16(tD0 + 128 * bd + lane_base + cb + 16 * h, d);
           ptx::tmem_wait_ld();
 #pragma unroll
           for (int x4 = 0; x4 < 4; ++x4) {
             const int c0 = cb + 16 * h + 4 * x4;
-            const float4 sv4 = *reinterpret_cast<const float4*>(&sm.vcf[bq][0][c0]);
-            const float4 mv4 = *reinterpret_cast<const float4*>(&sm.vcf[bq][1][c0]);
-            const float4 y4 = *reinterpret_cast<const float4*>(&sm.vcf[bq][2][c0]);
+            const float4 sv4 = *reinterpret_cast<const float4*>(&sm.vcf[bj][0][c0]);
+            const float4 mv4 = *reinterpret_cast<const float4*>(&sm.vcf[bj][1][c0]);
+            const float4 y4 = *reinterpret_cast<const float4*>(&sm.vcf[bj][2][c0]);
 #pragma unroll
             for (int pr = 0; pr < 2; ++pr) {
               const int xo = 4 * x4 + 2 * pr;
@@ -384,9 +537,9 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_tc_kernel(
               const float2 mvp = pr ? make_float2(mv4.z, mv4.w) : make_float2(mv4.x, mv4.y);
               const float2 yp = pr ? make_float2(y4.z, y4.w) : make_float2(y4.x, y4.y);
               const float2 t = ptx::fmul2(svp, E);  // s_v 2D_s
-              float2 o = ptx::ffma2(ap2, t, o2[oi]);
-              o = ptx::ffma2(xp2, mvp, o);
-              o2[oi] = ptx::ffma2(mp2, yp, o);
+              float2 a = ptx::ffma2(ap2, t, o2[oi]);
+              a = ptx::ffma2(xp2, mvp, a);
+              o2[oi] = ptx::ffma2(mp2, yp, a);
             }
           }
         }
@@ -402,7 +555,7 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_tc_kernel(
           const float pt = sm.ptail[r][t];
           const uint4* vr = reinterpret_cast<const uint4*>(tail + t * 128);
 #pragma unroll
-          for (int c8 = 0; c8 < 4; ++c8) {
+          for (int c8 = 0; c8 < 8; ++c8) {
             const uint4 raw = vr[c8];
             const __half2* h2 = reinterpret_cast<const __half2*>(&raw);
 #pragma unroll
@@ -411,174 +564,22 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_tc_kernel(
           }
         }
       }
-      ptx::mbar_arrive(&sm.v_free[bq]);
-    };
-
-#pragma unroll 1
-    for (int j = 0; j < nkt; ++j) {
-      const int bj = j % NB, t0 = j * BN;
-      const uint32_t ph = (j / NB) & 1;
-      const bool full = (t0 + BN - 1) <= i0;  // every key visible to every row of the CTA
-      ptx::mbar_wait(&sm.s_full, j & 1);
-      ptx::tc_fence_after();
-      float s[16];
-#pragma unroll
-      for (int beta = 0; beta < 2; ++beta) {  // one d-block at a time (register pressure)
-        uint32_t d[16];
-        const uint32_t ta = tS + lane_base + 64 * beta + kb;
-        ptx::tmem_ld16(ta, d);
-        ptx::tmem_wait_ld();
-        const float2 A = beta ? qa1 : qa0, X = beta ? qx1 : qx0, M = beta ? qm1 : qm0;
-#pragma unroll
-        for (int g4 = 0; g4 < 4; ++g4) {
-          const int kl = kb + 4 * g4;  // first of 4 keys
-          const float4 sk4 = *reinterpret_cast<const float4*>(&sm.kcf[bj][beta][0][kl]);
-          const float4 mk4 = *reinterpret_cast<const float4*>(&sm.kcf[bj][beta][1][kl]);
-          const float4 y4 = *reinterpret_cast<const float4*>(&sm.kcf[bj][beta][2][kl]);
-#pragma unroll
-          for (int pr = 0; pr < 2; ++pr) {
-            const int k2 = 4 * g4 + 2 * pr;
-            const float2 E = make_float2(u2f(d[k2]), u2f(d[k2 + 1]));
-            const float2 skp = pr ? make_float2(sk4.z, sk4.w) : make_float2(sk4.x, sk4.y);
-            const float2 mkp = pr ? make_float2(mk4.z, mk4.w) : make_float2(mk4.x, mk4.y);
-            const float2 yp = pr ? make_float2(y4.z, y4.w) : make_float2(y4.x, y4.y);
-            const float2 t = ptx::fmul2(skp, E);  // s_k 2D_s
-            float2 a = beta ? ptx::ffma2(X, mkp, make_float2(s[k2], s[k2 + 1])) : ptx::fmul2(X, mkp);
-            a = ptx::ffma2(M, yp, a);
-            a = ptx::ffma2(A, t, a);
-            s[k2] = a.x;
-            s[k2 + 1] = a.y;
-          }
-        }
-      }
-      ptx::tc_fence_before();
-      ptx::mbar_arrive(&sm.s_free);      // S columns may now be overwritten by QK(j+1)
-      ptx::mbar_arrive(&sm.k_free[bj]);  // K' tile + key coefficients may be refilled
-      bool masked = false;
-      if (!full) {
-#pragma unroll
-        for (int kk = 0; kk < 16; ++kk) {
-          const bool vis = (t0 + kb + kk) <= i;  // causal mask (R8)
-          masked |= !vis;
-          s[kk] = vis ? s[kk] : -INFINITY;
-        }
-      }
-      float mx = s[0], mn = s[0];
-#pragma unroll
-      for (int kk = 1; kk < 16; ++kk) {
-        mx = fmaxf(mx, s[kk]);
-        mn = fminf(mn, s[kk]);
-      }
-      if (masked) {  // min over the visible keys only
-        mn = INFINITY;
-#pragma unroll
-        for (int kk = 0; kk < 16; ++kk) mn = fminf(mn, s[kk] == -INFINITY ? INFINITY : s[kk]);
-      }
-      sm.xch[j & 1][w][r] = make_float2(mx, masked ? -INFINITY : mn);
-      ptx::named_bar_sync(qbar, 128);
-      bool any_masked = false;
-      mn = INFINITY;
-      mx = -INFINITY;
-#pragma unroll
-      for (int x = 0; x < NWG; ++x) {
-        const float2 o = sm.xch[j & 1][x][r];
-        mx = fmaxf(mx, o.x);
-        any_masked |= (o.y == -INFINITY);
-        mn = fminf(mn, o.y == -INFINITY ? INFINITY : o.y);
-      }
-      // lazy rescaling: move the running max only when some row of this warp outgrew it by
-      // more than kRescaleTh (identical decision in the 4 warps sharing these rows)
-      float al = 1.f;
-      const bool resc = __any_sync(0xffffffffu, mx > m_run + kRescaleTh);
-      if (resc) {
-        const float m_new = fmaxf(m_run, mx);
-        al = (m_run == -INFINITY) ? 0.f : ex2(m_run - m_new);
-        m_run = m_new;
-      }
-      float2 ls2 = make_float2(0.f, 0.f);
-      const float2 mneg = make_float2(-m_run, -m_run);
-#pragma unroll
-      for (int kk = 0; kk < 16; kk += 2) {
-        const float2 a2 = ptx::fadd2(make_float2(s[kk], s[kk + 1]), mneg);
-        s[kk] = ex2(a2.x);  // ex2(-inf) = +0 for masked keys
-        s[kk + 1] = ex2(a2.y);
-        ls2 = ptx::fadd2(ls2, make_float2(s[kk], s[kk + 1]));
-      }
-      l_run = l_run * al + (ls2.x + ls2.y);
-      float pm_s = 0.f, pm_m = 0.f;
-      if (j < nfull) {
-        // (a6) P' per (row, V block): 8-bit RN on p~ (codes invariant to the row scale);
-        // y = (p - lo) / s rounded with the 1.5*2^23 magic number (y in [0, 255])
-        const float plo = any_masked ? 0.f : ex2(mn - m_run);
-        const float phi = ex2(mx - m_run);
-        QMeta pm = meta_fp32(plo, phi, 255);
-        if (!(pm.s > 1e-30f)) {
-          pm.s = 0.f;
-          pm.inv = 0.f;
-        }
-        pm_s = pm.s;
-        pm_m = pm.m;
-        const float2 inv2 = make_float2(pm.inv, pm.inv), nlo2 = make_float2(-plo * pm.inv, -plo * pm.inv);
-        const float2 magic = make_float2(kMagic, kMagic);
-        uint32_t bits[16];
-#pragma unroll
-        for (int kk = 0; kk < 16; kk += 2) {
-          const float2 y = ptx::fadd2(ptx::ffma2(make_float2(s[kk], s[kk + 1]), inv2, nlo2), magic);
-          bits[kk] = __float_as_uint(y.x);
-          bits[kk + 1] = __float_as_uint(y.y);
-        }
-        uint32_t cw[4];
-        uint32_t sum = 0;
-#pragma unroll
-        for (int x4 = 0; x4 < 4; ++x4) {
-          // byte position p of this 16-key chunk holds local key perm_src(p)
-          const uint32_t lo2 = ptx::prmt(bits[perm_src<BITS>(4 * x4 + 0)], bits[perm_src<BITS>(4 * x4 + 1)], 0x0040u);
-          const uint32_t hi2 = ptx::prmt(bits[perm_src<BITS>(4 * x4 + 2)], bits[perm_src<BITS>(4 * x4 + 3)], 0x0040u);
-          cw[x4] = ptx::prmt(lo2, hi2, 0x5410u);
-          sum = __dp4a(cw[x4], 0x01010101u, sum);
-        }
-        ptx::mbar_wait(&sm.p_free[bj], ph ^ 1);
-        *reinterpret_cast<uint4*>(sm.p[bj] + kmaj_off(r, kb, 512)) =
-            make_uint4(cw[0] ^ 0x80808080u, cw[1] ^ 0x80808080u, cw[2] ^ 0x80808080u, cw[3] ^ 0x80808080u);
-        if (dbg_pcodes != nullptr && i0 + r < L) {
-          uint8_t* dp = dbg_pcodes + ((int64_t)(start + i0 + r) * kc.Hq + hq) * dbg_stride + t0 + kb;
-#pragma unroll
-          for (int pos = 0; pos < 16; ++pos)
-            dp[perm_src<BITS>(pos)] = (uint8_t)((cw[pos >> 2] >> (8 * (pos & 3))) & 0xFF);
-        }
-        sm.sp_part[bj][w][r] = (int)sum;
-        ptx::fence_proxy_async_smem();
-      } else {
-#pragma unroll
-        for (int kk = 0; kk < 16; ++kk) sm.ptail[r][kb + kk] = s[kk];
-      }
-      ptx::mbar_arrive(&sm.p_ready[bj]);
-      if (j >= 1) o_update(j - 1);  // overlaps the PV MMA of tile j with S of tile j+1
-      pend_al = al;
-      pend_resc = resc;
-      pend_s = pm_s;
-      pend_m = pm_m;
+      ptx::mbar_arrive(&sm.o_done[bj]);
     }
-    ptx::named_bar_sync(qbar, 128);  // sp_part / ptail of the last tile complete
-    o_update(nkt - 1);
-    sm.lpart[w][r] = l_run;
-    ptx::named_bar_sync(qbar, 128);
+    ptx::mbar_wait(&sm.l_ready, 0);
     if (i0 + r < L) {
-      float l = 0.f;
-#pragma unroll
-      for (int x = 0; x < NWG; ++x) l += sm.lpart[x][r];
-      const float inv_l = 1.f / l;
+      const float inv_l = 1.f / (sm.lpart[0][r] + sm.lpart[1][r]);
       const int64_t base = ((int64_t)(start + i0 + r) * kc.Hq + hq) * 128 + cb;
       if (kc.out_fp32) {
         float4* op = reinterpret_cast<float4*>(reinterpret_cast<float*>(out) + base);
 #pragma unroll
-        for (int c4 = 0; c4 < 8; ++c4)
+        for (int c4 = 0; c4 < 16; ++c4)
           op[c4] = make_float4(o2[2 * c4].x * inv_l, o2[2 * c4].y * inv_l, o2[2 * c4 + 1].x * inv_l,
                                o2[2 * c4 + 1].y * inv_l);
       } else {
         uint4* op = reinterpret_cast<uint4*>(reinterpret_cast<__half*>(out) + base);
 #pragma unroll
-        for (int c8 = 0; c8 < 4; ++c8) {
+        for (int c8 = 0; c8 < 8; ++c8) {
           __half2 hh[4];
 #pragma unroll
           for (int e = 0; e < 4; ++e) hh[e] = __floats2half2_rn(o2[4 * c8 + e].x * inv_l, o2[4 * c8 + e].y * inv_l);
