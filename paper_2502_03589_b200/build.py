@@ -58,7 +58,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
         o = os.path.join(BUILD, os.path.basename(s) + ".o")
         objs.append(o)
         if force or _newer([s] + headers, o):
-            cmd = [NVCC, *ARCH, *CFLAGS, "-I", inc, "-I", os.path.join(ROOT, "include"), "-c", s, "-o", o]
+            extra = os.environ.get("HACK_EXTRA_NVCC_FLAGS", "").split()  # experiments only
+            cmd = [NVCC, *ARCH, *CFLAGS, *extra, "-I", inc, "-I", os.path.join(ROOT, "include"), "-c", s, "-o", o]
             jobs.append((s, cmd))
 
     def run(job):

@@ -178,6 +178,19 @@ HACK_DEV constexpr uint32_t idesc_s8u8(int M, int N) { return idesc_u8(M, N) | (
 // u8 A (unsigned codes) x s8 B (code - 128).
 HACK_DEV constexpr uint32_t idesc_u8s8(int M, int N) { return idesc_u8(M, N) | (1u << 10); }
 
+// kind::f16 with bf16 A/B and an f32 accumulator (used to pre-set accumulators to a
+// constant: the f32 bits it writes are then accumulated onto by kind::i8 MMAs).
+HACK_DEV constexpr uint32_t idesc_bf16(int M, int N) {
+  return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
+HACK_DEV void mma_bf16(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+
 // D[tmem] (+)= A[smem] . B[smem]^T, issued by ONE thread.
 HACK_DEV void mma_u8(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc, uint32_t accumulate) {
   asm volatile(

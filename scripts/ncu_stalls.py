@@ -37,3 +37,15 @@ for n, r in enumerate(data):
     if any(m in r[isrc] for m in marks):
         print(f"{n:5d} {r[isrc][:58]:58s} seg={acc - last:6d} cum={acc}")
         last = acc
+
+# per-region stall reasons: pass regions as a:b pairs after the report path
+reasons = [c for c in h if c.startswith("stall_") and "Not Issued" not in c]
+for spec in sys.argv[2:]:
+    a, b = (int(x) for x in spec.split(":"))
+    tot = {c: sum(int(data[n][h.index(c)] or 0) for n in range(a, b)) for c in reasons}
+    s = sum(tot.values())
+    print(f"region {a}:{b} samples={s}: " + ", ".join(f"{k[6:]}={v}" for k, v in sorted(tot.items(), key=lambda t: -t[1]) if v))
+    worst = sorted(range(a, b), key=lambda n: -int(data[n][iss]))[:12]
+    for n in sorted(worst):
+        top = max(reasons, key=lambda c: int(data[n][h.index(c)] or 0))
+        print(f"   {n:5d} {data[n][isrc][:60]:60s} {data[n][iss]:>6s} ({top[6:]})")
