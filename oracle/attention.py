@@ -282,16 +282,24 @@ def decode_step(state: KVState, q_new: np.ndarray, k_new: np.ndarray, v_new: np.
     k_new (own partitions), append v_new to the FP16 tail and flush at
     Pi, then attend with L_Q = 1 over every cached token.
     q_new [Hq, d], k_new/v_new [Hkv, d] fp16.  Returns O [Hq, d] fp64."""
-    cfg = state.cfg
     state.append_k(k_new[None])
     state.append_v(v_new)
+    return decode_attend(state, q_new, keep_diag=keep_diag)
+
+
+def decode_attend(state: KVState, q_new: np.ndarray, pcodes_override=None, keep_diag=False):
+    """The attention half of decode_step: q_new (position length-1) over every cached
+    token of the state as it stands.  `pcodes_override` {hq: [1, committed]} replaces
+    the P codes (near-tie protocol)."""
+    cfg = state.cfg
     pos = state.length - 1
     st = state.arrays()
     qc, qm, qs, qsum = quantize_q(cfg, q_new[None], np.array([pos]), state.rng_id)
     O = np.zeros((cfg.Hq, cfg.d))
     diag = {}
     for hq in range(cfg.Hq):
-        o, dg = _attend(cfg, st, qc[:, hq], qm[:, hq], qs[:, hq], qsum[:, hq], [pos], hq)
+        ov = None if pcodes_override is None else pcodes_override.get(hq)
+        o, dg = _attend(cfg, st, qc[:, hq], qm[:, hq], qs[:, hq], qsum[:, hq], [pos], hq, ov)
         O[hq] = o[0]
         if keep_diag:
             diag[hq] = dg

@@ -1,9 +1,10 @@
 // dispatch.cu -- chooses the attention kernel for a launch.
 //
 // Prefill: the tcgen05 kernel (prefill_tc.cu) for Pi = 64, else the CUDA-core kernel
-// (prefill_simt.cu).  Decode: the split-KV mma.sync kernel (decode_mma.cu) for Pi = 64,
-// G <= 8, else decode_simt.cu.  HACK_PREFILL_IMPL / HACK_DECODE_IMPL = "simt" force the
-// baseline kernels (parity cross-checks).  csrc/experimental/decode_tc.cu (a tcgen05
+// (prefill_simt.cu).  Decode: the paired-page mma.sync kernel (decode_pair.cu) for b = 2,
+// Pi = 64, G <= 4; the general split-KV mma.sync kernel (decode_mma.cu) for Pi = 64,
+// G <= 8; else decode_simt.cu.  HACK_PREFILL_IMPL / HACK_DECODE_IMPL = "simt" force the
+// baseline kernels (parity cross-checks); HACK_DECODE_IMPL = "mma" skips the paired kernel.  csrc/experimental/decode_tc.cu (a tcgen05
 // decode with K/V operands unpacked into TMEM) is not built: it was slower than the
 // mma.sync kernel and hangs in some configurations (round-2 work).
 #include <cstdlib>
@@ -29,7 +30,14 @@ cudaError_t launch_decode_mma(const KernelCfg& kc, const void* q_new, const int3
                               int max_seqlen, const CacheView& cv, void* out, void* workspace,
                               const hack_debug_t* dbg, cudaStream_t st);
 
+bool decode_pair_supported(const KernelCfg& kc);
+size_t decode_pair_workspace(const KernelCfg& kc, int batch, int max_seqlen);
+cudaError_t launch_decode_pair(const KernelCfg& kc, const void* q_new, const int32_t* slots, int batch,
+                               int max_seqlen, const CacheView& cv, void* out, void* workspace,
+                               const hack_debug_t* dbg, cudaStream_t st);
+
 static bool use_decode_mma(const KernelCfg& kc);
+static bool use_decode_pair(const KernelCfg& kc);
 
 
 static bool env_is(const char* name, const char* val) {
@@ -55,13 +63,20 @@ static bool use_decode_mma(const KernelCfg& kc) {
   return decode_mma_supported(kc) && !env_is("HACK_DECODE_IMPL", "simt");
 }
 
+static bool use_decode_pair(const KernelCfg& kc) {
+  return decode_pair_supported(kc) && !env_is("HACK_DECODE_IMPL", "simt") && !env_is("HACK_DECODE_IMPL", "mma");
+}
+
 size_t decode_workspace_bytes(const KernelCfg& kc, int batch, int max_seqlen) {
+  if (use_decode_pair(kc)) return decode_pair_workspace(kc, batch, max_seqlen);
   return use_decode_mma(kc) ? decode_mma_workspace(kc, batch, max_seqlen) : 0;
 }
 
 cudaError_t launch_decode_attention(const KernelCfg& kc, const void* q_new, const int32_t* slots, int batch,
                                     int max_seqlen, const CacheView& cv, void* out, void* workspace,
                                     const hack_debug_t* dbg, cudaStream_t st) {
+  if (use_decode_pair(kc))
+    return launch_decode_pair(kc, q_new, slots, batch, max_seqlen, cv, out, workspace, dbg, st);
   if (use_decode_mma(kc))
     return launch_decode_mma(kc, q_new, slots, batch, max_seqlen, cv, out, workspace, dbg, st);
   return launch_decode_simt(kc, q_new, slots, batch, cv, out, dbg, st);
