@@ -13,7 +13,7 @@ print('ns', os.environ.get('HACK_DECODE_NSPLIT'), 'prefill', round(d['value'],1)
 PY
 done
 if [ "${NCU:-0}" = 1 ]; then
-timeout 600 /usr/local/cuda/bin/ncu --set full --clock-control none --import-source on -k regex:decode_pair -s 3 -c 1 \
+timeout 600 /usr/local/cuda/bin/ncu --set full --clock-control none --import-source on -k regex:${KREGEX:-decode_pair_kernel} -s 3 -c 1 \
   -o gpurun_out/dec_pair -f python bench.py --steps 1 --warmup 3 --no-cpu-baseline > gpurun_out/dec_ncu.log 2>&1
 tail -1 gpurun_out/dec_ncu.log
 fi
