@@ -37,10 +37,19 @@ namespace hack {
 namespace {
 
 constexpr int PI = 64;
-constexpr int NW = 4;       // compute warps per CTA
-constexpr int NSTG = 12;    // page slots per CTA
+#ifndef HACK_DEC_NW
+#define HACK_DEC_NW 4
+#endif
+#ifndef HACK_DEC_NSTG
+#define HACK_DEC_NSTG 12
+#endif
+#ifndef HACK_DEC_CTAS
+#define HACK_DEC_CTAS 3
+#endif
+constexpr int NW = HACK_DEC_NW;        // compute warps per CTA
+constexpr int NSTG = HACK_DEC_NSTG;    // page slots per CTA
 constexpr int kThreads = (NW + 1) * 32;
-constexpr int kCtasPerSm = 3;
+constexpr int kCtasPerSm = HACK_DEC_CTAS;
 constexpr int PB = 5376;    // page bytes at d = 128, Pi = 64, b = 2
 constexpr int kPart = 130;  // floats per partial row: m, l, O[128]
 constexpr uint32_t kMagic = 0x4B400000u;   // bits of 1.5 * 2^23

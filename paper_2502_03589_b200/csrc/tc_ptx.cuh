@@ -45,6 +45,10 @@ HACK_DEV bool mbar_try_wait_sleep(uint64_t* bar, uint32_t parity) {
       : "memory");
   return ok != 0;
 }
+HACK_DEV void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
+  while (!mbar_try_wait_sleep(bar, parity)) {
+  }
+}
 HACK_DEV void mbar_wait(uint64_t* bar, uint32_t parity) {
 #ifdef HACK_WAIT_SLEEP
   while (!mbar_try_wait_sleep(bar, parity)) {
