@@ -58,6 +58,9 @@ struct TcSmem {
   alignas(128) uint8_t k[NB][BN * 128];   // K' (u8), K-major, SBO 1024
   alignas(128) uint8_t v[NB][128 * BN];   // V' (u8), K-major (keys = K), SBO 512
   alignas(128) uint8_t p[NB][BM * BN];    // P' - 128 (s8), K-major, SBO 512
+  alignas(128) float ar[BM * 24];         // rank-term A operand (tf32, K-major, SBO 768): per row, per beta
+                                          //   X and M split 3 ways (kRankA)
+  alignas(128) float br[NB][BN * 24];     // rank-term B operand per key: m_k and y_k split 3 ways (kRankB)
   alignas(16) float kcf[NB][2][3][BN];    // [buf][beta][field][key]: s_k, m_k, y_k
   alignas(16) float vcf[NB][3][128];      // [buf][field][channel]: s_v, m_v, y_v
   float4 qconst[2][BM];                   // per (beta, row): cs s_q / 2, cs s_q SQ_s, cs mu_q
@@ -72,6 +75,26 @@ struct TcSmem {
 };
 
 HACK_DEV float u2f(uint32_t x) { return __int2float_rn((int)x); }
+
+// Exact 3-way tf32 split x = h + m + l (11 + 11 + <= 2 significant bits); a product x y is
+// then hh' + hm' + mh' + hl' + lh' + mm' up to ~2^-33 relative (the dropped ml', lm', ll').
+// A-side (row constant) and B-side (key coefficient) orders pair up those six terms.
+HACK_DEV void split3(float x, float& h, float& m, float& l) {
+  h = ptx::tf32_hi(x);
+  const float r = x - h;
+  m = ptx::tf32_hi(r);
+  l = r - m;
+}
+HACK_DEV void rank_a(float x, float* v) {
+  float h, m, l;
+  split3(x, h, m, l);
+  v[0] = h; v[1] = h; v[2] = m; v[3] = h; v[4] = l; v[5] = m;
+}
+HACK_DEV void rank_b(float y, float* v) {
+  float h, m, l;
+  split3(y, h, m, l);
+  v[0] = h; v[1] = m; v[2] = h; v[3] = l; v[4] = h; v[5] = m;
+}
 
 template <int BITS>
 __global__ void __launch_bounds__(kThreads, 1) prefill_tc_kernel(
@@ -129,6 +152,7 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_tc_kernel(
   const uint32_t tmem = sm.tmem_base;
   const uint32_t tS = tmem;         // columns 0..127: D_0 | D_1
   const uint32_t tD0 = tmem + 128;  // D'[0] columns 128..255, D'[1] 256..383
+  const uint32_t tR = tmem + 384;   // rank terms of S (64 columns): sum_beta X m_k + M y_k (3xTF32 MMA)
 
   if (warp < 4) {
     // register budget (launch: 96 x 640): service 40, S 88, O 128 -> 9216 freed >= 8192 taken
@@ -166,6 +190,14 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_tc_kernel(
                 ptx::mma_u8(tS + 64 * beta, ptx::smem_desc_kmajor(qa + koff, 128, 1024),
                             ptx::smem_desc_kmajor(ka + koff, 128, 1024), idesc_qk, ks > 0);
               }
+            // rank-2-per-block terms of Eq. 4 on the tensor pipe: R = [X | M] [m_k ; y_k]
+            // with both sides split 3 ways (exact tf32 parts, fp32-level product), so the S
+            // epilogue keeps one FMUL2 + FFMA2 per key pair and block
+            const uint32_t ra = ptx::smem_u32(sm.ar), rb = ptx::smem_u32(sm.br[bq]);
+#pragma unroll
+            for (int ks = 0; ks < 3; ++ks)
+              ptx::mma_tf32(tR, ptx::smem_desc_kmajor(ra + ks * 256, 128, 768),
+                            ptx::smem_desc_kmajor(rb + ks * 256, 128, 768), ptx::idesc_tf32(BM, BN), ks > 0);
             ptx::mma_commit(&sm.s_full);
           }
           __syncwarp();
@@ -231,8 +263,14 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_tc_kernel(
             c2 = fmaf(s2, (float)sum, PI * m);  // y_k = s_k SK + Pi m_k
           }
           sm.kcf[bj][beta][0][key] = c0;
-          sm.kcf[bj][beta][1][key] = c1;
-          sm.kcf[bj][beta][2][key] = c2;
+          float rv[12];
+          rank_b(c1, rv);
+          rank_b(c2, rv + 6);
+          uint8_t* brk = reinterpret_cast<uint8_t*>(sm.br[bj]);
+#pragma unroll
+          for (int x = 0; x < 12; x += 4)
+            *reinterpret_cast<float4*>(brk + kmaj_off(key, 4 * (12 * beta + x), 768)) =
+                make_float4(rv[x], rv[x + 1], rv[x + 2], rv[x + 3]);
         }
         ptx::fence_proxy_async_smem();
         ptx::mbar_arrive(&sm.k_ready[bj]);
@@ -338,13 +376,23 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_tc_kernel(
       const int sqs = sum - 128 * PI;  // sum (q' - 128)
       sm.qconst[sw][r] =
           make_float4(cscale * qm.s * 0.5f, cscale * qm.s * (float)sqs, cscale * (qm.m + 128.f * qm.s), 0.f);
+      {
+        const float X = cscale * qm.s * (float)sqs, M = cscale * (qm.m + 128.f * qm.s);
+        float av[12];
+        rank_a(X, av);
+        rank_a(M, av + 6);
+        uint8_t* arr = reinterpret_cast<uint8_t*>(sm.ar);
+#pragma unroll
+        for (int x = 0; x < 12; x += 4)
+          *reinterpret_cast<float4*>(arr + kmaj_off(r, 4 * (12 * sw + x), 768)) =
+              make_float4(av[x], av[x + 1], av[x + 2], av[x + 3]);
+      }
       ptx::fence_proxy_async_smem();
       ptx::mbar_arrive(&sm.q_ready);
     }
     ptx::named_bar_sync(qbar, 64);  // both halves of the Q row constants visible
     const float4 qc0 = sm.qconst[0][r], qc1 = sm.qconst[1][r];
-    const float2 qa0 = make_float2(qc0.x, qc0.x), qx0 = make_float2(qc0.y, qc0.y), qm0 = make_float2(qc0.z, qc0.z);
-    const float2 qa1 = make_float2(qc1.x, qc1.x), qx1 = make_float2(qc1.y, qc1.y), qm1 = make_float2(qc1.z, qc1.z);
+    const float2 qa0 = make_float2(qc0.x, qc0.x), qa1 = make_float2(qc1.x, qc1.x);
     float m_run = -INFINITY, l_run = 0.f;
 
 #pragma unroll 1
@@ -356,8 +404,16 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_tc_kernel(
       ptx::tc_fence_after();
       float s[32];
 #pragma unroll
+      for (int h = 0; h < 2; ++h) {  // rank terms (tensor pipe) seed the accumulation
+        uint32_t d[16];
+        ptx::tmem_ld16(tR + lane_base + kb + 16 * h, d);
+        ptx::tmem_wait_ld();
+#pragma unroll
+        for (int x = 0; x < 16; ++x) s[16 * h + x] = __uint_as_float(d[x]);
+      }
+#pragma unroll
       for (int beta = 0; beta < 2; ++beta) {
-        const float2 A = beta ? qa1 : qa0, X = beta ? qx1 : qx0, M = beta ? qm1 : qm0;
+        const float2 A = beta ? qa1 : qa0;
 #pragma unroll
         for (int h = 0; h < 2; ++h) {  // 16 keys per TMEM load (register pressure)
           uint32_t d[16];
@@ -367,19 +423,13 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_tc_kernel(
           for (int g4 = 0; g4 < 4; ++g4) {
             const int kl = kb + 16 * h + 4 * g4;  // first of 4 keys
             const float4 sk4 = *reinterpret_cast<const float4*>(&sm.kcf[bj][beta][0][kl]);
-            const float4 mk4 = *reinterpret_cast<const float4*>(&sm.kcf[bj][beta][1][kl]);
-            const float4 y4 = *reinterpret_cast<const float4*>(&sm.kcf[bj][beta][2][kl]);
 #pragma unroll
             for (int pr = 0; pr < 2; ++pr) {
               const int k2 = 4 * g4 + 2 * pr, ks = 16 * h + k2;
               const float2 E = make_float2(u2f(d[k2]), u2f(d[k2 + 1]));
               const float2 skp = pr ? make_float2(sk4.z, sk4.w) : make_float2(sk4.x, sk4.y);
-              const float2 mkp = pr ? make_float2(mk4.z, mk4.w) : make_float2(mk4.x, mk4.y);
-              const float2 yp = pr ? make_float2(y4.z, y4.w) : make_float2(y4.x, y4.y);
               const float2 t = ptx::fmul2(skp, E);  // s_k 2D_s
-              float2 a = beta ? ptx::ffma2(X, mkp, make_float2(s[ks], s[ks + 1])) : ptx::fmul2(X, mkp);
-              a = ptx::ffma2(M, yp, a);
-              a = ptx::ffma2(A, t, a);
+              const float2 a = ptx::ffma2(A, t, make_float2(s[ks], s[ks + 1]));
               s[ks] = a.x;
               s[ks + 1] = a.y;
             }
