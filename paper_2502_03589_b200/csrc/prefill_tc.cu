@@ -61,6 +61,8 @@ struct TcSmem {
   alignas(128) float ar[BM * 24];         // rank-term A operand (tf32, K-major, SBO 768): per row, per beta
                                           //   X and M split 3 ways (kRankA)
   alignas(128) float br[NB][BN * 24];     // rank-term B operand per key: m_k and y_k split 3 ways (kRankB)
+  alignas(128) uint16_t pre_a[128 * 16];  // bf16 preset operands: A[:, 0] = 1, B[:, 0] = 1.5 * 2^23 (K-major,
+  alignas(128) uint16_t pre_b[128 * 16];  //   SBO 256): one kind::f16 MMA writes the magic into D
   alignas(16) float kcf[NB][2][3][BN];    // [buf][beta][field][key]: s_k, m_k, y_k
   alignas(16) float vcf[NB][3][128];      // [buf][field][channel]: s_v, m_v, y_v
   float4 qconst[2][BM];                   // per (beta, row): cs s_q / 2, cs s_q SQ_s, cs mu_q
@@ -74,7 +76,12 @@ struct TcSmem {
   uint32_t tmem_base;
 };
 
-HACK_DEV float u2f(uint32_t x) { return __int2float_rn((int)x); }
+// Integer accumulators are preset to the fp32 bits of 1.5*2^23 by one bf16 MMA (A = e_0,
+// B = 1.5*2^23 e_0) before the kind::i8 MMAs accumulate onto them, so the float view of an
+// accumulated integer E (|E| < 2^22) is 1.5*2^23 + E and one FADD2 converts two exactly.
+HACK_DEV float2 acc2f(uint32_t a, uint32_t b) {
+  return ptx::fadd2(make_float2(__uint_as_float(a), __uint_as_float(b)), make_float2(-kMagic, -kMagic));
+}
 
 // Exact 3-way tf32 split x = h + m + l (11 + 11 + <= 2 significant bits); a product x y is
 // then hh' + hm' + mh' + hl' + lh' + mm' up to ~2^-33 relative (the dropped ml', lm', ll').
@@ -173,6 +180,9 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_tc_kernel(
       // ---------------------------------------------------------------- MMA issuer
       const uint32_t idesc_qk = ptx::idesc_s8u8(BM, BN), idesc_pv = ptx::idesc_s8u8(BM, 128);
       const uint32_t qa = ptx::smem_u32(sm.q);
+      const uint64_t pre_a = ptx::smem_desc_kmajor(ptx::smem_u32(sm.pre_a), 128, 256);
+      const uint64_t pre_b = ptx::smem_desc_kmajor(ptx::smem_u32(sm.pre_b), 128, 256);
+      const uint32_t idesc_pre = ptx::idesc_bf16(BM, 128);
       ptx::mbar_wait(&sm.q_ready, 0);
       for (int j = 0; j <= nkt; ++j) {
         if (j < nkt) {
@@ -182,13 +192,14 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_tc_kernel(
           ptx::tc_fence_after();
           if (lane == 0) {
             const uint32_t ka = ptx::smem_u32(sm.k[bq]);
+            ptx::mma_bf16(tS, pre_a, pre_b, idesc_pre, 0u);  // D_0 | D_1 := 1.5 * 2^23
 #pragma unroll
             for (int beta = 0; beta < 2; ++beta)
 #pragma unroll
               for (int ks = 0; ks < PI / 32; ++ks) {
                 const uint32_t koff = (uint32_t)(beta * 4 + ks * 2) * 128;  // 16-byte K chunks
                 ptx::mma_u8(tS + 64 * beta, ptx::smem_desc_kmajor(qa + koff, 128, 1024),
-                            ptx::smem_desc_kmajor(ka + koff, 128, 1024), idesc_qk, ks > 0);
+                            ptx::smem_desc_kmajor(ka + koff, 128, 1024), idesc_qk, 1u);
               }
             // rank-2-per-block terms of Eq. 4 on the tensor pipe: R = [X | M] [m_k ; y_k]
             // with both sides split 3 ways (exact tf32 parts, fp32-level product), so the S
@@ -212,10 +223,11 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_tc_kernel(
           ptx::tc_fence_after();
           if (lane == 0) {
             const uint32_t pa = ptx::smem_u32(sm.p[bq]), va = ptx::smem_u32(sm.v[bq]);
+            ptx::mma_bf16(tD0 + 128 * bd, pre_a, pre_b, idesc_pre, 0u);  // D' := 1.5 * 2^23
 #pragma unroll
             for (int ks = 0; ks < BN / 32; ++ks)
               ptx::mma_u8(tD0 + 128 * bd, ptx::smem_desc_kmajor(pa + ks * 256, 128, 512),
-                          ptx::smem_desc_kmajor(va + ks * 256, 128, 512), idesc_pv, ks > 0);
+                          ptx::smem_desc_kmajor(va + ks * 256, 128, 512), idesc_pv, 1u);
             ptx::mma_commit(&sm.d_full[bd]);
             ptx::mma_commit(&sm.p_free[bq]);
           }
@@ -225,6 +237,17 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_tc_kernel(
     } else {
       // ---------------------------------------------------------------- unpack (64 threads)
       const int ut = tid - 64;
+      // bf16 preset operands (visible to the MMA through the proxy fence before k_ready)
+#pragma unroll
+      for (int rr = 0; rr < 2; ++rr) {
+        const int row = ut + 64 * rr;
+        *reinterpret_cast<uint4*>(reinterpret_cast<uint8_t*>(sm.pre_a) + kmaj_off(row, 0, 256)) =
+            make_uint4(0x3F80u, 0u, 0u, 0u);  // bf16 1.0 at k = 0
+        *reinterpret_cast<uint4*>(reinterpret_cast<uint8_t*>(sm.pre_a) + kmaj_off(row, 16, 256)) = make_uint4(0u, 0u, 0u, 0u);
+        *reinterpret_cast<uint4*>(reinterpret_cast<uint8_t*>(sm.pre_b) + kmaj_off(row, 0, 256)) =
+            make_uint4(0x4B40u, 0u, 0u, 0u);  // bf16 1.5 * 2^23 at k = 0
+        *reinterpret_cast<uint4*>(reinterpret_cast<uint8_t*>(sm.pre_b) + kmaj_off(row, 16, 256)) = make_uint4(0u, 0u, 0u, 0u);
+      }
 #pragma unroll 1
       for (int j = 0; j < nkt; ++j) {
         const int s = j % NS, bj = j % NB;
@@ -426,7 +449,7 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_tc_kernel(
 #pragma unroll
             for (int pr = 0; pr < 2; ++pr) {
               const int k2 = 4 * g4 + 2 * pr, ks = 16 * h + k2;
-              const float2 E = make_float2(u2f(d[k2]), u2f(d[k2 + 1]));
+              const float2 E = acc2f(d[k2], d[k2 + 1]);
               const float2 skp = pr ? make_float2(sk4.z, sk4.w) : make_float2(sk4.x, sk4.y);
               const float2 t = ptx::fmul2(skp, E);  // s_k 2D_s
               const float2 a = ptx::ffma2(A, t, make_float2(s[ks], s[ks + 1]));
@@ -587,7 +610,7 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_tc_kernel(
             for (int pr = 0; pr < 2; ++pr) {
               const int xo = 4 * x4 + 2 * pr;
               const int oi = 8 * h + 2 * x4 + pr;
-              const float2 E = make_float2(u2f(d[xo]), u2f(d[xo + 1]));
+              const float2 E = acc2f(d[xo], d[xo + 1]);
               const float2 svp = pr ? make_float2(sv4.z, sv4.w) : make_float2(sv4.x, sv4.y);
               const float2 mvp = pr ? make_float2(mv4.z, mv4.w) : make_float2(mv4.x, mv4.y);
               const float2 yp = pr ? make_float2(y4.z, y4.w) : make_float2(y4.x, y4.y);
