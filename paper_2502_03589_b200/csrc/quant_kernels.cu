@@ -148,6 +148,96 @@ __global__ void __launch_bounds__(128) ingest_v_kernel(const __half* __restrict_
   store_sum(pg + PL.v_sums, c, PL.sum_bytes, sum);
 }
 
+// Full V blocks -> pages (a2) at Pi = 64, 4 threads per (block, head, channel): CTA =
+// 4 warps x 32 consecutive channels of one (block, head); warp q owns tokens 16q..16q+15,
+// so a warp's token loads are 64-byte coalesced rows and each thread packs exactly 16
+// codes (one u32 at b = 2, one u64 at b = 4).  Partition min/max and code sums are
+// combined across the 4 warps in shared memory.  Same per-element op sequence and
+// Philox counters as quant_vcol (R1, R3, R4), hence the same codes.  Blocks j == nfull
+// copy the ragged remainder to the FP16 tail (R10); block 0 sets seq_lens.
+template <int BITS>
+__global__ void __launch_bounds__(128) ingest_v64_kernel(const __half* __restrict__ v,
+                                                         const int32_t* __restrict__ cu_seqlens,
+                                                         const int32_t* __restrict__ slots, CacheView cv,
+                                                         KernelCfg kc) {
+  constexpr int PI = 64, qmax = (1 << BITS) - 1;
+  __shared__ float red_lo[4][32], red_hi[4][32];
+  __shared__ int red_sum[4][32];
+  const int b = blockIdx.y;
+  const int start = cu_seqlens[b], L = cu_seqlens[b + 1] - start;
+  const int slot = slots[b];
+  const int H = kc.Hkv;
+  const int nfull = L / PI;
+  const int cg = blockIdx.x & 3, h = (blockIdx.x >> 2) % H, j = (blockIdx.x >> 2) / H;
+  const int q = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int c = 32 * cg + lane;
+  if (blockIdx.x == 0 && threadIdx.x == 0) cv.seq_lens[slot] = L;
+  if (j > nfull) return;
+  const __half* xc = v + ((int64_t)(start + j * PI) * H + h) * 128 + c;
+  const int64_t ts = (int64_t)H * 128;
+  if (j == nfull) {  // FP16 tail rows (reading R10)
+    __half* tail = reinterpret_cast<__half*>(cv.v_tail) + (((int64_t)slot * H + h) * PI) * 128 + c;
+    for (int t = q; t < L - nfull * PI; t += 4) tail[t * 128] = xc[(int64_t)t * ts];
+    return;
+  }
+  float x[16];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) x[i] = __half2float(xc[(int64_t)(16 * q + i) * ts]);
+  float lo = x[0], hi = x[0];
+#pragma unroll
+  for (int i = 1; i < 16; ++i) {
+    lo = fminf(lo, x[i]);
+    hi = fmaxf(hi, x[i]);
+  }
+  red_lo[q][lane] = lo;
+  red_hi[q][lane] = hi;
+  __syncthreads();
+#pragma unroll
+  for (int w = 0; w < 4; ++w) {
+    lo = fminf(lo, red_lo[w][lane]);
+    hi = fmaxf(hi, red_hi[w][lane]);
+  }
+  const QMeta qm = meta_fp16(lo, hi, qmax);
+  const uint32_t rng_id = cv.rng_ids[slot];
+  const uint32_t c3 = stream_c3(kc.layer, kTagV, kc.head_base + h);
+  const int64_t pos = (int64_t)j * PI + 16 * q;  // absolute position of this thread's first token
+  uint64_t packed = 0;
+  int sum = 0;
+#pragma unroll
+  for (int k4 = 0; k4 < 4; ++k4) {
+    int cc[4];
+    if (kc.kv_round == HACK_ROUND_STOCHASTIC) {
+      // element (pos+t, ch): Philox block n = ((pos+t) >> 2)*d + ch, word (pos+t) & 3 (R3)
+      const Philox4 r = philox_block(kc.seed, rng_id, c3, (uint64_t)((pos + 4 * k4) >> 2) * 128u + (uint64_t)c);
+      cc[0] = quant_sr(x[4 * k4 + 0], qm, u24(r.x), qmax);
+      cc[1] = quant_sr(x[4 * k4 + 1], qm, u24(r.y), qmax);
+      cc[2] = quant_sr(x[4 * k4 + 2], qm, u24(r.z), qmax);
+      cc[3] = quant_sr(x[4 * k4 + 3], qm, u24(r.w), qmax);
+    } else {
+#pragma unroll
+      for (int i = 0; i < 4; ++i) cc[i] = quant_rn(x[4 * k4 + i], qm, qmax);
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      packed |= (uint64_t)cc[i] << (BITS * (4 * k4 + i));
+      sum += cc[i];
+    }
+  }
+  const PageLayout& PL = kc.pl;
+  uint8_t* pg = page_ptr(cv, slot, j, h);
+  if (BITS == 2)
+    reinterpret_cast<uint32_t*>(pg + PL.v_codes + c * 16)[q] = (uint32_t)packed;
+  else
+    reinterpret_cast<uint2*>(pg + PL.v_codes + c * 32)[q] = make_uint2((uint32_t)packed, (uint32_t)(packed >> 32));
+  red_sum[q][lane] = sum;
+  __syncthreads();
+  if (q == 0) {
+    const int tot = red_sum[0][lane] + red_sum[1][lane] + red_sum[2][lane] + red_sum[3][lane];
+    reinterpret_cast<__half2*>(pg + PL.v_meta)[c] = make_meta(qm.m, qm.s);
+    store_sum(pg + PL.v_sums, c, PL.sum_bytes, tot);
+  }
+}
+
 // -------------------------------------------------------------------------- decode append (a8)
 // One CTA per request, 128 threads (= d channels), looping over KV heads:
 // quantize k_new into its own partitions in the current page, write v_new
@@ -249,12 +339,20 @@ cudaError_t launch_ingest(const KernelCfg& kc, const void* k, const void* v, con
   const __half* vh = reinterpret_cast<const __half*>(v);
   dim3 gk((max_seqlen * kc.Hkv + 15) / 16, batch);
   dim3 gv(((max_seqlen / kc.Pi + 1) * kc.Hkv * 128 + 127) / 128, batch);
+  dim3 gv64((max_seqlen / kc.Pi + 1) * kc.Hkv * 4, batch);  // (block, head, 32-channel group)
+  const bool v64 = kc.Pi == 64;
   if (kc.bits == 2) {
     ingest_k_kernel<2><<<gk, 256, 0, st>>>(kh, cu_seqlens, slots, cv, kc);
-    ingest_v_kernel<2><<<gv, 128, 0, st>>>(vh, cu_seqlens, slots, cv, kc);
+    if (v64)
+      ingest_v64_kernel<2><<<gv64, 128, 0, st>>>(vh, cu_seqlens, slots, cv, kc);
+    else
+      ingest_v_kernel<2><<<gv, 128, 0, st>>>(vh, cu_seqlens, slots, cv, kc);
   } else {
     ingest_k_kernel<4><<<gk, 256, 0, st>>>(kh, cu_seqlens, slots, cv, kc);
-    ingest_v_kernel<4><<<gv, 128, 0, st>>>(vh, cu_seqlens, slots, cv, kc);
+    if (v64)
+      ingest_v64_kernel<4><<<gv64, 128, 0, st>>>(vh, cu_seqlens, slots, cv, kc);
+    else
+      ingest_v_kernel<4><<<gv, 128, 0, st>>>(vh, cu_seqlens, slots, cv, kc);
   }
   note_launch(2);
   return cudaGetLastError();
