@@ -79,6 +79,9 @@ struct TcSmem {
 // Integer accumulators are preset to the fp32 bits of 1.5*2^23 by one bf16 MMA (A = e_0,
 // B = 1.5*2^23 e_0) before the kind::i8 MMAs accumulate onto them, so the float view of an
 // accumulated integer E (|E| < 2^22) is 1.5*2^23 + E and one FADD2 converts two exactly.
+#ifndef HACK_ABL
+#define HACK_ABL 0  // timing ablations only (scripts/ablate_pre.sh); results are wrong for != 0
+#endif
 HACK_DEV float2 acc2f(uint32_t a, uint32_t b) {
   return ptx::fadd2(make_float2(__uint_as_float(a), __uint_as_float(b)), make_float2(-kMagic, -kMagic));
 }
@@ -435,7 +438,7 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_tc_kernel(
         for (int x = 0; x < 16; ++x) s[16 * h + x] = __uint_as_float(d[x]);
       }
 #pragma unroll
-      for (int beta = 0; beta < 2; ++beta) {
+      for (int beta = 0; beta < 2 && HACK_ABL != 3; ++beta) {
         const float2 A = beta ? qa1 : qa0;
 #pragma unroll
         for (int h = 0; h < 2; ++h) {  // 16 keys per TMEM load (register pressure)
@@ -502,8 +505,13 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_tc_kernel(
 #pragma unroll
       for (int kk = 0; kk < 32; kk += 2) {
         const float2 a2 = ptx::fadd2(make_float2(s[kk], s[kk + 1]), mneg);
+#if HACK_ABL == 4
+        s[kk] = a2.x;
+        s[kk + 1] = a2.y;
+#else
         s[kk] = ex2(a2.x);  // ex2(-inf) = +0 for masked keys
         s[kk + 1] = ex2(a2.y);
+#endif
         ls2 = ptx::fadd2(ls2, make_float2(s[kk], s[kk + 1]));
       }
       l_run = l_run * al + (ls2.x + ls2.y);
@@ -525,6 +533,11 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_tc_kernel(
 #pragma unroll
         for (int c16 = 0; c16 < 2; ++c16) {
           uint32_t bits[16];
+#if HACK_ABL == 2
+#pragma unroll
+          for (int kk = 0; kk < 16; ++kk) bits[kk] = __float_as_uint(s[16 * c16 + kk]);
+          if (false)
+#endif
 #pragma unroll
           for (int kk = 0; kk < 16; kk += 2) {
             const float2 y =
@@ -600,6 +613,9 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_tc_kernel(
           uint32_t d[16];
           ptx::tmem_ld16(tD0 + 128 * bd + lane_base + cb + 16 * h, d);
           ptx::tmem_wait_ld();
+#if HACK_ABL == 1
+          if (d[0] == 0x12345u) o2[h].x += 1.f;  // (ablation: no PV Eq. 4 math)
+#else
 #pragma unroll
           for (int x4 = 0; x4 < 4; ++x4) {
             const int c0 = cb + 16 * h + 4 * x4;
@@ -620,6 +636,7 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_tc_kernel(
               o2[oi] = ptx::ffma2(mp2, yp, a);
             }
           }
+#endif
         }
         ptx::tc_fence_before();
         ptx::mbar_arrive(&sm.d_free[bd]);
