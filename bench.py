@@ -361,20 +361,54 @@ def run_decode(args, h, dev, rank, world, peaks, traffic, seed, flush):
 
     for _ in range(args.warmup):
         step()
+    torch.cuda.synchronize()
     barrier(world)
     n_before = int(cache.seq_lens[0].item())
-    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
-    n0 = h.kernel_launches()
-    with ClockSampler(dev.index if dev.index is not None else 0) as clk:
-        barrier(world)
-        for i in range(args.steps):
-            step(evs[i])
-        barrier(world)
-    launches = h.kernel_launches() - n0
-    step_ms = [e[0].elapsed_time(e[2]) for e in evs]
-    attn_ms = [e[1].elapsed_time(e[2]) for e in evs]
-    ms = max_over_ranks(sum(step_ms) / len(step_ms), world)
-    attn_avg = max_over_ranks(sum(attn_ms) / len(attn_ms), world)
+    if args.no_graph:
+        evs = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
+        n0 = h.kernel_launches()
+        with ClockSampler(dev.index if dev.index is not None else 0) as clk:
+            barrier(world)
+            for i in range(args.steps):
+                step(evs[i])
+            barrier(world)
+        launches = h.kernel_launches() - n0
+        step_ms = [e[0].elapsed_time(e[2]) for e in evs]
+        attn_ms = [e[1].elapsed_time(e[2]) for e in evs]
+        ms = max_over_ranks(sum(step_ms) / len(step_ms), world)
+        attn_avg = max_over_ranks(sum(attn_ms) / len(attn_ms), world)
+        attn_ctx = [n_before + i + 1 for i in range(args.steps)]
+    else:
+        # One decode step per layer is a few tens of microseconds, so host launch latency
+        # (ctypes + 3 launches) would be timed too: the K timed steps (append + attention,
+        # each step's own inputs) are captured once as a CUDA graph and replayed (SURVEY d-5).
+        # The attention kernel alone is timed the same way: a graph of K launches of
+        # hack_decode_attention_cached at the context reached after the K steps.
+        g_step, g_attn = torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()
+        n0 = h.kernel_launches()
+        with torch.cuda.graph(g_step):
+            for i in range(args.steps):
+                step()
+        launches = h.kernel_launches() - n0
+        with torch.cuda.graph(g_attn):
+            for i in range(args.steps):
+                h.decode_attention_cached(cfg, qn[(it[0] + i) % nsteps], slots_all, max_len, cache, out, workspace=ws)
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+        torch.cuda.synchronize()
+        with ClockSampler(dev.index if dev.index is not None else 0) as clk:
+            barrier(world)
+            ev[0].record(stream)
+            g_step.replay()
+            ev[1].record(stream)
+            barrier(world)
+            ev[2].record(stream)
+            g_attn.replay()
+            ev[3].record(stream)
+            barrier(world)
+        torch.cuda.synchronize()
+        ms = max_over_ranks(ev[0].elapsed_time(ev[1]) / args.steps, world)
+        attn_avg = max_over_ranks(ev[2].elapsed_time(ev[3]) / args.steps, world)
+        attn_ctx = [n_before + args.steps] * args.steps
     # algorithmic bytes of one attention launch (context n after the append): committed
     # tokens at 84 B/token/head (packed K+V, meta, sums), tail tokens at K-row bytes +
     # fp16 V, plus q in and out.
@@ -382,8 +416,7 @@ def run_decode(args, h, dev, rank, world, peaks, traffic, seed, flush):
     pb = h.page_bytes(cfg)
     krow = sum(lay[x][1] for x in ("k_codes", "k_meta", "k_sums")) // Pi
     nbytes = []
-    for i in range(args.steps):
-        n = n_before + i + 1
+    for n in attn_ctx:
         C = (n // Pi) * Pi
         T = n - C
         nbytes.append(B * Hkv * (C * pb / Pi + T * (krow + 256)) + B * Hq * 128 * 2 * 2)
@@ -417,6 +450,8 @@ def run_decode(args, h, dev, rank, world, peaks, traffic, seed, flush):
         "config": {"workload": DECODE_WORKLOAD, "batch": B, "context": ctx, "num_q_heads": Hq,
                    "num_kv_heads": Hkv, "partition": Pi, "kv_bits": C3["bits"],
                    "step": "hack_decode_append (a8) + hack_decode_attention_cached (a9)",
+                   "timing": "eager launches" if args.no_graph else
+                   "CUDA-graph replay of the K timed steps (each with its own inputs)",
                    "l2": "cache 352 MB > L2"},
         "roofline": {"bound": "hbm", "achieved": gbs, "peak": peaks["hbm"], "unit": "GB/s",
                      "frac": gbs / peaks["hbm"], "traffic": tr, "bytes_per_launch": avg_bytes,
@@ -436,6 +471,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["hack", "reference"], default="hack")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-graph", action="store_true",
+                    help="decode: launch eagerly instead of replaying a CUDA graph of the K timed steps")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                     help="process-group backend for barriers / max-over-ranks (gloo: several ranks on one GPU, tests)")
     args = ap.parse_args()

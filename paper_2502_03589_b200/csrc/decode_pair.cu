@@ -229,7 +229,10 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
         const int y = __shfl_up_sync(0xffffffffu, v, o);
         if (lane >= o) v += y;
       }
-      if (c == 0 && b < batch) ws_meta[kMetaInts + b] = P + v - n;  // flattened offset of request b
+      if (c == 0 && b < batch) {
+        ws_meta[kMetaInts + b] = P + v - n;            // flattened offset of request b
+        ws_meta[kMetaInts + batch + b] = n / Hkv;      // its pages (per unit)
+      }
       P += __shfl_sync(0xffffffffu, v, 31);
     }
     const int R = max(1, (P + (int)gridDim.x - 1) / (int)gridDim.x);
@@ -572,35 +575,51 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
 
 // out[b][hk*G + n][c] = sum_parts e^(m - M) O / sum_parts e^(m - M) l over the partials of
 // unit u = b*Hkv + hk: CTAs c_first..c_last of its flattened page range, NW warps each.
-__global__ void decode_pair_combine(const int* __restrict__ ws_meta, const float* __restrict__ part,
-                                    const int32_t* __restrict__ slots, CacheView cv, KernelCfg kc,
-                                    void* __restrict__ out) {
-  const int b = blockIdx.x, hq = blockIdx.y, ch = threadIdx.x;
+__global__ void __launch_bounds__(128) decode_pair_combine(const int* __restrict__ ws_meta,
+                                                           const float* __restrict__ part, KernelCfg kc,
+                                                           void* __restrict__ out) {
+  const int b = blockIdx.x, hq = blockIdx.y, c = threadIdx.x, batch = gridDim.x;
   const int hk = hq / kc.G, n = hq % kc.G;
+  // launched with programmatic stream serialization: wait for the main kernel's results
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   const int R = ws_meta[0];
-  const int npg = (cv.seq_lens[slots[b]] + PI - 1) / PI;
+  const int npg = ws_meta[kMetaInts + batch + b];
   const int off = ws_meta[kMetaInts + b] + hk * npg;
   const int u = b * kc.Hkv + hk;
   const int c0 = off / R, c1 = (off + npg - 1) / R;
-  float M = -INFINITY, L = 0.f, O = 0.f;  // one pass, online rescaling
-  for (int c = c0; c <= c1; ++c)
+  // all partial loads are issued before any is consumed (two dependent round trips in
+  // total instead of one per partial); units spanning more than 4 CTAs loop
+  const int np = (c1 - c0 + 1) * NW;
+  const float* base = part + ((((int64_t)(u + c0)) * NW) * kc.G + n) * kPart;  // partial k at + k G kPart
+  const int64_t stride = (int64_t)kc.G * kPart;
+  float M = -INFINITY, L = 0.f, O = 0.f;
+  for (int k0 = 0; k0 < np; k0 += 16) {
+    float ms[16], ls[16], os[16];
 #pragma unroll
-    for (int w = 0; w < NW; ++w) {
-      const float* src = part + ((((int64_t)(u + c)) * NW + w) * kc.G + n) * kPart;
-      const float ms = src[0];
-      if (ms == -INFINITY) continue;
-      if (ms > M) {
-        const float r = ex2(M - ms);  // 0 when M = -inf
-        L *= r;
-        O *= r;
-        M = ms;
-      }
-      const float f = ex2(ms - M);
-      L += f * src[1];
-      O += f * src[2 + ch];
+    for (int k = 0; k < 16; ++k) {
+      const bool ok = k0 + k < np;
+      const float* src = base + (k0 + k) * stride;
+      ms[k] = ok ? src[0] : -INFINITY;
+      ls[k] = ok ? src[1] : 0.f;
+      os[k] = ok ? src[2 + c] : 0.f;
     }
+    float Mn = M;
+#pragma unroll
+    for (int k = 0; k < 16; ++k) Mn = fmaxf(Mn, ms[k]);
+    if (Mn == -INFINITY) continue;
+    const float r = ex2(M - Mn);  // 0 when M = -inf
+    L *= r;
+    O *= r;
+    M = Mn;
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+      const float f = ex2(ms[k] - M);  // ex2(-inf) = 0 for empty partials
+      L = fmaf(f, ls[k], L);
+      O = fmaf(f, os[k], O);
+    }
+  }
   const float v = O / L;
-  const int64_t idx = ((int64_t)b * kc.Hq + hq) * 128 + ch;
+  const int64_t idx = ((int64_t)b * kc.Hq + hq) * 128 + c;
   if (kc.out_fp32)
     reinterpret_cast<float*>(out)[idx] = v;
   else
@@ -618,7 +637,7 @@ int grid_size() {
   return g;
 }
 
-size_t meta_bytes(int batch) { return ((size_t)(kMetaInts + batch) * sizeof(int) + 255) / 256 * 256; }
+size_t meta_bytes(int batch) { return ((size_t)(kMetaInts + 2 * batch) * sizeof(int) + 255) / 256 * 256; }
 
 }  // namespace
 
@@ -641,11 +660,27 @@ cudaError_t launch_decode_pair(const KernelCfg& kc, const void* q_new, const int
   const size_t smem = sizeof(PairSmem);
   const bool with_dbg = dbg != nullptr && dbg->pcodes != nullptr;  // P-code dump: parity runs only
   auto kern = with_dbg ? decode_pair_kernel<true> : decode_pair_kernel<false>;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return e;
+  static bool attr_set[2] = {false, false};  // once per process (keeps graph capture free of it)
+  if (!attr_set[with_dbg]) {
+    const cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    attr_set[with_dbg] = true;
+  }
   kern<<<grid_size(), kThreads, smem, st>>>(reinterpret_cast<const __half*>(q_new), slots, batch, cv, kc, meta, part,
                                             with_dbg ? dbg->pcodes : nullptr, with_dbg ? dbg->pcodes_stride : 0);
-  decode_pair_combine<<<dim3(batch, kc.Hq), 128, 0, st>>>(meta, part, slots, cv, kc, out);
+  // the merge is launched as a programmatic dependent of the main kernel (PDL): its CTAs can
+  // be resident before the main grid drains and wait in griddepcontrol.wait
+  cudaLaunchConfig_t lc = {};
+  lc.gridDim = dim3(batch, kc.Hq);
+  lc.blockDim = dim3(128);
+  lc.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  lc.attrs = at;
+  lc.numAttrs = 1;
+  const cudaError_t e2 = cudaLaunchKernelEx(&lc, decode_pair_combine, (const int*)meta, (const float*)part, kc, out);
+  if (e2 != cudaSuccess) return e2;
   note_launch(2);
   return cudaGetLastError();
 }
