@@ -21,7 +21,7 @@
 //     per page from the fp16 meta and cached sums and staged in shared memory.
 //   * persistent, stream-K style work split: the flattened sequence of all pages of all
 //     (request, KV head) units is cut into equal page ranges, one per CTA (3 CTAs/SM);
-//     a CTA walks the unit segments of its range, a single producer lane streams the
+//     a CTA walks the unit segments of its range, a producer warp streams the
 //     pages in order (cp.async.bulk into a 12-slot ring), the 4 compute warps take page
 //     pairs round-robin and flush one (m, l, O) partial per (segment, warp) to global
 //     memory.  Partial slot of (unit u, CTA c) = u + c (injective: units and CTA ranges
@@ -275,19 +275,33 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
 
   if (warp == NW) {
     // ------------------------------------------------------------------ producer
-    if (lane == 0) {
-      Seg s;
-      int k = 0;
-      while (walk.next(cv, slots, Hkv, s)) {
-        const int32_t* bt = cv.block_table + (int64_t)slots[s.b] * cv.max_pages_per_req;
-        for (int p = s.p0; p < s.p1; ++p, ++k) {
-          const int st = k % NSTG;
-          // sleep-wait: a spinning producer lane steals issue slots from the compute warps
-          while (!ptx::mbar_try_wait_sleep(&sm.empty[st], ((k / NSTG) & 1) ^ 1)) {
+    // The whole warp walks the segments; block-table entries are fetched 32 pages at a
+    // time with one coalesced load, so the issuing lane never waits on a dependent global
+    // load between two page copies (one such wait per page capped the issue rate).
+    Seg s;
+    int k = 0;
+    while (walk.next(cv, slots, Hkv, s)) {
+      const int32_t* bt = cv.block_table + (int64_t)slots[s.b] * cv.max_pages_per_req;
+      for (int p0 = s.p0; p0 < s.p1; p0 += 32) {
+        const int n = min(32, s.p1 - p0);
+        const int ent = lane < n ? bt[p0 + lane] : 0;
+        for (int x = 0; x < n; ++x, ++k) {
+          const int pid = __shfl_sync(0xffffffffu, ent, x);
+          if (lane == 0) {
+            const int st = k % NSTG;
+#ifdef HACK_DEC_SPIN
+            while (!ptx::mbar_try_wait(&sm.empty[st], ((k / NSTG) & 1) ^ 1)) {
+            }
+#else
+            // sleep-wait: a spinning producer lane steals issue slots from the compute warps
+            while (!ptx::mbar_try_wait_sleep(&sm.empty[st], ((k / NSTG) & 1) ^ 1)) {
+            }
+#endif
+            ptx::mbar_arrive_expect_tx(&sm.full[st], PB);
+            const uint8_t* pg = cv.pages + ((int64_t)pid * cv.num_kv_heads + s.hk) * cv.page_bytes;
+            ptx::bulk_g2s(sm.stage[st], pg, PB, &sm.full[st]);
           }
-          ptx::mbar_arrive_expect_tx(&sm.full[st], PB);
-          const uint8_t* pg = cv.pages + ((int64_t)bt[p] * cv.num_kv_heads + s.hk) * cv.page_bytes;
-          ptx::bulk_g2s(sm.stage[st], pg, PB, &sm.full[st]);
+          __syncwarp();
         }
       }
     }
