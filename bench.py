@@ -35,6 +35,7 @@ import numpy as np  # noqa: E402
 
 C2 = dict(Hq=32, Hkv=8, L=4096, Pi=64, bits=2)
 C3 = dict(Hq=32, Hkv=8, B=64, ctx=8192, Pi=64, bits=2)
+C4 = dict(Hq=64, Hkv=8, L=32768, B=16, Pi=64)
 WORKLOAD = ("C2: Mistral-7B-shaped homomorphic prefill attention (32 Q / 8 KV heads, d=128), "
             "one 4096-token causal prompt, 2-bit K/V, Pi=64, Q/P 8-bit")
 DECODE_WORKLOAD = ("C3: Llama-3.1-8B-shaped decode attention (32 Q / 8 KV heads, d=128), batch 64, "
@@ -286,6 +287,7 @@ def run_hack(args, rank, local_rank, world):
 
     # ---------------- C3 decode (a8, a9)
     dec = run_decode(args, h, dev, rank, world, peaks, traffic, seed, flush)
+    c4 = None if args.no_c4 else run_c4(args, h, dev, world, seed, flush)
 
     # ---------------- CPU oracle baseline (rank 0, N = 1)
     cpu = None
@@ -316,8 +318,80 @@ def run_hack(args, rank, local_rank, world):
             "gpu_launches": launches,
             "clocks": clk.summary(),
             "decode": dec,
+            "c4": c4,
         }
         print(json.dumps(line), flush=True)
+
+
+def run_c4(args, h, dev, world, seed, flush):
+    """C4 (BASELINE configs[3]) on this GPU: Llama-3.1-70B-shaped attention (64 Q / 8 KV heads,
+    G = 8), one 32K-token causal prefill (ingest + attention) and a batch-16 decode step at 32K
+    context, 2-bit vs 4-bit K/V.  (The 8-GPU layout gives every GPU one KV head; here one GPU
+    runs all eight.)  Reported beside the headline, not as it."""
+    import torch
+    Hq, Hkv, L, B, Pi = C4["Hq"], C4["Hkv"], C4["L"], C4["B"], C4["Pi"]
+    stream = torch.cuda.current_stream()
+    res = {"workload": "C4: Llama-3.1-70B-shaped (64 Q / 8 KV heads, d=128), 32K causal prefill + "
+                       "batch-16 decode at 32K context, one GPU", "per_bits": {}}
+    q = dev_normal((L, Hq, 128), seed + 41, dev)
+    k = dev_normal((L, Hkv, 128), seed + 42, dev)
+    v = dev_normal((L, Hkv, 128), seed + 43, dev)
+    cu = torch.tensor([0, L], dtype=torch.int32, device=dev)
+    out = torch.empty((L, Hq, 128), dtype=torch.float16, device=dev)
+    ops = prefill_ops(L, Hq)
+    n_pre, n_dec = 3, 8
+    for bits in (2, 4):
+        cfg = h.config(num_q_heads=Hq, num_kv_heads=Hkv, partition=Pi, kv_bits=bits, out_fp32=False, layer=2)
+        mp = (L + n_dec + 2 + Pi - 1) // Pi + 1
+        cache = h.KVCache.allocate(cfg, max_reqs=B, max_pages_per_req=mp, device=dev)
+        cache.rng_ids.copy_(torch.arange(B, dtype=torch.int32, device=dev))
+        sl0 = torch.zeros(1, dtype=torch.int32, device=dev)
+        ms = []
+        for i in range(n_pre + 1):
+            flush.fill_(1)
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            h.cache_ingest(cfg, k, v, cu, sl0, L, cache)
+            h.prefill_attention_cached(cfg, q, cu, sl0, L, cache, out)
+            b.record(stream)
+            b.synchronize()
+            if i:
+                ms.append(a.elapsed_time(b))
+        pre_ms = sum(ms) / len(ms)
+        # decode: every request holds the same 32K-token prompt (values never affect speed)
+        for r in range(1, B):
+            h.cache_ingest(cfg, k, v, cu, torch.tensor([r], dtype=torch.int32, device=dev), L, cache)
+        slots = torch.arange(B, dtype=torch.int32, device=dev)
+        qn = dev_normal((n_dec, B, Hq, 128), seed + 44, dev)
+        kn = dev_normal((n_dec, B, Hkv, 128), seed + 45, dev)
+        vn = dev_normal((n_dec, B, Hkv, 128), seed + 46, dev)
+        dout = torch.empty((B, Hq, 128), dtype=torch.float16, device=dev)
+        ws = torch.empty(max(h.decode_workspace_size(cfg, B, L + n_dec + 2), 1), dtype=torch.uint8, device=dev)
+        h.decode_append(cfg, kn[0], vn[0], slots, cache)      # warm-up step
+        h.decode_attention_cached(cfg, qn[0], slots, L + n_dec + 2, cache, dout, workspace=ws)
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            for i in range(1, n_dec):
+                h.decode_append(cfg, kn[i], vn[i], slots, cache)
+                h.decode_attention_cached(cfg, qn[i], slots, L + n_dec + 2, cache, dout, workspace=ws)
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        g.replay()
+        b.record(stream)
+        b.synchronize()
+        dec_ms = a.elapsed_time(b) / (n_dec - 1)
+        pb = h.page_bytes(cfg)
+        n = L + n_dec // 2 + 1
+        dec_bytes = B * Hkv * (n // Pi) * pb + B * Hq * 128 * 2 * 2
+        res["per_bits"][str(bits)] = {
+            "prefill_tops": ops / (pre_ms * 1e-3) / 1e12, "prefill_ms": pre_ms,
+            "decode_step_ms": dec_ms, "decode_tokens_per_s": B / (dec_ms * 1e-3),
+            "decode_kv_gbs": dec_bytes / (dec_ms * 1e-3) / 1e9, "page_bytes": pb,
+            "bytes_per_token_head": pb / Pi}
+        del cache, ws, qn, kn, vn
+    return res
 
 
 def run_decode(args, h, dev, rank, world, peaks, traffic, seed, flush):
@@ -471,6 +545,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["hack", "reference"], default="hack")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-c4", action="store_true", help="skip the C4 (70B-shaped, 2- vs 4-bit) sub-benchmark")
     ap.add_argument("--no-graph", action="store_true",
                     help="decode: launch eagerly instead of replaying a CUDA graph of the K timed steps")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
