@@ -20,9 +20,9 @@
 //   * Eq. 4 coefficients of a page (per token for K, per channel for V) are computed once
 //     per page from the fp16 meta and cached sums and staged in shared memory.
 //   * persistent, stream-K style work split: the flattened sequence of all pages of all
-//     (request, KV head) units is cut into equal page ranges, one per CTA (3 CTAs/SM);
+//     (request, KV head) units is cut into equal page ranges, one per CTA (4 CTAs/SM);
 //     a CTA walks the unit segments of its range, a producer warp streams the
-//     pages in order (cp.async.bulk into a 12-slot ring), the 4 compute warps take page
+//     pages in order (cp.async.bulk into a 9-slot ring), the 3 compute warps take page
 //     pairs round-robin and flush one (m, l, O) partial per (segment, warp) to global
 //     memory.  Partial slot of (unit u, CTA c) = u + c (injective: units and CTA ranges
 //     are both monotone along the flattened order).  decode_pair_combine merges them.
@@ -38,13 +38,13 @@ namespace {
 
 constexpr int PI = 64;
 #ifndef HACK_DEC_NW
-#define HACK_DEC_NW 4
+#define HACK_DEC_NW 3
 #endif
 #ifndef HACK_DEC_NSTG
-#define HACK_DEC_NSTG 12
+#define HACK_DEC_NSTG 9
 #endif
 #ifndef HACK_DEC_CTAS
-#define HACK_DEC_CTAS 3
+#define HACK_DEC_CTAS 4
 #endif
 constexpr int NW = HACK_DEC_NW;        // compute warps per CTA
 constexpr int NSTG = HACK_DEC_NSTG;    // page slots per CTA
