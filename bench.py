@@ -483,6 +483,20 @@ def run_decode(args, h, dev, rank, world, peaks, traffic, seed, flush):
         ms = max_over_ranks(ev[0].elapsed_time(ev[1]) / args.steps, world)
         attn_avg = max_over_ranks(ev[2].elapsed_time(ev[3]) / args.steps, world)
         attn_ctx = [n_before + args.steps] * args.steps
+        # SURVEY f2 (HACK/SE ablation): the same attention launches with the code
+        # sums recomputed from the codes every step instead of read from the summation cache
+        os.environ["HACK_DECODE_NO_SE"] = "1"
+        g_nose = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g_nose):
+            for i in range(args.steps):
+                h.decode_attention_cached(cfg, qn[(it[0] + i) % nsteps], slots_all, max_len, cache, out, workspace=ws)
+        del os.environ["HACK_DECODE_NO_SE"]
+        torch.cuda.synchronize()
+        ev[2].record(stream)
+        g_nose.replay()
+        ev[3].record(stream)
+        torch.cuda.synchronize()
+        no_se_ms = max_over_ranks(ev[2].elapsed_time(ev[3]) / args.steps, world)
     # algorithmic bytes of one attention launch (context n after the append): committed
     # tokens at 84 B/token/head (packed K+V, meta, sums), tail tokens at K-row bytes +
     # fp16 V, plus q in and out.
@@ -496,6 +510,10 @@ def run_decode(args, h, dev, rank, world, peaks, traffic, seed, flush):
         nbytes.append(B * Hkv * (C * pb / Pi + T * (krow + 256)) + B * Hq * 128 * 2 * 2)
     avg_bytes = sum(nbytes) / len(nbytes)
     gbs = avg_bytes / (attn_avg * 1e-3) / 1e9
+    ablation = None if args.no_graph else {
+        "no_summation_elimination": {"attn_ms": no_se_ms, "kv_gbs": avg_bytes / (no_se_ms * 1e-3) / 1e9,
+                                     "slowdown": no_se_ms / attn_avg,
+                                     "what": "code sums recomputed from the codes every step (HACK/SE, P:1036-1042)"}}
     tok_s = B * world / (ms * 1e-3)
     # e2e: host q/k/v in, host out back, through hack_decode_attention (append + attend)
     qh = torch.empty((B, Hq, 128), dtype=torch.float16).pin_memory()
@@ -535,6 +553,7 @@ def run_decode(args, h, dev, rank, world, peaks, traffic, seed, flush):
                 "ms_per_step": e2e_ms},
         "gpu_launches": launches,
         "clocks": clk.summary(),
+        "ablation": ablation,
     }
 
 

@@ -131,6 +131,13 @@ struct SegWalker {
 
 // Per-page K-side Eq. 4 coefficients (beta0, beta1 pairs) from fp16 meta + cached sums (SE):
 // kcs[2t] = (s_k, mu_k), kcs[2t+1] = (y_k, -1.5*2^23 - 510 SK).  Two tokens per lane.
+// Sum of the 16 2-bit codes of a word: popc(w & 0x55..) + 2 popc(w & 0xAA..).
+HACK_DEV uint32_t codesum2(uint32_t w) { return __popc(w & 0x55555555u) + 2u * __popc(w & 0xAAAAAAAAu); }
+
+// SE = false is the "HACK/SE" ablation: the code sums are
+// recomputed from the codes on every decode step instead of read from the summation cache.
+// The result is bit-identical; only the cost differs.
+template <bool SE>
 HACK_DEV void stage_kc(const uint8_t* pg, const PageLayout& PL, float4* kcs, int lane) {
   uint2 mh[2];
   uint32_t sums[2];
@@ -138,7 +145,15 @@ HACK_DEV void stage_kc(const uint8_t* pg, const PageLayout& PL, float4* kcs, int
   for (int x = 0; x < 2; ++x) {  // issue all loads first
     const int t = lane + 32 * x;
     mh[x] = *reinterpret_cast<const uint2*>(pg + PL.k_meta + t * 8);
-    sums[x] = *reinterpret_cast<const uint16_t*>(pg + PL.k_sums + t * 2);
+    if (SE) {
+      sums[x] = *reinterpret_cast<const uint16_t*>(pg + PL.k_sums + t * 2);
+    } else {  // beta0: words 0..3 of the token row, beta1: words 4..7
+      const uint4 a = *reinterpret_cast<const uint4*>(pg + PL.k_codes + t * 32);
+      const uint4 b = *reinterpret_cast<const uint4*>(pg + PL.k_codes + t * 32 + 16);
+      const uint32_t s0 = codesum2(a.x) + codesum2(a.y) + codesum2(a.z) + codesum2(a.w);
+      const uint32_t s1 = codesum2(b.x) + codesum2(b.y) + codesum2(b.z) + codesum2(b.w);
+      sums[x] = s0 | (s1 << 8);
+    }
   }
 #pragma unroll
   for (int x = 0; x < 2; ++x) {
@@ -196,7 +211,7 @@ HACK_DEV void qk_page(const uint8_t* pg, const PageLayout& PL, const float4* kcs
   }
 }
 
-template <bool DBG>
+template <bool DBG, bool SE>
 __global__ void __launch_bounds__(kThreads, kCtasPerSm)
     decode_pair_kernel(const __half* __restrict__ q_new, const int32_t* __restrict__ slots, int batch, CacheView cv,
                        KernelCfg kc, int* __restrict__ ws_meta, float* __restrict__ part,
@@ -391,7 +406,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
         float sa[4][2], sbv[4][2];
         float mxA, mnA, mxB = -INFINITY, mnB = INFINITY;
         ptx::mbar_wait(&sm.full[sA], (kA / NSTG) & 1);
-        stage_kc(pgA, PL, &ws.scr[0][0], lane);
+        stage_kc<SE>(pgA, PL, &ws.scr[0][0], lane);
         __syncwarp();
         if (tail_item)
           qk_page<true>(pgA, PL, &ws.scr[0][0], g, tig, nkA, qb, QA, QX, QM, rc0, rc1, sa, mxA, mnA);
@@ -400,7 +415,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
         if (hasB) {
           ptx::mbar_wait(&sm.full[sB], (kB / NSTG) & 1);
           __syncwarp();
-          stage_kc(pgB, PL, &ws.scr[0][0], lane);
+          stage_kc<SE>(pgB, PL, &ws.scr[0][0], lane);
           __syncwarp();
           qk_page<false>(pgB, PL, &ws.scr[0][0], g, tig, PI, qb, QA, QX, QM, rc0, rc1, sbv, mxB, mnB);
         } else {
@@ -419,7 +434,19 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
             const __half2 hB = reinterpret_cast<const __half2*>(pgB + PL.v_meta)[ch];
             const float2 mv = f2(__low2float(hA), hasB ? __low2float(hB) : 0.f);
             const float2 sv = f2(__high2float(hA), hasB ? __high2float(hB) : 0.f);
-            const uint32_t sumA = pgA[PL.v_sums + ch], sumB = hasB ? pgB[PL.v_sums + ch] : 0u;
+            uint32_t sumA, sumB;
+            if (SE) {  // cached sums (summation elimination)
+              sumA = pgA[PL.v_sums + ch];
+              sumB = hasB ? pgB[PL.v_sums + ch] : 0u;
+            } else {   // HACK/SE ablation: the channel's 64 codes are 4 words of its V row
+              const uint4 a = *reinterpret_cast<const uint4*>(pgA + PL.v_codes + ch * 16);
+              sumA = codesum2(a.x) + codesum2(a.y) + codesum2(a.z) + codesum2(a.w);
+              sumB = 0u;
+              if (hasB) {
+                const uint4 b2 = *reinterpret_cast<const uint4*>(pgB + PL.v_codes + ch * 16);
+                sumB = codesum2(b2.x) + codesum2(b2.y) + codesum2(b2.z) + codesum2(b2.w);
+              }
+            }
             const float2 sum = ptx::fadd2(asf2(0x4B000000u | sumA, 0x4B000000u | sumB), f2(-8388608.f, -8388608.f));
             const float2 mu = ptx::ffma2(sv, f2(1.5f, 1.5f), mv);
             const float2 yv = ptx::ffma2(sv, ptx::fadd2(sum, f2(-96.f, -96.f)), ptx::fmul2(f2(64.f, 64.f), mu));
@@ -673,12 +700,15 @@ cudaError_t launch_decode_pair(const KernelCfg& kc, const void* q_new, const int
   float* part = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(workspace) + meta_bytes(batch));
   const size_t smem = sizeof(PairSmem);
   const bool with_dbg = dbg != nullptr && dbg->pcodes != nullptr;  // P-code dump: parity runs only
-  auto kern = with_dbg ? decode_pair_kernel<true> : decode_pair_kernel<false>;
-  static bool attr_set[2] = {false, false};  // once per process (keeps graph capture free of it)
-  if (!attr_set[with_dbg]) {
+  const bool no_se = getenv("HACK_DECODE_NO_SE") != nullptr;  // f2 ablation only
+  auto kern = with_dbg ? (no_se ? decode_pair_kernel<true, false> : decode_pair_kernel<true, true>)
+                       : (no_se ? decode_pair_kernel<false, false> : decode_pair_kernel<false, true>);
+  const int ki = (with_dbg ? 2 : 0) + (no_se ? 1 : 0);
+  static bool attr_set[4] = {false, false, false, false};  // once per process (graph capture safe)
+  if (!attr_set[ki]) {
     const cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    attr_set[with_dbg] = true;
+    attr_set[ki] = true;
   }
   kern<<<grid_size(), kThreads, smem, st>>>(reinterpret_cast<const __half*>(q_new), slots, batch, cv, kc, meta, part,
                                             with_dbg ? dbg->pcodes : nullptr, with_dbg ? dbg->pcodes_stride : 0);

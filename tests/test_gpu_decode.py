@@ -164,3 +164,33 @@ def test_c3_full_size_sampled_requests():
             assert err <= ROW_TOL, f"step {s} req {i}: row error {err:.3g}"
     for i in sampled:
         compare_pages(cache, i, states[i])
+
+
+def test_no_se_ablation_bit_identical(monkeypatch):
+    """SURVEY f2, HACK/SE: recomputing the code sums on every decode step
+    instead of reading the summation cache must give bit-identical outputs (same integers
+    into the same Eq. 4 arithmetic); only the cost differs.  Also meets the oracle bar."""
+    h = hk()
+    ocfg = att.Config(Hq=8, Hkv=2, Pi=64, bits=2, seed=12)
+    monkeypatch.setenv("HACK_DECODE_NO_SE", "1")
+    run_decode(ocfg, [300, 64, 1000], 5, check_every=2)
+    cfg = gpu_cfg(ocfg)
+    cache = make_cache(cfg, max_reqs=3, max_len=2100, seed=2)
+    L = [2047, 700, 129]
+    for i, n in enumerate(L):
+        _, k, v = hack_inputs.qkv(40 + i, n, 1, ocfg.Hkv)
+        h.cache_ingest(cfg, torch.from_numpy(k).cuda(), torch.from_numpy(v).cuda(),
+                       torch.tensor([0, n], dtype=torch.int32, device="cuda"),
+                       torch.tensor([i], dtype=torch.int32, device="cuda"), n, cache)
+    qd, _, _ = hack_inputs.decode_tokens(3, 1, 3, ocfg.Hq, ocfg.Hkv)
+    sl = torch.arange(3, dtype=torch.int32, device="cuda")
+    outs = []
+    for flag in ("1", None):
+        if flag:
+            monkeypatch.setenv("HACK_DECODE_NO_SE", flag)
+        else:
+            monkeypatch.delenv("HACK_DECODE_NO_SE", raising=False)
+        o = torch.zeros((3, ocfg.Hq, 128), dtype=torch.float32, device="cuda")
+        h.decode_attention_cached(cfg, torch.from_numpy(qd[0]).cuda(), sl, 2100, cache, o)
+        outs.append(o.cpu().numpy())
+    assert np.array_equal(outs[0].view(np.uint32), outs[1].view(np.uint32))
