@@ -510,6 +510,31 @@ def run_decode(args, h, dev, rank, world, peaks, traffic, seed, flush):
         nbytes.append(B * Hkv * (C * pb / Pi + T * (krow + 256)) + B * Hq * 128 * 2 * 2)
     avg_bytes = sum(nbytes) / len(nbytes)
     gbs = avg_bytes / (attn_avg * 1e-3) / 1e9
+    comparator = None
+    if not args.no_comparator:
+        # a dequantize-first system on the same pages --
+        # hack_dequantize_cache expands them to dense fp16 K-hat/V-hat, then PyTorch SDPA
+        # (library attention, GQA) attends; timed per layer-step like the HACK call.
+        L_now = int(cache.seq_lens[0].item())
+        kh = torch.empty((B, Hkv, L_now, 128), dtype=torch.float16, device=dev)
+        vh = torch.empty_like(kh)
+        q4 = qn[0][:, :, None, :]
+        cms = []
+        for i in range(args.warmup + 5):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            h.dequantize_cache(cfg, slots_all, L_now, cache, kh, vh)
+            o4 = torch.nn.functional.scaled_dot_product_attention(q4, kh, vh, enable_gqa=True)
+            b.record(stream)
+            b.synchronize()
+            if i >= args.warmup:
+                cms.append(a.elapsed_time(b))
+        c_ms = max_over_ranks(sum(cms) / len(cms), world)
+        comparator = {"what": "dequantize-first: hack_dequantize_cache (packed pages -> dense fp16) + "
+                              "torch SDPA (GQA) -- the KVQuant/CacheGen-style path HACK avoids",
+                      "ms_per_layer_step": c_ms, "hack_attn_ms": attn_avg, "hack_speedup": c_ms / attn_avg,
+                      "fp16_cache_bytes": 2 * kh.numel() * 2}
+        del kh, vh, o4
     ablation = None if args.no_graph else {
         "no_summation_elimination": {"attn_ms": no_se_ms, "kv_gbs": avg_bytes / (no_se_ms * 1e-3) / 1e9,
                                      "slowdown": no_se_ms / attn_avg,
@@ -554,6 +579,7 @@ def run_decode(args, h, dev, rank, world, peaks, traffic, seed, flush):
         "gpu_launches": launches,
         "clocks": clk.summary(),
         "ablation": ablation,
+        "comparator": comparator,
     }
 
 
@@ -565,6 +591,7 @@ def main():
     ap.add_argument("--impl", choices=["hack", "reference"], default="hack")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-c4", action="store_true", help="skip the C4 (70B-shaped, 2- vs 4-bit) sub-benchmark")
+    ap.add_argument("--no-comparator", action="store_true", help="skip the dequantize-first comparator (f4)")
     ap.add_argument("--no-graph", action="store_true",
                     help="decode: launch eagerly instead of replaying a CUDA graph of the K timed steps")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],

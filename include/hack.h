@@ -189,6 +189,18 @@ hack_status_t hack_decode_attention_cached(const hack_config_t* cfg, const void*
                                            size_t workspace_bytes, const hack_debug_t* debug,
                                            void* stream);
 
+/* ---- comparator export: dequantize-first baseline ------------- */
+/* NOT part of the HACK path.  Expands the packed pages of every request into dense FP16
+ * K-hat = m + s*code and V-hat = m + s*code per partition (P:575-578 meta, fp32 FMA, one
+ * rounding to fp16), the FP16 last V block copied unchanged, as KV-quantization
+ * systems that dequantize before attention do (KVQuant / CacheGen).
+ * k_out, v_out: device fp16 [batch][num_kv_heads][max_seqlen][head_dim], caller-owned;
+ * rows >= seq_len are not written.  Errors: INVALID_ARG (NULL, empty), CAPACITY
+ * (max_seqlen beyond the block table), CUDA. */
+hack_status_t hack_dequantize_cache(const hack_config_t* cfg, const int32_t* slots, int32_t batch,
+                                    int32_t max_seqlen, const hack_kv_cache_t* cache, void* k_out,
+                                    void* v_out, void* stream);
+
 /* ---- test export: Eq. 4 homomorphic matmul on codes (N9) ---------------- */
 /* A: 8-bit codes u8 [M][Z], meta fp32 (m,s) [M][Z/Pi][2], sums u16 [M][Z/Pi];
  * B: kv_bits codes packed per column u8 [N][Z*b/8] (column j's Z codes LSB-first),

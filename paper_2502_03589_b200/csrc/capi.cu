@@ -278,6 +278,23 @@ hack_status_t hack_decode_attention(const hack_config_t* cfg, const void* q_new,
   return hack_decode_attention_cached(cfg, q_new, slots, batch, max_seqlen, cache, out, ws, ws_bytes, dbg, stream);
 }
 
+hack_status_t hack_dequantize_cache(const hack_config_t* cfg, const int32_t* slots, int32_t batch,
+                                    int32_t max_seqlen, const hack_kv_cache_t* cache, void* k_out, void* v_out,
+                                    void* stream) {
+  KernelCfg kc;
+  CacheView cv;
+  hack_status_t st = make_kernel_cfg(cfg, &kc);
+  if (st != HACK_OK) return st;
+  if ((st = make_cache_view(kc, cache, &cv)) != HACK_OK) return st;
+  if (!slots || !k_out || !v_out) return fail(HACK_ERR_INVALID_ARG, "dequantize_cache: NULL pointer");
+  if (batch <= 0 || max_seqlen <= 0) return fail(HACK_ERR_INVALID_ARG, "dequantize_cache: empty batch");
+  if ((max_seqlen + kc.Pi - 1) / kc.Pi > cache->max_pages_per_req)
+    return fail(HACK_ERR_CAPACITY, "dequantize_cache: max_seqlen needs more pages than max_pages_per_req");
+  if ((st = check_device()) != HACK_OK) return st;
+  return cuda_status(launch_dequantize_cache(kc, slots, batch, max_seqlen, cv, k_out, v_out, (cudaStream_t)stream),
+                     "dequantize_cache");
+}
+
 hack_status_t hack_homomorphic_matmul(const hack_config_t* cfg, const uint8_t* a_codes, const float* a_meta,
                                       const uint16_t* a_sums, const uint8_t* b_packed, const void* b_meta,
                                       const void* b_sums, int32_t M, int32_t N, int32_t Z, int32_t* d_blocks,

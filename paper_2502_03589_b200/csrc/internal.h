@@ -50,6 +50,9 @@ cudaError_t launch_decode_attention(const KernelCfg& kc, const void* q_new, cons
                                     int max_seqlen, const CacheView& cv, void* out, void* workspace,
                                     const hack_debug_t* dbg, cudaStream_t st);
 
+cudaError_t launch_dequantize_cache(const KernelCfg& kc, const int32_t* slots, int batch, int max_seqlen,
+                                    const CacheView& cv, void* k_out, void* v_out, cudaStream_t st);
+
 cudaError_t launch_homomorphic_matmul(const KernelCfg& kc, const uint8_t* a_codes, const float* a_meta,
                                       const uint16_t* a_sums, const uint8_t* b_packed, const void* b_meta,
                                       const void* b_sums, int M, int N, int Z, int32_t* d_blocks, float* c,

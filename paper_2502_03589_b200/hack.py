@@ -88,6 +88,8 @@ _lib.hack_decode_attention.argtypes = [C.POINTER(Config), _P, _P, _P, _P, C.c_in
 _lib.hack_decode_attention_cached.argtypes = [C.POINTER(Config), _P, _P, C.c_int32, C.c_int32,
                                               C.POINTER(CacheStruct), _P, _P, C.c_size_t,
                                               C.POINTER(DebugStruct), _P]
+_lib.hack_dequantize_cache.argtypes = [C.POINTER(Config), _P, C.c_int32, C.c_int32, C.POINTER(CacheStruct), _P, _P,
+                                       _P]
 _lib.hack_homomorphic_matmul.argtypes = [C.POINTER(Config), _P, _P, _P, _P, _P, _P, C.c_int32, C.c_int32,
                                          C.c_int32, _P, _P, _P]
 _lib.hack_prefill_workspace_size.argtypes = [C.POINTER(Config), C.c_int32, C.c_int32]
@@ -304,6 +306,14 @@ def decode_attention_cached(cfg: Config, q_new, slots, max_seqlen: int, cache: K
     _check(_lib.hack_decode_attention_cached(C.byref(cfg), _ptr(q_new), _ptr(slots), slots.shape[0], max_seqlen,
                                              C.byref(cs), _ptr(out), _ptr(ws), nb, _dbg(debug_pcodes),
                                              _stream(stream)), "decode_attention_cached")
+
+
+def dequantize_cache(cfg: Config, slots, max_seqlen: int, cache: KVCache, k_out, v_out, stream=None):
+    """Comparator only (not the HACK path): dense fp16 K-hat / V-hat
+    [batch, H_kv, max_seqlen, d] of every request, dequantized from the same pages."""
+    cs = cache.struct()
+    _check(_lib.hack_dequantize_cache(C.byref(cfg), _ptr(slots), slots.shape[0], max_seqlen, C.byref(cs),
+                                      _ptr(k_out), _ptr(v_out), _stream(stream)), "dequantize_cache")
 
 
 def homomorphic_matmul(cfg: Config, a_codes, a_meta, a_sums, b_packed, b_meta, b_sums, M, N, Z, c,
