@@ -397,21 +397,37 @@ def run_c4(args, h, dev, world, seed, flush):
 def run_decode(args, h, dev, rank, world, peaks, traffic, seed, flush):
     import torch
     B, ctx, Hq, Hkv, Pi = C3["B"], C3["ctx"], C3["Hq"], C3["Hkv"], C3["Pi"]
-    cfg = h.config(num_q_heads=Hq, num_kv_heads=Hkv, partition=Pi, kv_bits=C3["bits"], out_fp32=False, layer=1)
+    # C3 shards KV heads over the GPUs (BASELINE configs[2]: "heads sharded 1/2/4/8 GPUs"):
+    # rank r owns KV heads [r Hkv/N, (r+1) Hkv/N) and their G query heads for all requests;
+    # head_base keeps every head's Philox streams those of the unsharded run (R3).
+    shard = world > 1 and Hkv % world == 0
+    if shard:
+        Hkv, Hq = Hkv // world, Hq // world
+    cfg = h.config(num_q_heads=Hq, num_kv_heads=Hkv, partition=Pi, kv_bits=C3["bits"], out_fp32=False, layer=1,
+                   head_base=rank * Hkv if shard else 0)
     nsteps = args.warmup * 2 + args.steps * 2 + 2
     max_len = ctx + nsteps
     mp = (max_len + Pi - 1) // Pi
-    cache = h.KVCache.allocate(cfg, max_reqs=B, max_pages_per_req=mp, device=dev)
-    cache.rng_ids.copy_(torch.arange(B, dtype=torch.int32, device=dev) + 1000 * rank)
-    # fill every request with an 8192-token prompt through the ingest path (chunks of 8 requests)
+    # enough layers that one pass over them exceeds 2x the 126 MB L2 (a sharded layer can be
+    # L2-sized); consecutive layer-steps walk the layers as a real decode step does (SURVEY d-5)
+    layer_bytes = B * Hkv * mp * h.page_bytes(cfg)
+    n_layers = max(1, min(32, -(-2 * 126_000_000 // layer_bytes)))
     slots_all = torch.arange(B, dtype=torch.int32, device=dev)
+    caches = []
+    for _ in range(n_layers):
+        c_ = h.KVCache.allocate(cfg, max_reqs=B, max_pages_per_req=mp, device=dev)
+        c_.rng_ids.copy_(torch.arange(B, dtype=torch.int32, device=dev))
+        caches.append(c_)
+    # fill every request with an 8192-token prompt through the ingest path (chunks of 8 requests)
     for c0 in range(0, B, 8):
         kk = dev_normal((8 * ctx, Hkv, 128), seed + 100 + c0, dev)
         vv = dev_normal((8 * ctx, Hkv, 128), seed + 200 + c0, dev)
         cu = torch.arange(0, 9, dtype=torch.int32, device=dev) * ctx
-        h.cache_ingest(cfg, kk, vv, cu, slots_all[c0:c0 + 8].contiguous(), ctx, cache)
+        for c_ in caches:
+            h.cache_ingest(cfg, kk, vv, cu, slots_all[c0:c0 + 8].contiguous(), ctx, c_)
         del kk, vv
     torch.cuda.synchronize()
+    cache = caches[0]
     qn = dev_normal((nsteps, B, Hq, 128), seed + 300, dev)
     kn = dev_normal((nsteps, B, Hkv, 128), seed + 301, dev)
     vn = dev_normal((nsteps, B, Hkv, 128), seed + 302, dev)
@@ -421,15 +437,22 @@ def run_decode(args, h, dev, rank, world, peaks, traffic, seed, flush):
     stream = torch.cuda.current_stream()
     it = [0]
 
+    lens = [ctx] * n_layers   # host mirror of each layer's context length
+    attn_lens = []
+
     def step(evs=None):
         i = it[0]
         it[0] += 1
+        lay = i % n_layers
+        c_ = caches[lay]
         if evs:
             evs[0].record(stream)
-        h.decode_append(cfg, kn[i], vn[i], slots_all, cache)
+        h.decode_append(cfg, kn[i % nsteps], vn[i % nsteps], slots_all, c_)
+        lens[lay] += 1
+        attn_lens.append(lens[lay])
         if evs:
             evs[1].record(stream)
-        h.decode_attention_cached(cfg, qn[i], slots_all, max_len, cache, out, workspace=ws)
+        h.decode_attention_cached(cfg, qn[i % nsteps], slots_all, max_len, c_, out, workspace=ws)
         if evs:
             evs[2].record(stream)
 
@@ -437,7 +460,7 @@ def run_decode(args, h, dev, rank, world, peaks, traffic, seed, flush):
         step()
     torch.cuda.synchronize()
     barrier(world)
-    n_before = int(cache.seq_lens[0].item())
+    attn_lens.clear()
     if args.no_graph:
         evs = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
         n0 = h.kernel_launches()
@@ -451,7 +474,7 @@ def run_decode(args, h, dev, rank, world, peaks, traffic, seed, flush):
         attn_ms = [e[1].elapsed_time(e[2]) for e in evs]
         ms = max_over_ranks(sum(step_ms) / len(step_ms), world)
         attn_avg = max_over_ranks(sum(attn_ms) / len(attn_ms), world)
-        attn_ctx = [n_before + i + 1 for i in range(args.steps)]
+        attn_ctx = list(attn_lens)
     else:
         # One decode step per layer is a few tens of microseconds, so host launch latency
         # (ctypes + 3 launches) would be timed too: the K timed steps (append + attention,
@@ -466,7 +489,10 @@ def run_decode(args, h, dev, rank, world, peaks, traffic, seed, flush):
         launches = h.kernel_launches() - n0
         with torch.cuda.graph(g_attn):
             for i in range(args.steps):
-                h.decode_attention_cached(cfg, qn[(it[0] + i) % nsteps], slots_all, max_len, cache, out, workspace=ws)
+                lay = (it[0] + i) % n_layers
+                h.decode_attention_cached(cfg, qn[(it[0] + i) % nsteps], slots_all, max_len, caches[lay], out,
+                                          workspace=ws)
+        attn_ctx = [lens[(it[0] + i) % n_layers] for i in range(args.steps)]
         ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
         torch.cuda.synchronize()
         with ClockSampler(dev.index if dev.index is not None else 0) as clk:
@@ -482,14 +508,15 @@ def run_decode(args, h, dev, rank, world, peaks, traffic, seed, flush):
         torch.cuda.synchronize()
         ms = max_over_ranks(ev[0].elapsed_time(ev[1]) / args.steps, world)
         attn_avg = max_over_ranks(ev[2].elapsed_time(ev[3]) / args.steps, world)
-        attn_ctx = [n_before + args.steps] * args.steps
         # SURVEY f2 (HACK/SE ablation): the same attention launches with the code
         # sums recomputed from the codes every step instead of read from the summation cache
         os.environ["HACK_DECODE_NO_SE"] = "1"
         g_nose = torch.cuda.CUDAGraph()
         with torch.cuda.graph(g_nose):
             for i in range(args.steps):
-                h.decode_attention_cached(cfg, qn[(it[0] + i) % nsteps], slots_all, max_len, cache, out, workspace=ws)
+                lay = (it[0] + i) % n_layers
+                h.decode_attention_cached(cfg, qn[(it[0] + i) % nsteps], slots_all, max_len, caches[lay], out,
+                                          workspace=ws)
         del os.environ["HACK_DECODE_NO_SE"]
         torch.cuda.synchronize()
         ev[2].record(stream)
@@ -539,7 +566,10 @@ def run_decode(args, h, dev, rank, world, peaks, traffic, seed, flush):
         "no_summation_elimination": {"attn_ms": no_se_ms, "kv_gbs": avg_bytes / (no_se_ms * 1e-3) / 1e9,
                                      "slowdown": no_se_ms / attn_avg,
                                      "what": "code sums recomputed from the codes every step (HACK/SE, P:1036-1042)"}}
-    tok_s = B * world / (ms * 1e-3)
+    # strong scaling when heads are sharded (every rank serves the same B requests), weak
+    # (independent replicas) otherwise
+    req_factor = 1 if shard else world
+    tok_s = B * req_factor / (ms * 1e-3)
     # e2e: host q/k/v in, host out back, through hack_decode_attention (append + attend)
     qh = torch.empty((B, Hq, 128), dtype=torch.float16).pin_memory()
     kh = torch.empty((B, Hkv, 128), dtype=torch.float16).pin_memory()
@@ -563,17 +593,19 @@ def run_decode(args, h, dev, rank, world, peaks, traffic, seed, flush):
     tr = traffic.get("decode_attention", {}).get("dram_bytes_per_launch")
     return {
         "metric": "decode attn tokens/s", "value": tok_s, "unit": "tokens/s (per layer)",
-        "kv_gbs": gbs, "ms_per_step": ms, "attn_ms": attn_avg, "steps": args.steps,
-        "config": {"workload": DECODE_WORKLOAD, "batch": B, "context": ctx, "num_q_heads": Hq,
-                   "num_kv_heads": Hkv, "partition": Pi, "kv_bits": C3["bits"],
+        "scaling": "strong (KV heads sharded over ranks)" if shard else ("weak" if world > 1 else None),
+        "kv_gbs": gbs * world, "kv_gbs_per_gpu": gbs, "ms_per_step": ms, "attn_ms": attn_avg, "steps": args.steps,
+        "config": {"workload": DECODE_WORKLOAD, "batch": B, "context": ctx, "num_q_heads_per_rank": Hq,
+                   "num_kv_heads_per_rank": Hkv, "partition": Pi, "kv_bits": C3["bits"],
+                   "layers_cycled": n_layers,
                    "step": "hack_decode_append (a8) + hack_decode_attention_cached (a9)",
                    "timing": "eager launches" if args.no_graph else
                    "CUDA-graph replay of the K timed steps (each with its own inputs)",
-                   "l2": "cache 352 MB > L2"},
+                   "l2": f"{n_layers} layer cache(s) of {layer_bytes / 1e6:.0f} MB per rank cycled (> 2x L2)"},
         "roofline": {"bound": "hbm", "achieved": gbs, "peak": peaks["hbm"], "unit": "GB/s",
                      "frac": gbs / peaks["hbm"], "traffic": tr, "bytes_per_launch": avg_bytes,
                      "kernel": "decode attention (hack_decode_attention_cached)", "peak_src": peaks["src"]},
-        "e2e": {"value": B * world / (e2e_ms * 1e-3), "unit": "tokens/s (per layer)",
+        "e2e": {"value": B * req_factor / (e2e_ms * 1e-3), "unit": "tokens/s (per layer)",
                 "h2d_bytes_per_step": qh.nbytes + kh.nbytes + vh.nbytes, "d2h_bytes_per_step": oh.nbytes,
                 "ms_per_step": e2e_ms},
         "gpu_launches": launches,
