@@ -82,17 +82,15 @@ HACK_DEV uint8_t* page_ptr(const CacheView& cv, int slot, int blk, int h) {
 
 // K rows of every prompt token -> pages (a1).
 template <int BITS>
-__global__ void __launch_bounds__(256) ingest_k_kernel(const __half* __restrict__ k,
-                                                       const int32_t* __restrict__ cu_seqlens,
-                                                       const int32_t* __restrict__ slots, CacheView cv,
-                                                       KernelCfg kc) {
-  const int b = blockIdx.y;
+HACK_DEV void ingest_k_body(const __half* __restrict__ k, const int32_t* __restrict__ cu_seqlens,
+                            const int32_t* __restrict__ slots, const CacheView& cv, const KernelCfg& kc, int bx,
+                            int b, int tid) {
   const int start = cu_seqlens[b], L = cu_seqlens[b + 1] - start;
   const int slot = slots[b];
   const int H = kc.Hkv;
-  const int lane16 = threadIdx.x & 15;
-  const int r = blockIdx.x * 16 + (threadIdx.x >> 4);
-  if (blockIdx.x * 16 >= L * H) return;  // whole block out of range (uniform)
+  const int lane16 = tid & 15;
+  const int r = bx * 16 + (tid >> 4);
+  if (bx * 16 >= L * H) return;  // whole block out of range (uniform)
   const bool valid = r < L * H;
   const int rr = valid ? r : L * H - 1;
   const int t = rr / H, h = rr % H;
@@ -114,6 +112,14 @@ __global__ void __launch_bounds__(256) ingest_k_kernel(const __half* __restrict_
     reinterpret_cast<__half2*>(pg + PL.k_meta)[row * nb + beta] = make_meta(m, s);
     store_sum(pg + PL.k_sums, row * nb + beta, PL.sum_bytes, sum);
   }
+}
+
+template <int BITS>
+__global__ void __launch_bounds__(256) ingest_k_kernel(const __half* __restrict__ k,
+                                                       const int32_t* __restrict__ cu_seqlens,
+                                                       const int32_t* __restrict__ slots, CacheView cv,
+                                                       KernelCfg kc) {
+  ingest_k_body<BITS>(k, cu_seqlens, slots, cv, kc, blockIdx.x, blockIdx.y, threadIdx.x);
 }
 
 // Full V blocks -> pages (a2); ragged remainder -> FP16 tail (R10); seq_lens.
@@ -155,23 +161,27 @@ __global__ void __launch_bounds__(128) ingest_v_kernel(const __half* __restrict_
 // combined across the 4 warps in shared memory.  Same per-element op sequence and
 // Philox counters as quant_vcol (R1, R3, R4), hence the same codes.  Blocks j == nfull
 // copy the ragged remainder to the FP16 tail (R10); block 0 sets seq_lens.
+struct V64Red {
+  float lo[4][32], hi[4][32];
+  int sum[4][32];
+};
+
+// One (block, head, 32-channel group) unit on 128 threads; `bar` is the named barrier of
+// those 128 threads (two units share a CTA in the fused ingest kernel).
 template <int BITS>
-__global__ void __launch_bounds__(128) ingest_v64_kernel(const __half* __restrict__ v,
-                                                         const int32_t* __restrict__ cu_seqlens,
-                                                         const int32_t* __restrict__ slots, CacheView cv,
-                                                         KernelCfg kc) {
+HACK_DEV void ingest_v64_body(const __half* __restrict__ v, const int32_t* __restrict__ cu_seqlens,
+                              const int32_t* __restrict__ slots, const CacheView& cv, const KernelCfg& kc, int bx,
+                              int b, int tid, int bar, V64Red& red) {
   constexpr int PI = 64, qmax = (1 << BITS) - 1;
-  __shared__ float red_lo[4][32], red_hi[4][32];
-  __shared__ int red_sum[4][32];
-  const int b = blockIdx.y;
+  auto sync = [&]() { asm volatile("bar.sync %0, 128;" ::"r"(bar) : "memory"); };
   const int start = cu_seqlens[b], L = cu_seqlens[b + 1] - start;
   const int slot = slots[b];
   const int H = kc.Hkv;
   const int nfull = L / PI;
-  const int cg = blockIdx.x & 3, h = (blockIdx.x >> 2) % H, j = (blockIdx.x >> 2) / H;
-  const int q = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int cg = bx & 3, h = (bx >> 2) % H, j = (bx >> 2) / H;
+  const int q = tid >> 5, lane = tid & 31;
   const int c = 32 * cg + lane;
-  if (blockIdx.x == 0 && threadIdx.x == 0) cv.seq_lens[slot] = L;
+  if (bx == 0 && tid == 0) cv.seq_lens[slot] = L;
   if (j > nfull) return;
   const __half* xc = v + ((int64_t)(start + j * PI) * H + h) * 128 + c;
   const int64_t ts = (int64_t)H * 128;
@@ -189,13 +199,13 @@ __global__ void __launch_bounds__(128) ingest_v64_kernel(const __half* __restric
     lo = fminf(lo, x[i]);
     hi = fmaxf(hi, x[i]);
   }
-  red_lo[q][lane] = lo;
-  red_hi[q][lane] = hi;
-  __syncthreads();
+  red.lo[q][lane] = lo;
+  red.hi[q][lane] = hi;
+  sync();
 #pragma unroll
   for (int w = 0; w < 4; ++w) {
-    lo = fminf(lo, red_lo[w][lane]);
-    hi = fmaxf(hi, red_hi[w][lane]);
+    lo = fminf(lo, red.lo[w][lane]);
+    hi = fmaxf(hi, red.hi[w][lane]);
   }
   const QMeta qm = meta_fp16(lo, hi, qmax);
   const uint32_t rng_id = cv.rng_ids[slot];
@@ -229,13 +239,40 @@ __global__ void __launch_bounds__(128) ingest_v64_kernel(const __half* __restric
     reinterpret_cast<uint32_t*>(pg + PL.v_codes + c * 16)[q] = (uint32_t)packed;
   else
     reinterpret_cast<uint2*>(pg + PL.v_codes + c * 32)[q] = make_uint2((uint32_t)packed, (uint32_t)(packed >> 32));
-  red_sum[q][lane] = sum;
-  __syncthreads();
+  red.sum[q][lane] = sum;
+  sync();
   if (q == 0) {
-    const int tot = red_sum[0][lane] + red_sum[1][lane] + red_sum[2][lane] + red_sum[3][lane];
+    const int tot = red.sum[0][lane] + red.sum[1][lane] + red.sum[2][lane] + red.sum[3][lane];
     reinterpret_cast<__half2*>(pg + PL.v_meta)[c] = make_meta(qm.m, qm.s);
     store_sum(pg + PL.v_sums, c, PL.sum_bytes, tot);
   }
+}
+
+template <int BITS>
+__global__ void __launch_bounds__(128) ingest_v64_kernel(const __half* __restrict__ v,
+                                                         const int32_t* __restrict__ cu_seqlens,
+                                                         const int32_t* __restrict__ slots, CacheView cv,
+                                                         KernelCfg kc) {
+  __shared__ V64Red red;
+  ingest_v64_body<BITS>(v, cu_seqlens, slots, cv, kc, blockIdx.x, blockIdx.y, threadIdx.x, 0, red);
+}
+
+// K rows and V blocks of a prompt in ONE launch (Pi = 64): blocks [0, nk) quantize K rows,
+// the rest carry two V units each (threads 0-127 and 128-255), so the two ALU-bound
+// quantizers overlap instead of running back to back.
+template <int BITS>
+__global__ void __launch_bounds__(256) ingest_kv64_kernel(const __half* __restrict__ k, const __half* __restrict__ v,
+                                                          const int32_t* __restrict__ cu_seqlens,
+                                                          const int32_t* __restrict__ slots, CacheView cv,
+                                                          KernelCfg kc, int nk, int nv) {
+  __shared__ V64Red red[2];
+  if ((int)blockIdx.x < nk) {
+    ingest_k_body<BITS>(k, cu_seqlens, slots, cv, kc, blockIdx.x, blockIdx.y, threadIdx.x);
+    return;
+  }
+  const int half = threadIdx.x >> 7;
+  const int vb = 2 * ((int)blockIdx.x - nk) + half;
+  if (vb < nv) ingest_v64_body<BITS>(v, cu_seqlens, slots, cv, kc, vb, blockIdx.y, threadIdx.x & 127, 1 + half, red[half]);
 }
 
 // -------------------------------------------------------------------------- decode append (a8)
@@ -341,6 +378,16 @@ cudaError_t launch_ingest(const KernelCfg& kc, const void* k, const void* v, con
   dim3 gv(((max_seqlen / kc.Pi + 1) * kc.Hkv * 128 + 127) / 128, batch);
   dim3 gv64((max_seqlen / kc.Pi + 1) * kc.Hkv * 4, batch);  // (block, head, 32-channel group)
   const bool v64 = kc.Pi == 64;
+  if (v64) {
+    const int nk = gk.x, nv = gv64.x;
+    dim3 g(nk + (nv + 1) / 2, batch);
+    if (kc.bits == 2)
+      ingest_kv64_kernel<2><<<g, 256, 0, st>>>(kh, vh, cu_seqlens, slots, cv, kc, nk, nv);
+    else
+      ingest_kv64_kernel<4><<<g, 256, 0, st>>>(kh, vh, cu_seqlens, slots, cv, kc, nk, nv);
+    note_launch(1);
+    return cudaGetLastError();
+  }
   if (kc.bits == 2) {
     ingest_k_kernel<2><<<gk, 256, 0, st>>>(kh, cu_seqlens, slots, cv, kc);
     if (v64)
