@@ -44,6 +44,10 @@ constexpr int BM = 128;
 constexpr int BN = 64;
 constexpr int NS = 4;          // page stages
 constexpr int NB = 3;          // K/V/P tile buffer sets
+#ifndef HACK_PRE_NDB
+#define HACK_PRE_NDB 2
+#endif
+constexpr int NDB = HACK_PRE_NDB;  // D' (PV accumulator) TMEM buffers
 constexpr int kThreads = 640;  // 4 service warps + 2 S warpgroups + 2 O warpgroups
 constexpr int NSW = 256;       // S-warpgroup threads
 constexpr int NOW = 256;       // O-warpgroup threads
@@ -218,11 +222,11 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_tc_kernel(
         }
         const int jj = j - 1;  // PV of the previous tile, after QK of this one (overlap)
         if (jj >= 0 && jj < nfull) {
-          const int bd = jj & 1, bq = jj % NB;
+          const int bd = jj % NDB, bq = jj % NB;
           const uint32_t ph = (jj / NB) & 1;
           ptx::mbar_wait(&sm.p_ready[bq], ph);
           ptx::mbar_wait(&sm.v_ready[bq], ph);
-          ptx::mbar_wait(&sm.d_free[bd], ((jj >> 1) & 1) ^ 1);
+          ptx::mbar_wait(&sm.d_free[bd], ((jj / NDB) & 1) ^ 1);
           ptx::tc_fence_after();
           if (lane == 0) {
             const uint32_t pa = ptx::smem_u32(sm.p[bq]), va = ptx::smem_u32(sm.v[bq]);
@@ -590,7 +594,7 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_tc_kernel(
     for (int x = 0; x < 32; ++x) o2[x] = make_float2(0.f, 0.f);
 #pragma unroll 1
     for (int j = 0; j < nkt; ++j) {
-      const int bj = j % NB, bd = j & 1;
+      const int bj = j % NB, bd = j % NDB;
       const uint32_t ph = (j / NB) & 1;
       ptx::mbar_wait(&sm.p_ready[bj], ph);
       const float4 pi4 = sm.pinfo[bj][r];
@@ -606,7 +610,7 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_tc_kernel(
         const float2 xp2 = make_float2(pi4.z * (float)sps, pi4.z * (float)sps);
         const float2 mp2 = make_float2(pi4.w + 128.f * pi4.z, pi4.w + 128.f * pi4.z);
         ptx::mbar_wait(&sm.v_ready[bj], ph);
-        ptx::mbar_wait(&sm.d_full[bd], (j >> 1) & 1);
+        ptx::mbar_wait(&sm.d_full[bd], (j / NDB) & 1);
         ptx::tc_fence_after();
 #pragma unroll
         for (int h = 0; h < 4; ++h) {
