@@ -194,3 +194,10 @@ def test_no_se_ablation_bit_identical(monkeypatch):
         h.decode_attention_cached(cfg, torch.from_numpy(qd[0]).cuda(), sl, 2100, cache, o)
         outs.append(o.cpu().numpy())
     assert np.array_equal(outs[0].view(np.uint32), outs[1].view(np.uint32))
+
+
+def test_decode_long_context_tiny_cta_ranges():
+    """One 96K-token request (G = 4): the persistent split gives every CTA a range of only
+    a few pages (odd sizes, single-page items, segments that start mid-pair) and the
+    merge combines ~600 CTAs x warps partials of one unit."""
+    run_decode(att.Config(Hq=4, Hkv=1, Pi=64, bits=2, seed=31), [96000], 2)
