@@ -43,6 +43,9 @@ constexpr int PI = 64;
 #ifndef HACK_DEC_NSTG
 #define HACK_DEC_NSTG 9
 #endif
+#ifndef HACK_DEC_SPLIT
+#define HACK_DEC_SPLIT 0
+#endif
 #ifndef HACK_DEC_CTAS
 #define HACK_DEC_CTAS 4
 #endif
@@ -65,7 +68,7 @@ struct PairSmem {
   } w[NW];
   int range_b0, range_base;  // request holding the CTA's first page, flattened offset of its first unit
   int R, P;
-  uint64_t full[NSTG], empty[NSTG];
+  uint64_t full[NSTG], fullv[NSTG], empty[NSTG];  // fullv: the V half of a split page copy
 };
 
 HACK_DEV void mma16832(uint32_t (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3, uint32_t b0,
@@ -228,6 +231,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
   if (tid == 0) {
     for (int s = 0; s < NSTG; ++s) {
       ptx::mbar_init(&sm.full[s], 1);
+      ptx::mbar_init(&sm.fullv[s], 1);
       ptx::mbar_init(&sm.empty[s], 1);
     }
     ptx::fence_mbar_init();
@@ -312,9 +316,21 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
             while (!ptx::mbar_try_wait_sleep(&sm.empty[st], ((k / NSTG) & 1) ^ 1)) {
             }
 #endif
+#if HACK_DEC_SPLIT
+            // two copies: the K half (codes + meta + sums) lands first and QK can start
+            const uint32_t kb = (uint32_t)kc.pl.v_codes;
+            ptx::mbar_arrive_expect_tx(&sm.full[st], kb);
+#else
             ptx::mbar_arrive_expect_tx(&sm.full[st], PB);
+#endif
             const uint8_t* pg = cv.pages + ((int64_t)pid * cv.num_kv_heads + s.hk) * cv.page_bytes;
+#if HACK_DEC_SPLIT
+            ptx::bulk_g2s(sm.stage[st], pg, kb, &sm.full[st]);
+            ptx::mbar_arrive_expect_tx(&sm.fullv[st], PB - kb);
+            ptx::bulk_g2s(sm.stage[st] + kb, pg + kb, PB - kb, &sm.fullv[st]);
+#else
             ptx::bulk_g2s(sm.stage[st], pg, PB, &sm.full[st]);
+#endif
           }
           __syncwarp();
         }
@@ -423,6 +439,10 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
           for (int mt = 0; mt < 4; ++mt) sbv[mt][0] = sbv[mt][1] = -INFINITY;
         }
         __syncwarp();  // K codes/meta of the pair and the K coefficients are dead from here on
+#if HACK_DEC_SPLIT
+        ptx::mbar_wait(&sm.fullv[sA], (kA / NSTG) & 1);
+        if (hasB) ptx::mbar_wait(&sm.fullv[sB], (kB / NSTG) & 1);
+#endif
 
         // ---- V coefficients of the pair (cached sums, SE): channel c -> (A, B) pairs
         float4* vc_lo = reinterpret_cast<float4*>(pgA + PL.k_codes);  // channels 0..63
