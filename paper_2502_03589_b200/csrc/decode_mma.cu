@@ -26,8 +26,18 @@ namespace hack {
 namespace {
 
 constexpr int PI = 64;
-constexpr int NW = 4;        // compute warps per CTA
-constexpr int NSTG = 8;      // page stages per CTA
+#ifndef HACK_DMMA_NW
+#define HACK_DMMA_NW 4
+#endif
+#ifndef HACK_DMMA_NSTG
+#define HACK_DMMA_NSTG 8
+#endif
+#ifndef HACK_DMMA_CTAS
+#define HACK_DMMA_CTAS 3
+#endif
+constexpr int NW = HACK_DMMA_NW;      // compute warps per CTA
+constexpr int NSTG = HACK_DMMA_NSTG;  // page stages per CTA
+constexpr int kCtas = HACK_DMMA_CTAS;  // resident CTAs per SM (launch bounds)
 constexpr int kThreads = (NW + 1) * 32;
 constexpr uint32_t kMagicI = 0x4B000000u;  // bits of 2^23
 
@@ -69,7 +79,7 @@ HACK_DEV uint32_t plane(uint32_t w, int sh) {
 // Token / channel index held by byte i of plane `tig` of packed word W (16-code words at
 // b=2: index 16W + 4i + tig; at b=4 words hold 8 codes: index 8W + 2i + tig, tig in {0,1}).
 template <int BITS>
-__global__ void __launch_bounds__(kThreads, 3) decode_mma_kernel(const __half* __restrict__ q_new,
+__global__ void __launch_bounds__(kThreads, kCtas) decode_mma_kernel(const __half* __restrict__ q_new,
                                                               const int32_t* __restrict__ slots, CacheView cv,
                                                               KernelCfg kc, float* __restrict__ part, int nsplit,
                                                               uint8_t* __restrict__ dbg_pcodes, int64_t dbg_stride) {
@@ -100,8 +110,8 @@ __global__ void __launch_bounds__(kThreads, 3) decode_mma_kernel(const __half* _
     ptx::fence_mbar_init();
   }
   // ---- (a3) quantize the G query rows (8-bit SR, fp32 meta): warps 0-3, 16 lanes per row
-  if (warp < NW) {
-    const int row = warp * 2 + (lane >> 4), lane16 = lane & 15;  // rows 0..7
+  for (int row0 = 2 * warp; warp < NW && row0 < 8; row0 += 2 * NW) {
+    const int row = row0 + (lane >> 4), lane16 = lane & 15;  // rows 0..7
     const int rr = min(row, G - 1);
     const int hq = hk * G + rr;
     const uint4 raw = reinterpret_cast<const uint4*>(q_new + ((int64_t)b * kc.Hq + hq) * 128)[lane16];
@@ -517,7 +527,7 @@ int decode_nsplit(const KernelCfg& kc, int batch, int max_seqlen) {
   const int max_pages = (max_seqlen + PI - 1) / PI;
   const int units = batch * kc.Hkv;
   // aim for ~4 waves of resident CTAs (148 SMs x 3), at least ~8 pages per split
-  int ns = (148 * 3 * 4 + units - 1) / units;
+  int ns = (148 * kCtas * 4 + units - 1) / units;
   ns = max(1, min(ns, (max_pages + 7) / 8));
   return min(ns, 64);
 }
