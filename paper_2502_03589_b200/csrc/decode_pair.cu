@@ -214,29 +214,13 @@ HACK_DEV void qk_page(const uint8_t* pg, const PageLayout& PL, const float4* kcs
   }
 }
 
-template <bool DBG, bool SE>
-__global__ void __launch_bounds__(kThreads, kCtasPerSm)
-    decode_pair_kernel(const __half* __restrict__ q_new, const int32_t* __restrict__ slots, int batch, CacheView cv,
-                       KernelCfg kc, int* __restrict__ ws_meta, float* __restrict__ part,
-                       uint8_t* __restrict__ dbg_pcodes, int64_t dbg_stride) {
-  constexpr int qkm = 3;
-  extern __shared__ __align__(128) uint8_t smem_raw[];
-  PairSmem& sm = *reinterpret_cast<PairSmem*>(smem_raw);
-  const int G = kc.G, Hkv = kc.Hkv;
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int g = lane >> 2, tig = lane & 3;
+// This CTA's page range of the flattened (request, KV head, page) sequence: P = total
+// pages, R = ceil(P / grid); the request holding the first page and its flattened offset.
+// CTA 0 also publishes the per-request offsets and page counts for the merge kernel.
+template <class SMT>
+HACK_DEV void locate_range(SMT& sm, const CacheView& cv, const int32_t* __restrict__ slots, int batch, int Hkv,
+                           int* __restrict__ ws_meta, int warp, int lane) {
   const int c = blockIdx.x;
-  const PageLayout PL = kc.pl;
-
-  if (tid == 0) {
-    for (int s = 0; s < NSTG; ++s) {
-      ptx::mbar_init(&sm.full[s], 1);
-      ptx::mbar_init(&sm.fullv[s], 1);
-      ptx::mbar_init(&sm.empty[s], 1);
-    }
-    ptx::fence_mbar_init();
-  }
-  // ---- locate this CTA's page range: P = total pages of all units, R = ceil(P / grid)
   if (warp == 0) {
     int P = 0;
     for (int b0 = 0; b0 < batch; b0 += 32) {
@@ -288,54 +272,86 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
       }
     }
   }
+}
+
+// Producer warp: streams the CTA's pages in order into an N-slot ring (cp.async.bulk).
+template <int N, class SMT>
+HACK_DEV void produce_pages(SMT& sm, SegWalker walk, const CacheView& cv, const int32_t* __restrict__ slots,
+                            int Hkv, const KernelCfg& kc, int lane) {
+    // ------------------------------------------------------------------ producer
+  // The whole warp walks the segments; block-table entries are fetched 32 pages at a
+  // time with one coalesced load, so the issuing lane never waits on a dependent global
+  // load between two page copies (one such wait per page capped the issue rate).
+  Seg s;
+  int k = 0;
+  while (walk.next(cv, slots, Hkv, s)) {
+    const int32_t* bt = cv.block_table + (int64_t)slots[s.b] * cv.max_pages_per_req;
+    for (int p0 = s.p0; p0 < s.p1; p0 += 32) {
+      const int n = min(32, s.p1 - p0);
+      const int ent = lane < n ? bt[p0 + lane] : 0;
+      for (int x = 0; x < n; ++x, ++k) {
+        const int pid = __shfl_sync(0xffffffffu, ent, x);
+        if (lane == 0) {
+          const int st = k % N;
+#ifdef HACK_DEC_SPIN
+          while (!ptx::mbar_try_wait(&sm.empty[st], ((k / N) & 1) ^ 1)) {
+          }
+#else
+          // sleep-wait: a spinning producer lane steals issue slots from the compute warps
+          while (!ptx::mbar_try_wait_sleep(&sm.empty[st], ((k / N) & 1) ^ 1)) {
+          }
+#endif
+#if HACK_DEC_SPLIT
+          // two copies: the K half (codes + meta + sums) lands first and QK can start
+          const uint32_t kb = (uint32_t)kc.pl.v_codes;
+          ptx::mbar_arrive_expect_tx(&sm.full[st], kb);
+#else
+          ptx::mbar_arrive_expect_tx(&sm.full[st], PB);
+#endif
+          const uint8_t* pg = cv.pages + ((int64_t)pid * cv.num_kv_heads + s.hk) * cv.page_bytes;
+#if HACK_DEC_SPLIT
+          ptx::bulk_g2s(sm.stage[st], pg, kb, &sm.full[st]);
+          ptx::mbar_arrive_expect_tx(&sm.fullv[st], PB - kb);
+          ptx::bulk_g2s(sm.stage[st] + kb, pg + kb, PB - kb, &sm.fullv[st]);
+#else
+          ptx::bulk_g2s(sm.stage[st], pg, PB, &sm.full[st]);
+#endif
+        }
+        __syncwarp();
+      }
+    }
+  }
+}
+
+template <bool DBG, bool SE>
+__global__ void __launch_bounds__(kThreads, kCtasPerSm)
+    decode_pair_kernel(const __half* __restrict__ q_new, const int32_t* __restrict__ slots, int batch, CacheView cv,
+                       KernelCfg kc, int* __restrict__ ws_meta, float* __restrict__ part,
+                       uint8_t* __restrict__ dbg_pcodes, int64_t dbg_stride) {
+  constexpr int qkm = 3;
+  extern __shared__ __align__(128) uint8_t smem_raw[];
+  PairSmem& sm = *reinterpret_cast<PairSmem*>(smem_raw);
+  const int G = kc.G, Hkv = kc.Hkv;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int g = lane >> 2, tig = lane & 3;
+  const int c = blockIdx.x;
+  const PageLayout PL = kc.pl;
+
+  if (tid == 0) {
+    for (int s = 0; s < NSTG; ++s) {
+      ptx::mbar_init(&sm.full[s], 1);
+      ptx::mbar_init(&sm.fullv[s], 1);
+      ptx::mbar_init(&sm.empty[s], 1);
+    }
+    ptx::fence_mbar_init();
+  }
+  locate_range(sm, cv, slots, batch, Hkv, ws_meta, warp, lane);
   __syncthreads();
   const int R = sm.R, P = sm.P;
   SegWalker walk{sm.range_b0, sm.range_base, min(c * R, P), min(c * R + R, P)};
 
   if (warp == NW) {
-    // ------------------------------------------------------------------ producer
-    // The whole warp walks the segments; block-table entries are fetched 32 pages at a
-    // time with one coalesced load, so the issuing lane never waits on a dependent global
-    // load between two page copies (one such wait per page capped the issue rate).
-    Seg s;
-    int k = 0;
-    while (walk.next(cv, slots, Hkv, s)) {
-      const int32_t* bt = cv.block_table + (int64_t)slots[s.b] * cv.max_pages_per_req;
-      for (int p0 = s.p0; p0 < s.p1; p0 += 32) {
-        const int n = min(32, s.p1 - p0);
-        const int ent = lane < n ? bt[p0 + lane] : 0;
-        for (int x = 0; x < n; ++x, ++k) {
-          const int pid = __shfl_sync(0xffffffffu, ent, x);
-          if (lane == 0) {
-            const int st = k % NSTG;
-#ifdef HACK_DEC_SPIN
-            while (!ptx::mbar_try_wait(&sm.empty[st], ((k / NSTG) & 1) ^ 1)) {
-            }
-#else
-            // sleep-wait: a spinning producer lane steals issue slots from the compute warps
-            while (!ptx::mbar_try_wait_sleep(&sm.empty[st], ((k / NSTG) & 1) ^ 1)) {
-            }
-#endif
-#if HACK_DEC_SPLIT
-            // two copies: the K half (codes + meta + sums) lands first and QK can start
-            const uint32_t kb = (uint32_t)kc.pl.v_codes;
-            ptx::mbar_arrive_expect_tx(&sm.full[st], kb);
-#else
-            ptx::mbar_arrive_expect_tx(&sm.full[st], PB);
-#endif
-            const uint8_t* pg = cv.pages + ((int64_t)pid * cv.num_kv_heads + s.hk) * cv.page_bytes;
-#if HACK_DEC_SPLIT
-            ptx::bulk_g2s(sm.stage[st], pg, kb, &sm.full[st]);
-            ptx::mbar_arrive_expect_tx(&sm.fullv[st], PB - kb);
-            ptx::bulk_g2s(sm.stage[st] + kb, pg + kb, PB - kb, &sm.fullv[st]);
-#else
-            ptx::bulk_g2s(sm.stage[st], pg, PB, &sm.full[st]);
-#endif
-          }
-          __syncwarp();
-        }
-      }
-    }
+    produce_pages<NSTG>(sm, walk, cv, slots, Hkv, kc, lane);
     return;
   }
 
@@ -634,6 +650,339 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
   }
 }
 
+// ============================================================================ G in (4, 8]
+// The same pipeline for GQA groups of up to 8 query rows (C4, Llama-3.1-70B: G = 8).
+// S^T = K' Q'^T runs on TWO n-tiles of (row, d-block) columns (rows 0-3 and 4-7), so a lane
+// holds rows tig and 4 + tig.  P'V' runs per page with the 8 N-columns = query rows (the
+// 8 rows fill them without page pairing): a lane holds rows 2 tig, 2 tig + 1 and the
+// per-row P meta / rescale factors move between the two row ownerships through a small
+// per-warp table.  Items are single pages.
+#ifndef HACK_DEC8_NSTG
+#define HACK_DEC8_NSTG 8
+#endif
+#ifndef HACK_DEC8_CTAS
+#define HACK_DEC8_CTAS 4
+#endif
+constexpr int NSTG8 = HACK_DEC8_NSTG;
+constexpr int kCtas8 = HACK_DEC8_CTAS;
+
+struct G8Smem {
+  uint8_t stage[NSTG8][PB];
+  struct Warp {
+    float4 scr[64][2];      // K coefficients of the page in QK; V coefficients (float4 per channel) in PV
+    uint8_t qcode[8][128];  // Q' rows of the current unit
+    float4 qc[8][2];        // per row: (QA0, QA1, QX0, QX1), (QM0, QM1, RC0, RC1)
+    float4 rowinfo[8];      // per row, this page: alpha, s_p, m_p, SP (as float)
+  } w[NW];
+  int range_b0, range_base;
+  int R, P;
+  uint64_t full[NSTG8], fullv[NSTG8], empty[NSTG8];
+};
+
+template <bool DBG>
+__global__ void __launch_bounds__(kThreads, kCtas8)
+    decode_g8_kernel(const __half* __restrict__ q_new, const int32_t* __restrict__ slots, int batch, CacheView cv,
+                     KernelCfg kc, int* __restrict__ ws_meta, float* __restrict__ part,
+                     uint8_t* __restrict__ dbg_pcodes, int64_t dbg_stride) {
+  constexpr int qkm = 3;
+  extern __shared__ __align__(128) uint8_t smem_raw[];
+  G8Smem& sm = *reinterpret_cast<G8Smem*>(smem_raw);
+  const int G = kc.G, Hkv = kc.Hkv;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int g = lane >> 2, tig = lane & 3;
+  const int c = blockIdx.x;
+  const PageLayout PL = kc.pl;
+  if (tid == 0) {
+    for (int s = 0; s < NSTG8; ++s) {
+      ptx::mbar_init(&sm.full[s], 1);
+      ptx::mbar_init(&sm.fullv[s], 1);
+      ptx::mbar_init(&sm.empty[s], 1);
+    }
+    ptx::fence_mbar_init();
+  }
+  locate_range(sm, cv, slots, batch, Hkv, ws_meta, warp, lane);
+  __syncthreads();
+  const int R = sm.R, P = sm.P;
+  SegWalker walk{sm.range_b0, sm.range_base, min(c * R, P), min(c * R + R, P)};
+  if (warp == NW) {
+    produce_pages<NSTG8>(sm, walk, cv, slots, Hkv, kc, lane);
+    return;
+  }
+
+  typename G8Smem::Warp& ws = sm.w[warp];
+  const float cscale = 1.4426950408889634f / sqrtf(128.f);
+  const int n0 = 2 * tig, n1 = 2 * tig + 1;  // rows of this lane in the PV fragments
+  Seg s;
+  int it_base = 0, k_base = 0;
+  while (walk.next(cv, slots, Hkv, s)) {
+    const int slot = slots[s.b];
+    const int len = cv.seq_lens[slot];
+    const int nfull = len / PI;
+    const int nitems = s.p1 - s.p0;  // single pages
+    const int my0 = ((warp - it_base) % NW + NW) % NW;
+    const int u = s.b * Hkv + s.hk;
+    float m_run[2] = {-INFINITY, -INFINITY}, l_run[2] = {0.f, 0.f};  // rows tig, 4 + tig
+    float2 o[8][2];  // [m-tile][channel g / g+8] -> rows (n0, n1)
+#pragma unroll
+    for (int mt = 0; mt < 8; ++mt) o[mt][0] = o[mt][1] = f2(0.f, 0.f);
+
+    if (my0 < nitems) {
+      const uint32_t rng_id = cv.rng_ids[slot];
+      // ---- (a3) quantize the unit's 8 query rows (8-bit SR, fp32 meta), 16 lanes per row
+#pragma unroll 1
+      for (int r2 = 0; r2 < 4; ++r2) {
+        const int row = 2 * r2 + (lane >> 4), lane16 = lane & 15;
+        const int hq = s.hk * G + min(row, G - 1);
+        const uint4 raw = reinterpret_cast<const uint4*>(q_new + ((int64_t)s.b * kc.Hq + hq) * 128)[lane16];
+        uint64_t packed;
+        float m, sc;
+        int sum;
+        quant_row16<8, false>(raw, lane16, PI, len - 1, kc.seed, rng_id,
+                              stream_c3(kc.layer, kTagQ, kc.head_base * G + hq), kc.q_round, packed, m, sc, sum);
+        const bool ok = row < G;
+        *reinterpret_cast<uint2*>(&ws.qcode[row][lane16 * 8]) =
+            ok ? make_uint2((uint32_t)packed, (uint32_t)(packed >> 32)) : make_uint2(0u, 0u);
+        const int beta = lane16 >> 3;
+        float* qcf = reinterpret_cast<float*>(&ws.qc[row][0]);
+        if ((lane16 & 7) == 0) {
+          qcf[beta] = ok ? cscale * sc * 0.25f : 0.f;
+          qcf[2 + beta] = ok ? cscale * sc * ((float)sum - 127.5f * PI) : 0.f;
+          qcf[4 + beta] = ok ? cscale * (m + 127.5f * sc) : 0.f;
+          qcf[6 + beta] = __int_as_float(ok ? -(2 * qkm * sum - PI * 255 * qkm) : 0);
+        }
+      }
+      __syncwarp();
+      // B fragments of Q' for n-tile nt, column n = g = (row 4 nt + (g>>1), block g&1)
+      uint32_t qb[2][4][2];
+#pragma unroll
+      for (int nt = 0; nt < 2; ++nt) {
+        const int r = 4 * nt + (g >> 1);
+        const bool live = r < G && (tig >> 1) == (g & 1);
+#pragma unroll
+        for (int ks = 0; ks < 4; ++ks) {
+          const int q = ks == 0 ? 0 : (ks == 1 ? 2 : (ks == 2 ? 1 : 3));
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            uint32_t v = 0;
+#pragma unroll
+            for (int i = 0; i < 4; ++i) v |= (uint32_t)ws.qcode[r][32 * tig + 16 * h + 4 * i + q] << (8 * i);
+            qb[nt][ks][h] = live ? v : 0u;
+          }
+        }
+      }
+      float2 QA[2], QX[2], QM[2];
+      uint32_t rc[2][2];
+#pragma unroll
+      for (int nt = 0; nt < 2; ++nt) {
+        const float4 q0 = ws.qc[4 * nt + tig][0], q1 = ws.qc[4 * nt + tig][1];
+        QA[nt] = f2(q0.x, q0.y);
+        QX[nt] = f2(q0.z, q0.w);
+        QM[nt] = f2(q1.x, q1.y);
+        rc[nt][0] = kMagic + __float_as_uint(q1.z);
+        rc[nt][1] = kMagic + __float_as_uint(q1.w);
+      }
+
+#pragma unroll 1
+      for (int j = my0; j < nitems; j += NW) {
+        const int k = k_base + j;
+        const int st = k % NSTG8;
+        const int jp = s.p0 + j;
+        const bool committed = jp < nfull;
+        const int nk = committed ? PI : len - jp * PI;
+        uint8_t* pg = sm.stage[st];
+        ptx::mbar_wait(&sm.full[st], (k / NSTG8) & 1);
+        stage_kc<true>(pg, PL, &ws.scr[0][0], lane);
+        __syncwarp();
+        // ---- (a4) S^T for the 8 rows: sc[nt][mt][hh] = row 4 nt + tig, token 16 mt + g + 8 hh
+        float sc[2][4][2];
+        float mx[2] = {-INFINITY, -INFINITY}, mn[2] = {INFINITY, INFINITY};
+        const float4* kcs = &ws.scr[0][0];
+#pragma unroll
+        for (int mt = 0; mt < 4; ++mt) {
+          const int t0 = 16 * mt + g, t1 = t0 + 8;
+          const uint2 w0 = *reinterpret_cast<const uint2*>(pg + PL.k_codes + t0 * 32 + 8 * tig);
+          const uint2 w1 = *reinterpret_cast<const uint2*>(pg + PL.k_codes + t1 * 32 + 8 * tig);
+          const Planes a0 = planes2(w0.x), a1 = planes2(w1.x), a2 = planes2(w0.y), a3 = planes2(w1.y);
+#pragma unroll
+          for (int nt = 0; nt < 2; ++nt) {
+            uint32_t acc0[4], acc1[4];
+            mma16832c(acc0, a0.p0, a1.p0, a2.p0, a3.p0, qb[nt][0][0], qb[nt][0][1], 0u, 0u);
+            mma16832(acc0, a0.p2, a1.p2, a2.p2, a3.p2, qb[nt][1][0], qb[nt][1][1]);
+            mma16832c(acc1, a0.p1, a1.p1, a2.p1, a3.p1, qb[nt][2][0], qb[nt][2][1], rc[nt][0], rc[nt][1]);
+            mma16832(acc1, a0.p3, a1.p3, a2.p3, a3.p3, qb[nt][3][0], qb[nt][3][1]);
+#pragma unroll
+            for (int hh = 0; hh < 2; ++hh) {
+              const int t = hh ? t1 : t0;
+              const float4 c0 = kcs[2 * t], c1 = kcs[2 * t + 1];
+              const uint32_t e0 = (acc0[2 * hh] << 2) + acc1[2 * hh], e1 = (acc0[2 * hh + 1] << 2) + acc1[2 * hh + 1];
+              const float2 e = ptx::fadd2(asf2(e0, e1), f2(c1.z, c1.w));
+              const float2 s2 = ptx::ffma2(QA[nt], ptx::fmul2(f2(c0.x, c0.y), e),
+                                           ptx::ffma2(QX[nt], f2(c0.z, c0.w), ptx::fmul2(QM[nt], f2(c1.x, c1.y))));
+              float sv = s2.x + s2.y;
+              if (t >= nk) sv = -INFINITY;
+              sc[nt][mt][hh] = sv;
+              mx[nt] = fmaxf(mx[nt], sv);
+              if (t < nk) mn[nt] = fminf(mn[nt], sv);
+            }
+          }
+        }
+        __syncwarp();  // K codes/meta and K coefficients are dead
+        // ---- (a5) online softmax, rows tig and 4 + tig
+        float al[2], ls[2] = {0.f, 0.f};
+#pragma unroll
+        for (int nt = 0; nt < 2; ++nt) {
+#pragma unroll
+          for (int o2 = 4; o2 < 32; o2 <<= 1) {
+            mx[nt] = fmaxf(mx[nt], __shfl_xor_sync(0xffffffffu, mx[nt], o2));
+            mn[nt] = fminf(mn[nt], __shfl_xor_sync(0xffffffffu, mn[nt], o2));
+          }
+          const float mnew = fmaxf(m_run[nt], mx[nt]);
+          al[nt] = m_run[nt] == -INFINITY ? 0.f : ex2(m_run[nt] - mnew);
+          m_run[nt] = mnew;
+#pragma unroll
+          for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+            for (int hh = 0; hh < 2; ++hh) {
+              sc[nt][mt][hh] = ex2(sc[nt][mt][hh] - mnew);
+              ls[nt] += sc[nt][mt][hh];
+            }
+#pragma unroll
+          for (int o2 = 4; o2 < 32; o2 <<= 1) ls[nt] += __shfl_xor_sync(0xffffffffu, ls[nt], o2);
+          l_run[nt] = l_run[nt] * al[nt] + ls[nt];
+        }
+        uint8_t* pcode = pg + PL.k_meta;                          // [row 8][64] in B-fragment order
+        float* ptl = reinterpret_cast<float*>(pg + PL.k_codes);    // [row 8][64] p~ of a partial page
+        if (committed) {
+          // ---- (a6) P' per row (RN 8-bit on p~) + the row table for the PV lanes
+          const int base = 4 * (g & 3) + (g >> 2);
+#pragma unroll
+          for (int nt = 0; nt < 2; ++nt) {
+            const int row = 4 * nt + tig;
+            QMeta pm = meta_fp32(ex2(mn[nt] - m_run[nt]), ex2(mx[nt] - m_run[nt]), 255);
+            if (!(pm.s > 1e-30f)) { pm.s = 0.f; pm.inv = 0.f; }
+            const float nlo = -pm.m * pm.inv;
+            uint32_t sp = 0;
+#pragma unroll
+            for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+              for (int hh = 0; hh < 2; ++hh) {
+                const float y = fmaf(sc[nt][mt][hh], pm.inv, nlo) + kMagicF;
+                const uint32_t cc = __float_as_uint(y) & 0xFFu;
+                sp += cc;
+                pcode[row * 64 + 16 * mt + base + 2 * hh] = (uint8_t)cc;
+                if (DBG && row < G)
+                  dbg_pcodes[((int64_t)s.b * kc.Hq + s.hk * G + row) * dbg_stride + jp * PI + 16 * mt + g + 8 * hh] =
+                      (uint8_t)cc;
+              }
+#pragma unroll
+            for (int o2 = 4; o2 < 32; o2 <<= 1) sp += __shfl_xor_sync(0xffffffffu, sp, o2);
+            if (g == 0) ws.rowinfo[row] = make_float4(al[nt], pm.s, pm.m, (float)sp);
+          }
+          __syncwarp();  // K region free: V coefficients overwrite the K coefficient scratch
+#pragma unroll
+          for (int x = 0; x < 4; ++x) {
+            const int ch = lane + 32 * x;
+            const __half2 hm = reinterpret_cast<const __half2*>(pg + PL.v_meta)[ch];
+            const float mv = __low2float(hm), sv = __high2float(hm);
+            const float sum = (float)pg[PL.v_sums + ch];
+            const float mu = fmaf(sv, 1.5f, mv);
+            reinterpret_cast<float4*>(&ws.scr[0][0])[ch] =
+                make_float4(sv, mu, fmaf(sv, sum - 96.f, 64.f * mu), fmaf(sum, -510.f, -kMagicF));
+          }
+          __syncwarp();
+          // PV lanes: rows n0, n1
+          const float4 r0 = ws.rowinfo[n0], r1 = ws.rowinfo[n1];
+          const float2 alp = f2(r0.x, r1.x);
+#pragma unroll
+          for (int mt = 0; mt < 8; ++mt) {
+            o[mt][0] = ptx::fmul2(o[mt][0], alp);
+            o[mt][1] = ptx::fmul2(o[mt][1], alp);
+          }
+          const float2 AP = f2(r0.y * 0.25f, r1.y * 0.25f);
+          const float2 XP = f2(r0.y * (r0.w - 127.5f * PI), r1.y * (r1.w - 127.5f * PI));
+          const float2 MP = f2(r0.z + 127.5f * r0.y, r1.z + 127.5f * r1.y);
+          const uint32_t rp0 = kMagic + (uint32_t)(-(2 * qkm * (int)r0.w - PI * 255 * qkm));
+          const uint32_t rp1 = kMagic + (uint32_t)(-(2 * qkm * (int)r1.w - PI * 255 * qkm));
+          // B fragments of P'^T: column n = g = row g; k-steps u: tokens 16 tig + 4 i + q(u, h)
+          const uint4 Rw = *reinterpret_cast<const uint4*>(pcode + g * 64 + 16 * tig);
+          const float4* vcs = reinterpret_cast<const float4*>(&ws.scr[0][0]);
+#pragma unroll
+          for (int mt = 0; mt < 8; ++mt) {
+            const int c0 = 16 * mt + g, c1 = c0 + 8;
+            const Planes va = planes2(*reinterpret_cast<const uint32_t*>(pg + PL.v_codes + c0 * 16 + 4 * tig));
+            const Planes vb = planes2(*reinterpret_cast<const uint32_t*>(pg + PL.v_codes + c1 * 16 + 4 * tig));
+            uint32_t acc0[4], acc1[4];
+            mma16832c(acc0, va.p0, vb.p0, va.p2, vb.p2, Rw.x, Rw.z, 0u, 0u);
+            mma16832c(acc1, va.p1, vb.p1, va.p3, vb.p3, Rw.y, Rw.w, rp0, rp1);
+#pragma unroll
+            for (int hh = 0; hh < 2; ++hh) {
+              const float4 v4 = vcs[hh ? c1 : c0];
+              const uint32_t e0 = (acc0[2 * hh] << 2) + acc1[2 * hh], e1 = (acc0[2 * hh + 1] << 2) + acc1[2 * hh + 1];
+              const float2 e = ptx::fadd2(asf2(e0, e1), f2(v4.w, v4.w));
+              const float2 t2 = ptx::ffma2(AP, ptx::fmul2(f2(v4.x, v4.x), e),
+                                           ptx::ffma2(XP, f2(v4.y, v4.y), ptx::fmul2(MP, f2(v4.z, v4.z))));
+              o[mt][hh] = ptx::fadd2(o[mt][hh], t2);
+            }
+          }
+        } else {
+          // ---- FP16 last V block (RQE)
+#pragma unroll
+          for (int nt = 0; nt < 2; ++nt) {
+            const int row = 4 * nt + tig;
+#pragma unroll
+            for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+              for (int hh = 0; hh < 2; ++hh) ptl[row * 64 + 16 * mt + g + 8 * hh] = sc[nt][mt][hh];
+            if (g == 0) ws.rowinfo[row] = make_float4(al[nt], 0.f, 0.f, 0.f);
+          }
+          __syncwarp();
+          const float2 alp = f2(ws.rowinfo[n0].x, ws.rowinfo[n1].x);
+#pragma unroll
+          for (int mt = 0; mt < 8; ++mt) {
+            o[mt][0] = ptx::fmul2(o[mt][0], alp);
+            o[mt][1] = ptx::fmul2(o[mt][1], alp);
+          }
+          const __half* tail = reinterpret_cast<const __half*>(cv.v_tail) + ((int64_t)slot * Hkv + s.hk) * PI * 128;
+          for (int t = 0; t < nk; ++t) {
+            const float2 p2 = f2(ptl[n0 * 64 + t], ptl[n1 * 64 + t]);
+#pragma unroll
+            for (int mt = 0; mt < 8; ++mt)
+#pragma unroll
+              for (int hh = 0; hh < 2; ++hh) {
+                const float v = __half2float(tail[t * 128 + 16 * mt + g + 8 * hh]);
+                o[mt][hh] = ptx::ffma2(p2, f2(v, v), o[mt][hh]);
+              }
+          }
+        }
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive(&sm.empty[st]);
+      }
+    }
+    // -- flush: (m, l) from the QK-side rows (tig, 4 + tig), O from the PV-side rows (n0, n1)
+    float* dst = part + (((int64_t)(u + c)) * NW + warp) * G * kPart;
+    if (g == 0) {
+#pragma unroll
+      for (int nt = 0; nt < 2; ++nt) {
+        const int row = 4 * nt + tig;
+        if (row < G) {
+          dst[row * kPart] = m_run[nt];
+          dst[row * kPart + 1] = l_run[nt];
+        }
+      }
+    }
+#pragma unroll
+    for (int mt = 0; mt < 8; ++mt)
+#pragma unroll
+      for (int hh = 0; hh < 2; ++hh) {
+        const int ch = 16 * mt + g + 8 * hh;
+        if (n0 < G) dst[n0 * kPart + 2 + ch] = o[mt][hh].x;
+        if (n1 < G) dst[n1 * kPart + 2 + ch] = o[mt][hh].y;
+      }
+    it_base += nitems;
+    k_base += s.p1 - s.p0;
+  }
+}
+
 // out[b][hk*G + n][c] = sum_parts e^(m - M) O / sum_parts e^(m - M) l over the partials of
 // unit u = b*Hkv + hk: CTAs c_first..c_last of its flattened page range, NW warps each.
 __global__ void __launch_bounds__(128) decode_pair_combine(const int* __restrict__ ws_meta,
@@ -687,15 +1036,15 @@ __global__ void __launch_bounds__(128) decode_pair_combine(const int* __restrict
     reinterpret_cast<__half*>(out)[idx] = __float2half_rn(v);
 }
 
-int grid_size() {
-  static int g = 0;
-  if (!g) {
-    int dev = 0, sms = 148;
+int grid_size(bool g8 = false) {
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    sms = 148;
     if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    g = sms * kCtasPerSm;
-    if (const char* e = getenv("HACK_DECODE_GRID")) g = atoi(e);
   }
-  return g;
+  if (const char* e = getenv("HACK_DECODE_GRID")) return atoi(e);
+  return sms * (g8 ? kCtas8 : kCtasPerSm);
 }
 
 size_t meta_bytes(int batch) { return ((size_t)(kMetaInts + 2 * batch) * sizeof(int) + 255) / 256 * 256; }
@@ -703,12 +1052,13 @@ size_t meta_bytes(int batch) { return ((size_t)(kMetaInts + 2 * batch) * sizeof(
 }  // namespace
 
 bool decode_pair_supported(const KernelCfg& kc) {
-  return kc.Pi == 64 && kc.d == 128 && kc.bits == 2 && kc.G <= 4 && kc.pl.page_bytes == PB;
+  return kc.Pi == 64 && kc.d == 128 && kc.bits == 2 && kc.G <= 8 && kc.pl.page_bytes == PB &&
+         !(kc.G > 4 && getenv("HACK_DECODE_NO_G8"));
 }
 
 size_t decode_pair_workspace(const KernelCfg& kc, int batch, int max_seqlen) {
   (void)max_seqlen;
-  const size_t slots = (size_t)batch * kc.Hkv + grid_size();
+  const size_t slots = (size_t)batch * kc.Hkv + grid_size(kc.G > 4);
   return meta_bytes(batch) + slots * NW * kc.G * kPart * sizeof(float);
 }
 
@@ -718,19 +1068,21 @@ cudaError_t launch_decode_pair(const KernelCfg& kc, const void* q_new, const int
   (void)max_seqlen;
   int* meta = reinterpret_cast<int*>(workspace);
   float* part = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(workspace) + meta_bytes(batch));
-  const size_t smem = sizeof(PairSmem);
+  const bool g8 = kc.G > 4;
+  const size_t smem = g8 ? sizeof(G8Smem) : sizeof(PairSmem);
   const bool with_dbg = dbg != nullptr && dbg->pcodes != nullptr;  // P-code dump: parity runs only
-  const bool no_se = getenv("HACK_DECODE_NO_SE") != nullptr;  // f2 ablation only
-  auto kern = with_dbg ? (no_se ? decode_pair_kernel<true, false> : decode_pair_kernel<true, true>)
-                       : (no_se ? decode_pair_kernel<false, false> : decode_pair_kernel<false, true>);
-  const int ki = (with_dbg ? 2 : 0) + (no_se ? 1 : 0);
-  static bool attr_set[4] = {false, false, false, false};  // once per process (graph capture safe)
+  const bool no_se = !g8 && getenv("HACK_DECODE_NO_SE") != nullptr;  // f2 ablation only
+  auto kern = g8 ? (with_dbg ? decode_g8_kernel<true> : decode_g8_kernel<false>)
+                 : with_dbg ? (no_se ? decode_pair_kernel<true, false> : decode_pair_kernel<true, true>)
+                            : (no_se ? decode_pair_kernel<false, false> : decode_pair_kernel<false, true>);
+  const int ki = (g8 ? 4 : 0) + (with_dbg ? 2 : 0) + (no_se ? 1 : 0);
+  static bool attr_set[8] = {false, false, false, false, false, false, false, false};  // once per process
   if (!attr_set[ki]) {
     const cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     attr_set[ki] = true;
   }
-  kern<<<grid_size(), kThreads, smem, st>>>(reinterpret_cast<const __half*>(q_new), slots, batch, cv, kc, meta, part,
+  kern<<<grid_size(g8), kThreads, smem, st>>>(reinterpret_cast<const __half*>(q_new), slots, batch, cv, kc, meta, part,
                                             with_dbg ? dbg->pcodes : nullptr, with_dbg ? dbg->pcodes_stride : 0);
   // the merge is launched as a programmatic dependent of the main kernel (PDL): its CTAs can
   // be resident before the main grid drains and wait in griddepcontrol.wait

@@ -201,3 +201,14 @@ def test_decode_long_context_tiny_cta_ranges():
     a few pages (odd sizes, single-page items, segments that start mid-pair) and the
     merge combines ~600 CTAs x warps partials of one unit."""
     run_decode(att.Config(Hq=4, Hkv=1, Pi=64, bits=2, seed=31), [96000], 2)
+
+
+@pytest.mark.parametrize("Hq", [8, 6])
+def test_decode_group8_paired_kernel(Hq):
+    # decode_g8_kernel: G in (4, 8] (C4 70B shape has G = 8), flushes, tails, mixed lengths
+    run_decode(att.Config(Hq=Hq, Hkv=1, Pi=64, bits=2, seed=14), [300, 64, 1000, 1], 70, check_every=9)
+
+
+def test_decode_general_mma_kernel_g8(monkeypatch):
+    monkeypatch.setenv("HACK_DECODE_IMPL", "mma")
+    run_decode(att.Config(Hq=16, Hkv=2, Pi=64, bits=2, seed=15), [300, 129], 20, check_every=7)
