@@ -42,7 +42,10 @@ namespace {
 constexpr int PI = 64;
 constexpr int BM = 128;
 constexpr int BN = 64;
-constexpr int NS = 4;          // page stages
+#ifndef HACK_PRE_NS
+#define HACK_PRE_NS 4
+#endif
+constexpr int NS = HACK_PRE_NS;  // page stages
 constexpr int NB = 3;          // K/V/P tile buffer sets
 #ifndef HACK_PRE_NDB
 #define HACK_PRE_NDB 2
