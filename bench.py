@@ -406,7 +406,7 @@ def run_decode(args, h, dev, rank, world, peaks, traffic, seed, flush):
     cfg = h.config(num_q_heads=Hq, num_kv_heads=Hkv, partition=Pi, kv_bits=C3["bits"], out_fp32=False, layer=1,
                    head_base=rank * Hkv if shard else 0)
     nsteps = args.warmup * 2 + args.steps * 2 + 2
-    max_len = ctx + nsteps
+    max_len = ctx + nsteps + 2 * Pi     # + the two Pi-step append graphs of the RQE ablation
     mp = (max_len + Pi - 1) // Pi
     # enough layers that one pass over them exceeds 2x the 126 MB L2 (a sharded layer can be
     # L2-sized); consecutive layer-steps walk the layers as a real decode step does (SURVEY d-5)
@@ -524,6 +524,28 @@ def run_decode(args, h, dev, rank, world, peaks, traffic, seed, flush):
         ev[3].record(stream)
         torch.cuda.synchronize()
         no_se_ms = max_over_ranks(ev[2].elapsed_time(ev[3]) / args.steps, world)
+        # SURVEY f2 (HACK/RQE ablation): Pi consecutive appends (every tail
+        # length 1..Pi once per request and layer) with the partial V block requantized at
+        # every step, vs the same appends with requantization elimination
+        rqe_ms = {}
+        for mode in ("rqe", "no_rqe"):
+            if mode == "no_rqe":
+                os.environ["HACK_DECODE_NO_RQE"] = "1"
+            g_app = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g_app):
+                for i in range(Pi):
+                    for lay in range(n_layers):
+                        h.decode_append(cfg, kn[(it[0] + i) % nsteps], vn[(it[0] + i) % nsteps], slots_all,
+                                        caches[lay])
+            os.environ.pop("HACK_DECODE_NO_RQE", None)
+            it[0] += Pi
+            torch.cuda.synchronize()
+            ev[2].record(stream)
+            g_app.replay()
+            ev[3].record(stream)
+            torch.cuda.synchronize()
+            rqe_ms[mode] = max_over_ranks(ev[2].elapsed_time(ev[3]) / (Pi * n_layers), world)
+            del g_app
     # algorithmic bytes of one attention launch (context n after the append): committed
     # tokens at 84 B/token/head (packed K+V, meta, sums), tail tokens at K-row bytes +
     # fp16 V, plus q in and out.
@@ -565,7 +587,13 @@ def run_decode(args, h, dev, rank, world, peaks, traffic, seed, flush):
     ablation = None if args.no_graph else {
         "no_summation_elimination": {"attn_ms": no_se_ms, "kv_gbs": avg_bytes / (no_se_ms * 1e-3) / 1e9,
                                      "slowdown": no_se_ms / attn_avg,
-                                     "what": "code sums recomputed from the codes every step (HACK/SE, P:1036-1042)"}}
+                                     "what": "code sums recomputed from the codes every step (HACK/SE, P:1036-1042)"},
+        "no_requantization_elimination": {
+            "append_ms": rqe_ms["no_rqe"], "append_ms_with_rqe": rqe_ms["rqe"],
+            "step_ms": ms - rqe_ms["rqe"] + rqe_ms["no_rqe"],
+            "slowdown": (ms - rqe_ms["rqe"] + rqe_ms["no_rqe"]) / ms,
+            "what": "partial last V block requantized at every append (HACK/RQE, P:704-724, P:1040); "
+                    "append averaged over Pi steps (tail lengths 1..Pi), step = measured step with that append"}}
     # strong scaling when heads are sharded (every rank serves the same B requests), weak
     # (independent replicas) otherwise
     req_factor = 1 if shard else world

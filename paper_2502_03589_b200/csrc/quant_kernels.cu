@@ -13,6 +13,8 @@
 // and sums reduce with xor-shuffles over the Pi/8 lanes of the partition.
 // V blocks: one thread per (block, head, channel) streams the Pi tokens twice
 // (min/max, then quantize + pack), one Philox block per 4 tokens.
+#include <cstdlib>
+
 #include "common.cuh"
 #include "internal.h"
 
@@ -280,7 +282,7 @@ __global__ void __launch_bounds__(256) ingest_kv64_kernel(const __half* __restri
 // quantize k_new into its own partitions in the current page, write v_new
 // to the FP16 tail, flush the tail into the page's V section when it reaches Pi
 // (P:723), then seq_lens += 1.
-template <int BITS>
+template <int BITS, bool RQE>
 __global__ void __launch_bounds__(128) append_kernel(const __half* __restrict__ k_new,
                                                      const __half* __restrict__ v_new,
                                                      const int32_t* __restrict__ slots, CacheView cv,
@@ -324,6 +326,51 @@ __global__ void __launch_bounds__(128) append_kernel(const __half* __restrict__ 
                        stream_c3(kc.layer, kTagV, kc.head_base + h), kc.kv_round,
                        pg + PL.v_codes + c * (Pi * BITS / 8), m, s, sum);
       reinterpret_cast<__half2*>(pg + PL.v_meta)[c] = make_meta(m, s);
+      store_sum(pg + PL.v_sums, c, PL.sum_bytes, sum);
+    } else if (!RQE) {
+      // "HACK/RQE" ablation: without requantization
+      // elimination the partially filled last V block is requantized at every step, as one
+      // partition of its row + 1 tokens per channel (same quantizer and position-keyed SR
+      // counters as a flush), into the page's (otherwise unused) V section.  Attention still
+      // reads the FP16 tail, so this variant measures the requantization cost only.
+      __syncthreads();
+      constexpr int qmax = (1 << BITS) - 1;
+      const int nk = row + 1;
+      const __half* xc = tail + c;
+      float lo = __half2float(xc[0]), hi = lo;
+      for (int tt = 1; tt < nk; ++tt) {
+        const float v = __half2float(xc[tt * 128]);
+        lo = fminf(lo, v);
+        hi = fmaxf(hi, v);
+      }
+      const QMeta q = meta_fp16(lo, hi, qmax);
+      uint32_t* dst = reinterpret_cast<uint32_t*>(pg + PL.v_codes + c * (Pi * BITS / 8));
+      uint32_t word = 0;
+      int sum = 0;
+      const uint32_t c3 = stream_c3(kc.layer, kTagV, kc.head_base + h);
+      for (int t0 = 0; t0 < nk; t0 += 4) {
+        float u[4] = {0.f, 0.f, 0.f, 0.f};
+        if (kc.kv_round == HACK_ROUND_STOCHASTIC) {
+          const Philox4 r = philox_block(kc.seed, rng_id, c3, (uint64_t)((blk * Pi + t0) >> 2) * 128u + (uint64_t)c);
+          u[0] = u24(r.x); u[1] = u24(r.y); u[2] = u24(r.z); u[3] = u24(r.w);
+        }
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int tt = t0 + i;
+          if (tt < nk) {
+            const float x = __half2float(xc[tt * 128]);
+            const int cc = kc.kv_round == HACK_ROUND_STOCHASTIC ? quant_sr(x, q, u[i], qmax) : quant_rn(x, q, qmax);
+            word |= (uint32_t)cc << ((tt * BITS) & 31);
+            sum += cc;
+          }
+          if (tt == nk - 1) dst[(tt * BITS) >> 5] = word;  // last (partial) word; codes past nk are 0
+          if (((tt + 1) * BITS & 31) == 0) {
+            if (tt < nk - 1) dst[(tt * BITS) >> 5] = word;
+            word = 0;
+          }
+        }
+      }
+      reinterpret_cast<__half2*>(pg + PL.v_meta)[c] = make_meta(q.m, q.s);
       store_sum(pg + PL.v_sums, c, PL.sum_bytes, sum);
     }
   }
@@ -409,10 +456,18 @@ cudaError_t launch_append(const KernelCfg& kc, const void* k_new, const void* v_
                           int batch, const CacheView& cv, cudaStream_t st) {
   const __half* kh = reinterpret_cast<const __half*>(k_new);
   const __half* vh = reinterpret_cast<const __half*>(v_new);
+  if (getenv("HACK_DECODE_NO_RQE") && kc.Pi == 64) {  // f2 ablation only
+    if (kc.bits == 2)
+      append_kernel<2, false><<<batch, 128, 0, st>>>(kh, vh, slots, cv, kc);
+    else
+      append_kernel<4, false><<<batch, 128, 0, st>>>(kh, vh, slots, cv, kc);
+    note_launch();
+    return cudaGetLastError();
+  }
   if (kc.bits == 2)
-    append_kernel<2><<<batch, 128, 0, st>>>(kh, vh, slots, cv, kc);
+    append_kernel<2, true><<<batch, 128, 0, st>>>(kh, vh, slots, cv, kc);
   else
-    append_kernel<4><<<batch, 128, 0, st>>>(kh, vh, slots, cv, kc);
+    append_kernel<4, true><<<batch, 128, 0, st>>>(kh, vh, slots, cv, kc);
   note_launch();
   return cudaGetLastError();
 }
