@@ -278,7 +278,8 @@ __global__ void __launch_bounds__(256) ingest_kv64_kernel(const __half* __restri
 }
 
 // -------------------------------------------------------------------------- decode append (a8)
-// One CTA per request, 128 threads (= d channels), looping over KV heads:
+// One cluster of CL CTAs per request (grid CL x batch, CL | Hkv, CL <= 8), 128 threads
+// (= d channels); CTA x serves KV heads x, x + CL, ...:
 // quantize k_new into its own partitions in the current page, write v_new
 // to the FP16 tail, flush the tail into the page's V section when it reaches Pi
 // (P:723), then seq_lens += 1.
@@ -287,7 +288,7 @@ __global__ void __launch_bounds__(128) append_kernel(const __half* __restrict__ 
                                                      const __half* __restrict__ v_new,
                                                      const int32_t* __restrict__ slots, CacheView cv,
                                                      KernelCfg kc) {
-  const int b = blockIdx.x;
+  const int b = blockIdx.y;
   const int slot = slots[b];
   const int H = kc.Hkv, Pi = kc.Pi;
   const int t = cv.seq_lens[slot];
@@ -295,7 +296,7 @@ __global__ void __launch_bounds__(128) append_kernel(const __half* __restrict__ 
   const uint32_t rng_id = cv.rng_ids[slot];
   const int c = threadIdx.x;
   const PageLayout& PL = kc.pl;
-  for (int h = 0; h < H; ++h) {
+  for (int h = blockIdx.x; h < H; h += gridDim.x) {
     uint8_t* pg = page_ptr(cv, slot, blk, h);
     if (threadIdx.x < 32) {  // K row: lanes 0-15 (16-31 duplicate, no store)
       const int lane16 = threadIdx.x & 15;
@@ -374,8 +375,13 @@ __global__ void __launch_bounds__(128) append_kernel(const __half* __restrict__ 
       store_sum(pg + PL.v_sums, c, PL.sum_bytes, sum);
     }
   }
-  __syncthreads();  // every thread has read seq_lens before it changes
-  if (threadIdx.x == 0) cv.seq_lens[slot] = t + 1;
+  // every thread of the request's cluster has read seq_lens before it changes
+  if (gridDim.x > 1) {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+  } else {
+    __syncthreads();
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) cv.seq_lens[slot] = t + 1;
 }
 
 // -------------------------------------------------------------------------- launchers
@@ -454,22 +460,36 @@ cudaError_t launch_ingest(const KernelCfg& kc, const void* k, const void* v, con
 
 cudaError_t launch_append(const KernelCfg& kc, const void* k_new, const void* v_new, const int32_t* slots,
                           int batch, const CacheView& cv, cudaStream_t st) {
+  if (batch <= 0) return cudaSuccess;
   const __half* kh = reinterpret_cast<const __half*>(k_new);
   const __half* vh = reinterpret_cast<const __half*>(v_new);
-  if (getenv("HACK_DECODE_NO_RQE") && kc.Pi == 64) {  // f2 ablation only
-    if (kc.bits == 2)
-      append_kernel<2, false><<<batch, 128, 0, st>>>(kh, vh, slots, cv, kc);
-    else
-      append_kernel<4, false><<<batch, 128, 0, st>>>(kh, vh, slots, cv, kc);
-    note_launch();
-    return cudaGetLastError();
+  // KV heads of one request spread over a cluster (a serial head loop in one CTA left the
+  // 64-request C3 append latency-bound at ~16 us, 13 % of the decode step)
+  int cl = 1;
+  for (int c = 8; c > 1; --c)
+    if (kc.Hkv % c == 0) { cl = c; break; }
+  if (const char* e = getenv("HACK_APPEND_CL")) {  // timing knob: 1 = the serial head loop
+    const int v = atoi(e);
+    if (v >= 1 && v <= 8 && kc.Hkv % v == 0) cl = v;
   }
-  if (kc.bits == 2)
-    append_kernel<2, true><<<batch, 128, 0, st>>>(kh, vh, slots, cv, kc);
-  else
-    append_kernel<4, true><<<batch, 128, 0, st>>>(kh, vh, slots, cv, kc);
+  const bool no_rqe = getenv("HACK_DECODE_NO_RQE") && kc.Pi == 64;  // f2 ablation only
+  void (*kern)(const __half*, const __half*, const int32_t*, CacheView, KernelCfg) =
+      kc.bits == 2 ? (no_rqe ? append_kernel<2, false> : append_kernel<2, true>)
+                   : (no_rqe ? append_kernel<4, false> : append_kernel<4, true>);
+  cudaLaunchConfig_t lc = {};
+  lc.gridDim = dim3(cl, batch);
+  lc.blockDim = dim3(128);
+  lc.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = cl;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  lc.attrs = at;
+  lc.numAttrs = cl > 1 ? 1 : 0;
+  const cudaError_t err = cudaLaunchKernelEx(&lc, kern, kh, vh, slots, cv, kc);
   note_launch();
-  return cudaGetLastError();
+  return err != cudaSuccess ? err : cudaGetLastError();
 }
 
 }  // namespace hack
