@@ -46,6 +46,9 @@ constexpr int PI = 64;
 #ifndef HACK_DEC_SPLIT
 #define HACK_DEC_SPLIT 0
 #endif
+#ifndef HACK_DEC_PF
+#define HACK_DEC_PF 8
+#endif
 #ifndef HACK_DEC_CTAS
 #define HACK_DEC_CTAS 4
 #endif
@@ -289,8 +292,14 @@ HACK_DEV void produce_pages(SMT& sm, SegWalker walk, const CacheView& cv, const 
     for (int p0 = s.p0; p0 < s.p1; p0 += 32) {
       const int n = min(32, s.p1 - p0);
       const int ent = lane < n ? bt[p0 + lane] : 0;
+      // entries of the next 32 pages of the segment: L2 prefetch HACK_DEC_PF pages ahead
+      // (the ring slots hold pages being computed on, so the pages in flight per SM are
+      // few; the L2 prefetch keeps more bytes in flight without smem)
+      const int ent2 = HACK_DEC_PF > 0 && lane < s.p1 - p0 - 32 ? bt[p0 + 32 + lane] : 0;
       for (int x = 0; x < n; ++x, ++k) {
         const int pid = __shfl_sync(0xffffffffu, ent, x);
+        const int xf = x + HACK_DEC_PF;
+        const int pfa = __shfl_sync(0xffffffffu, ent, xf & 31), pfb = __shfl_sync(0xffffffffu, ent2, xf & 31);
         if (lane == 0) {
           const int st = k % N;
 #ifdef HACK_DEC_SPIN
@@ -316,6 +325,10 @@ HACK_DEV void produce_pages(SMT& sm, SegWalker walk, const CacheView& cv, const 
 #else
           ptx::bulk_g2s(sm.stage[st], pg, PB, &sm.full[st]);
 #endif
+          if (HACK_DEC_PF > 0 && p0 + xf < s.p1) {
+            const int pidf = xf < 32 ? pfa : pfb;
+            ptx::bulk_prefetch_l2(cv.pages + ((int64_t)pidf * cv.num_kv_heads + s.hk) * cv.page_bytes, PB);
+          }
         }
         __syncwarp();
       }

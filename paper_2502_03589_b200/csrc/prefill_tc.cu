@@ -89,6 +89,20 @@ struct TcSmem {
 #ifndef HACK_ABL
 #define HACK_ABL 0  // timing ablations only (scripts/ablate_pre.sh); results are wrong for != 0
 #endif
+// Waits per role: bit set in HACK_PRE_SLEEP -> that role waits with a suspend hint
+// (NANOSLEEP.SYNCS, wakes on the phase flip) instead of a polling loop that takes issue
+// slots from the epilogue warps.  Bits: 0 producer, 1 MMA issuer, 2 unpack, 3 S, 4 O.
+#ifndef HACK_PRE_SLEEP
+#define HACK_PRE_SLEEP 0
+#endif
+template <int ROLE>
+HACK_DEV void rwait(uint64_t* bar, uint32_t parity) {
+  if ((HACK_PRE_SLEEP >> ROLE) & 1)
+    ptx::mbar_wait_sleep(bar, parity);
+  else
+    ptx::mbar_wait(bar, parity);
+}
+
 HACK_DEV float2 acc2f(uint32_t a, uint32_t b) {
   return ptx::fadd2(make_float2(__uint_as_float(a), __uint_as_float(b)), make_float2(-kMagic, -kMagic));
 }
@@ -180,7 +194,7 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_tc_kernel(
         const int32_t* bt = cv.block_table + (int64_t)slot * cv.max_pages_per_req;
         for (int j = 0; j < nkt; ++j) {
           const int s = j % NS;
-          ptx::mbar_wait(&sm.empty[s], ((j / NS) & 1) ^ 1);
+          rwait<0>(&sm.empty[s], ((j / NS) & 1) ^ 1);
           ptx::mbar_arrive_expect_tx(&sm.full[s], SM::PB);
           const uint8_t* pg = cv.pages + ((int64_t)bt[j] * cv.num_kv_heads + hk) * cv.page_bytes;
           ptx::bulk_g2s(sm.stage[s], pg, SM::PB, &sm.full[s]);
@@ -193,12 +207,12 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_tc_kernel(
       const uint64_t pre_a = ptx::smem_desc_kmajor(ptx::smem_u32(sm.pre_a), 128, 256);
       const uint64_t pre_b = ptx::smem_desc_kmajor(ptx::smem_u32(sm.pre_b), 128, 256);
       const uint32_t idesc_pre = ptx::idesc_bf16(BM, 128);
-      ptx::mbar_wait(&sm.q_ready, 0);
+      rwait<1>(&sm.q_ready, 0);
       for (int j = 0; j <= nkt; ++j) {
         if (j < nkt) {
           const int bq = j % NB;
-          ptx::mbar_wait(&sm.k_ready[bq], (j / NB) & 1);
-          ptx::mbar_wait(&sm.s_free, (j & 1) ^ 1);
+          rwait<1>(&sm.k_ready[bq], (j / NB) & 1);
+          rwait<1>(&sm.s_free, (j & 1) ^ 1);
           ptx::tc_fence_after();
           if (lane == 0) {
             const uint32_t ka = ptx::smem_u32(sm.k[bq]);
@@ -227,9 +241,9 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_tc_kernel(
         if (jj >= 0 && jj < nfull) {
           const int bd = jj % NDB, bq = jj % NB;
           const uint32_t ph = (jj / NB) & 1;
-          ptx::mbar_wait(&sm.p_ready[bq], ph);
-          ptx::mbar_wait(&sm.v_ready[bq], ph);
-          ptx::mbar_wait(&sm.d_free[bd], ((jj / NDB) & 1) ^ 1);
+          rwait<1>(&sm.p_ready[bq], ph);
+          rwait<1>(&sm.v_ready[bq], ph);
+          rwait<1>(&sm.d_free[bd], ((jj / NDB) & 1) ^ 1);
           ptx::tc_fence_after();
           if (lane == 0) {
             const uint32_t pa = ptx::smem_u32(sm.p[bq]), va = ptx::smem_u32(sm.v[bq]);
@@ -262,8 +276,8 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_tc_kernel(
       for (int j = 0; j < nkt; ++j) {
         const int s = j % NS, bj = j % NB;
         const uint32_t ph = (j / NB) & 1;
-        ptx::mbar_wait(&sm.full[s], (j / NS) & 1);
-        ptx::mbar_wait(&sm.k_free[bj], ph ^ 1);
+        rwait<2>(&sm.full[s], (j / NS) & 1);
+        rwait<2>(&sm.k_free[bj], ph ^ 1);
         const uint8_t* pg = sm.stage[s];
         const int nk = min(BN, L - j * BN);
         {  // K' codes: thread = key; 8 consecutive keys fill one 128-byte core matrix per store
@@ -307,7 +321,7 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_tc_kernel(
         }
         ptx::fence_proxy_async_smem();
         ptx::mbar_arrive(&sm.k_ready[bj]);
-        ptx::mbar_wait(&sm.o_done[bj], ph ^ 1);  // O warps done with tile j - NB
+        rwait<2>(&sm.o_done[bj], ph ^ 1);  // O warps done with tile j - NB
         if (j < nfull) {
 #pragma unroll
           for (int c2 = 0; c2 < 2; ++c2) {
@@ -433,7 +447,7 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_tc_kernel(
       const int bj = j % NB, t0 = j * BN;
       const uint32_t ph = (j / NB) & 1;
       const bool full = (t0 + BN - 1) <= i0;  // every key visible to every row of the CTA
-      ptx::mbar_wait(&sm.s_full, j & 1);
+      rwait<3>(&sm.s_full, j & 1);
       ptx::tc_fence_after();
       float s[32];
 #pragma unroll
@@ -523,7 +537,7 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_tc_kernel(
       }
       l_run = l_run * al + (ls2.x + ls2.y);
       // tile j-NB must be fully consumed by the O warps before its P / info slots are reused
-      ptx::mbar_wait(&sm.o_done[bj], ph ^ 1);
+      rwait<3>(&sm.o_done[bj], ph ^ 1);
       if (j < nfull) {
         // (a6) P' per (row, V block): 8-bit RN on p~ (codes invariant to the row scale);
         // y = (p - lo) / s rounded with the 1.5*2^23 magic number (y in [0, 255])
@@ -599,7 +613,7 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_tc_kernel(
     for (int j = 0; j < nkt; ++j) {
       const int bj = j % NB, bd = j % NDB;
       const uint32_t ph = (j / NB) & 1;
-      ptx::mbar_wait(&sm.p_ready[bj], ph);
+      rwait<4>(&sm.p_ready[bj], ph);
       const float4 pi4 = sm.pinfo[bj][r];
       if (pi4.y != 0.f) {  // warp-uniform (lazy rescaling decided per S warp = same 32 rows)
         const float2 al2 = make_float2(pi4.x, pi4.x);
@@ -612,8 +626,8 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_tc_kernel(
         const float2 ap2 = make_float2(0.5f * pi4.z, 0.5f * pi4.z);
         const float2 xp2 = make_float2(pi4.z * (float)sps, pi4.z * (float)sps);
         const float2 mp2 = make_float2(pi4.w + 128.f * pi4.z, pi4.w + 128.f * pi4.z);
-        ptx::mbar_wait(&sm.v_ready[bj], ph);
-        ptx::mbar_wait(&sm.d_full[bd], (j / NDB) & 1);
+        rwait<4>(&sm.v_ready[bj], ph);
+        rwait<4>(&sm.d_full[bd], (j / NDB) & 1);
         ptx::tc_fence_after();
 #pragma unroll
         for (int h = 0; h < 4; ++h) {
@@ -668,7 +682,7 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_tc_kernel(
       }
       ptx::mbar_arrive(&sm.o_done[bj]);
     }
-    ptx::mbar_wait(&sm.l_ready, 0);
+    rwait<4>(&sm.l_ready, 0);
     if (i0 + r < L) {
       const float inv_l = 1.f / (sm.lpart[0][r] + sm.lpart[1][r]);
       const int64_t base = ((int64_t)(start + i0 + r) * kc.Hq + hq) * 128 + cb;

@@ -68,6 +68,11 @@ HACK_DEV void bulk_g2s(void* dst_smem, const void* src_gmem, uint32_t bytes, uin
       : "memory");
 }
 
+// bulk prefetch of global memory into L2 (no smem, no completion tracking)
+HACK_DEV void bulk_prefetch_l2(const void* src_gmem, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src_gmem), "r"(bytes) : "memory");
+}
+
 // ---------------------------------------------------------------- fences / barriers
 HACK_DEV void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 HACK_DEV void named_bar_sync(uint32_t id, uint32_t nthreads) {
