@@ -288,6 +288,7 @@ def run_hack(args, rank, local_rank, world):
     # ---------------- C3 decode (a8, a9)
     dec = run_decode(args, h, dev, rank, world, peaks, traffic, seed, flush)
     c4 = None if args.no_c4 else run_c4(args, h, dev, world, seed, flush)
+    sweep = None if args.no_sweep or world > 1 else run_sweep(args, h, dev, seed, flush)
 
     # ---------------- CPU oracle baseline (rank 0, N = 1)
     cpu = None
@@ -319,8 +320,88 @@ def run_hack(args, rank, local_rank, world):
             "clocks": clk.summary(),
             "decode": dec,
             "c4": c4,
+            "pi_bits_sweep": sweep,
         }
         print(json.dumps(line), flush=True)
+
+
+def run_sweep(args, h, dev, seed, flush):
+    """SURVEY f (Pi/bit sweep): partition size Pi in {32, 64, 128} x K/V bits in
+    {2, 4} on a reduced C2/C3 shape (32 Q / 8 KV heads): one 2048-token causal prefill (ingest +
+    attention, L2 flushed) and a batch-16 decode step at 4096 context (append + attention,
+    CUDA graph).  Pi = 64 runs the tcgen05 prefill and the mma.sync decode kernels; Pi = 32
+    and 128 run the CUDA-core kernels (tensor-core versions are not built)."""
+    import torch
+    Hq, Hkv, L, B, ctx = 32, 8, 2048, 16, 4096
+    stream = torch.cuda.current_stream()
+    q = dev_normal((L, Hq, 128), seed + 51, dev)
+    k = dev_normal((L, Hkv, 128), seed + 52, dev)
+    v = dev_normal((L, Hkv, 128), seed + 53, dev)
+    kc_ = dev_normal((ctx, Hkv, 128), seed + 54, dev)
+    vc_ = dev_normal((ctx, Hkv, 128), seed + 55, dev)
+    cu = torch.tensor([0, L], dtype=torch.int32, device=dev)
+    cuc = torch.tensor([0, ctx], dtype=torch.int32, device=dev)
+    out = torch.empty((L, Hq, 128), dtype=torch.float16, device=dev)
+    ops = prefill_ops(L, Hq)
+    n_dec = 5
+    res = {"workload": f"Pi x bits sweep: {Hq} Q / {Hkv} KV heads, d=128; prefill L={L} causal; "
+                       f"decode batch {B} at {ctx} context", "points": []}
+    for Pi in (32, 64, 128):
+        for bits in (2, 4):
+            cfg = h.config(num_q_heads=Hq, num_kv_heads=Hkv, partition=Pi, kv_bits=bits, out_fp32=False, layer=3)
+            mp = (max(L, ctx) + n_dec + 2 + Pi - 1) // Pi + 1
+            cache = h.KVCache.allocate(cfg, max_reqs=B, max_pages_per_req=mp, device=dev)
+            cache.rng_ids.copy_(torch.arange(B, dtype=torch.int32, device=dev))
+            sl0 = torch.zeros(1, dtype=torch.int32, device=dev)
+            ms = []
+            for i in range(3):
+                flush.fill_(1)
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record(stream)
+                h.cache_ingest(cfg, k, v, cu, sl0, L, cache)
+                h.prefill_attention_cached(cfg, q, cu, sl0, L, cache, out)
+                b.record(stream)
+                b.synchronize()
+                if i:
+                    ms.append(a.elapsed_time(b))
+            pre_ms = sum(ms) / len(ms)
+            for r in range(B):
+                h.cache_ingest(cfg, kc_, vc_, cuc, torch.tensor([r], dtype=torch.int32, device=dev), ctx, cache)
+            slots = torch.arange(B, dtype=torch.int32, device=dev)
+            qn = dev_normal((n_dec, B, Hq, 128), seed + 56, dev)
+            kn = dev_normal((n_dec, B, Hkv, 128), seed + 57, dev)
+            vn = dev_normal((n_dec, B, Hkv, 128), seed + 58, dev)
+            dout = torch.empty((B, Hq, 128), dtype=torch.float16, device=dev)
+            ws = torch.empty(max(h.decode_workspace_size(cfg, B, ctx + n_dec + 2), 1), dtype=torch.uint8,
+                             device=dev)
+            h.decode_append(cfg, kn[0], vn[0], slots, cache)
+            h.decode_attention_cached(cfg, qn[0], slots, ctx + n_dec + 2, cache, dout, workspace=ws)
+            torch.cuda.synchronize()
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                for i in range(1, n_dec):
+                    h.decode_append(cfg, kn[i], vn[i], slots, cache)
+                    h.decode_attention_cached(cfg, qn[i], slots, ctx + n_dec + 2, cache, dout, workspace=ws)
+            torch.cuda.synchronize()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            g.replay()
+            b.record(stream)
+            b.synchronize()
+            dec_ms = a.elapsed_time(b) / (n_dec - 1)
+            pb = h.page_bytes(cfg)
+            n = ctx + n_dec // 2 + 1
+            dec_bytes = B * Hkv * (n // Pi) * pb + B * Hq * 128 * 2 * 2
+            res["points"].append({
+                "Pi": Pi, "bits": bits,
+                "prefill_kernel": "prefill_tc_kernel (tcgen05)" if Pi == 64 else "prefill_simt (CUDA cores)",
+                "decode_kernel": ("decode_pair_kernel (mma.sync)" if bits == 2 else "decode_mma_kernel (mma.sync)")
+                if Pi == 64 else "decode_simt (CUDA cores)",
+                "prefill_tops": ops / (pre_ms * 1e-3) / 1e12, "prefill_ms": pre_ms,
+                "decode_step_ms": dec_ms, "decode_kv_gbs": dec_bytes / (dec_ms * 1e-3) / 1e9,
+                "bytes_per_token_head": pb / Pi})
+            del cache, ws, qn, kn, vn, g
+    return res
 
 
 def run_c4(args, h, dev, world, seed, flush):
@@ -651,6 +732,7 @@ def main():
     ap.add_argument("--impl", choices=["hack", "reference"], default="hack")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-c4", action="store_true", help="skip the C4 (70B-shaped, 2- vs 4-bit) sub-benchmark")
+    ap.add_argument("--no-sweep", action="store_true", help="skip the Pi x bits sweep (SURVEY f)")
     ap.add_argument("--no-comparator", action="store_true", help="skip the dequantize-first comparator (f4)")
     ap.add_argument("--no-graph", action="store_true",
                     help="decode: launch eagerly instead of replaying a CUDA graph of the K timed steps")
