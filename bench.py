@@ -289,6 +289,7 @@ def run_hack(args, rank, local_rank, world):
     dec = run_decode(args, h, dev, rank, world, peaks, traffic, seed, flush)
     c4 = None if args.no_c4 else run_c4(args, h, dev, world, seed, flush)
     sweep = None if args.no_sweep or world > 1 else run_sweep(args, h, dev, seed, flush)
+    xfer = None if args.no_sweep or world > 1 else run_transfer(args, h, dev, seed)
 
     # ---------------- CPU oracle baseline (rank 0, N = 1)
     cpu = None
@@ -321,8 +322,56 @@ def run_hack(args, rank, local_rank, world):
             "decode": dec,
             "c4": c4,
             "pi_bits_sweep": sweep,
+            "kv_transfer": xfer,
         }
         print(json.dumps(line), flush=True)
+
+
+def run_transfer(args, h, dev, seed):
+    """a10 device work on this GPU: pack one C2 request (4096-token prompt, 8 KV heads, 2-bit)
+    of a 32-layer model into the wire buffer (hack_kv_pack, one launch) and unpack it into
+    another cache (hack_kv_unpack).  The link itself (NCCL over NVLink between two GPUs) is
+    not timed on one GPU."""
+    import torch
+    Hq, Hkv, L, layers = C2["Hq"], C2["Hkv"], C2["L"], 32
+    cfg = h.config(num_q_heads=Hq, num_kv_heads=Hkv, partition=C2["Pi"], kv_bits=C2["bits"], out_fp32=False)
+    mp = (L + 63) // 64
+    src = [h.KVCache.allocate(cfg, 1, mp, device=dev)]
+    src += [h.KVCache.allocate(cfg, 1, mp, num_pages=src[0].pages.shape[0], shared_tables=src[0], device=dev)
+            for _ in range(layers - 1)]
+    dst = [h.KVCache.allocate(cfg, 1, mp, device=dev)]
+    dst += [h.KVCache.allocate(cfg, 1, mp, num_pages=dst[0].pages.shape[0], shared_tables=dst[0], device=dev)
+            for _ in range(layers - 1)]
+    k = dev_normal((L, Hkv, 128), seed + 61, dev)
+    v = dev_normal((L, Hkv, 128), seed + 62, dev)
+    cu = torch.tensor([0, L], dtype=torch.int32, device=dev)
+    sl = torch.zeros(1, dtype=torch.int32, device=dev)
+    for c_ in src:
+        h.cache_ingest(cfg, k, v, cu, sl, L, c_)
+    nbytes = h.kv_transfer_bytes(cfg, layers, L)
+    wire = torch.empty(nbytes, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream()
+
+    def timed(fn, reps=5):
+        fn()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for _ in range(reps):
+            fn()
+        b.record(stream)
+        b.synchronize()
+        return a.elapsed_time(b) / reps
+
+    pack_ms = timed(lambda: h.kv_pack(cfg, src, 0, L, first_token=1, rng_id=0, staging=wire))
+    unpack_ms = timed(lambda: h.kv_unpack(cfg, dst, 0, L, wire))
+    fp16_bytes = layers * L * Hkv * 128 * 2 * 2
+    del src, dst, wire
+    return {"workload": f"one {L}-token request, {layers} layers x {Hkv} KV heads, 2-bit (C2 shape)",
+            "wire_bytes": nbytes, "fp16_kv_bytes": fp16_bytes, "ratio_vs_fp16": nbytes / fp16_bytes,
+            "pack_ms": pack_ms, "pack_gbs": 2 * nbytes / (pack_ms * 1e-3) / 1e9,
+            "unpack_ms": unpack_ms, "unpack_gbs": 2 * nbytes / (unpack_ms * 1e-3) / 1e9,
+            "note": "GB/s counts read + write; repeated packs of an 88 MB request can hit the 126 MB L2; "
+                    "the NVLink send/recv needs two GPUs and is not timed here"}
 
 
 def run_sweep(args, h, dev, seed, flush):

@@ -248,6 +248,23 @@ hack_status_t hack_kv_send(void* comm, int32_t peer, const hack_config_t* cfg,
 hack_status_t hack_kv_recv(void* comm, int32_t peer, const hack_config_t* cfg,
                            const hack_kv_cache_t* caches, int32_t num_layers, int32_t slot,
                            int32_t prompt_len, void* staging, int32_t* status_dev, void* stream);
+/* Layer-pipelined transfer (P:313-321 overlap of transfer with compute): the
+ * same wire bytes as hack_kv_send, sent as num_layers NCCL messages so that layer l leaves
+ * as soon as its prefill finished (stream-ordered after it) while later layers compute.
+ * hack_kv_layer_range: byte range [*begin_out, *begin_out + return) of layer `layer` in the
+ * wire buffer (layer 0 includes the 64-byte header); -1 on bad arguments.
+ * hack_kv_send_layer: pack layer `layer` of one request (and the header when layer == 0)
+ * into `staging` at that range and ncclSend the range.  caches: all num_layers layers.
+ * hack_kv_recv_layer: ncclRecv that range into `staging`.  After every layer arrived, one
+ * hack_kv_unpack(staging) validates the header and scatters all layers. */
+int64_t hack_kv_layer_range(const hack_config_t* cfg, int32_t num_layers, int32_t layer, int32_t prompt_len,
+                            int64_t* begin_out);
+hack_status_t hack_kv_send_layer(void* comm, int32_t peer, const hack_config_t* cfg,
+                                 const hack_kv_cache_t* caches, int32_t num_layers, int32_t layer, int32_t slot,
+                                 int32_t prompt_len, int32_t first_token, uint32_t rng_id, void* staging,
+                                 void* stream);
+hack_status_t hack_kv_recv_layer(void* comm, int32_t peer, const hack_config_t* cfg, int32_t num_layers,
+                                 int32_t layer, int32_t prompt_len, void* staging, void* stream);
 hack_status_t hack_comm_recv_bytes(void* comm, int32_t peer, void* buf, int64_t bytes, void* stream);
 hack_status_t hack_comm_group_start(void);
 hack_status_t hack_comm_group_end(void);

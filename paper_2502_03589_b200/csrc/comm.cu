@@ -63,11 +63,11 @@ HACK_DEV void copy16(uint8_t* dst, const uint8_t* src, int64_t bytes) {
     reinterpret_cast<uint4*>(dst)[i] = reinterpret_cast<const uint4*>(src)[i];
 }
 
-// grid (npages + 1, num_layers): block j < npages copies page j (all KV heads), block
-// npages copies the FP16 tail rows.
+// grid (npages + 1, layers): block j < npages copies page j (all KV heads), block npages
+// copies the FP16 tail rows; blockIdx.y = layer - layer0 (layer-pipelined send packs one).
 __global__ void gather_kernel(LayerPtrs lp, const int32_t* __restrict__ block_table, int max_pages_per_req,
-                              int slot, XferGeom g, WireHeader hdr, uint8_t* __restrict__ staging) {
-  const int j = blockIdx.x, l = blockIdx.y;
+                              int slot, XferGeom g, WireHeader hdr, uint8_t* __restrict__ staging, int layer0) {
+  const int j = blockIdx.x, l = layer0 + blockIdx.y;
   if (j == 0 && l == 0 && threadIdx.x == 0) *reinterpret_cast<WireHeader*>(staging) = hdr;
   uint8_t* dst = staging + kHeaderBytes + (int64_t)l * g.layer_bytes;
   const int64_t pbytes = (int64_t)g.Hkv * g.page_bytes;
@@ -226,7 +226,7 @@ hack_status_t hack_kv_pack(const hack_config_t* cfg, const hack_kv_cache_t* cach
   hdr.rng_id = rng_id;
   if ((st = check_device()) != HACK_OK) return st;
   gather_kernel<<<dim3(g.npages + 1, num_layers), 256, 0, (cudaStream_t)stream>>>(
-      lp, caches[0].block_table, caches[0].max_pages_per_req, slot, g, hdr, (uint8_t*)staging);
+      lp, caches[0].block_table, caches[0].max_pages_per_req, slot, g, hdr, (uint8_t*)staging, 0);
   note_launch();
   return cuda_status(cudaGetLastError(), "kv_pack gather");
 }
@@ -270,6 +270,53 @@ hack_status_t hack_kv_recv(void* comm, int32_t peer, const hack_config_t* cfg, c
       ncclRecv(staging, (size_t)bytes, ncclUint8, peer, (ncclComm_t)comm, (cudaStream_t)stream), "ncclRecv");
   if (st != HACK_OK) return st;
   return hack_kv_unpack(cfg, caches, num_layers, slot, prompt_len, staging, status_dev, stream);
+}
+
+int64_t hack_kv_layer_range(const hack_config_t* cfg, int32_t num_layers, int32_t layer, int32_t prompt_len,
+                            int64_t* begin_out) {
+  KernelCfg kc;
+  if (make_kernel_cfg(cfg, &kc) != HACK_OK || num_layers <= 0 || prompt_len <= 0 || layer < 0 || layer >= num_layers)
+    return -1;
+  const int64_t lb = layer_bytes(kc, prompt_len);
+  const int64_t b = layer == 0 ? 0 : kHeaderBytes + (int64_t)layer * lb;
+  if (begin_out) *begin_out = b;
+  return kHeaderBytes + (int64_t)(layer + 1) * lb - b;
+}
+
+hack_status_t hack_kv_send_layer(void* comm, int32_t peer, const hack_config_t* cfg, const hack_kv_cache_t* caches,
+                                 int32_t num_layers, int32_t layer, int32_t slot, int32_t prompt_len,
+                                 int32_t first_token, uint32_t rng_id, void* staging, void* stream) {
+  KernelCfg kc;
+  LayerPtrs lp;
+  XferGeom g;
+  WireHeader hdr;
+  if (!comm || !staging) return fail(HACK_ERR_INVALID_ARG, "kv_send_layer: NULL comm/staging");
+  if (layer < 0 || layer >= num_layers) return fail(HACK_ERR_INVALID_ARG, "kv_send_layer: layer out of range");
+  hack_status_t st = prepare(cfg, caches, num_layers, slot, prompt_len, &kc, &lp, &g, &hdr);
+  if (st != HACK_OK) return st;
+  hdr.first_token = first_token;
+  hdr.rng_id = rng_id;
+  if ((st = check_device()) != HACK_OK) return st;
+  gather_kernel<<<dim3(g.npages + 1, 1), 256, 0, (cudaStream_t)stream>>>(
+      lp, caches[0].block_table, caches[0].max_pages_per_req, slot, g, hdr, (uint8_t*)staging, layer);
+  note_launch();
+  if ((st = cuda_status(cudaGetLastError(), "kv_send_layer gather")) != HACK_OK) return st;
+  int64_t b = 0;
+  const int64_t n = hack_kv_layer_range(cfg, num_layers, layer, prompt_len, &b);
+  return nccl_status(ncclSend((uint8_t*)staging + b, (size_t)n, ncclUint8, peer, (ncclComm_t)comm,
+                              (cudaStream_t)stream),
+                     "ncclSend (layer)");
+}
+
+hack_status_t hack_kv_recv_layer(void* comm, int32_t peer, const hack_config_t* cfg, int32_t num_layers,
+                                 int32_t layer, int32_t prompt_len, void* staging, void* stream) {
+  if (!comm || !staging) return fail(HACK_ERR_INVALID_ARG, "kv_recv_layer: NULL comm/staging");
+  int64_t b = 0;
+  const int64_t n = hack_kv_layer_range(cfg, num_layers, layer, prompt_len, &b);
+  if (n < 0) return fail(HACK_ERR_INVALID_ARG, "kv_recv_layer: bad config/layer/prompt");
+  return nccl_status(ncclRecv((uint8_t*)staging + b, (size_t)n, ncclUint8, peer, (ncclComm_t)comm,
+                              (cudaStream_t)stream),
+                     "ncclRecv (layer)");
 }
 
 hack_status_t hack_comm_recv_bytes(void* comm, int32_t peer, void* buf, int64_t bytes, void* stream) {

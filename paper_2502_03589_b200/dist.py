@@ -54,6 +54,16 @@ def transfer_bytes(Hkv: int, d: int, Pi: int, bits: int, num_layers: int, prompt
     return HEADER_BYTES + num_layers * layer_bytes(Hkv, d, Pi, bits, prompt_len)
 
 
+def layer_range(Hkv: int, d: int, Pi: int, bits: int, num_layers: int, layer: int, prompt_len: int) -> tuple[int, int]:
+    """== hack_kv_layer_range: (begin, nbytes) of layer `layer` in the wire buffer; layer 0
+    carries the header.  The ranges of layers 0..num_layers-1 tile [0, transfer_bytes)."""
+    if not 0 <= layer < num_layers:
+        raise ValueError("layer out of range")
+    lb = layer_bytes(Hkv, d, Pi, bits, prompt_len)
+    begin = 0 if layer == 0 else HEADER_BYTES + layer * lb
+    return begin, HEADER_BYTES + (layer + 1) * lb - begin
+
+
 @dataclass
 class WireHeader:
     num_layers: int

@@ -69,7 +69,8 @@ for _name in ("hack_config_validate", "hack_page_layout", "hack_quantize_pack", 
               "hack_prefill_attention", "hack_prefill_attention_cached", "hack_decode_append",
               "hack_decode_attention", "hack_decode_attention_cached", "hack_homomorphic_matmul",
               "hack_comm_unique_id", "hack_comm_init", "hack_comm_destroy", "hack_kv_pack", "hack_kv_unpack",
-              "hack_kv_send", "hack_kv_recv", "hack_comm_recv_bytes", "hack_comm_group_start",
+              "hack_kv_send", "hack_kv_recv", "hack_kv_send_layer", "hack_kv_recv_layer",
+              "hack_comm_recv_bytes", "hack_comm_group_start",
               "hack_comm_group_end"):
     getattr(_lib, _name).restype = _S
 
@@ -108,6 +109,11 @@ _lib.hack_kv_send.argtypes = [_P, C.c_int32, C.POINTER(Config), C.POINTER(CacheS
 _lib.hack_kv_recv.argtypes = [_P, C.c_int32, C.POINTER(Config), C.POINTER(CacheStruct), C.c_int32, C.c_int32,
                               C.c_int32, _P, _P, _P]
 _lib.hack_comm_recv_bytes.argtypes = [_P, C.c_int32, _P, C.c_int64, _P]
+_lib.hack_kv_layer_range.restype = C.c_int64
+_lib.hack_kv_layer_range.argtypes = [C.POINTER(Config), C.c_int32, C.c_int32, C.c_int32, C.POINTER(C.c_int64)]
+_lib.hack_kv_send_layer.argtypes = [_P, C.c_int32, C.POINTER(Config), C.POINTER(CacheStruct), C.c_int32, C.c_int32,
+                                    C.c_int32, C.c_int32, C.c_int32, C.c_uint32, _P, _P]
+_lib.hack_kv_recv_layer.argtypes = [_P, C.c_int32, C.POINTER(Config), C.c_int32, C.c_int32, C.c_int32, _P, _P]
 
 
 def _check(st: int, where: str):
@@ -378,6 +384,26 @@ def kv_recv(comm, peer, cfg, caches, slot, prompt_len, staging, status=None, str
     arr = _caches_array(caches)
     _check(_lib.hack_kv_recv(comm, peer, C.byref(cfg), arr, len(caches), slot, prompt_len, _ptr(staging),
                              _ptr(status), _stream(stream)), "kv_recv")
+
+
+def kv_layer_range(cfg: Config, num_layers: int, layer: int, prompt_len: int) -> tuple[int, int]:
+    """(begin, nbytes) of one layer's slice of the wire buffer (layer 0 includes the header)."""
+    b = C.c_int64(0)
+    n = int(_lib.hack_kv_layer_range(C.byref(cfg), num_layers, layer, prompt_len, C.byref(b)))
+    if n < 0:
+        raise HackError(ERR_INVALID_ARG, "kv_layer_range: bad arguments")
+    return int(b.value), n
+
+
+def kv_send_layer(comm, peer, cfg, caches, layer, slot, prompt_len, first_token, rng_id, staging, stream=None):
+    arr = _caches_array(caches)
+    _check(_lib.hack_kv_send_layer(comm, peer, C.byref(cfg), arr, len(caches), layer, slot, prompt_len, first_token,
+                                   rng_id & 0xFFFFFFFF, _ptr(staging), _stream(stream)), "kv_send_layer")
+
+
+def kv_recv_layer(comm, peer, cfg, num_layers, layer, prompt_len, staging, stream=None):
+    _check(_lib.hack_kv_recv_layer(comm, peer, C.byref(cfg), num_layers, layer, prompt_len, _ptr(staging),
+                                   _stream(stream)), "kv_recv_layer")
 
 
 def comm_recv_bytes(comm, peer, buf, nbytes, stream=None):

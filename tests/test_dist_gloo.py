@@ -107,6 +107,40 @@ def _disagg_exchange(rank, world):
             hd.WireHeader.unpack(bad)
 
 
+def _layer_pipelined_exchange(rank, world):
+    """the prefill rank sends each layer's slice as soon as that layer is
+    ingested (one message per layer, layer 0 with the header); the decode rank receives
+    the slices into one buffer, which must equal the one-shot wire bytes."""
+    from paper_2502_03589_b200 import dist as hd
+    Hkv, L, layers = 2, 130, 3
+    nbytes = hd.transfer_bytes(Hkv, 128, 64, 2, layers, L)
+    hdr = hd.WireHeader(layers, Hkv, 128, 64, 2, L, first_token=7, rng_id=99, seed=5)
+    states = []
+    if rank == 0:
+        wire = np.zeros(nbytes, np.uint8)
+        for layer in range(layers):              # "prefill" of layer l, then its send
+            cfg = att.Config(Hq=4, Hkv=Hkv, layer=layer, seed=5)
+            _, k, v = hack_inputs.qkv(60 + layer, L, 4, Hkv)
+            states.append(att.ingest_prompt(cfg, k, v, rng_id=99))
+            full = _wire_bytes(states + [states[-1]] * (layers - len(states)), hdr)
+            b, n = hd.layer_range(Hkv, 128, 64, 2, layers, layer, L)
+            wire[b:b + n] = full[b:b + n]
+            dist.send(torch.from_numpy(wire[b:b + n].copy()), dst=1)
+    else:
+        buf = np.zeros(nbytes, np.uint8)
+        for layer in range(layers):
+            b, n = hd.layer_range(Hkv, 128, 64, 2, layers, layer, L)
+            t = torch.zeros(n, dtype=torch.uint8)
+            dist.recv(t, src=0)
+            buf[b:b + n] = t.numpy()
+        for layer in range(layers):
+            cfg = att.Config(Hq=4, Hkv=Hkv, layer=layer, seed=5)
+            _, k, v = hack_inputs.qkv(60 + layer, L, 4, Hkv)
+            states.append(att.ingest_prompt(cfg, k, v, rng_id=99))
+        assert np.array_equal(buf, _wire_bytes(states, hdr))
+        assert hd.WireHeader.unpack(buf).num_layers == layers
+
+
 def _max_over_ranks(rank, world):
     t = torch.tensor([1.5 + rank], dtype=torch.float64)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -121,6 +155,26 @@ def test_head_sharding_bit_identical_gloo():
 
 def test_disaggregated_wire_exchange_gloo():
     run_gloo("_disagg_exchange")
+
+
+def test_layer_pipelined_exchange_gloo():
+    run_gloo("_layer_pipelined_exchange")
+
+
+def test_layer_ranges_tile_the_wire_buffer():
+    from paper_2502_03589_b200 import dist as hd
+    from paper_2502_03589_b200 import hack as h
+    for (Hkv, Pi, bits) in ((8, 64, 2), (2, 32, 2), (8, 128, 4)):
+        c = h.config(num_q_heads=Hkv, num_kv_heads=Hkv, partition=Pi, kv_bits=bits)
+        for L in (1, 64, 1000):
+            end = 0
+            for layer in range(4):
+                b, n = hd.layer_range(Hkv, 128, Pi, bits, 4, layer, L)
+                assert b == end and n > 0 and (b, n) == h.kv_layer_range(c, 4, layer, L)
+                end = b + n
+            assert end == hd.transfer_bytes(Hkv, 128, Pi, bits, 4, L) == h.kv_transfer_bytes(c, 4, L)
+    with pytest.raises(ValueError):
+        hd.layer_range(8, 128, 64, 2, 4, 4, 10)
 
 
 def test_max_over_ranks_gloo():

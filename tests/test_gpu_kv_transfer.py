@@ -128,3 +128,40 @@ def test_nccl_self_loop():
         check_same(src, dst, 2, 1)
     finally:
         h.comm_destroy(comm)
+
+
+def test_layer_pipelined_nccl_self_loop():
+    """one NCCL message per layer (hack_kv_send_layer / hack_kv_recv_layer),
+    each issued right after that layer's prefill on the same stream; the reassembled
+    buffer equals the one-shot kv_pack bytes and unpacks to the same cache."""
+    h, cfgs, src = setup(7)
+    _, _, dst = setup(8)
+    slot, rid, L_ = 1, 555, L
+    src[0].rng_ids[slot] = rid
+    nbytes = h.kv_transfer_bytes(cfgs[0], LAYERS, L_)
+    comm = h.comm_init(1, 0, h.comm_unique_id())
+    try:
+        send_buf = torch.zeros(nbytes, dtype=torch.uint8, device="cuda")
+        recv_buf = torch.zeros(nbytes, dtype=torch.uint8, device="cuda")
+        cu = torch.tensor([0, L_], dtype=torch.int32, device="cuda")
+        sl = torch.tensor([slot], dtype=torch.int32, device="cuda")
+        for l in range(LAYERS):
+            q, k, v = hack_inputs.qkv(50 + l, L_, 8, 2)
+            out = torch.zeros((L_, 8, 128), dtype=torch.float32, device="cuda")
+            h.prefill_attention(cfgs[l], torch.from_numpy(q).cuda(), torch.from_numpy(k).cuda(),
+                                torch.from_numpy(v).cuda(), cu, sl, L_, src[l], out)
+            h.comm_group_start()
+            h.kv_send_layer(comm, 0, cfgs[0], src, l, slot, L_, first_token=3, rng_id=rid, staging=send_buf)
+            h.kv_recv_layer(comm, 0, cfgs[0], LAYERS, l, L_, recv_buf)
+            h.comm_group_end()
+        ref = torch.zeros(nbytes, dtype=torch.uint8, device="cuda")
+        h.kv_pack(cfgs[0], src, slot, L_, first_token=3, rng_id=rid, staging=ref)
+        torch.cuda.synchronize()
+        assert torch.equal(recv_buf, ref)
+        status = torch.zeros(2, dtype=torch.int32, device="cuda")
+        h.kv_unpack(cfgs[0], dst, 0, L_, recv_buf, status=status)
+        torch.cuda.synchronize()
+        assert status.tolist() == [0, 3]
+        check_same(src, dst, slot, 0)
+    finally:
+        h.comm_destroy(comm)
