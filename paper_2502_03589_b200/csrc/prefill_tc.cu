@@ -78,7 +78,7 @@ struct TcSmem {
   float2 xch[2][2][BM];                   // partial (max, min | -inf if masked)
   float ptail[BM][BN + 1];                // p~ of the FP16 tail tile
   float lpart[2][BM];
-  uint64_t full[NS], empty[NS], k_ready[NB], k_free[NB], v_ready[NB], o_done[NB], p_ready[NB], p_free[NB],
+  uint64_t full[NS], empty[NS], k_ready[NB], k_free[NB], v_ready[NB], o_done[NB], p_ready[NB],
       d_full[2], d_free[2], s_full, s_free, q_ready, l_ready;
   uint32_t tmem_base;
 };
@@ -164,7 +164,6 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_tc_kernel(
       ptx::mbar_init(&sm.v_ready[x], 64);
       ptx::mbar_init(&sm.o_done[x], NOW);
       ptx::mbar_init(&sm.p_ready[x], NSW);
-      ptx::mbar_init(&sm.p_free[x], 1);
     }
     for (int x = 0; x < 2; ++x) {
       ptx::mbar_init(&sm.d_full[x], 1);
@@ -253,7 +252,6 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_tc_kernel(
               ptx::mma_u8(tD0 + 128 * bd, ptx::smem_desc_kmajor(pa + ks * 256, 128, 512),
                           ptx::smem_desc_kmajor(va + ks * 256, 128, 512), idesc_pv, 1u);
             ptx::mma_commit(&sm.d_full[bd]);
-            ptx::mma_commit(&sm.p_free[bq]);
           }
           __syncwarp();
         }

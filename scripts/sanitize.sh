@@ -1,0 +1,17 @@
+#!/bin/bash
+# Run under gpurun: compute-sanitizer (memcheck, racecheck, synccheck) over smoke() and a few
+# small GPU tests that cover the clustered append, the no-RQE append, the paired / G=8
+# decode kernels and the KV pack/unpack.  Logs -> gpurun_out/san_<tool>.log
+OUT=gpurun_out
+mkdir -p $OUT
+SAN=/usr/local/cuda/bin/compute-sanitizer
+TESTS="tests/test_gpu_rqe_ablation.py::test_no_rqe_requantizes_partial_block[2] tests/test_gpu_decode.py::test_decode_paired_kernel_edges tests/test_gpu_decode.py::test_decode_group8_paired_kernel[8] tests/test_gpu_kv_transfer.py::test_pack_unpack_round_trip_and_decode_equivalence"
+for tool in ${TOOLS:-memcheck racecheck synccheck}; do
+  {
+    timeout 600 $SAN --tool $tool --error-exitcode 9 python -c "import __graft_entry__ as g; g.smoke()"
+    echo "smoke exit $?"
+    timeout 900 $SAN --tool $tool --error-exitcode 9 python -m pytest -x -q -p no:cacheprovider $TESTS
+    echo "tests exit $?"
+  } > $OUT/san_$tool.log 2>&1
+  grep -E "ERROR SUMMARY|exit|passed|failed" $OUT/san_$tool.log | tail -6
+done
