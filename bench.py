@@ -638,44 +638,46 @@ def run_decode(args, h, dev, rank, world, peaks, traffic, seed, flush):
         torch.cuda.synchronize()
         ms = max_over_ranks(ev[0].elapsed_time(ev[1]) / args.steps, world)
         attn_avg = max_over_ranks(ev[2].elapsed_time(ev[3]) / args.steps, world)
-        # SURVEY f2 (HACK/SE ablation): the same attention launches with the code
-        # sums recomputed from the codes every step instead of read from the summation cache
-        os.environ["HACK_DECODE_NO_SE"] = "1"
-        g_nose = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(g_nose):
-            for i in range(args.steps):
-                lay = (it[0] + i) % n_layers
-                h.decode_attention_cached(cfg, qn[(it[0] + i) % nsteps], slots_all, max_len, caches[lay], out,
-                                          workspace=ws)
-        del os.environ["HACK_DECODE_NO_SE"]
-        torch.cuda.synchronize()
-        ev[2].record(stream)
-        g_nose.replay()
-        ev[3].record(stream)
-        torch.cuda.synchronize()
-        no_se_ms = max_over_ranks(ev[2].elapsed_time(ev[3]) / args.steps, world)
-        # SURVEY f2 (HACK/RQE ablation): Pi consecutive appends (every tail
-        # length 1..Pi once per request and layer) with the partial V block requantized at
-        # every step, vs the same appends with requantization elimination
-        rqe_ms = {}
-        for mode in ("rqe", "no_rqe"):
-            if mode == "no_rqe":
-                os.environ["HACK_DECODE_NO_RQE"] = "1"
-            g_app = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(g_app):
-                for i in range(Pi):
-                    for lay in range(n_layers):
-                        h.decode_append(cfg, kn[(it[0] + i) % nsteps], vn[(it[0] + i) % nsteps], slots_all,
-                                        caches[lay])
-            os.environ.pop("HACK_DECODE_NO_RQE", None)
-            it[0] += Pi
+        no_se_ms, rqe_ms = None, None
+        if not args.no_ablation:
+            # SURVEY f2 (HACK/SE ablation): the same attention launches with the code
+            # sums recomputed from the codes every step instead of read from the summation cache
+            os.environ["HACK_DECODE_NO_SE"] = "1"
+            g_nose = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g_nose):
+                for i in range(args.steps):
+                    lay = (it[0] + i) % n_layers
+                    h.decode_attention_cached(cfg, qn[(it[0] + i) % nsteps], slots_all, max_len, caches[lay], out,
+                                              workspace=ws)
+            del os.environ["HACK_DECODE_NO_SE"]
             torch.cuda.synchronize()
             ev[2].record(stream)
-            g_app.replay()
+            g_nose.replay()
             ev[3].record(stream)
             torch.cuda.synchronize()
-            rqe_ms[mode] = max_over_ranks(ev[2].elapsed_time(ev[3]) / (Pi * n_layers), world)
-            del g_app
+            no_se_ms = max_over_ranks(ev[2].elapsed_time(ev[3]) / args.steps, world)
+            # SURVEY f2 (HACK/RQE ablation): Pi consecutive appends (every tail
+            # length 1..Pi once per request and layer) with the partial V block requantized at
+            # every step, vs the same appends with requantization elimination
+            rqe_ms = {}
+            for mode in ("rqe", "no_rqe"):
+                if mode == "no_rqe":
+                    os.environ["HACK_DECODE_NO_RQE"] = "1"
+                g_app = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g_app):
+                    for i in range(Pi):
+                        for lay in range(n_layers):
+                            h.decode_append(cfg, kn[(it[0] + i) % nsteps], vn[(it[0] + i) % nsteps], slots_all,
+                                            caches[lay])
+                os.environ.pop("HACK_DECODE_NO_RQE", None)
+                it[0] += Pi
+                torch.cuda.synchronize()
+                ev[2].record(stream)
+                g_app.replay()
+                ev[3].record(stream)
+                torch.cuda.synchronize()
+                rqe_ms[mode] = max_over_ranks(ev[2].elapsed_time(ev[3]) / (Pi * n_layers), world)
+                del g_app
     # algorithmic bytes of one attention launch (context n after the append): committed
     # tokens at 84 B/token/head (packed K+V, meta, sums), tail tokens at K-row bytes +
     # fp16 V, plus q in and out.
@@ -714,7 +716,7 @@ def run_decode(args, h, dev, rank, world, peaks, traffic, seed, flush):
                       "ms_per_layer_step": c_ms, "hack_attn_ms": attn_avg, "hack_speedup": c_ms / attn_avg,
                       "fp16_cache_bytes": 2 * kh.numel() * 2}
         del kh, vh, o4
-    ablation = None if args.no_graph else {
+    ablation = None if args.no_graph or args.no_ablation else {
         "no_summation_elimination": {"attn_ms": no_se_ms, "kv_gbs": avg_bytes / (no_se_ms * 1e-3) / 1e9,
                                      "slowdown": no_se_ms / attn_avg,
                                      "what": "code sums recomputed from the codes every step (HACK/SE, P:1036-1042)"},
@@ -783,6 +785,7 @@ def main():
     ap.add_argument("--no-c4", action="store_true", help="skip the C4 (70B-shaped, 2- vs 4-bit) sub-benchmark")
     ap.add_argument("--no-sweep", action="store_true", help="skip the Pi x bits sweep (SURVEY f)")
     ap.add_argument("--no-comparator", action="store_true", help="skip the dequantize-first comparator (f4)")
+    ap.add_argument("--no-ablation", action="store_true", help="skip the SE / RQE ablation timings (f2)")
     ap.add_argument("--no-graph", action="store_true",
                     help="decode: launch eagerly instead of replaying a CUDA graph of the K timed steps")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
