@@ -378,8 +378,8 @@ def run_sweep(args, h, dev, seed, flush):
     """SURVEY f (Pi/bit sweep): partition size Pi in {32, 64, 128} x K/V bits in
     {2, 4} on a reduced C2/C3 shape (32 Q / 8 KV heads): one 2048-token causal prefill (ingest +
     attention, L2 flushed) and a batch-16 decode step at 4096 context (append + attention,
-    CUDA graph).  Pi = 64 runs the tcgen05 prefill and the mma.sync decode kernels; Pi = 32
-    and 128 run the CUDA-core kernels (tensor-core versions are not built)."""
+    CUDA graph).  Decode runs on the mma.sync tensor-core kernels at every Pi; prefill runs the
+    tcgen05 kernel at Pi = 64 and the CUDA-core kernel at Pi = 32 and 128."""
     import torch
     Hq, Hkv, L, B, ctx = 32, 8, 2048, 16, 4096
     stream = torch.cuda.current_stream()
@@ -444,8 +444,8 @@ def run_sweep(args, h, dev, seed, flush):
             res["points"].append({
                 "Pi": Pi, "bits": bits,
                 "prefill_kernel": "prefill_tc_kernel (tcgen05)" if Pi == 64 else "prefill_simt (CUDA cores)",
-                "decode_kernel": ("decode_pair_kernel (mma.sync)" if bits == 2 else "decode_mma_kernel (mma.sync)")
-                if Pi == 64 else "decode_simt (CUDA cores)",
+                "decode_kernel": "decode_pair_kernel (mma.sync)" if Pi == 64 and bits == 2
+                else f"decode_mma_kernel<{bits}, {Pi}> (mma.sync)",
                 "prefill_tops": ops / (pre_ms * 1e-3) / 1e12, "prefill_ms": pre_ms,
                 "decode_step_ms": dec_ms, "decode_kv_gbs": dec_bytes / (dec_ms * 1e-3) / 1e9,
                 "bytes_per_token_head": pb / Pi})

@@ -25,7 +25,6 @@ namespace hack {
 
 namespace {
 
-constexpr int PI = 64;
 #ifndef HACK_DMMA_NW
 #define HACK_DMMA_NW 4
 #endif
@@ -41,23 +40,44 @@ constexpr int kCtas = HACK_DMMA_CTAS;  // resident CTAs per SM (launch bounds)
 constexpr int kThreads = (NW + 1) * 32;
 constexpr uint32_t kMagicI = 0x4B000000u;  // bits of 2^23
 
-template <int BITS>
+constexpr int up16(int x) { return (x + 15) / 16 * 16; }
+// Page bytes at d = 128 (the closed form of hack_page_bytes).
+constexpr int page_bytes_of(int bits, int pi) {
+  const int nb = 128 / pi, sw = (bits == 2 ? pi * 3 : pi * 15) > 255 ? 2 : 1;
+  return up16(pi * 128 * bits / 8) + up16(pi * nb * 4) + up16(pi * nb * sw) + up16(128 * pi * bits / 8) +
+         up16(128 * 4) + up16(128 * sw);
+}
+
+// PI_ = partition size Pi in {32, 64, 128}: a page holds PI_ tokens (one V partition per
+// channel), a K row holds NB = 128 / PI_ partitions (beta), the QK m-tiles per page are
+// PI_ / 16 and the PV k-steps per page PI_ / 32.
+template <int BITS, int PI_>
 struct DecSmem {
-  static constexpr int PB = BITS == 2 ? 5376 : 9728;
+  static constexpr int PI = PI_;
+  static constexpr int NB = 128 / PI_;
+  static constexpr int PB = page_bytes_of(BITS, PI_);
+  // ring depth: NSTG pages at Pi = 64 (as tuned); other Pi keep the ring within ~48 KB.
+  // NS must be a multiple of NW: warp w takes pages w, w + NW, ..., so slot k % NS is then
+  // only ever refilled for the same warp and a phase-parity wait can never alias a fill
+  // two phases behind.
+  static constexpr int NS_FIT = 48 * 1024 / PB / NW * NW;
+  static constexpr int NS = (PI_ == 64 || PB * NSTG <= 48 * 1024) ? NSTG : (NS_FIT < NW ? NW : NS_FIT);
+  static_assert(NS % NW == 0, "ring depth must be a multiple of the compute warps");
+  static constexpr int RING = PB * NS > NW * 8 * 128 * 4 ? PB * NS : NW * 8 * 128 * 4;
   union {
-    uint8_t stage[NSTG][PB];
+    uint8_t stage[RING];      // NS page slots of PB bytes
     float mrg_o[NW][8][128];  // after the page loop: per-warp partial O for the CTA merge
   };
   struct Warp {
-    float4 kc[2][PI];                 // [beta][token]: sk, mu_k, y_k, -r_k
+    float4 kc[NB][PI];                // [beta][token]: sk, mu_k, y_k, -r_k
     float4 vc[128];                   // [channel]: sv, mu_v, y_v, -r_v
     alignas(16) uint8_t pcode[8][PI]; // P' in B-fragment order
     float ptl[8][PI];                 // p~ of the FP16 tail page
   } w[NW];
   uint8_t qcode[8][128];              // Q' rows (natural channel order)
-  float4 qconst[2][8];                // per (beta, row): aq, xq, mu_q, -r_q
+  float4 qconst[NB][8];               // per (beta, row): aq, xq, mu_q, -r_q
   float mrg_m[NW][8], mrg_l[NW][8];
-  uint64_t full[NSTG], empty[NSTG];
+  uint64_t full[NS], empty[NS];
 };
 
 HACK_DEV float u2f(uint32_t x) { return __int2float_rn((int)x); }
@@ -78,12 +98,14 @@ HACK_DEV uint32_t plane(uint32_t w, int sh) {
 
 // Token / channel index held by byte i of plane `tig` of packed word W (16-code words at
 // b=2: index 16W + 4i + tig; at b=4 words hold 8 codes: index 8W + 2i + tig, tig in {0,1}).
-template <int BITS>
+template <int BITS, int PI_>
 __global__ void __launch_bounds__(kThreads, kCtas) decode_mma_kernel(const __half* __restrict__ q_new,
                                                               const int32_t* __restrict__ slots, CacheView cv,
                                                               KernelCfg kc, float* __restrict__ part, int nsplit,
                                                               uint8_t* __restrict__ dbg_pcodes, int64_t dbg_stride) {
-  using SM = DecSmem<BITS>;
+  using SM = DecSmem<BITS, PI_>;
+  constexpr int PI = PI_, NB = SM::NB, NS = SM::NS;
+  constexpr int MT = PI / 16, KSV = PI / 32;  // QK m-tiles, PV k-steps per page
   constexpr int qkm = (1 << BITS) - 1;
   extern __shared__ __align__(128) uint8_t smem_raw[];
   SM& sm = *reinterpret_cast<SM*>(smem_raw);
@@ -103,7 +125,7 @@ __global__ void __launch_bounds__(kThreads, kCtas) decode_mma_kernel(const __hal
   const uint32_t rng_id = cv.rng_ids[slot];
 
   if (tid == 0) {
-    for (int s = 0; s < NSTG; ++s) {
+    for (int s = 0; s < NS; ++s) {
       ptx::mbar_init(&sm.full[s], 1);
       ptx::mbar_init(&sm.empty[s], 1);
     }
@@ -122,8 +144,8 @@ __global__ void __launch_bounds__(kThreads, kCtas) decode_mma_kernel(const __hal
                           stream_c3(kc.layer, kTagQ, kc.head_base * G + hq), kc.q_round, packed, m, s, sum);
     *reinterpret_cast<uint2*>(&sm.qcode[row][lane16 * 8]) =
         row < G ? make_uint2((uint32_t)packed, (uint32_t)(packed >> 32)) : make_uint2(0u, 0u);
-    if ((lane16 & 7) == 0) {
-      const int beta = lane16 >> 3;
+    if ((lane16 & (PI / 8 - 1)) == 0) {  // first lane of the row's partition beta
+      const int beta = lane16 / (PI / 8);
       const float cscale = 1.4426950408889634f / sqrtf(128.f);
       sm.qconst[beta][row] = row < G ? make_float4(cscale * s * 0.25f, cscale * s * ((float)sum - 127.5f * PI),
                                                    cscale * (m + 127.5f * s), -(float)(2 * qkm * sum - PI * 255 * qkm))
@@ -143,11 +165,11 @@ __global__ void __launch_bounds__(kThreads, kCtas) decode_mma_kernel(const __hal
     if (lane == 0) {
       const int32_t* bt = cv.block_table + (int64_t)slot * cv.max_pages_per_req;
       for (int k = 0; k < np; ++k) {
-        const int s = k % NSTG;
-        ptx::mbar_wait(&sm.empty[s], ((k / NSTG) & 1) ^ 1);
+        const int s = k % NS;
+        ptx::mbar_wait(&sm.empty[s], ((k / NS) & 1) ^ 1);
         ptx::mbar_arrive_expect_tx(&sm.full[s], SM::PB);
         const uint8_t* pg = cv.pages + ((int64_t)bt[p_beg + k] * cv.num_kv_heads + hk) * cv.page_bytes;
-        ptx::bulk_g2s(sm.stage[s], pg, SM::PB, &sm.full[s]);
+        ptx::bulk_g2s(sm.stage + s * SM::PB, pg, SM::PB, &sm.full[s]);
       }
     }
   } else {
@@ -167,9 +189,9 @@ __global__ void __launch_bounds__(kThreads, kCtas) decode_mma_kernel(const __hal
         }
         qb[ks][h] = v;
       }
-    float2 QA[2], QX[2], QM[2], QN[2];
+    float2 QA[NB], QX[NB], QM[NB], QN[NB];
 #pragma unroll
-    for (int beta = 0; beta < 2; ++beta) {
+    for (int beta = 0; beta < NB; ++beta) {
       const float4 c0 = sm.qconst[beta][n0], c1 = sm.qconst[beta][n1];
       QA[beta] = make_float2(c0.x, c1.x);
       QX[beta] = make_float2(c0.y, c1.y);
@@ -180,17 +202,17 @@ __global__ void __launch_bounds__(kThreads, kCtas) decode_mma_kernel(const __hal
 
 #pragma unroll 1
     for (int k = warp; k < np; k += NW) {
-      const int s = k % NSTG;
+      const int s = k % NS;
       const int jp = p_beg + k;              // page index in the request
       const bool committed = jp < nfull;
       const int nk = min(PI, len - jp * PI);
-      ptx::mbar_wait(&sm.full[s], (k / NSTG) & 1);
-      const uint8_t* pg = sm.stage[s];
+      ptx::mbar_wait(&sm.full[s], (k / NS) & 1);
+      const uint8_t* pg = sm.stage + s * SM::PB;
       // -- per-token (beta) and per-channel Eq. 4 coefficients from fp16 meta + cached sums
 #pragma unroll
       for (int x = 0; x < 4; ++x) {
-        const int e = lane + 32 * x;        // (token, beta) = (e >> 1, e & 1)
-        const int t = e >> 1, beta = e & 1;
+        const int e = lane + 32 * x;        // (token, beta) = (e / NB, e % NB): PI x NB = 128 entries
+        const int t = e / NB, beta = e % NB;
         float c0 = 0.f, c1 = 0.f, c2 = 0.f, c3 = 0.f;
         if (t < nk) {
           const __half2 mh = reinterpret_cast<const __half2*>(pg + PL.k_meta)[e];
@@ -217,10 +239,10 @@ __global__ void __launch_bounds__(kThreads, kCtas) decode_mma_kernel(const __hal
       }
       __syncwarp();
       // -- S^T = K' Q'^T per m-tile of 16 tokens; Eq. 4 on (row n0, n1) pairs
-      float2 sv2[4][2];  // [m-tile][token g / g+8]
+      float2 sv2[MT][2];  // [m-tile][token g / g+8]
       float2 mx2 = make_float2(-INFINITY, -INFINITY), mn2 = make_float2(INFINITY, INFINITY);
 #pragma unroll
-      for (int mt = 0; mt < 4; ++mt) {
+      for (int mt = 0; mt < MT; ++mt) {
         const int t0 = 16 * mt + g, t1 = t0 + 8;
         const uint4* r0 = reinterpret_cast<const uint4*>(pg + PL.k_codes + t0 * (128 * BITS / 8));
         const uint4* r1 = reinterpret_cast<const uint4*>(pg + PL.k_codes + t1 * (128 * BITS / 8));
@@ -232,7 +254,9 @@ __global__ void __launch_bounds__(kThreads, kCtas) decode_mma_kernel(const __hal
           w1[4 * x] = c.x; w1[4 * x + 1] = c.y; w1[4 * x + 2] = c.z; w1[4 * x + 3] = c.w;
         }
         // accumulate on top of 0x4B000000: asfloat(acc) = 2^23 + D exactly (D < 2^22)
-        uint32_t acc[2][4] = {{kMagicI, kMagicI, kMagicI, kMagicI}, {kMagicI, kMagicI, kMagicI, kMagicI}};
+        uint32_t acc[NB][4];
+#pragma unroll
+        for (int beta = 0; beta < NB; ++beta) acc[beta][0] = acc[beta][1] = acc[beta][2] = acc[beta][3] = kMagicI;
 #pragma unroll
         for (int ks = 0; ks < 4; ++ks) {
           uint32_t a[4];
@@ -249,7 +273,7 @@ __global__ void __launch_bounds__(kThreads, kCtas) decode_mma_kernel(const __hal
             a[2] = plane<4>(odd ? w0[4 * ks + 3] : w0[4 * ks + 2], sh);
             a[3] = plane<4>(odd ? w1[4 * ks + 3] : w1[4 * ks + 2], sh);
           }
-          mma16832(acc[ks >> 1], a, qb[ks][0], qb[ks][1]);
+          mma16832(acc[ks * 32 / PI], a, qb[ks][0], qb[ks][1]);  // k-step ks: channels 32ks.. of block beta
         }
         float2 st[2];
 #pragma unroll
@@ -257,7 +281,7 @@ __global__ void __launch_bounds__(kThreads, kCtas) decode_mma_kernel(const __hal
           const int t = hh ? t1 : t0;
           float2 accf = make_float2(0.f, 0.f);
 #pragma unroll
-          for (int beta = 0; beta < 2; ++beta) {
+          for (int beta = 0; beta < NB; ++beta) {
             const float4 k4 = ws.kc[beta][t];
             const float sk = k4.x, mu = k4.y, yk = k4.z, nr = k4.w;
             const float2 df = ptx::fadd2(make_float2(__uint_as_float(acc[beta][2 * hh]), __uint_as_float(acc[beta][2 * hh + 1])),
@@ -287,7 +311,7 @@ __global__ void __launch_bounds__(kThreads, kCtas) decode_mma_kernel(const __hal
                                     m_run.y == -INFINITY ? 0.f : ex2(m_run.y - mnew.y));
       float2 ls = make_float2(0.f, 0.f);
 #pragma unroll
-      for (int mt = 0; mt < 4; ++mt)
+      for (int mt = 0; mt < MT; ++mt)
 #pragma unroll
         for (int hh = 0; hh < 2; ++hh) {
           const float2 a2 = ptx::fadd2(sv2[mt][hh], make_float2(-mnew.x, -mnew.y));
@@ -316,7 +340,7 @@ __global__ void __launch_bounds__(kThreads, kCtas) decode_mma_kernel(const __hal
         const float2 inv2 = make_float2(pm0.inv, pm1.inv), nlo2 = make_float2(-lo.x * pm0.inv, -lo.y * pm1.inv);
         uint32_t sp0 = 0, sp1 = 0;
 #pragma unroll
-        for (int mt = 0; mt < 4; ++mt)
+        for (int mt = 0; mt < MT; ++mt)
 #pragma unroll
           for (int hh = 0; hh < 2; ++hh) {
             const int t = 16 * mt + g + 8 * hh;
@@ -346,9 +370,9 @@ __global__ void __launch_bounds__(kThreads, kCtas) decode_mma_kernel(const __hal
           }
         }
         // P' B fragments (row n = g): positions 32ks + 4tig (b0) and 32ks + 16 + 4tig (b1)
-        uint32_t pb[2][2];
+        uint32_t pb[KSV][2];
 #pragma unroll
-        for (int ks = 0; ks < 2; ++ks) {
+        for (int ks = 0; ks < KSV; ++ks) {
           pb[ks][0] = *reinterpret_cast<const uint32_t*>(&ws.pcode[g][32 * ks + 4 * tig]);
           pb[ks][1] = *reinterpret_cast<const uint32_t*>(&ws.pcode[g][32 * ks + 16 + 4 * tig]);
         }
@@ -361,24 +385,27 @@ __global__ void __launch_bounds__(kThreads, kCtas) decode_mma_kernel(const __hal
 #pragma unroll
         for (int mt = 0; mt < 8; ++mt) {
           const int c0 = 16 * mt + g, c1 = c0 + 8;
-          const uint4 va = *reinterpret_cast<const uint4*>(pg + PL.v_codes + c0 * (PI * BITS / 8));
-          const uint4 vb = *reinterpret_cast<const uint4*>(pg + PL.v_codes + c1 * (PI * BITS / 8));
+          // the channel's PI codes: PI * BITS / 32 words (2 per 32-token k-step at b = 2, 4 at b = 4)
+          constexpr int NWD = PI * BITS / 32;
+          uint32_t wa[NWD], wb[NWD];
+#pragma unroll
+          for (int x = 0; x < NWD; x += 2) {
+            const uint2 a2 = *reinterpret_cast<const uint2*>(pg + PL.v_codes + c0 * (PI * BITS / 8) + 4 * x);
+            const uint2 b2 = *reinterpret_cast<const uint2*>(pg + PL.v_codes + c1 * (PI * BITS / 8) + 4 * x);
+            wa[x] = a2.x; wa[x + 1] = a2.y;
+            wb[x] = b2.x; wb[x + 1] = b2.y;
+          }
           uint32_t dacc[4] = {kMagicI, kMagicI, kMagicI, kMagicI};
           if (BITS == 2) {
-            const uint32_t wa[4] = {va.x, va.y, va.z, va.w}, wb[4] = {vb.x, vb.y, vb.z, vb.w};
 #pragma unroll
-            for (int ks = 0; ks < 2; ++ks) {
+            for (int ks = 0; ks < KSV; ++ks) {
               const uint32_t a[4] = {plane<2>(wa[2 * ks], sh), plane<2>(wb[2 * ks], sh), plane<2>(wa[2 * ks + 1], sh),
                                      plane<2>(wb[2 * ks + 1], sh)};
               mma16832(dacc, a, pb[ks][0], pb[ks][1]);
             }
           } else {
-            const uint4 va2 = *reinterpret_cast<const uint4*>(pg + PL.v_codes + c0 * (PI * BITS / 8) + 16);
-            const uint4 vb2 = *reinterpret_cast<const uint4*>(pg + PL.v_codes + c1 * (PI * BITS / 8) + 16);
-            const uint32_t wa[8] = {va.x, va.y, va.z, va.w, va2.x, va2.y, va2.z, va2.w};
-            const uint32_t wb[8] = {vb.x, vb.y, vb.z, vb.w, vb2.x, vb2.y, vb2.z, vb2.w};
 #pragma unroll
-            for (int ks = 0; ks < 2; ++ks) {
+            for (int ks = 0; ks < KSV; ++ks) {
               const bool odd = tig >> 1;
               const uint32_t a[4] = {plane<4>(odd ? wa[4 * ks + 1] : wa[4 * ks], sh),
                                      plane<4>(odd ? wb[4 * ks + 1] : wb[4 * ks], sh),
@@ -403,7 +430,7 @@ __global__ void __launch_bounds__(kThreads, kCtas) decode_mma_kernel(const __hal
       } else {
         // -- FP16 last V block (RQE): O^T += V_tail^T p~ in fp32
 #pragma unroll
-        for (int mt = 0; mt < 4; ++mt)
+        for (int mt = 0; mt < MT; ++mt)
 #pragma unroll
           for (int hh = 0; hh < 2; ++hh) {
             const int t = 16 * mt + g + 8 * hh;
@@ -497,11 +524,12 @@ __global__ void decode_combine_kernel(const float* __restrict__ part, int nsplit
     reinterpret_cast<__half*>(out)[idx] = __float2half_rn(v);
 }
 
-template <int BITS>
+template <int BITS, int PI_>
 cudaError_t launch_t(const KernelCfg& kc, const void* q_new, const int32_t* slots, int batch, int nsplit,
                      const CacheView& cv, void* out, float* part, const hack_debug_t* dbg, cudaStream_t st) {
-  const size_t smem = sizeof(DecSmem<BITS>);
-  auto kern = decode_mma_kernel<BITS>;
+  if (kc.pl.page_bytes != DecSmem<BITS, PI_>::PB) return cudaErrorInvalidValue;  // layout drift guard
+  const size_t smem = sizeof(DecSmem<BITS, PI_>);
+  auto kern = decode_mma_kernel<BITS, PI_>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   kern<<<dim3(batch, kc.Hkv, nsplit), kThreads, smem, st>>>(reinterpret_cast<const __half*>(q_new), slots, cv, kc,
@@ -521,10 +549,12 @@ cudaError_t launch_decode_combine(const float* part, int nsplit, const KernelCfg
   return cudaGetLastError();
 }
 
-bool decode_mma_supported(const KernelCfg& kc) { return kc.Pi == 64 && kc.G <= 8; }
+bool decode_mma_supported(const KernelCfg& kc) {
+  return (kc.Pi == 32 || kc.Pi == 64 || kc.Pi == 128) && kc.d == 128 && kc.G <= 8;
+}
 
 int decode_nsplit(const KernelCfg& kc, int batch, int max_seqlen) {
-  const int max_pages = (max_seqlen + PI - 1) / PI;
+  const int max_pages = (max_seqlen + kc.Pi - 1) / kc.Pi;
   const int units = batch * kc.Hkv;
   // aim for ~4 waves of resident CTAs (148 SMs x 3), at least ~8 pages per split
   int ns = (148 * kCtas * 4 + units - 1) / units;
@@ -541,8 +571,15 @@ cudaError_t launch_decode_mma(const KernelCfg& kc, const void* q_new, const int3
                               const hack_debug_t* dbg, cudaStream_t st) {
   const int ns = decode_nsplit(kc, batch, max_seqlen);
   float* part = reinterpret_cast<float*>(workspace);
-  if (kc.bits == 2) return launch_t<2>(kc, q_new, slots, batch, ns, cv, out, part, dbg, st);
-  return launch_t<4>(kc, q_new, slots, batch, ns, cv, out, part, dbg, st);
+  switch (kc.Pi * 8 + kc.bits) {
+    case 32 * 8 + 2: return launch_t<2, 32>(kc, q_new, slots, batch, ns, cv, out, part, dbg, st);
+    case 32 * 8 + 4: return launch_t<4, 32>(kc, q_new, slots, batch, ns, cv, out, part, dbg, st);
+    case 64 * 8 + 2: return launch_t<2, 64>(kc, q_new, slots, batch, ns, cv, out, part, dbg, st);
+    case 64 * 8 + 4: return launch_t<4, 64>(kc, q_new, slots, batch, ns, cv, out, part, dbg, st);
+    case 128 * 8 + 2: return launch_t<2, 128>(kc, q_new, slots, batch, ns, cv, out, part, dbg, st);
+    case 128 * 8 + 4: return launch_t<4, 128>(kc, q_new, slots, batch, ns, cv, out, part, dbg, st);
+    default: return cudaErrorInvalidValue;
+  }
 }
 
 }  // namespace hack

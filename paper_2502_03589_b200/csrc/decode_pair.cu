@@ -72,6 +72,7 @@ struct PairSmem {
   int range_b0, range_base;  // request holding the CTA's first page, flattened offset of its first unit
   int R, P;
   uint64_t full[NSTG], fullv[NSTG], empty[NSTG];  // fullv: the V half of a split page copy
+  int tag[NSTG];  // page index of the slot's latest issued fill (see wait_fill)
 };
 
 HACK_DEV void mma16832(uint32_t (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3, uint32_t b0,
@@ -277,6 +278,20 @@ HACK_DEV void locate_range(SMT& sm, const CacheView& cv, const int32_t* __restri
   }
 }
 
+// Consumer wait for page k in slot k % N.  Pages are not consumed by a fixed warp per slot
+// (items rotate over the warps per segment), so a warp may start waiting for fill k of a
+// slot while fill k - N is still in flight; a bare phase-parity wait would then match the
+// phase of fill k - 2N.  The producer tags each slot with the page index before issuing its
+// fill, and fill k is only issued after fill k - N was consumed, so once the tag reads k
+// the parity wait is exact.
+template <int N, class SMT>
+HACK_DEV void wait_fill(SMT& sm, int k) {
+  const int s = k % N;
+  while (*reinterpret_cast<volatile int*>(&sm.tag[s]) != k) {
+  }
+  ptx::mbar_wait(&sm.full[s], (k / N) & 1);
+}
+
 // Producer warp: streams the CTA's pages in order into an N-slot ring (cp.async.bulk).
 template <int N, class SMT>
 HACK_DEV void produce_pages(SMT& sm, SegWalker walk, const CacheView& cv, const int32_t* __restrict__ slots,
@@ -310,6 +325,7 @@ HACK_DEV void produce_pages(SMT& sm, SegWalker walk, const CacheView& cv, const 
           while (!ptx::mbar_try_wait_sleep(&sm.empty[st], ((k / N) & 1) ^ 1)) {
           }
 #endif
+          *reinterpret_cast<volatile int*>(&sm.tag[st]) = k;  // fill k of slot st is being issued
 #if HACK_DEC_SPLIT
           // two copies: the K half (codes + meta + sums) lands first and QK can start
           const uint32_t kb = (uint32_t)kc.pl.v_codes;
@@ -354,6 +370,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
     for (int s = 0; s < NSTG; ++s) {
       ptx::mbar_init(&sm.full[s], 1);
       ptx::mbar_init(&sm.fullv[s], 1);
+      sm.tag[s] = -1;
       ptx::mbar_init(&sm.empty[s], 1);
     }
     ptx::fence_mbar_init();
@@ -450,7 +467,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
         // ---- (a4) homomorphic S^T for page A (and B)
         float sa[4][2], sbv[4][2];
         float mxA, mnA, mxB = -INFINITY, mnB = INFINITY;
-        ptx::mbar_wait(&sm.full[sA], (kA / NSTG) & 1);
+        wait_fill<NSTG>(sm, kA);
         stage_kc<SE>(pgA, PL, &ws.scr[0][0], lane);
         __syncwarp();
         if (tail_item)
@@ -458,7 +475,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
         else
           qk_page<false>(pgA, PL, &ws.scr[0][0], g, tig, PI, qb, QA, QX, QM, rc0, rc1, sa, mxA, mnA);
         if (hasB) {
-          ptx::mbar_wait(&sm.full[sB], (kB / NSTG) & 1);
+          wait_fill<NSTG>(sm, kB);
           __syncwarp();
           stage_kc<SE>(pgB, PL, &ws.scr[0][0], lane);
           __syncwarp();
@@ -690,6 +707,7 @@ struct G8Smem {
   int range_b0, range_base;
   int R, P;
   uint64_t full[NSTG8], fullv[NSTG8], empty[NSTG8];
+  int tag[NSTG8];
 };
 
 template <bool DBG>
@@ -709,6 +727,7 @@ __global__ void __launch_bounds__(kThreads, kCtas8)
     for (int s = 0; s < NSTG8; ++s) {
       ptx::mbar_init(&sm.full[s], 1);
       ptx::mbar_init(&sm.fullv[s], 1);
+      sm.tag[s] = -1;
       ptx::mbar_init(&sm.empty[s], 1);
     }
     ptx::fence_mbar_init();
@@ -803,7 +822,7 @@ __global__ void __launch_bounds__(kThreads, kCtas8)
         const bool committed = jp < nfull;
         const int nk = committed ? PI : len - jp * PI;
         uint8_t* pg = sm.stage[st];
-        ptx::mbar_wait(&sm.full[st], (k / NSTG8) & 1);
+        wait_fill<NSTG8>(sm, k);
         stage_kc<true>(pg, PL, &ws.scr[0][0], lane);
         __syncwarp();
         // ---- (a4) S^T for the 8 rows: sc[nt][mt][hh] = row 4 nt + tig, token 16 mt + g + 8 hh

@@ -87,9 +87,23 @@ def test_decode_batch_gqa_mixed_lengths():
     run_decode(att.Config(Hq=8, Hkv=2, Pi=64, bits=2, seed=99, layer=1), [100, 1, 64, 255], 40, check_every=5)
 
 
-@pytest.mark.parametrize("Pi,bits", [(32, 2), (128, 2), (64, 4), (128, 4)])
+@pytest.mark.parametrize("Pi,bits", [(32, 2), (128, 2), (64, 4), (128, 4), (32, 4)])
 def test_decode_partition_and_bits(Pi, bits):
+    # Pi in {32, 128}: decode_mma_kernel<BITS, Pi>; Pi = 64, b = 4: decode_mma too
     run_decode(att.Config(Hq=4, Hkv=2, Pi=Pi, bits=bits), [150, 129], 2 * Pi + 3, check_every=11)
+
+
+@pytest.mark.parametrize("Pi,bits,Hq", [(32, 2, 8), (128, 4, 6), (128, 2, 1)])
+def test_decode_partition_group_shapes(Pi, bits, Hq):
+    # G = 8, 6 (two row pairs padded), 1 at the non-64 partitions; ragged lengths incl. 1 token
+    run_decode(att.Config(Hq=Hq, Hkv=1, Pi=Pi, bits=bits, seed=13), [1, 2 * Pi + 5, 300], Pi + 2, check_every=17)
+
+
+@pytest.mark.parametrize("Pi,bits", [(32, 2), (128, 4)])
+def test_decode_simt_other_partitions(Pi, bits, monkeypatch):
+    # the CUDA-core kernel stays a parity-checked baseline at Pi != 64
+    monkeypatch.setenv("HACK_DECODE_IMPL", "simt")
+    run_decode(att.Config(Hq=4, Hkv=2, Pi=Pi, bits=bits), [150, 129], Pi + 3, check_every=13)
 
 
 def test_decode_group_16():
