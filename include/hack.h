@@ -170,7 +170,10 @@ hack_status_t hack_prefill_attention_cached(const hack_config_t* cfg, const void
 /* ---- (a8-a9) decode ------------------------------------------------------ */
 /* Append one token per request (a8): quantize k_new into its own partitions,
  * put v_new in the FP16 tail, flush the tail into a V block when it reaches Pi
- * (R12), seq_lens[slot] += 1.  k_new, v_new: device fp16 [batch][H_kv][d]. */
+ * (R12), seq_lens[slot] += 1.  k_new, v_new: device fp16 [batch][H_kv][d].
+ * Every append advances the cache's seq_lens, so the layers of a model must each decode on
+ * their own seq_lens array (they may share pages' block_table and rng_ids; the KV
+ * transfer calls, which need one seq_lens for all layers, only run before decode). */
 hack_status_t hack_decode_append(const hack_config_t* cfg, const void* k_new, const void* v_new,
                                  const int32_t* slots, int32_t batch, const hack_kv_cache_t* cache,
                                  void* stream);
