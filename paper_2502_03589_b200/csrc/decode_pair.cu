@@ -1116,8 +1116,14 @@ cudaError_t launch_decode_pair(const KernelCfg& kc, const void* q_new, const int
   }
   kern<<<grid_size(g8), kThreads, smem, st>>>(reinterpret_cast<const __half*>(q_new), slots, batch, cv, kc, meta, part,
                                             with_dbg ? dbg->pcodes : nullptr, with_dbg ? dbg->pcodes_stride : 0);
+#ifdef HACK_DEC_NOCOMBINE
+  note_launch();  // timing experiment only (the merge costs ~9.7 us of 117 on C3): no outputs
+  return cudaGetLastError();
+#endif
   // the merge is launched as a programmatic dependent of the main kernel (PDL): its CTAs can
-  // be resident before the main grid drains and wait in griddepcontrol.wait
+  // be resident before the main grid drains and wait in griddepcontrol.wait.  (Computing the
+  // page geometry from seq_lens before the wait, with an early launch_dependents trigger in
+  // the main grid, measured 2 us slower.)
   cudaLaunchConfig_t lc = {};
   lc.gridDim = dim3(batch, kc.Hq);
   lc.blockDim = dim3(128);
