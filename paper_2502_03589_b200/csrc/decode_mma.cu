@@ -98,8 +98,16 @@ HACK_DEV uint32_t plane(uint32_t w, int sh) {
 
 // Token / channel index held by byte i of plane `tig` of packed word W (16-code words at
 // b=2: index 16W + 4i + tig; at b=4 words hold 8 codes: index 8W + 2i + tig, tig in {0,1}).
+// resident CTAs per SM the shared memory allows (up to kCtas): the register budget of the
+// launch bounds follows it (a 104 KB b = 4 ring fits twice, so 204 registers, no spills)
 template <int BITS, int PI_>
-__global__ void __launch_bounds__(kThreads, kCtas) decode_mma_kernel(const __half* __restrict__ q_new,
+constexpr int dmma_ctas() {
+  constexpr size_t sm = sizeof(DecSmem<BITS, PI_>) + 1024;
+  return sm * kCtas <= 227 * 1024 ? kCtas : (sm * 2 <= 227 * 1024 ? 2 : 1);
+}
+
+template <int BITS, int PI_>
+__global__ void __launch_bounds__(kThreads, dmma_ctas<BITS, PI_>()) decode_mma_kernel(const __half* __restrict__ q_new,
                                                               const int32_t* __restrict__ slots, CacheView cv,
                                                               KernelCfg kc, float* __restrict__ part, int nsplit,
                                                               uint8_t* __restrict__ dbg_pcodes, int64_t dbg_stride) {
@@ -388,12 +396,22 @@ __global__ void __launch_bounds__(kThreads, kCtas) decode_mma_kernel(const __hal
           // the channel's PI codes: PI * BITS / 32 words (2 per 32-token k-step at b = 2, 4 at b = 4)
           constexpr int NWD = PI * BITS / 32;
           uint32_t wa[NWD], wb[NWD];
+          if constexpr (NWD % 4 == 0) {  // 16-byte loads (all but Pi = 32, b = 2)
 #pragma unroll
-          for (int x = 0; x < NWD; x += 2) {
-            const uint2 a2 = *reinterpret_cast<const uint2*>(pg + PL.v_codes + c0 * (PI * BITS / 8) + 4 * x);
-            const uint2 b2 = *reinterpret_cast<const uint2*>(pg + PL.v_codes + c1 * (PI * BITS / 8) + 4 * x);
-            wa[x] = a2.x; wa[x + 1] = a2.y;
-            wb[x] = b2.x; wb[x + 1] = b2.y;
+            for (int x = 0; x < NWD; x += 4) {
+              const uint4 a4 = *reinterpret_cast<const uint4*>(pg + PL.v_codes + c0 * (PI * BITS / 8) + 4 * x);
+              const uint4 b4 = *reinterpret_cast<const uint4*>(pg + PL.v_codes + c1 * (PI * BITS / 8) + 4 * x);
+              wa[x] = a4.x; wa[x + 1] = a4.y; wa[x + 2] = a4.z; wa[x + 3] = a4.w;
+              wb[x] = b4.x; wb[x + 1] = b4.y; wb[x + 2] = b4.z; wb[x + 3] = b4.w;
+            }
+          } else {
+#pragma unroll
+            for (int x = 0; x < NWD; x += 2) {
+              const uint2 a2 = *reinterpret_cast<const uint2*>(pg + PL.v_codes + c0 * (PI * BITS / 8) + 4 * x);
+              const uint2 b2 = *reinterpret_cast<const uint2*>(pg + PL.v_codes + c1 * (PI * BITS / 8) + 4 * x);
+              wa[x] = a2.x; wa[x + 1] = a2.y;
+              wb[x] = b2.x; wb[x + 1] = b2.y;
+            }
           }
           uint32_t dacc[4] = {kMagicI, kMagicI, kMagicI, kMagicI};
           if (BITS == 2) {
