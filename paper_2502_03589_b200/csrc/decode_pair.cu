@@ -688,7 +688,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
 // per-row P meta / rescale factors move between the two row ownerships through a small
 // per-warp table.  Items are single pages.
 #ifndef HACK_DEC8_NSTG
-#define HACK_DEC8_NSTG 8
+#define HACK_DEC8_NSTG 6
 #endif
 #ifndef HACK_DEC8_CTAS
 #define HACK_DEC8_CTAS 4
