@@ -242,8 +242,17 @@ def run_disagg(args, rank, local_rank, world):
                                            device=dev) for l in range(1, layers)]
     rids = [7 * pair + i for i in range(R)]
     nccl = args.dist_backend == "nccl"
+    pull = args.transport == "pull"
     comm = None
-    if nccl:  # one 2-rank NCCL communicator per prefill/decode pair, ids exchanged over the group
+    if pull:  # the decode rank maps the prefill rank's caches through CUDA IPC (peer memory)
+        from torch.multiprocessing.reductions import reduce_tensor
+        mine = ([[reduce_tensor(t) for t in (c.pages, c.v_tail, c.block_table, c.seq_lens, c.rng_ids)]
+                 for c in caches] if prefill else None)
+        shared = [None] * world
+        dist.all_gather_object(shared, mine)
+        if not prefill:
+            remote = [h.KVCache(cfgs[l], *[fn(*a) for fn, a in shared[peer][l]]) for l in range(layers)]
+    elif nccl:  # one 2-rank NCCL communicator per prefill/decode pair, ids exchanged over the group
         uid = h.comm_unique_id() if prefill else None
         ids = [None] * world
         dist.all_gather_object(ids, uid)
@@ -267,7 +276,10 @@ def run_disagg(args, rank, local_rank, world):
             for l in range(layers):
                 q, k, v = qkv[i][l]
                 h.prefill_attention(cfgs[l], q, k, v, cu, sl, L, caches[l], out[:L])
-            if nccl:
+            if pull:  # tell the decode rank that request i is complete (its pull reads our memory)
+                torch.cuda.synchronize()
+                dist.send(torch.tensor([i], dtype=torch.int32, device=dev if nccl else "cpu"), dst=peer)
+            elif nccl:
                 h.kv_send(comm, 1, cfgs[0], caches, i, L, first_token=i, rng_id=rids[i], staging=staging[i])
             else:
                 h.kv_pack(cfgs[0], caches, i, L, first_token=i, rng_id=rids[i], staging=staging[i])
@@ -291,7 +303,12 @@ def run_disagg(args, rank, local_rank, world):
         barrier(world)
         ev[0].record(stream)
         for i, L in enumerate(lens):
-            if nccl:
+            if pull:
+                t = torch.zeros(1, dtype=torch.int32, device=dev if nccl else "cpu")
+                dist.recv(t, src=peer)
+                h.kv_pull(cfgs[0], remote, caches, i, i, L)
+                status[i, 1] = i
+            elif nccl:
                 h.kv_recv(comm, 0, cfgs[0], caches, i, L, staging[i], status=status[i])
             else:
                 buf = torch.empty(staging[i].numel(), dtype=torch.uint8)
@@ -314,6 +331,10 @@ def run_disagg(args, rank, local_rank, world):
         res = {"role": "decode", "recv_ms": recv_ms, "decode_ms": dec_ms,
                "decode_tokens_per_s": B * C5["dec_steps"] / (dec_ms * 1e-3)}
         jct = recv_ms + dec_ms
+    if pull:
+        dist.barrier()  # the prefill ranks keep their caches mapped until every pull finished
+        if not prefill:
+            del remote
     all_res = [None] * world
     dist.all_gather_object(all_res, res)
     jct_max = max_over_ranks(jct, world)
@@ -329,7 +350,8 @@ def run_disagg(args, rank, local_rank, world):
                 "config": {"workload": f"C5: {P} prefill + {P} decode ranks, {R} mixed-length requests per pair "
                                        f"({C5['lmin']}-{C5['lmax']} tokens), {layers} layers x {Hq}/{Hkv} heads, "
                                        f"2-bit, {C5['dec_steps']} decode steps",
-                           "transport": "hack_kv_send/recv (NCCL p2p)" if nccl else "kv_pack + gloo host send/recv",
+                           "transport": ("hack_kv_pull over CUDA IPC peer memory (fused, no staging)" if pull else
+                                         "hack_kv_send/recv (NCCL p2p)" if nccl else "kv_pack + gloo host send/recv"),
                            "lengths_pair0": c5_trace(0)},
                 "jct_ms": jct_max,
                 "prefill_tops_incl_send": sum(r["prefill_tops_incl_send"] for r in pre),
@@ -506,12 +528,16 @@ def run_transfer(args, h, dev, seed):
 
     pack_ms = timed(lambda: h.kv_pack(cfg, src, 0, L, first_token=1, rng_id=0, staging=wire))
     unpack_ms = timed(lambda: h.kv_unpack(cfg, dst, 0, L, wire))
+    pull_ms = timed(lambda: h.kv_pull(cfg, src, dst, 0, 0, L))
     fp16_bytes = layers * L * Hkv * 128 * 2 * 2
     del src, dst, wire
     return {"workload": f"one {L}-token request, {layers} layers x {Hkv} KV heads, 2-bit (C2 shape)",
             "wire_bytes": nbytes, "fp16_kv_bytes": fp16_bytes, "ratio_vs_fp16": nbytes / fp16_bytes,
             "pack_ms": pack_ms, "pack_gbs": 2 * nbytes / (pack_ms * 1e-3) / 1e9,
             "unpack_ms": unpack_ms, "unpack_gbs": 2 * nbytes / (unpack_ms * 1e-3) / 1e9,
+            "pull_ms": pull_ms, "pull_gbs": 2 * (nbytes - 64) / (pull_ms * 1e-3) / 1e9,
+            "pull": "hack_kv_pull: cache -> cache in one kernel, no staging (f1 fused transfer; across GPUs the "
+                    "source is a peer cache opened through CUDA IPC and the loads cross NVLink)",
             "note": "GB/s counts read + write; repeated packs of an 88 MB request can hit the 126 MB L2; "
                     "the NVLink send/recv needs two GPUs and is not timed here"}
 
@@ -932,6 +958,8 @@ def main():
                     help="decode: launch eagerly instead of replaying a CUDA graph of the K timed steps")
     ap.add_argument("--mode", default="flagship", choices=["flagship", "disagg"],
                     help="disagg: the C5 disaggregated prefill -> decode trace (needs an even N >= 2)")
+    ap.add_argument("--transport", default="nccl", choices=["nccl", "pull"],
+                    help="disagg: packed KV over the library's NCCL send/recv, or hack_kv_pull on CUDA IPC peer memory")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                     help="process-group backend for barriers / max-over-ranks (gloo: several ranks on one GPU, tests)")
     args = ap.parse_args()

@@ -268,6 +268,19 @@ hack_status_t hack_kv_send_layer(void* comm, int32_t peer, const hack_config_t* 
                                  void* stream);
 hack_status_t hack_kv_recv_layer(void* comm, int32_t peer, const hack_config_t* cfg, int32_t num_layers,
                                  int32_t layer, int32_t prompt_len, void* staging, void* stream);
+/* hack_kv_pull (fused transfer): copy one request of num_layers layers from
+ * `src` caches straight into `dst` caches in ONE kernel, with no staging buffer, header or
+ * NCCL: pages through both block tables (codes + fp16 meta + cached sums), the FP16 tail
+ * rows, then dst seq_lens[dst_slot] = prompt_len and dst rng_ids[dst_slot] = src
+ * rng_ids[src_slot].  src may be any device-accessible memory, e.g. a prefill rank's
+ * cache on a peer GPU opened through CUDA IPC (the loads then cross NVLink) or a cache of
+ * another process on the same GPU.  The caller guarantees src is complete (its prefill
+ * finished) and stays valid until the pull's stream work completes; dst block tables
+ * must already hold pages for the prompt.  Both sides: <= 128 layers sharing
+ * block_table/seq_lens/rng_ids.  Errors: INVALID_ARG / SHAPE / CAPACITY as hack_kv_pack. */
+hack_status_t hack_kv_pull(const hack_config_t* cfg, const hack_kv_cache_t* src, const hack_kv_cache_t* dst,
+                           int32_t num_layers, int32_t src_slot, int32_t dst_slot, int32_t prompt_len,
+                           void* stream);
 hack_status_t hack_comm_recv_bytes(void* comm, int32_t peer, void* buf, int64_t bytes, void* stream);
 hack_status_t hack_comm_group_start(void);
 hack_status_t hack_comm_group_end(void);

@@ -58,9 +58,21 @@ int64_t layer_bytes(const KernelCfg& kc, int prompt_len) {
   return (int64_t)npages * kc.Hkv * kc.pl.page_bytes + (int64_t)kc.Hkv * T * 128 * 2;
 }
 
+// 16-byte copy by the whole CTA; four loads in flight per thread before their stores (the
+// pointers may alias as far as the compiler knows, so a plain loop serialises load/store)
 HACK_DEV void copy16(uint8_t* dst, const uint8_t* src, int64_t bytes) {
-  for (int64_t i = threadIdx.x; i < bytes / 16; i += blockDim.x)
-    reinterpret_cast<uint4*>(dst)[i] = reinterpret_cast<const uint4*>(src)[i];
+  const uint4* s = reinterpret_cast<const uint4*>(src);
+  uint4* d = reinterpret_cast<uint4*>(dst);
+  const int64_t n = bytes / 16, bd = blockDim.x;
+  int64_t i = threadIdx.x;
+  for (; i + 3 * bd < n; i += 4 * bd) {
+    const uint4 a = s[i], b = s[i + bd], c = s[i + 2 * bd], e = s[i + 3 * bd];
+    d[i] = a;
+    d[i + bd] = b;
+    d[i + 2 * bd] = c;
+    d[i + 3 * bd] = e;
+  }
+  for (; i < n; i += bd) d[i] = s[i];
 }
 
 // grid (npages + 1, layers): block j < npages copies page j (all KV heads), block npages
@@ -163,6 +175,32 @@ hack_status_t prepare(const hack_config_t* cfg, const hack_kv_cache_t* caches, i
   hdr->payload_bytes = (uint64_t)g->layer_bytes * num_layers;
   hdr->seed = kc->seed;
   return HACK_OK;
+}
+
+// Fused transfer (f1): grid (npages + 1, layers); block j < npages copies page j of every KV
+// head from the source cache (any device-accessible memory: a peer GPU's cache mapped with
+// CUDA IPC / peer access, so the loads cross NVLink) straight into the destination page,
+// both resolved through their own block tables; block npages copies the FP16 tail rows.
+// No staging buffer and no header: both sides' geometry comes from (cfg, prompt_len).
+__global__ void pull_kernel(LayerPtrs src, LayerPtrs dst, const int32_t* __restrict__ src_bt, int src_mpr,
+                            int src_slot, const uint32_t* __restrict__ src_rng, const int32_t* __restrict__ dst_bt,
+                            int dst_mpr, int dst_slot, int32_t* __restrict__ dst_seq, uint32_t* __restrict__ dst_rng,
+                            XferGeom g, int prompt_len) {
+  const int j = blockIdx.x, l = blockIdx.y;
+  if (j == 0 && l == 0 && threadIdx.x == 0) {
+    dst_seq[dst_slot] = prompt_len;
+    dst_rng[dst_slot] = src_rng[src_slot];
+  }
+  const int64_t pbytes = (int64_t)g.Hkv * g.page_bytes;
+  if (j < g.npages) {
+    const int sp = src_bt[(int64_t)src_slot * src_mpr + j], dp = dst_bt[(int64_t)dst_slot * dst_mpr + j];
+    copy16(dst.pages[l] + dp * pbytes, src.pages[l] + sp * pbytes, pbytes);
+  } else if (g.tail_len) {
+    const int64_t rowb = (int64_t)g.tail_len * 128 * 2;
+    for (int h = 0; h < g.Hkv; ++h)
+      copy16(reinterpret_cast<uint8_t*>(dst.tail[l] + ((int64_t)dst_slot * g.Hkv + h) * g.Pi * 128),
+             reinterpret_cast<const uint8_t*>(src.tail[l] + ((int64_t)src_slot * g.Hkv + h) * g.Pi * 128), rowb);
+  }
 }
 
 hack_status_t nccl_status(ncclResult_t r, const char* where) {
@@ -317,6 +355,25 @@ hack_status_t hack_kv_recv_layer(void* comm, int32_t peer, const hack_config_t* 
   return nccl_status(ncclRecv((uint8_t*)staging + b, (size_t)n, ncclUint8, peer, (ncclComm_t)comm,
                               (cudaStream_t)stream),
                      "ncclRecv (layer)");
+}
+
+hack_status_t hack_kv_pull(const hack_config_t* cfg, const hack_kv_cache_t* src, const hack_kv_cache_t* dst,
+                           int32_t num_layers, int32_t src_slot, int32_t dst_slot, int32_t prompt_len, void* stream) {
+  KernelCfg kc;
+  LayerPtrs sp, dp;
+  XferGeom g;
+  WireHeader hdr;
+  hack_status_t st = prepare(cfg, src, num_layers, src_slot, prompt_len, &kc, &sp, &g, &hdr);
+  if (st != HACK_OK) return st;
+  XferGeom g2;
+  if ((st = prepare(cfg, dst, num_layers, dst_slot, prompt_len, &kc, &dp, &g2, &hdr)) != HACK_OK) return st;
+  if ((st = check_device()) != HACK_OK) return st;
+  pull_kernel<<<dim3(g.npages + 1, num_layers), 256, 0, (cudaStream_t)stream>>>(
+      sp, dp, src[0].block_table, src[0].max_pages_per_req, src_slot, reinterpret_cast<const uint32_t*>(src[0].rng_ids),
+      dst[0].block_table, dst[0].max_pages_per_req, dst_slot, dst[0].seq_lens,
+      reinterpret_cast<uint32_t*>(dst[0].rng_ids), g, prompt_len);
+  note_launch();
+  return cuda_status(cudaGetLastError(), "kv_pull");
 }
 
 hack_status_t hack_comm_recv_bytes(void* comm, int32_t peer, void* buf, int64_t bytes, void* stream) {

@@ -69,7 +69,7 @@ for _name in ("hack_config_validate", "hack_page_layout", "hack_quantize_pack", 
               "hack_prefill_attention", "hack_prefill_attention_cached", "hack_decode_append",
               "hack_decode_attention", "hack_decode_attention_cached", "hack_homomorphic_matmul",
               "hack_comm_unique_id", "hack_comm_init", "hack_comm_destroy", "hack_kv_pack", "hack_kv_unpack",
-              "hack_kv_send", "hack_kv_recv", "hack_kv_send_layer", "hack_kv_recv_layer",
+              "hack_kv_send", "hack_kv_recv", "hack_kv_send_layer", "hack_kv_recv_layer", "hack_kv_pull",
               "hack_comm_recv_bytes", "hack_comm_group_start",
               "hack_comm_group_end"):
     getattr(_lib, _name).restype = _S
@@ -109,6 +109,8 @@ _lib.hack_kv_send.argtypes = [_P, C.c_int32, C.POINTER(Config), C.POINTER(CacheS
 _lib.hack_kv_recv.argtypes = [_P, C.c_int32, C.POINTER(Config), C.POINTER(CacheStruct), C.c_int32, C.c_int32,
                               C.c_int32, _P, _P, _P]
 _lib.hack_comm_recv_bytes.argtypes = [_P, C.c_int32, _P, C.c_int64, _P]
+_lib.hack_kv_pull.argtypes = [C.POINTER(Config), C.POINTER(CacheStruct), C.POINTER(CacheStruct), C.c_int32,
+                              C.c_int32, C.c_int32, C.c_int32, _P]
 _lib.hack_kv_layer_range.restype = C.c_int64
 _lib.hack_kv_layer_range.argtypes = [C.POINTER(Config), C.c_int32, C.c_int32, C.c_int32, C.POINTER(C.c_int64)]
 _lib.hack_kv_send_layer.argtypes = [_P, C.c_int32, C.POINTER(Config), C.POINTER(CacheStruct), C.c_int32, C.c_int32,
@@ -393,6 +395,14 @@ def kv_layer_range(cfg: Config, num_layers: int, layer: int, prompt_len: int) ->
     if n < 0:
         raise HackError(ERR_INVALID_ARG, "kv_layer_range: bad arguments")
     return int(b.value), n
+
+
+def kv_pull(cfg, src_caches, dst_caches, src_slot, dst_slot, prompt_len, stream=None):
+    """Fused transfer: src (e.g. a peer GPU's cache opened through CUDA IPC) -> dst, one kernel."""
+    if len(src_caches) != len(dst_caches):
+        raise ValueError("kv_pull: src and dst need the same number of layers")
+    _check(_lib.hack_kv_pull(C.byref(cfg), _caches_array(src_caches), _caches_array(dst_caches), len(src_caches),
+                             src_slot, dst_slot, prompt_len, _stream(stream)), "kv_pull")
 
 
 def kv_send_layer(comm, peer, cfg, caches, layer, slot, prompt_len, first_token, rng_id, staging, stream=None):

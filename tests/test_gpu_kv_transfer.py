@@ -165,3 +165,50 @@ def test_layer_pipelined_nccl_self_loop():
         check_same(src, dst, slot, 0)
     finally:
         h.comm_destroy(comm)
+
+
+def test_kv_pull_fused_transfer():
+    """hack_kv_pull copies a request cache-to-cache in one kernel, no
+    staging; the result equals the pack -> unpack route byte for byte and decodes the same."""
+    h, cfgs, src = setup(9)
+    _, _, dst = setup(10)
+    _, _, dst2 = setup(11)
+    prefill_all(h, cfgs, src, slot=0, rng_id=777)
+    h.kv_pull(cfgs[0], src, dst, 0, 2, L)
+    nbytes = h.kv_transfer_bytes(cfgs[0], LAYERS, L)
+    staging = torch.zeros(nbytes, dtype=torch.uint8, device="cuda")
+    h.kv_pack(cfgs[0], src, 0, L, first_token=1, rng_id=777, staging=staging)
+    h.kv_unpack(cfgs[0], dst2, 2, L, staging)
+    torch.cuda.synchronize()
+    check_same(src, dst, 0, 2)
+    check_same(dst2, dst, 2, 2)
+    for a, b in zip(decode_once(h, cfgs, src, 0), decode_once(h, cfgs, dst, 2)):
+        assert np.array_equal(a, b)
+
+
+def test_kv_pull_cuda_ipc():
+    """The pull reads another process's cache through CUDA IPC (the same mechanism maps a
+    peer GPU's memory over NVLink); the pulled request equals the source bytes."""
+    import torch.multiprocessing as mp
+    h, cfgs, src = setup(12)
+    prefill_all(h, cfgs, src, slot=1, rng_id=4321)
+    torch.cuda.synchronize()
+    ctx = mp.get_context("spawn")
+    q_in, q_out = ctx.Queue(), ctx.Queue()
+    from . import ipc_child
+    p = ctx.Process(target=ipc_child.pull_child, args=(q_in, q_out))
+    p.start()
+    try:
+        q_in.put({"cfg": dict(num_q_heads=8, num_kv_heads=2, out_fp32=True),
+                  "tensors": [(c.pages, c.v_tail, c.block_table, c.seq_lens, c.rng_ids) for c in src],
+                  "L": L, "src_slot": 1, "dst_slot": 3})
+        out = q_out.get(timeout=300)
+        q_in.put("done")
+    finally:
+        p.join(timeout=120)
+    assert p.exitcode == 0
+    assert out["seq_len"] == L and out["rng_id"] == 4321
+    for l, c in enumerate(src):
+        pa, ta = request_bytes(c, 1, L)
+        assert np.array_equal(pa, out["pages"][l])
+        assert np.array_equal(ta.view(np.uint16), out["tails"][l].view(np.uint16))
