@@ -284,10 +284,19 @@ HACK_DEV void locate_range(SMT& sm, const CacheView& cv, const int32_t* __restri
 // phase of fill k - 2N.  The producer tags each slot with the page index before issuing its
 // fill, and fill k is only issued after fill k - N was consumed, so once the tag reads k
 // the parity wait is exact.
+// The slot tag is a flag, not data: relaxed (memory-model "strong") shared accesses, so
+// they are neither reordered away nor counted as data races.
+HACK_DEV int tag_load(const int* p) {
+  int v;
+  asm volatile("ld.relaxed.cta.shared.b32 %0, [%1];" : "=r"(v) : "r"(ptx::smem_u32(p)) : "memory");
+  return v;
+}
+HACK_DEV void tag_store(int* p, int v) { atomicExch(p, v); }  // producer side, once per page
+
 template <int N, class SMT>
 HACK_DEV void wait_fill(SMT& sm, int k) {
   const int s = k % N;
-  while (*reinterpret_cast<volatile int*>(&sm.tag[s]) != k) {
+  while (tag_load(&sm.tag[s]) != k) {
   }
   ptx::mbar_wait(&sm.full[s], (k / N) & 1);
 }
@@ -325,7 +334,7 @@ HACK_DEV void produce_pages(SMT& sm, SegWalker walk, const CacheView& cv, const 
           while (!ptx::mbar_try_wait_sleep(&sm.empty[st], ((k / N) & 1) ^ 1)) {
           }
 #endif
-          *reinterpret_cast<volatile int*>(&sm.tag[st]) = k;  // fill k of slot st is being issued
+          tag_store(&sm.tag[st], k);  // fill k of slot st is being issued
 #if HACK_DEC_SPLIT
           // two copies: the K half (codes + meta + sums) lands first and QK can start
           const uint32_t kb = (uint32_t)kc.pl.v_codes;

@@ -5,7 +5,7 @@
 OUT=gpurun_out
 mkdir -p $OUT
 SAN=/usr/local/cuda/bin/compute-sanitizer
-TESTS="tests/test_gpu_rqe_ablation.py::test_no_rqe_requantizes_partial_block[2] tests/test_gpu_decode.py::test_decode_paired_kernel_edges tests/test_gpu_decode.py::test_decode_group8_paired_kernel[8] tests/test_gpu_kv_transfer.py::test_pack_unpack_round_trip_and_decode_equivalence"
+TESTS="tests/test_gpu_rqe_ablation.py::test_no_rqe_requantizes_partial_block[2] tests/test_gpu_decode.py::test_decode_paired_kernel_edges tests/test_gpu_decode.py::test_decode_group8_paired_kernel[8] tests/test_gpu_kv_transfer.py::test_pack_unpack_round_trip_and_decode_equivalence tests/test_gpu_decode.py::test_decode_partition_and_bits tests/test_gpu_kv_transfer.py::test_kv_pull_fused_transfer tests/test_gpu_kv_transfer.py::test_layer_pipelined_nccl_self_loop"
 for tool in ${TOOLS:-memcheck racecheck synccheck}; do
   {
     timeout 600 $SAN --tool $tool --error-exitcode 9 python -c "import __graft_entry__ as g; g.smoke()"
