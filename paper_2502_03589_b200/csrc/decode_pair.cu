@@ -384,6 +384,11 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
     }
     ptx::fence_mbar_init();
   }
+#ifndef HACK_DEC_NOPDL
+  // launched as a programmatic dependent of the append kernel: everything above touched
+  // only shared memory; seq_lens, pages and the FP16 tail are read after this wait
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+#endif
   locate_range(sm, cv, slots, batch, Hkv, ws_meta, warp, lane);
   __syncthreads();
   const int R = sm.R, P = sm.P;
@@ -741,6 +746,11 @@ __global__ void __launch_bounds__(kThreads, kCtas8)
     }
     ptx::fence_mbar_init();
   }
+#ifndef HACK_DEC_NOPDL
+  // launched as a programmatic dependent of the append kernel: everything above touched
+  // only shared memory; seq_lens, pages and the FP16 tail are read after this wait
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+#endif
   locate_range(sm, cv, slots, batch, Hkv, ws_meta, warp, lane);
   __syncthreads();
   const int R = sm.R, P = sm.P;
@@ -1123,8 +1133,29 @@ cudaError_t launch_decode_pair(const KernelCfg& kc, const void* q_new, const int
     if (e != cudaSuccess) return e;
     attr_set[ki] = true;
   }
-  kern<<<grid_size(g8), kThreads, smem, st>>>(reinterpret_cast<const __half*>(q_new), slots, batch, cv, kc, meta, part,
-                                            with_dbg ? dbg->pcodes : nullptr, with_dbg ? dbg->pcodes_stride : 0);
+  {
+    // programmatic dependent launch: the grid launches (and its prologue runs) while the
+    // preceding kernel on the stream (the append) drains; griddepcontrol.wait in the
+    // kernel orders its global reads after that kernel's writes
+    cudaLaunchConfig_t mc = {};
+    mc.gridDim = dim3(grid_size(g8));
+    mc.blockDim = dim3(kThreads);
+    mc.dynamicSmemBytes = smem;
+    mc.stream = st;
+    cudaLaunchAttribute ma[1];
+    ma[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    ma[0].val.programmaticStreamSerializationAllowed = 1;
+    mc.attrs = ma;
+#ifdef HACK_DEC_NOPDL
+    mc.numAttrs = 0;
+#else
+    mc.numAttrs = 1;
+#endif
+    const cudaError_t e1 = cudaLaunchKernelEx(&mc, kern, reinterpret_cast<const __half*>(q_new), slots, batch, cv, kc,
+                                              meta, part, with_dbg ? dbg->pcodes : (uint8_t*)nullptr,
+                                              with_dbg ? dbg->pcodes_stride : (int64_t)0);
+    if (e1 != cudaSuccess) return e1;
+  }
 #ifdef HACK_DEC_NOCOMBINE
   note_launch();  // timing experiment only (the merge costs ~9.7 us of 117 on C3): no outputs
   return cudaGetLastError();
