@@ -545,19 +545,19 @@ def run_transfer(args, h, dev, seed):
 def run_sweep(args, h, dev, seed, flush):
     """SURVEY f (Pi/bit sweep): partition size Pi in {32, 64, 128} x K/V bits in
     {2, 4} on a reduced C2/C3 shape (32 Q / 8 KV heads): one 2048-token causal prefill (ingest +
-    attention, L2 flushed) and a batch-16 decode step at 4096 context (append + attention,
+    attention, L2 flushed) and a C3-sized decode step (batch 64 at 8K context, append + attention,
     CUDA graph).  Decode runs on the mma.sync tensor-core kernels at every Pi; prefill runs the
     tcgen05 kernel at Pi = 64 and the CUDA-core kernel at Pi = 32 and 128."""
     import torch
-    Hq, Hkv, L, B, ctx = 32, 8, 2048, 16, 4096
+    Hq, Hkv, L, B, ctx = 32, 8, 2048, C3["B"], C3["ctx"]
     stream = torch.cuda.current_stream()
     q = dev_normal((L, Hq, 128), seed + 51, dev)
     k = dev_normal((L, Hkv, 128), seed + 52, dev)
     v = dev_normal((L, Hkv, 128), seed + 53, dev)
-    kc_ = dev_normal((ctx, Hkv, 128), seed + 54, dev)
-    vc_ = dev_normal((ctx, Hkv, 128), seed + 55, dev)
+    kc_ = dev_normal((8 * ctx, Hkv, 128), seed + 54, dev)   # 8 requests per ingest call
+    vc_ = dev_normal((8 * ctx, Hkv, 128), seed + 55, dev)
     cu = torch.tensor([0, L], dtype=torch.int32, device=dev)
-    cuc = torch.tensor([0, ctx], dtype=torch.int32, device=dev)
+    cuc = torch.arange(0, 9, dtype=torch.int32, device=dev) * ctx
     out = torch.empty((L, Hq, 128), dtype=torch.float16, device=dev)
     ops = prefill_ops(L, Hq)
     n_dec = 5
@@ -582,8 +582,8 @@ def run_sweep(args, h, dev, seed, flush):
                 if i:
                     ms.append(a.elapsed_time(b))
             pre_ms = sum(ms) / len(ms)
-            for r in range(B):
-                h.cache_ingest(cfg, kc_, vc_, cuc, torch.tensor([r], dtype=torch.int32, device=dev), ctx, cache)
+            for r0 in range(0, B, 8):
+                h.cache_ingest(cfg, kc_, vc_, cuc, torch.arange(r0, r0 + 8, dtype=torch.int32, device=dev), ctx, cache)
             slots = torch.arange(B, dtype=torch.int32, device=dev)
             qn = dev_normal((n_dec, B, Hq, 128), seed + 56, dev)
             kn = dev_normal((n_dec, B, Hkv, 128), seed + 57, dev)
