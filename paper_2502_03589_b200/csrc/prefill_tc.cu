@@ -42,13 +42,16 @@ namespace {
 constexpr int PI = 64;
 constexpr int BM = 128;
 constexpr int BN = 64;
+#ifndef HACK_PRE_ORANK
+#define HACK_PRE_ORANK 0  // O-side Eq. 4 rank terms on the tensor pipe (experiment: correct, 17 % slower)
+#endif
 #ifndef HACK_PRE_NS
-#define HACK_PRE_NS 4
+#define HACK_PRE_NS (HACK_PRE_ORANK ? 2 : 4)
 #endif
 constexpr int NS = HACK_PRE_NS;  // page stages
 constexpr int NB = 3;          // K/V/P tile buffer sets
 #ifndef HACK_PRE_NDB
-#define HACK_PRE_NDB 2
+#define HACK_PRE_NDB (HACK_PRE_ORANK ? 1 : 2)
 #endif
 constexpr int NDB = HACK_PRE_NDB;  // D' (PV accumulator) TMEM buffers
 constexpr int kThreads = 640;  // 4 service warps + 2 S warpgroups + 2 O warpgroups
@@ -78,6 +81,11 @@ struct TcSmem {
   float2 xch[2][2][BM];                   // partial (max, min | -inf if masked)
   float ptail[BM][BN + 1];                // p~ of the FP16 tail tile
   float lpart[2][BM];
+#if HACK_PRE_ORANK
+  alignas(128) float ora[BM * 16];        // O-rank A operand (tf32, K-major, SBO 512): x_p, mu_p split 3 ways
+  alignas(128) float orb[128 * 16];       // O-rank B operand per channel: m_v, y_v split 3 ways
+  uint64_t a_ready, or_done;
+#endif
   uint64_t full[NS], empty[NS], k_ready[NB], k_free[NB], v_ready[NB], o_done[NB], p_ready[NB],
       d_full[2], d_free[2], s_full, s_free, q_ready, l_ready;
   uint32_t tmem_base;
@@ -171,6 +179,10 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_tc_kernel(
     }
     ptx::mbar_init(&sm.s_full, 1);
     ptx::mbar_init(&sm.s_free, NSW);
+#if HACK_PRE_ORANK
+    ptx::mbar_init(&sm.a_ready, NOW);
+    ptx::mbar_init(&sm.or_done, 1);
+#endif
     ptx::mbar_init(&sm.q_ready, NSW);
     ptx::mbar_init(&sm.l_ready, NSW);
     ptx::fence_mbar_init();
@@ -183,6 +195,10 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_tc_kernel(
   const uint32_t tS = tmem;         // columns 0..127: D_0 | D_1
   const uint32_t tD0 = tmem + 128;  // D'[0] columns 128..255, D'[1] 256..383
   const uint32_t tR = tmem + 384;   // rank terms of S (64 columns): sum_beta X m_k + M y_k (3xTF32 MMA)
+#if HACK_PRE_ORANK
+  static_assert(NDB == 1, "the O-rank accumulator takes the second D' buffer's columns");
+  const uint32_t tOR = tmem + 256;  // O-side rank terms, all tiles: sum_j x_p m_v + mu_p y_v (3xTF32 MMA)
+#endif
 
   if (warp < 4) {
     // register budget (launch: 96 x 640): service 40, S 88, O 128 -> 9216 freed >= 8192 taken
@@ -254,6 +270,22 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_tc_kernel(
             ptx::mma_commit(&sm.d_full[bd]);
           }
           __syncwarp();
+#if HACK_PRE_ORANK
+          // O-side rank-2 terms of tile jj into the persistent fp32 accumulator (the O warps
+          // wrote A after reading tile jj's P meta and rescaled the accumulator if needed)
+          rwait<1>(&sm.a_ready, jj & 1);
+          ptx::tc_fence_after();
+          if (lane == 0) {
+            const uint32_t oa = ptx::smem_u32(sm.ora), ob = ptx::smem_u32(sm.orb);
+#pragma unroll
+            for (int ks = 0; ks < 2; ++ks)
+              ptx::mma_tf32(tOR, ptx::smem_desc_kmajor(oa + ks * 256, 128, 512),
+                            ptx::smem_desc_kmajor(ob + ks * 256, 128, 512), ptx::idesc_tf32(BM, 128),
+                            (jj > 0 || ks > 0) ? 1u : 0u);
+            ptx::mma_commit(&sm.or_done);
+          }
+          __syncwarp();
+#endif
         }
       }
     } else {
@@ -321,6 +353,9 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_tc_kernel(
         ptx::mbar_arrive(&sm.k_ready[bj]);
         rwait<2>(&sm.o_done[bj], ph ^ 1);  // O warps done with tile j - NB
         if (j < nfull) {
+#if HACK_PRE_ORANK
+          if (j > 0) rwait<2>(&sm.or_done, (j - 1) & 1);  // the single B operand buffer is free
+#endif
 #pragma unroll
           for (int c2 = 0; c2 < 2; ++c2) {
             const int ch = ut + 64 * c2;
@@ -344,6 +379,19 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_tc_kernel(
             sm.vcf[bj][0][ch] = s2;
             sm.vcf[bj][1][ch] = m;
             sm.vcf[bj][2][ch] = fmaf(s2, (float)sum, PI * m);  // y_v = s_v SV + Pi m_v
+#if HACK_PRE_ORANK
+            {
+              float bv[16];
+              rank_b(m, bv);
+              rank_b(fmaf(s2, (float)sum, PI * m), bv + 6);
+              bv[12] = bv[13] = bv[14] = bv[15] = 0.f;
+              uint8_t* obr = reinterpret_cast<uint8_t*>(sm.orb);
+#pragma unroll
+              for (int x = 0; x < 16; x += 4)
+                *reinterpret_cast<float4*>(obr + kmaj_off(ch, 4 * x, 512)) =
+                    make_float4(bv[x], bv[x + 1], bv[x + 2], bv[x + 3]);
+            }
+#endif
           }
         }
         ptx::fence_proxy_async_smem();
@@ -617,7 +665,43 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_tc_kernel(
         const float2 al2 = make_float2(pi4.x, pi4.x);
 #pragma unroll
         for (int x = 0; x < 32; ++x) o2[x] = ptx::fmul2(o2[x], al2);
+#if HACK_PRE_ORANK
+        if (j > 0 && j - 1 < nfull) {  // the O-rank accumulator (tiles < j) rescales too
+          rwait<4>(&sm.or_done, (j - 1) & 1);
+          ptx::tc_fence_after();
+#pragma unroll
+          for (int h = 0; h < 4; ++h) {
+            uint32_t d[16];
+            ptx::tmem_ld16(tOR + lane_base + cb + 16 * h, d);
+            ptx::tmem_wait_ld();
+#pragma unroll
+            for (int x = 0; x < 16; ++x) d[x] = __float_as_uint(__uint_as_float(d[x]) * pi4.x);
+            ptx::tmem_st16(tOR + lane_base + cb + 16 * h, d);
+          }
+          ptx::tmem_wait_st();
+        }
+#endif
       }
+#if HACK_PRE_ORANK
+      if (j < nfull) {
+        if (ow == 0) {  // A operand row r of tile j: x_p and mu_p (Eq. 4 P side), split 3 ways
+          if (j > 0) rwait<4>(&sm.or_done, (j - 1) & 1);  // A of tile j - 1 consumed
+          const int sps0 = sm.sp_part[bj][0][r] + sm.sp_part[bj][1][r] - 128 * PI;
+          float av[16];
+          rank_a(pi4.z * (float)sps0, av);
+          rank_a(pi4.w + 128.f * pi4.z, av + 6);
+          av[12] = av[13] = av[14] = av[15] = 0.f;
+          uint8_t* oar = reinterpret_cast<uint8_t*>(sm.ora);
+#pragma unroll
+          for (int x = 0; x < 16; x += 4)
+            *reinterpret_cast<float4*>(oar + kmaj_off(r, 4 * x, 512)) =
+                make_float4(av[x], av[x + 1], av[x + 2], av[x + 3]);
+          ptx::fence_proxy_async_smem();
+        }
+        ptx::tc_fence_before();
+        ptx::mbar_arrive(&sm.a_ready);
+      }
+#endif
       if (j < nfull) {
         // (a7) O += (s_p/2) s_v E + s_p SP_s m_v + mu_p y_v on D' of this tile
         const int sps = sm.sp_part[bj][0][r] + sm.sp_part[bj][1][r] - 128 * PI;  // sum (p' - 128)
@@ -639,20 +723,26 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_tc_kernel(
           for (int x4 = 0; x4 < 4; ++x4) {
             const int c0 = cb + 16 * h + 4 * x4;
             const float4 sv4 = *reinterpret_cast<const float4*>(&sm.vcf[bj][0][c0]);
+#if !HACK_PRE_ORANK
             const float4 mv4 = *reinterpret_cast<const float4*>(&sm.vcf[bj][1][c0]);
             const float4 y4 = *reinterpret_cast<const float4*>(&sm.vcf[bj][2][c0]);
+#endif
 #pragma unroll
             for (int pr = 0; pr < 2; ++pr) {
               const int xo = 4 * x4 + 2 * pr;
               const int oi = 8 * h + 2 * x4 + pr;
               const float2 E = acc2f(d[xo], d[xo + 1]);
               const float2 svp = pr ? make_float2(sv4.z, sv4.w) : make_float2(sv4.x, sv4.y);
+              const float2 t = ptx::fmul2(svp, E);  // s_v 2D_s
+#if HACK_PRE_ORANK
+              o2[oi] = ptx::ffma2(ap2, t, o2[oi]);  // rank terms: TMEM accumulator (tensor pipe)
+#else
               const float2 mvp = pr ? make_float2(mv4.z, mv4.w) : make_float2(mv4.x, mv4.y);
               const float2 yp = pr ? make_float2(y4.z, y4.w) : make_float2(y4.x, y4.y);
-              const float2 t = ptx::fmul2(svp, E);  // s_v 2D_s
               float2 a = ptx::ffma2(ap2, t, o2[oi]);
               a = ptx::ffma2(xp2, mvp, a);
               o2[oi] = ptx::ffma2(mp2, yp, a);
+#endif
             }
           }
 #endif
@@ -680,6 +770,22 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_tc_kernel(
       }
       ptx::mbar_arrive(&sm.o_done[bj]);
     }
+#if HACK_PRE_ORANK
+    const int nor = min(nkt, nfull);  // O-rank tiles of this CTA (its key tiles that are committed)
+    if (nor > 0) {  // add the O-side rank terms accumulated on the tensor pipe
+      rwait<4>(&sm.or_done, (nor - 1) & 1);
+      ptx::tc_fence_after();
+#pragma unroll
+      for (int h = 0; h < 4; ++h) {
+        uint32_t d[16];
+        ptx::tmem_ld16(tOR + lane_base + cb + 16 * h, d);
+        ptx::tmem_wait_ld();
+#pragma unroll
+        for (int x = 0; x < 8; ++x)
+          o2[8 * h + x] = ptx::fadd2(o2[8 * h + x], make_float2(__uint_as_float(d[2 * x]), __uint_as_float(d[2 * x + 1])));
+      }
+    }
+#endif
     rwait<4>(&sm.l_ready, 0);
     if (i0 + r < L) {
       const float inv_l = 1.f / (sm.lpart[0][r] + sm.lpart[1][r]);
