@@ -699,6 +699,9 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_tc_kernel(
           ptx::fence_proxy_async_smem();
         }
         ptx::tc_fence_before();
+        // FIXME(experiment): one 256-count barrier for both O warpgroups lets warpgroup 1
+        // arrive for tile j + 1 before warpgroup 0 arrived for tile j (not observed in the
+        // tests); use one barrier per warpgroup before enabling this path
         ptx::mbar_arrive(&sm.a_ready);
       }
 #endif
