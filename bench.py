@@ -149,20 +149,21 @@ def barrier(world):
 
 # ----------------------------------------------------------------------------- CPU oracle (baseline)
 
-def oracle_sample(seconds_hint=False, L=4096, heads=1):
-    """Time the oracle (as it stands) on a bounded sample of the C2 workload: one KV
-    head group's first `heads` query heads over the full 4096-token prompt.  Returns
-    (TOPS, seconds, ops, description)."""
+def oracle_sample(seconds_hint=False, L=4096, heads=1, groups=1):
+    """Time the oracle (as it stands) on a bounded sample of the C2 workload: `groups` KV
+    head groups (4 query heads each), of which the first `heads` query heads, over the
+    full 4096-token prompt.  Returns (TOPS, seconds, ops, description)."""
     import hack_inputs
     from oracle import attention as att
-    q, k, v = hack_inputs.qkv(hack_inputs.DATA_SEED, L, 4, 1)
-    cfg = att.Config(Hq=4, Hkv=1, Pi=C2["Pi"], bits=C2["bits"])
+    G = C2["Hq"] // C2["Hkv"]
+    q, k, v = hack_inputs.qkv(hack_inputs.DATA_SEED, L, G * groups, groups)
+    cfg = att.Config(Hq=G * groups, Hkv=groups, Pi=C2["Pi"], bits=C2["bits"])
     t0 = time.perf_counter()
     att.prefill(cfg, q, k, v, heads=list(range(heads)))
     dt = time.perf_counter() - t0
     ops = prefill_ops(L, heads)
-    desc = (f"oracle prefill of {heads} of 32 query heads (1 KV head group) of the C2 4096-token prompt, "
-            f"incl. K/V quantization of that KV head")
+    desc = (f"oracle prefill of {heads} of 32 query heads ({groups} KV head group(s)) of the C2 4096-token "
+            f"prompt, incl. K/V quantization of those KV heads")
     return ops / dt / 1e12, dt, ops, desc
 
 
@@ -458,7 +459,7 @@ def run_hack(args, rank, local_rank, world):
     # ---------------- CPU oracle baseline (rank 0, N = 1)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        v_c, dt, ops_s, desc = oracle_sample(heads=2)
+        v_c, dt, ops_s, desc = oracle_sample(heads=8, groups=2)  # ~10-15 s of host CPU
         cpu = {"value": v_c, "unit": "TOPS", "cores": cpu_threads(), "kind": "oracle",
                "sample": f"{desc}; {dt:.1f} s wall"}
 
