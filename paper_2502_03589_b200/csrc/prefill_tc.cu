@@ -45,6 +45,9 @@ constexpr int BN = 64;
 #ifndef HACK_PRE_ORANK
 #define HACK_PRE_ORANK 0  // O-side Eq. 4 rank terms on the tensor pipe (experiment: correct, 17 % slower)
 #endif
+#ifndef HACK_PRE_GP
+#define HACK_PRE_GP 2  // query heads of one KV head packed into a CTA's 128 rows (1: one head x 128 positions)
+#endif
 #ifndef HACK_PRE_NS
 #define HACK_PRE_NS (HACK_PRE_ORANK ? 2 : 4)
 #endif
@@ -135,6 +138,11 @@ HACK_DEV void rank_b(float y, float* v) {
   v[0] = h; v[1] = m; v[2] = h; v[3] = l; v[4] = h; v[5] = m;
 }
 
+// Query heads packed per CTA (they share the KV head): HACK_PRE_GP if it divides the GQA group.
+__host__ __device__ __forceinline__ int pack_heads(const KernelCfg& kc) {
+  return (HACK_PRE_GP >= 4 && kc.G % 4 == 0) ? 4 : ((HACK_PRE_GP >= 2 && kc.G % 2 == 0) ? 2 : 1);
+}
+
 template <int BITS>
 __global__ void __launch_bounds__(kThreads, 1) prefill_tc_kernel(
     const __half* __restrict__ q, const int32_t* __restrict__ cu_seqlens, const int32_t* __restrict__ slots,
@@ -147,17 +155,21 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_tc_kernel(
   // heaviest-first (longest causal rows of every head before any lighter tile): greedy
   // block scheduling then balances the SMs (LPT), ~15% shorter than per-head ordering.
   const int b = blockIdx.z;
+  // GQA row packing: the 128 MMA rows are gp query heads (of one KV head) x pbp positions,
+  // so the K'/V' tiles a CTA unpacks serve gp heads and the causal diagonal is pbp wide.
+  const int gp = pack_heads(kc), pbp = BM / gp;
   const int lin = blockIdx.x + gridDim.x * blockIdx.y;
-  const int rank = lin / kc.Hq, hq = lin % kc.Hq;
+  const int npk = kc.Hq / gp;
+  const int rank = lin / npk, hq0 = (lin % npk) * gp;  // heads hq0 .. hq0 + gp - 1
   const int start = cu_seqlens[b], L = cu_seqlens[b + 1] - start;
-  const int nqt = (L + BM - 1) / BM;
+  const int nqt = (L + pbp - 1) / pbp;
   if (rank >= nqt) return;
   const int qt = nqt - 1 - rank;  // heavy (long causal rows) tiles first
-  const int i0 = qt * BM;
+  const int i0 = qt * pbp;        // first position of the CTA
   const int slot = slots[b];
-  const int hk = hq / kc.G;
+  const int hk = hq0 / kc.G;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int nkt = min((i0 + BM - 1) / BN, (L - 1) / BN) + 1;  // key tiles (causal)
+  const int nkt = min((i0 + pbp - 1) / BN, (L - 1) / BN) + 1;  // key tiles (causal)
   const int nfull = L / PI;                                    // committed V blocks
   const PageLayout PL = kc.pl;
 
@@ -405,7 +417,8 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_tc_kernel(
     asm volatile("setmaxnreg.dec.sync.aligned.u32 88;");
     const int sw = (warp - 4) >> 2;
     const int r = (tid - 128) & (BM - 1);
-    const int i = min(i0 + r, L - 1);  // this thread's query position (padding rows clamp)
+    const int pos = i0 + (r & (pbp - 1)), hq = hq0 + r / pbp;  // this row's position and head
+    const int i = min(pos, L - 1);  // this thread's query position (padding rows clamp)
     const uint32_t lane_base = (uint32_t)(32 * (warp & 3)) << 16;
     const uint32_t qbar = 3 + (warp & 3);  // the 2 S warps sharing these 32 rows
     const float cscale = 1.4426950408889634f / sqrtf(128.f);
@@ -625,8 +638,8 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_tc_kernel(
           }
           *reinterpret_cast<uint4*>(sm.p[bj] + kmaj_off(r, kb + 16 * c16, 512)) =
               make_uint4(cw[0] ^ 0x80808080u, cw[1] ^ 0x80808080u, cw[2] ^ 0x80808080u, cw[3] ^ 0x80808080u);
-          if (dbg_pcodes != nullptr && i0 + r < L) {
-            uint8_t* dp = dbg_pcodes + ((int64_t)(start + i0 + r) * kc.Hq + hq) * dbg_stride + t0 + kb + 16 * c16;
+          if (dbg_pcodes != nullptr && pos < L) {
+            uint8_t* dp = dbg_pcodes + ((int64_t)(start + pos) * kc.Hq + hq) * dbg_stride + t0 + kb + 16 * c16;
 #pragma unroll
             for (int pos = 0; pos < 16; ++pos)
               dp[perm_src<BITS>(pos)] = (uint8_t)((cw[pos >> 2] >> (8 * (pos & 3))) & 0xFF);
@@ -650,6 +663,7 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_tc_kernel(
     asm volatile("setmaxnreg.inc.sync.aligned.u32 128;");
     const int ow = (warp - 12) >> 2;
     const int r = (tid - 384) & (BM - 1);
+    const int pos = i0 + (r & (pbp - 1)), hq = hq0 + r / pbp;
     const uint32_t lane_base = (uint32_t)(32 * (warp & 3)) << 16;
     const int cb = 64 * ow;
     float2 o2[32];  // channels cb + 2x, cb + 2x + 1
@@ -790,9 +804,9 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_tc_kernel(
     }
 #endif
     rwait<4>(&sm.l_ready, 0);
-    if (i0 + r < L) {
+    if (pos < L) {
       const float inv_l = 1.f / (sm.lpart[0][r] + sm.lpart[1][r]);
-      const int64_t base = ((int64_t)(start + i0 + r) * kc.Hq + hq) * 128 + cb;
+      const int64_t base = ((int64_t)(start + pos) * kc.Hq + hq) * 128 + cb;
       if (kc.out_fp32) {
         float4* op = reinterpret_cast<float4*>(reinterpret_cast<float*>(out) + base);
 #pragma unroll
@@ -823,7 +837,8 @@ cudaError_t launch_t(const KernelCfg& kc, const void* q, const int32_t* cu, cons
   auto kern = prefill_tc_kernel<BITS>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  dim3 grid((max_seqlen + BM - 1) / BM, kc.Hq, batch);
+  const int gp = pack_heads(kc);
+  dim3 grid((max_seqlen + BM / gp - 1) / (BM / gp), kc.Hq / gp, batch);
   kern<<<grid, kThreads, smem, st>>>(reinterpret_cast<const __half*>(q), cu, slots, cv, kc, out,
                                      dbg ? dbg->pcodes : nullptr, dbg ? dbg->pcodes_stride : 0);
   note_launch();
