@@ -168,12 +168,43 @@ def oracle_sample(seconds_hint=False, L=4096, heads=1, groups=1):
 
 
 def cpu_threads():
+    """Threads the oracle's BLAS pool actually uses (its only parallelism)."""
     try:
         import threadpoolctl
         info = threadpoolctl.threadpool_info()
         return max([i.get("num_threads", 1) for i in info] + [1])
     except Exception:
         return os.cpu_count()
+
+
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    import platform
+    return platform.processor() or "unknown"
+
+
+def oracle_one_thread(heads=1):
+    """The same oracle sample with its BLAS pool limited to one thread (SURVEY d-3)."""
+    try:
+        import threadpoolctl
+        with threadpoolctl.threadpool_limits(1):
+            return oracle_sample(heads=heads)
+    except ImportError:
+        return None
+
+
+def cpu_record(value, desc, dt, one=None):
+    rec = {"value": value, "unit": "TOPS", "cores": cpu_threads(), "kind": "oracle", "sample": f"{desc}; {dt:.1f} s wall",
+           "host_cpus": os.cpu_count(), "cpu_model": cpu_model()}
+    if one is not None:
+        rec["value_1thread"] = one[0]
+        rec["sample_1thread"] = f"{one[3]}; {one[1]:.1f} s wall, 1 BLAS thread"
+    return rec
 
 
 # ----------------------------------------------------------------------------- reference arm
@@ -194,8 +225,7 @@ def run_reference(args, rank):
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic", "config": {"workload": WORKLOAD, "batch": 1, "seq_len": C2["L"],
                                             "parallelism": "cpu oracle, rank 0 only"},
-            "cpu_baseline": {"value": value, "unit": "TOPS", "cores": cpu_threads(), "kind": "oracle",
-                             "sample": desc + " per step"},
+            "cpu_baseline": cpu_record(value, desc + " per step", statistics.mean(secs)),
             "e2e": {"value": value, "unit": "TOPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -459,9 +489,8 @@ def run_hack(args, rank, local_rank, world):
     # ---------------- CPU oracle baseline (rank 0, N = 1)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        v_c, dt, ops_s, desc = oracle_sample(heads=8, groups=2)  # ~10-15 s of host CPU
-        cpu = {"value": v_c, "unit": "TOPS", "cores": cpu_threads(), "kind": "oracle",
-               "sample": f"{desc}; {dt:.1f} s wall"}
+        v_c, dt, ops_s, desc = oracle_sample(heads=8, groups=2)  # ~10-15 s of host CPU, all BLAS threads
+        cpu = cpu_record(v_c, desc, dt, oracle_one_thread(heads=1))   # + one query head on 1 thread
 
     if rank == 0:
         line = {
@@ -473,7 +502,7 @@ def run_hack(args, rank, local_rank, world):
                        "parallelism": f"replicas x{world} (independent requests per GPU)",
                        "l2": "flushed (512 MB write) before every step, outside the events",
                        "baseline_metric": BASELINE_METRIC},
-            "roofline": {"bound": "tensor", "achieved": achieved, "peak": int8_peak, "unit": "TFLOP/s",
+            "roofline": {"bound": "tensor", "achieved": achieved, "peak": int8_peak, "unit": "TOPS",
                          "frac": achieved / int8_peak, "traffic": tr,
                          "kernel": "prefill attention (hack_prefill_attention_cached)",
                          "peak_src": f"{peaks['src']} bf16 burst {peaks['bf16']} x 2 (nominal int8:bf16 4.5:2.25)",
@@ -944,6 +973,19 @@ def run_decode(args, h, dev, rank, world, peaks, traffic, seed, flush):
     }
 
 
+def spawn_ranks(n):
+    """`bench.py --gpus N` without a launcher: start N ranks (one process per GPU) through
+    torch.distributed.run on 127.0.0.1 with the same arguments; rank 0 prints the line."""
+    import socket
+    import subprocess
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes", "1", "--nproc-per-node", str(n),
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.call(cmd)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -965,9 +1007,13 @@ def main():
                     help="process-group backend for barriers / max-over-ranks (gloo: several ranks on one GPU, tests)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "hack" else args.warmup
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        sys.exit(spawn_ranks(args.gpus))
     rank = int(os.environ.get("RANK", 0))
     local_rank = int(os.environ.get("LOCAL_RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))
+    if world != args.gpus:
+        sys.exit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world} ranks were launched")
     if args.impl == "reference":
         run_reference(args, rank)
         return
@@ -975,6 +1021,8 @@ def main():
         import torch
         import torch.distributed as dist
         ndev = torch.cuda.device_count()
+        if ndev < world and args.dist_backend == "nccl":
+            sys.exit(f"bench.py: {world} ranks need {world} GPUs, this node has {ndev}")
         local_dev = local_rank % ndev
         torch.cuda.set_device(local_dev)
         if args.dist_backend == "nccl":

@@ -42,7 +42,7 @@ extern "C" {
 #pragma GCC visibility push(default)
 #endif
 
-#define HACK_ABI_VERSION 1
+#define HACK_ABI_VERSION 2
 
 typedef enum {
   HACK_OK = 0,
@@ -105,12 +105,45 @@ typedef struct {
 } hack_kv_cache_t;
 
 /* Optional debug dumps (parity protocol); pass NULL in production.
+ * Every pointer may be NULL independently; the dumps do not change any result.
  * pcodes: device u8 [total_q_rows][H_q][pcodes_stride]: the GPU's 8-bit P codes of
- * committed V blocks, key t at column t (row-major per query row). */
+ *   committed V blocks, key t at column t (row-major per query row).
+ * qk_acc: device int32 [total_q_rows][H_q][d/Pi][acc_stride]: for every key t the query
+ *   row attends to, the QK integer MMA's own block accumulator of d-block beta, exactly as
+ *   the kernel holds it (conversion bias removed).  It is an exact affine function of the
+ *   paper's D_beta = sum_{z in beta} q'_z k'_z (Eq. 4) whose form is
+ *   hack_debug_acc_form() (below).
+ * pv_acc: device int32 [total_q_rows][H_q][acc_stride/Pi][d]: per committed V block j and
+ *   channel c, the PV MMA's block accumulator, an exact affine function of
+ *   D'_j = sum_{t in block j} p'_t v'_tc (the GPU's own P codes) of the same form.
+ * acc_stride: keys per (row, head, beta) in qk_acc; >= max_seqlen, a multiple of Pi.
+ * acc_head: -1 = every query head (the H_q dimension above); h >= 0 = only query head h
+ *   (sampled dumps at full size), the arrays then being [total_q_rows][1][...]. */
 typedef struct {
   uint8_t* pcodes;
   int64_t pcodes_stride;
+  int32_t* qk_acc;
+  int32_t* pv_acc;
+  int64_t acc_stride;
+  int32_t acc_head;
+  int32_t reserved;
 } hack_debug_t;
+
+/* Affine form of the dumped accumulators, per hack_debug_acc_form(cfg, op):
+ *   HACK_ACC_PLAIN     acc = D                                  (decode_mma: u8 x u8 on 2^23 bias)
+ *   HACK_ACC_S8_2B     acc = 2 D - 256 S_B                      (prefill_tc: A' - 128 (s8) x 2 B' (u8))
+ *   HACK_ACC_CENTERED4 acc = 4 D - 2(2^b-1) S_A + Pi 255 (2^b-1) (decode_pair / decode_g8: split planes)
+ * with S_A the 8-bit operand's block code sum (SQ / SP) and S_B the b-bit operand's (SK / SV).
+ * HACK_ACC_NONE: the kernel serving (cfg, op) has no accumulator dump (CUDA-core baselines);
+ * a call with qk_acc / pv_acc set then returns HACK_ERR_UNSUPPORTED. */
+typedef enum {
+  HACK_ACC_NONE = 0,
+  HACK_ACC_PLAIN = 1,
+  HACK_ACC_S8_2B = 2,
+  HACK_ACC_CENTERED4 = 3
+} hack_acc_form_t;
+/* op: 0 = prefill attention, 1 = decode attention (dispatch as the next call would). */
+int32_t hack_debug_acc_form(const hack_config_t* cfg, int32_t op);
 
 /* ---- configuration and layout ------------------------------------------ */
 void hack_config_default(hack_config_t* cfg);          /* H=1/1, d=128, Pi=64, b=2, SR/SR/RN, fp16 out */
@@ -226,14 +259,18 @@ hack_status_t hack_comm_destroy(void* comm);
 /* hack_kv_pack: gather one request (slot) of num_layers caches (host array of structs,
  * <= 128 layers, sharing block_table/seq_lens/rng_ids) into `staging` (device, >=
  * hack_kv_transfer_bytes): 64-byte header (magic "HACK", version, dims, prompt_len,
- * tail_len, first_token, rng_id) + per layer the request's pages (codes, fp16
- * meta, cached sums, R19) + its FP16 tail rows (RQE).  first_token: the prefill
- * output token. */
+ * tail_len, first_token, rng_id, page_bytes, head_base, payload_bytes, seed) + per
+ * layer the request's pages (codes, fp16 meta, cached sums, R19) + its FP16 tail rows
+ * (RQE).  first_token: the prefill output token.  rng_id must equal the
+ * cache's rng_ids[slot] (the header carries rng_ids[slot]); a mismatch is detected on the
+ * device and poisons the header (magic 0), so the receiver reports HACK_ERR_PROTOCOL. */
 hack_status_t hack_kv_pack(const hack_config_t* cfg, const hack_kv_cache_t* caches, int32_t num_layers,
                            int32_t slot, int32_t prompt_len, int32_t first_token, uint32_t rng_id,
                            void* staging, void* stream);
 /* hack_kv_unpack: validate the header in `staging` on the device against (cfg,
- * num_layers, prompt_len) and scatter into `slot` of the local caches (block tables
+ * num_layers, prompt_len) -- dims, sizes, and the Philox seed and head_base, since this
+ * rank's later appends continue the same streams (R3) -- and scatter into `slot` of the
+ * local caches (block tables
  * already filled by the caller), setting seq_lens[slot] and rng_ids[slot].
  * status_dev (device int32[2], may be NULL) receives {hack_status_t, first_token}; a
  * header mismatch writes HACK_ERR_PROTOCOL and leaves the cache untouched. */

@@ -54,21 +54,25 @@ def build(force: bool = False, verbose: bool = False) -> str:
     sources = sorted(glob.glob(os.path.join(CSRC, "*.cu")))
     jobs = []
     objs = []
+    extra = os.environ.get("HACK_EXTRA_NVCC_FLAGS", "").split()  # experiments only
     for s in sources:
         o = os.path.join(BUILD, os.path.basename(s) + ".o")
         objs.append(o)
-        if force or _newer([s] + headers, o):
-            extra = os.environ.get("HACK_EXTRA_NVCC_FLAGS", "").split()  # experiments only
-            cmd = [NVCC, *ARCH, *CFLAGS, *extra, "-I", inc, "-I", os.path.join(ROOT, "include"), "-c", s, "-o", o]
+        cmd = [NVCC, *ARCH, *CFLAGS, *extra, "-I", inc, "-I", os.path.join(ROOT, "include"), "-c", s, "-o", o]
+        # the object's compile flags are stamped next to it: a flag change (e.g. an ablation
+        # build with HACK_EXTRA_NVCC_FLAGS left behind) forces a rebuild, not just an mtime change
+        stamp = o + ".flags"
+        old = open(stamp).read() if os.path.exists(stamp) else None
+        if force or _newer([s] + headers, o) or old != " ".join(cmd):
             jobs.append((s, cmd))
 
     def run(job):
         s, cmd = job
         r = subprocess.run(cmd, capture_output=True, text=True)
-        return s, r
+        return s, r, cmd
 
     with cf.ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 4)) as ex:
-        for s, r in ex.map(run, jobs):
+        for s, r, cmd in ex.map(run, jobs):
             if r.returncode != 0:
                 sys.stderr.write(r.stdout + r.stderr)
                 raise RuntimeError(f"nvcc failed on {os.path.basename(s)}")
@@ -76,6 +80,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
                 sys.stderr.write(f"== {os.path.basename(s)}\n" + r.stderr)
             with open(os.path.join(BUILD, os.path.basename(s) + ".ptxas.txt"), "w") as f:
                 f.write(r.stderr)
+            with open(os.path.join(BUILD, os.path.basename(s) + ".o.flags"), "w") as f:
+                f.write(" ".join(cmd))
     if force or jobs or _newer(objs, LIB):
         cmd = [NVCC, *ARCH, "-shared", "-o", LIB, *objs, "-L", libdir, "-l:libnccl.so.2",
                "-Xlinker", f"-rpath={libdir}", "-lcuda"]

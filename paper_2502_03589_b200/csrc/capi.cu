@@ -171,6 +171,82 @@ hack_status_t hack_quantize_pack(const hack_config_t* cfg, int32_t mode, const v
                      "quantize_pack");
 }
 
+}  // extern "C"
+
+namespace hack {
+namespace {
+
+// Argument checks of each compute step, run in full before ANY launch of a combined call
+// (hack.h: "argument errors are detected on the host before any launch"), so a rejected
+// call never leaves the cache half-updated.
+hack_status_t check_ingest(const KernelCfg& kc, const hack_kv_cache_t* cache, const void* k, const void* v,
+                           const int32_t* cu, const int32_t* slots, int batch, int max_seqlen) {
+  if (!k || !v || !cu || !slots) return fail(HACK_ERR_INVALID_ARG, "ingest: NULL pointer");
+  if (batch <= 0 || max_seqlen <= 0) return fail(HACK_ERR_INVALID_ARG, "ingest: empty batch/prompt (S:303)");
+  if ((max_seqlen + kc.Pi - 1) / kc.Pi > cache->max_pages_per_req)
+    return fail(HACK_ERR_CAPACITY, "ingest: max_seqlen needs more pages than max_pages_per_req");
+  if (batch > cache->max_reqs) return fail(HACK_ERR_CAPACITY, "ingest: batch > max_reqs");
+  return HACK_OK;
+}
+
+hack_status_t check_debug(const KernelCfg& kc, const hack_debug_t* dbg, int max_seqlen, int op, const char* who) {
+  if (!dbg) return HACK_OK;
+  if (dbg->pcodes && dbg->pcodes_stride < max_seqlen)
+    return fail(HACK_ERR_SHAPE, "%s: debug pcodes_stride < max_seqlen", who);
+  if (dbg->qk_acc || dbg->pv_acc) {
+    if (debug_acc_form(kc, op) == HACK_ACC_NONE)
+      return fail(HACK_ERR_UNSUPPORTED, "%s: the kernel serving this config has no accumulator dump", who);
+    if (dbg->acc_stride < max_seqlen || dbg->acc_stride % kc.Pi)
+      return fail(HACK_ERR_SHAPE, "%s: debug acc_stride must be >= max_seqlen and a multiple of Pi", who);
+    if (dbg->acc_head < -1 || dbg->acc_head >= kc.Hq)
+      return fail(HACK_ERR_INVALID_ARG, "%s: debug acc_head out of range", who);
+  }
+  return HACK_OK;
+}
+
+hack_status_t check_prefill(const KernelCfg& kc, const hack_kv_cache_t* cache, const void* q, const int32_t* cu,
+                            const int32_t* slots, int batch, int max_seqlen, const void* out, const void* ws,
+                            size_t ws_bytes, const hack_debug_t* dbg) {
+  if (!q || !cu || !slots || !out) return fail(HACK_ERR_INVALID_ARG, "prefill: NULL pointer");
+  if (batch <= 0 || max_seqlen <= 0) return fail(HACK_ERR_INVALID_ARG, "prefill: empty batch/prompt (S:303)");
+  if ((max_seqlen + kc.Pi - 1) / kc.Pi > cache->max_pages_per_req)
+    return fail(HACK_ERR_CAPACITY, "prefill: max_seqlen needs more pages than max_pages_per_req");
+  const size_t need = prefill_workspace_bytes(kc, batch, max_seqlen);
+  if (ws_bytes < need || (need && !ws)) return fail(HACK_ERR_CAPACITY, "prefill: workspace %zu < %zu", ws_bytes, need);
+  return check_debug(kc, dbg, max_seqlen, 0, "prefill");
+}
+
+hack_status_t check_append(const hack_kv_cache_t* cache, const void* k_new, const void* v_new, const int32_t* slots,
+                           int batch) {
+  if (!k_new || !v_new || !slots) return fail(HACK_ERR_INVALID_ARG, "decode_append: NULL pointer");
+  if (batch <= 0) return fail(HACK_ERR_INVALID_ARG, "decode_append: empty batch");
+  if (batch > cache->max_reqs) return fail(HACK_ERR_CAPACITY, "decode_append: batch > max_reqs");
+  return HACK_OK;
+}
+
+hack_status_t check_decode(const KernelCfg& kc, const hack_kv_cache_t* cache, const void* q_new, const int32_t* slots,
+                           int batch, int max_seqlen, const void* out, const void* ws, size_t ws_bytes,
+                           const hack_debug_t* dbg) {
+  if (!q_new || !slots || !out) return fail(HACK_ERR_INVALID_ARG, "decode: NULL pointer");
+  if (batch <= 0 || max_seqlen <= 0) return fail(HACK_ERR_INVALID_ARG, "decode: empty batch");
+  if ((max_seqlen + kc.Pi - 1) / kc.Pi > cache->max_pages_per_req)
+    return fail(HACK_ERR_CAPACITY, "decode: max_seqlen needs more pages than max_pages_per_req");
+  const size_t need = decode_workspace_bytes(kc, batch, max_seqlen);
+  if (ws_bytes < need || (need && !ws)) return fail(HACK_ERR_CAPACITY, "decode: workspace %zu < %zu", ws_bytes, need);
+  return check_debug(kc, dbg, max_seqlen, 1, "decode");
+}
+
+}  // namespace
+}  // namespace hack
+
+extern "C" {
+
+int32_t hack_debug_acc_form(const hack_config_t* cfg, int32_t op) {
+  KernelCfg kc;
+  if (make_kernel_cfg(cfg, &kc) != HACK_OK || (op != 0 && op != 1)) return HACK_ACC_NONE;
+  return debug_acc_form(kc, op);
+}
+
 hack_status_t hack_cache_ingest(const hack_config_t* cfg, const void* k, const void* v, const int32_t* cu,
                                 const int32_t* slots, int32_t batch, int32_t max_seqlen,
                                 const hack_kv_cache_t* cache, void* stream) {
@@ -179,11 +255,7 @@ hack_status_t hack_cache_ingest(const hack_config_t* cfg, const void* k, const v
   hack_status_t st = make_kernel_cfg(cfg, &kc);
   if (st != HACK_OK) return st;
   if ((st = make_cache_view(kc, cache, &cv)) != HACK_OK) return st;
-  if (!k || !v || !cu || !slots) return fail(HACK_ERR_INVALID_ARG, "ingest: NULL pointer");
-  if (batch <= 0 || max_seqlen <= 0) return fail(HACK_ERR_INVALID_ARG, "ingest: empty batch/prompt (S:303)");
-  if ((max_seqlen + kc.Pi - 1) / kc.Pi > cache->max_pages_per_req)
-    return fail(HACK_ERR_CAPACITY, "ingest: max_seqlen needs more pages than max_pages_per_req");
-  if (batch > cache->max_reqs) return fail(HACK_ERR_CAPACITY, "ingest: batch > max_reqs");
+  if ((st = check_ingest(kc, cache, k, v, cu, slots, batch, max_seqlen)) != HACK_OK) return st;
   if ((st = check_device()) != HACK_OK) return st;
   return cuda_status(launch_ingest(kc, k, v, cu, slots, batch, max_seqlen, cv, (cudaStream_t)stream), "ingest");
 }
@@ -203,14 +275,7 @@ hack_status_t hack_prefill_attention_cached(const hack_config_t* cfg, const void
   hack_status_t st = make_kernel_cfg(cfg, &kc);
   if (st != HACK_OK) return st;
   if ((st = make_cache_view(kc, cache, &cv)) != HACK_OK) return st;
-  if (!q || !cu || !slots || !out) return fail(HACK_ERR_INVALID_ARG, "prefill: NULL pointer");
-  if (batch <= 0 || max_seqlen <= 0) return fail(HACK_ERR_INVALID_ARG, "prefill: empty batch/prompt (S:303)");
-  if ((max_seqlen + kc.Pi - 1) / kc.Pi > cache->max_pages_per_req)
-    return fail(HACK_ERR_CAPACITY, "prefill: max_seqlen needs more pages than max_pages_per_req");
-  const size_t need = prefill_workspace_bytes(kc, batch, max_seqlen);
-  if (ws_bytes < need || (need && !ws)) return fail(HACK_ERR_CAPACITY, "prefill: workspace %zu < %zu", ws_bytes, need);
-  if (dbg && dbg->pcodes && dbg->pcodes_stride < max_seqlen)
-    return fail(HACK_ERR_SHAPE, "prefill: debug pcodes_stride < max_seqlen");
+  if ((st = check_prefill(kc, cache, q, cu, slots, batch, max_seqlen, out, ws, ws_bytes, dbg)) != HACK_OK) return st;
   if ((st = check_device()) != HACK_OK) return st;
   return cuda_status(launch_prefill_attention(kc, q, cu, slots, batch, max_seqlen, cv, out, ws, dbg,
                                               (cudaStream_t)stream),
@@ -221,9 +286,20 @@ hack_status_t hack_prefill_attention(const hack_config_t* cfg, const void* q, co
                                      const int32_t* cu, const int32_t* slots, int32_t batch, int32_t max_seqlen,
                                      const hack_kv_cache_t* cache, void* out, void* ws, size_t ws_bytes,
                                      const hack_debug_t* dbg, void* stream) {
-  hack_status_t st = hack_cache_ingest(cfg, k, v, cu, slots, batch, max_seqlen, cache, stream);
+  KernelCfg kc;
+  CacheView cv;
+  hack_status_t st = make_kernel_cfg(cfg, &kc);
   if (st != HACK_OK) return st;
-  return hack_prefill_attention_cached(cfg, q, cu, slots, batch, max_seqlen, cache, out, ws, ws_bytes, dbg, stream);
+  if ((st = make_cache_view(kc, cache, &cv)) != HACK_OK) return st;
+  if ((st = check_ingest(kc, cache, k, v, cu, slots, batch, max_seqlen)) != HACK_OK) return st;
+  if ((st = check_prefill(kc, cache, q, cu, slots, batch, max_seqlen, out, ws, ws_bytes, dbg)) != HACK_OK) return st;
+  if ((st = check_device()) != HACK_OK) return st;
+  if ((st = cuda_status(launch_ingest(kc, k, v, cu, slots, batch, max_seqlen, cv, (cudaStream_t)stream), "ingest")) !=
+      HACK_OK)
+    return st;
+  return cuda_status(launch_prefill_attention(kc, q, cu, slots, batch, max_seqlen, cv, out, ws, dbg,
+                                              (cudaStream_t)stream),
+                     "prefill_attention");
 }
 
 hack_status_t hack_decode_append(const hack_config_t* cfg, const void* k_new, const void* v_new,
@@ -233,9 +309,7 @@ hack_status_t hack_decode_append(const hack_config_t* cfg, const void* k_new, co
   hack_status_t st = make_kernel_cfg(cfg, &kc);
   if (st != HACK_OK) return st;
   if ((st = make_cache_view(kc, cache, &cv)) != HACK_OK) return st;
-  if (!k_new || !v_new || !slots) return fail(HACK_ERR_INVALID_ARG, "decode_append: NULL pointer");
-  if (batch <= 0) return fail(HACK_ERR_INVALID_ARG, "decode_append: empty batch");
-  if (batch > cache->max_reqs) return fail(HACK_ERR_CAPACITY, "decode_append: batch > max_reqs");
+  if ((st = check_append(cache, k_new, v_new, slots, batch)) != HACK_OK) return st;
   if ((st = check_device()) != HACK_OK) return st;
   return cuda_status(launch_append(kc, k_new, v_new, slots, batch, cv, (cudaStream_t)stream), "decode_append");
 }
@@ -255,14 +329,7 @@ hack_status_t hack_decode_attention_cached(const hack_config_t* cfg, const void*
   hack_status_t st = make_kernel_cfg(cfg, &kc);
   if (st != HACK_OK) return st;
   if ((st = make_cache_view(kc, cache, &cv)) != HACK_OK) return st;
-  if (!q_new || !slots || !out) return fail(HACK_ERR_INVALID_ARG, "decode: NULL pointer");
-  if (batch <= 0 || max_seqlen <= 0) return fail(HACK_ERR_INVALID_ARG, "decode: empty batch");
-  if ((max_seqlen + kc.Pi - 1) / kc.Pi > cache->max_pages_per_req)
-    return fail(HACK_ERR_CAPACITY, "decode: max_seqlen needs more pages than max_pages_per_req");
-  const size_t need = decode_workspace_bytes(kc, batch, max_seqlen);
-  if (ws_bytes < need || (need && !ws)) return fail(HACK_ERR_CAPACITY, "decode: workspace %zu < %zu", ws_bytes, need);
-  if (dbg && dbg->pcodes && dbg->pcodes_stride < max_seqlen)
-    return fail(HACK_ERR_SHAPE, "decode: debug pcodes_stride < max_seqlen");
+  if ((st = check_decode(kc, cache, q_new, slots, batch, max_seqlen, out, ws, ws_bytes, dbg)) != HACK_OK) return st;
   if ((st = check_device()) != HACK_OK) return st;
   return cuda_status(launch_decode_attention(kc, q_new, slots, batch, max_seqlen, cv, out, ws, dbg,
                                              (cudaStream_t)stream),
@@ -273,9 +340,20 @@ hack_status_t hack_decode_attention(const hack_config_t* cfg, const void* q_new,
                                     const void* v_new, const int32_t* slots, int32_t batch, int32_t max_seqlen,
                                     const hack_kv_cache_t* cache, void* out, void* ws, size_t ws_bytes,
                                     const hack_debug_t* dbg, void* stream) {
-  hack_status_t st = hack_decode_append(cfg, k_new, v_new, slots, batch, cache, stream);
+  KernelCfg kc;
+  CacheView cv;
+  hack_status_t st = make_kernel_cfg(cfg, &kc);
   if (st != HACK_OK) return st;
-  return hack_decode_attention_cached(cfg, q_new, slots, batch, max_seqlen, cache, out, ws, ws_bytes, dbg, stream);
+  if ((st = make_cache_view(kc, cache, &cv)) != HACK_OK) return st;
+  if ((st = check_append(cache, k_new, v_new, slots, batch)) != HACK_OK) return st;
+  if ((st = check_decode(kc, cache, q_new, slots, batch, max_seqlen, out, ws, ws_bytes, dbg)) != HACK_OK) return st;
+  if ((st = check_device()) != HACK_OK) return st;
+  if ((st = cuda_status(launch_append(kc, k_new, v_new, slots, batch, cv, (cudaStream_t)stream), "decode_append")) !=
+      HACK_OK)
+    return st;
+  return cuda_status(launch_decode_attention(kc, q_new, slots, batch, max_seqlen, cv, out, ws, dbg,
+                                             (cudaStream_t)stream),
+                     "decode_attention");
 }
 
 hack_status_t hack_dequantize_cache(const hack_config_t* cfg, const int32_t* slots, int32_t batch,

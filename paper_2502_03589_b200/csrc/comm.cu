@@ -77,10 +77,19 @@ HACK_DEV void copy16(uint8_t* dst, const uint8_t* src, int64_t bytes) {
 
 // grid (npages + 1, layers): block j < npages copies page j (all KV heads), block npages
 // copies the FP16 tail rows; blockIdx.y = layer - layer0 (layer-pipelined send packs one).
+// The header's rng_id is the cache's rng_ids[slot] (the stream the codes were drawn with, as
+// hack_kv_pull copies it); a caller-supplied rng_id that disagrees poisons the header
+// (magic 0), so the receiver's header check reports HACK_ERR_PROTOCOL.
 __global__ void gather_kernel(LayerPtrs lp, const int32_t* __restrict__ block_table, int max_pages_per_req,
-                              int slot, XferGeom g, WireHeader hdr, uint8_t* __restrict__ staging, int layer0) {
+                              const uint32_t* __restrict__ rng_ids, int slot, XferGeom g, WireHeader hdr,
+                              uint8_t* __restrict__ staging, int layer0) {
   const int j = blockIdx.x, l = layer0 + blockIdx.y;
-  if (j == 0 && l == 0 && threadIdx.x == 0) *reinterpret_cast<WireHeader*>(staging) = hdr;
+  if (j == 0 && l == 0 && threadIdx.x == 0) {
+    const uint32_t rid = rng_ids[slot];
+    if (rid != hdr.rng_id) hdr.magic = 0u;
+    hdr.rng_id = rid;
+    *reinterpret_cast<WireHeader*>(staging) = hdr;
+  }
   uint8_t* dst = staging + kHeaderBytes + (int64_t)l * g.layer_bytes;
   const int64_t pbytes = (int64_t)g.Hkv * g.page_bytes;
   if (j < g.npages) {
@@ -99,7 +108,8 @@ HACK_DEV bool header_ok(const WireHeader& h, const WireHeader& e) {
   return h.magic == e.magic && h.version == e.version && h.num_layers == e.num_layers &&
          h.num_kv_heads == e.num_kv_heads && h.head_dim == e.head_dim && h.partition == e.partition &&
          h.kv_bits == e.kv_bits && h.sum_bytes == e.sum_bytes && h.prompt_len == e.prompt_len &&
-         h.tail_len == e.tail_len && h.page_bytes == e.page_bytes && h.payload_bytes == e.payload_bytes;
+         h.tail_len == e.tail_len && h.page_bytes == e.page_bytes && h.payload_bytes == e.payload_bytes &&
+         h.seed == e.seed && h.head_base == e.head_base;  // same Philox streams as this rank's later appends
 }
 
 __global__ void scatter_kernel(LayerPtrs lp, const int32_t* __restrict__ block_table, int max_pages_per_req,
@@ -264,7 +274,8 @@ hack_status_t hack_kv_pack(const hack_config_t* cfg, const hack_kv_cache_t* cach
   hdr.rng_id = rng_id;
   if ((st = check_device()) != HACK_OK) return st;
   gather_kernel<<<dim3(g.npages + 1, num_layers), 256, 0, (cudaStream_t)stream>>>(
-      lp, caches[0].block_table, caches[0].max_pages_per_req, slot, g, hdr, (uint8_t*)staging, 0);
+      lp, caches[0].block_table, caches[0].max_pages_per_req, reinterpret_cast<const uint32_t*>(caches[0].rng_ids),
+      slot, g, hdr, (uint8_t*)staging, 0);
   note_launch();
   return cuda_status(cudaGetLastError(), "kv_pack gather");
 }
@@ -336,7 +347,8 @@ hack_status_t hack_kv_send_layer(void* comm, int32_t peer, const hack_config_t* 
   hdr.rng_id = rng_id;
   if ((st = check_device()) != HACK_OK) return st;
   gather_kernel<<<dim3(g.npages + 1, 1), 256, 0, (cudaStream_t)stream>>>(
-      lp, caches[0].block_table, caches[0].max_pages_per_req, slot, g, hdr, (uint8_t*)staging, layer);
+      lp, caches[0].block_table, caches[0].max_pages_per_req, reinterpret_cast<const uint32_t*>(caches[0].rng_ids),
+      slot, g, hdr, (uint8_t*)staging, layer);
   note_launch();
   if ((st = cuda_status(cudaGetLastError(), "kv_send_layer gather")) != HACK_OK) return st;
   int64_t b = 0;

@@ -106,11 +106,18 @@ constexpr int dmma_ctas() {
   return sm * kCtas <= 227 * 1024 ? kCtas : (sm * 2 <= 227 * 1024 ? 2 : 1);
 }
 
-template <int BITS, int PI_>
+// DBG: parity runs only (hack_debug_t): P-code and raw QK / PV accumulator dumps (the
+// accumulators hold 2^23 + D exactly: HACK_ACC_PLAIN).
+template <int BITS, int PI_, bool DBG>
 __global__ void __launch_bounds__(kThreads, dmma_ctas<BITS, PI_>()) decode_mma_kernel(const __half* __restrict__ q_new,
                                                               const int32_t* __restrict__ slots, CacheView cv,
                                                               KernelCfg kc, float* __restrict__ part, int nsplit,
-                                                              uint8_t* __restrict__ dbg_pcodes, int64_t dbg_stride) {
+                                                              uint8_t* __restrict__ dbg_pcodes, int64_t dbg_stride,
+                                                              int32_t* __restrict__ dbg_qk, int32_t* __restrict__ dbg_pv,
+                                                              int64_t acc_stride, int acc_head) {
+  // dumped head dimension and index of query row n (-1 = not dumped), hack_debug_t.acc_head
+  const int hdim = acc_head < 0 ? kc.Hq : 1;
+  auto hsel = [&](int n) { return acc_head < 0 ? blockIdx.y * kc.G + n : (blockIdx.y * kc.G + n == acc_head ? 0 : -1); };
   using SM = DecSmem<BITS, PI_>;
   constexpr int PI = PI_, NB = SM::NB, NS = SM::NS;
   constexpr int MT = PI / 16, KSV = PI / 32;  // QK m-tiles, PV k-steps per page
@@ -156,7 +163,7 @@ __global__ void __launch_bounds__(kThreads, dmma_ctas<BITS, PI_>()) decode_mma_k
       const int beta = lane16 / (PI / 8);
       const float cscale = 1.4426950408889634f / sqrtf(128.f);
       sm.qconst[beta][row] = row < G ? make_float4(cscale * s * 0.25f, cscale * s * ((float)sum - 127.5f * PI),
-                                                   cscale * (m + 127.5f * s), -(float)(2 * qkm * sum - PI * 255 * qkm))
+                                                   cscale * __fmaf_rn(127.5f, s, m), -(float)(2 * qkm * sum - PI * 255 * qkm))
                                      : make_float4(0.f, 0.f, 0.f, 0.f);
     }
   }
@@ -226,10 +233,10 @@ __global__ void __launch_bounds__(kThreads, dmma_ctas<BITS, PI_>()) decode_mma_k
           const __half2 mh = reinterpret_cast<const __half2*>(pg + PL.k_meta)[e];
           const float mk = __low2float(mh), sk = __high2float(mh);
           const int sum = load_sum(pg + PL.k_sums, e, PL.sum_bytes);  // cached (SE)
-          const float mu = mk + 0.5f * qkm * sk;
+          const float mu = __fmaf_rn(0.5f * qkm, sk, mk);
           c0 = sk;
           c1 = mu;
-          c2 = sk * ((float)sum - 0.5f * qkm * PI) + PI * mu;
+          c2 = __fmaf_rn(sk, (float)sum - 0.5f * qkm * PI, __fmul_rn((float)PI, mu));
           c3 = -(float)(510 * sum);
         }
         ws.kc[beta][t] = make_float4(c0, c1, c2, c3);
@@ -241,8 +248,9 @@ __global__ void __launch_bounds__(kThreads, dmma_ctas<BITS, PI_>()) decode_mma_k
           const __half2 mh = reinterpret_cast<const __half2*>(pg + PL.v_meta)[c];
           const float mv = __low2float(mh), sv = __high2float(mh);
           const int sum = load_sum(pg + PL.v_sums, c, PL.sum_bytes);  // cached (SE)
-          const float mu = mv + 0.5f * qkm * sv;
-          ws.vc[c] = make_float4(sv, mu, sv * ((float)sum - 0.5f * qkm * PI) + PI * mu, -(float)(510 * sum));
+          const float mu = __fmaf_rn(0.5f * qkm, sv, mv);
+          ws.vc[c] = make_float4(sv, mu, __fmaf_rn(sv, (float)sum - 0.5f * qkm * PI, __fmul_rn((float)PI, mu)),
+                                 -(float)(510 * sum));
         }
       }
       __syncwarp();
@@ -282,6 +290,21 @@ __global__ void __launch_bounds__(kThreads, dmma_ctas<BITS, PI_>()) decode_mma_k
             a[3] = plane<4>(odd ? w1[4 * ks + 3] : w1[4 * ks + 2], sh);
           }
           mma16832(acc[ks * 32 / PI], a, qb[ks][0], qb[ks][1]);  // k-step ks: channels 32ks.. of block beta
+        }
+        if (DBG && dbg_qk != nullptr) {  // rows n0, n1; tokens t0 / t1; every beta
+#pragma unroll
+          for (int hh = 0; hh < 2; ++hh) {
+            const int t = hh ? t1 : t0;
+            if (t < nk) {
+#pragma unroll
+              for (int beta = 0; beta < NB; ++beta) {
+                int32_t* dq = dbg_qk + (int64_t)b * hdim * NB * acc_stride + beta * acc_stride + jp * PI + t;
+                if (n0 < G && hsel(n0) >= 0) dq[(int64_t)hsel(n0) * NB * acc_stride] = (int32_t)(acc[beta][2 * hh] - kMagicI);
+                if (n1 < G && hsel(n1) >= 0)
+                  dq[(int64_t)hsel(n1) * NB * acc_stride] = (int32_t)(acc[beta][2 * hh + 1] - kMagicI);
+              }
+            }
+          }
         }
         float2 st[2];
 #pragma unroll
@@ -333,11 +356,8 @@ __global__ void __launch_bounds__(kThreads, dmma_ctas<BITS, PI_>()) decode_mma_k
       }
       l_run = ptx::ffma2(l_run, al, ls);
       m_run = mnew;
-#pragma unroll
-      for (int mt = 0; mt < 8; ++mt) {
-        o[mt][0] = ptx::fmul2(o[mt][0], al);
-        o[mt][1] = ptx::fmul2(o[mt][1], al);
-      }
+      // O *= al is fused into the PV update (o = o al + t, one explicit FFMA2): a separate
+      // FMUL2 + FADD2 pair may be contracted by ptxas or not depending on the surrounding code
       if (committed) {
         // -- (a6) P' per (row, V block): lo/hi from the score min/max (ex2 is monotone)
         const float2 lo = make_float2(ex2(mn2.x - mnew.x), ex2(mn2.y - mnew.y));
@@ -369,7 +389,7 @@ __global__ void __launch_bounds__(kThreads, dmma_ctas<BITS, PI_>()) decode_mma_k
           sp1 += __shfl_xor_sync(0xffffffffu, sp1, o2);
         }
         __syncwarp();
-        if (dbg_pcodes != nullptr && g < G) {  // debug dump (natural token order) of row g
+        if (DBG && dbg_pcodes != nullptr && g < G) {  // debug dump (natural token order) of row g
           for (int t = tig; t < PI; t += 4) {
             const int tp = t & 15;
             const int posn = BITS == 2 ? (t & ~15) + 4 * (tp & 3) + (tp >> 2)
@@ -386,7 +406,7 @@ __global__ void __launch_bounds__(kThreads, dmma_ctas<BITS, PI_>()) decode_mma_k
         }
         const float2 AP = make_float2(pm0.s * 0.25f, pm1.s * 0.25f);
         const float2 XP = make_float2(pm0.s * ((float)sp0 - 127.5f * PI), pm1.s * ((float)sp1 - 127.5f * PI));
-        const float2 MP = make_float2(pm0.m + 127.5f * pm0.s, pm1.m + 127.5f * pm1.s);
+        const float2 MP = make_float2(__fmaf_rn(127.5f, pm0.s, pm0.m), __fmaf_rn(127.5f, pm1.s, pm1.m));
         const float2 NRP = make_float2(-(float)(2 * qkm * (int)sp0 - PI * 255 * qkm),
                                        -(float)(2 * qkm * (int)sp1 - PI * 255 * qkm));
         // -- O^T += V' P'^T per m-tile of 16 channels; Eq. 4 (centered) with cached V sums
@@ -432,6 +452,15 @@ __global__ void __launch_bounds__(kThreads, dmma_ctas<BITS, PI_>()) decode_mma_k
               mma16832(dacc, a, pb[ks][0], pb[ks][1]);
             }
           }
+          if (DBG && dbg_pv != nullptr) {  // rows n0, n1; channels c0 / c1 of block jp
+            const int64_t nbk = acc_stride / PI;
+#pragma unroll
+            for (int hh = 0; hh < 2; ++hh) {
+              int32_t* dp = dbg_pv + (int64_t)b * hdim * nbk * 128 + (int64_t)jp * 128 + (hh ? c1 : c0);
+              if (n0 < G && hsel(n0) >= 0) dp[(int64_t)hsel(n0) * nbk * 128] = (int32_t)(dacc[2 * hh] - kMagicI);
+              if (n1 < G && hsel(n1) >= 0) dp[(int64_t)hsel(n1) * nbk * 128] = (int32_t)(dacc[2 * hh + 1] - kMagicI);
+            }
+          }
 #pragma unroll
           for (int hh = 0; hh < 2; ++hh) {
             const int c = hh ? c1 : c0;
@@ -442,11 +471,16 @@ __global__ void __launch_bounds__(kThreads, dmma_ctas<BITS, PI_>()) decode_mma_k
             const float2 e = ptx::ffma2(make_float2(4.f, 4.f), df, ptx::fadd2(NRP, make_float2(nr, nr)));
             const float2 t2 = ptx::ffma2(AP, ptx::fmul2(make_float2(svv, svv), e),
                                          ptx::ffma2(XP, make_float2(mu, mu), ptx::fmul2(MP, make_float2(yv, yv))));
-            o[mt][hh] = ptx::fadd2(o[mt][hh], t2);
+            o[mt][hh] = ptx::ffma2(o[mt][hh], al, t2);
           }
         }
       } else {
         // -- FP16 last V block (RQE): O^T += V_tail^T p~ in fp32
+#pragma unroll
+        for (int mt = 0; mt < 8; ++mt) {
+          o[mt][0] = ptx::fmul2(o[mt][0], al);
+          o[mt][1] = ptx::fmul2(o[mt][1], al);
+        }
 #pragma unroll
         for (int mt = 0; mt < MT; ++mt)
 #pragma unroll
@@ -503,8 +537,8 @@ __global__ void __launch_bounds__(kThreads, dmma_ctas<BITS, PI_>()) decode_mma_k
 #pragma unroll
         for (int w = 0; w < NW; ++w) {
           const float f = ex2(sm.mrg_m[w][n] - M);
-          L += f * sm.mrg_l[w][n];
-          O += f * sm.mrg_o[w][n][c];
+          L = __fmaf_rn(f, sm.mrg_l[w][n], L);
+          O = __fmaf_rn(f, sm.mrg_o[w][n][c], O);
         }
       }
       float* dst = part + ((((int64_t)b * kc.Hkv + hk) * nsplit + split) * G + n) * 130;
@@ -531,8 +565,8 @@ __global__ void decode_combine_kernel(const float* __restrict__ part, int nsplit
     const float ms = base[s * stride];
     if (ms == -INFINITY) continue;
     const float f = ex2(ms - M);
-    L += f * base[s * stride + 1];
-    O += f * base[s * stride + 2 + c];
+    L = __fmaf_rn(f, base[s * stride + 1], L);
+    O = __fmaf_rn(f, base[s * stride + 2 + c], O);
   }
   const float v = O / L;
   const int64_t idx = ((int64_t)b * kc.Hq + hq) * 128 + c;
@@ -547,12 +581,14 @@ cudaError_t launch_t(const KernelCfg& kc, const void* q_new, const int32_t* slot
                      const CacheView& cv, void* out, float* part, const hack_debug_t* dbg, cudaStream_t st) {
   if (kc.pl.page_bytes != DecSmem<BITS, PI_>::PB) return cudaErrorInvalidValue;  // layout drift guard
   const size_t smem = sizeof(DecSmem<BITS, PI_>);
-  auto kern = decode_mma_kernel<BITS, PI_>;
+  const bool with_dbg = dbg != nullptr && (dbg->pcodes != nullptr || dbg->qk_acc != nullptr || dbg->pv_acc != nullptr);
+  auto kern = with_dbg ? decode_mma_kernel<BITS, PI_, true> : decode_mma_kernel<BITS, PI_, false>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  kern<<<dim3(batch, kc.Hkv, nsplit), kThreads, smem, st>>>(reinterpret_cast<const __half*>(q_new), slots, cv, kc,
-                                                            part, nsplit, dbg ? dbg->pcodes : nullptr,
-                                                            dbg ? dbg->pcodes_stride : 0);
+  kern<<<dim3(batch, kc.Hkv, nsplit), kThreads, smem, st>>>(
+      reinterpret_cast<const __half*>(q_new), slots, cv, kc, part, nsplit, dbg ? dbg->pcodes : nullptr,
+      dbg ? dbg->pcodes_stride : 0, dbg ? dbg->qk_acc : nullptr, dbg ? dbg->pv_acc : nullptr,
+      dbg ? dbg->acc_stride : 0, dbg ? dbg->acc_head : -1);
   decode_combine_kernel<<<dim3(batch, kc.Hq), 128, 0, st>>>(part, nsplit, kc, out);
   note_launch(2);
   return cudaGetLastError();

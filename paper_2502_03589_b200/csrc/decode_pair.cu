@@ -182,10 +182,12 @@ HACK_DEV void stage_kc(const uint8_t* pg, const PageLayout& PL, float4* kcs, int
 
 // Homomorphic S^T for one 64-token page: sc[mt][hh] = log2(e)/sqrt(d) * S(token 16mt+g+8hh, row tig).
 // MASK: tokens >= nk (the partial last page) are -inf.  Also the per-lane max/min.
+// dq (debug runs only, else nullptr): this lane's query row's qk_acc at the page's first token;
+// receives the raw block accumulators 4 D_beta + RC (HACK_ACC_CENTERED4), beta 1 at + dstride.
 template <bool MASK>
 HACK_DEV void qk_page(const uint8_t* pg, const PageLayout& PL, const float4* kcs, int g, int tig, int nk,
                       const uint32_t (&qb)[4][2], float2 QA, float2 QX, float2 QM, uint32_t rc0, uint32_t rc1,
-                      float (&sc)[4][2], float& mx, float& mn) {
+                      float (&sc)[4][2], float& mx, float& mn, int32_t* dq = nullptr, int64_t dstride = 0) {
   mx = -INFINITY;
   mn = INFINITY;
 #pragma unroll
@@ -206,6 +208,10 @@ HACK_DEV void qk_page(const uint8_t* pg, const PageLayout& PL, const float4* kcs
       const int t = hh ? t1 : t0;
       const float4 c0 = kcs[2 * t], c1 = kcs[2 * t + 1];
       const uint32_t e0 = (acc0[2 * hh] << 2) + acc1[2 * hh], e1 = (acc0[2 * hh + 1] << 2) + acc1[2 * hh + 1];
+      if (dq != nullptr && t < nk) {
+        dq[t] = (int32_t)(e0 - kMagic);
+        dq[dstride + t] = (int32_t)(e1 - kMagic);
+      }
       const float2 e = ptx::fadd2(asf2(e0, e1), f2(c1.z, c1.w));  // exact centered integer (beta0, beta1)
       const float2 s2 = ptx::ffma2(QA, ptx::fmul2(f2(c0.x, c0.y), e),
                                    ptx::ffma2(QX, f2(c0.z, c0.w), ptx::fmul2(QM, f2(c1.x, c1.y))));
@@ -361,11 +367,25 @@ HACK_DEV void produce_pages(SMT& sm, SegWalker walk, const CacheView& cv, const 
   }
 }
 
+// DBG: parity runs only (hack_debug_t): P-code and raw QK / PV accumulator dumps.
+struct DecDbg {
+  uint8_t* pcodes;
+  int64_t pstride;
+  int32_t* qk;
+  int32_t* pv;
+  int64_t astride;
+  int head;  // hack_debug_t.acc_head
+  // dump row of query head hq: index in the dumped head dimension, -1 = not dumped
+  HACK_DEV int hsel(int hq) const { return head < 0 ? hq : (hq == head ? 0 : -1); }
+  HACK_DEV int hdim(int Hq) const { return head < 0 ? Hq : 1; }
+};
+
 template <bool DBG, bool SE>
 __global__ void __launch_bounds__(kThreads, kCtasPerSm)
     decode_pair_kernel(const __half* __restrict__ q_new, const int32_t* __restrict__ slots, int batch, CacheView cv,
-                       KernelCfg kc, int* __restrict__ ws_meta, float* __restrict__ part,
-                       uint8_t* __restrict__ dbg_pcodes, int64_t dbg_stride) {
+                       KernelCfg kc, int* __restrict__ ws_meta, float* __restrict__ part, DecDbg dbg) {
+  uint8_t* const dbg_pcodes = dbg.pcodes;
+  const int64_t dbg_stride = dbg.pstride;
   constexpr int qkm = 3;
   extern __shared__ __align__(128) uint8_t smem_raw[];
   PairSmem& sm = *reinterpret_cast<PairSmem*>(smem_raw);
@@ -439,7 +459,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
         if ((lane16 & 7) == 0) {  // every lane of a partition holds (m, s, sum)
           qcf[beta] = ok ? cscale * sc * 0.25f : 0.f;                                  // QA
           qcf[2 + beta] = ok ? cscale * sc * ((float)sum - 127.5f * PI) : 0.f;        // QX
-          qcf[4 + beta] = ok ? cscale * (m + 127.5f * sc) : 0.f;                      // QM
+          qcf[4 + beta] = ok ? cscale * __fmaf_rn(127.5f, sc, m) : 0.f;                  // QM
           qcf[6 + beta] = __int_as_float(ok ? -(2 * qkm * sum - PI * 255 * qkm) : 0);  // RC (int bits)
         }
       }
@@ -484,16 +504,21 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
         wait_fill<NSTG>(sm, kA);
         stage_kc<SE>(pgA, PL, &ws.scr[0][0], lane);
         __syncwarp();
+        int32_t* dqA = nullptr;
+        if (DBG && dbg.qk != nullptr && tig < G && dbg.hsel(s.hk * G + tig) >= 0)
+          dqA = dbg.qk + ((int64_t)s.b * dbg.hdim(kc.Hq) + dbg.hsel(s.hk * G + tig)) * 2 * dbg.astride + jpA * PI;
         if (tail_item)
-          qk_page<true>(pgA, PL, &ws.scr[0][0], g, tig, nkA, qb, QA, QX, QM, rc0, rc1, sa, mxA, mnA);
+          qk_page<true>(pgA, PL, &ws.scr[0][0], g, tig, nkA, qb, QA, QX, QM, rc0, rc1, sa, mxA, mnA, dqA, dbg.astride);
         else
-          qk_page<false>(pgA, PL, &ws.scr[0][0], g, tig, PI, qb, QA, QX, QM, rc0, rc1, sa, mxA, mnA);
+          qk_page<false>(pgA, PL, &ws.scr[0][0], g, tig, PI, qb, QA, QX, QM, rc0, rc1, sa, mxA, mnA, dqA,
+                         dbg.astride);
         if (hasB) {
           wait_fill<NSTG>(sm, kB);
           __syncwarp();
           stage_kc<SE>(pgB, PL, &ws.scr[0][0], lane);
           __syncwarp();
-          qk_page<false>(pgB, PL, &ws.scr[0][0], g, tig, PI, qb, QA, QX, QM, rc0, rc1, sbv, mxB, mnB);
+          qk_page<false>(pgB, PL, &ws.scr[0][0], g, tig, PI, qb, QA, QX, QM, rc0, rc1, sbv, mxB, mnB,
+                         dqA != nullptr ? dqA + PI : nullptr, dbg.astride);
         } else {
 #pragma unroll
           for (int mt = 0; mt < 4; ++mt) sbv[mt][0] = sbv[mt][1] = -INFINITY;
@@ -560,13 +585,12 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
           }
 #pragma unroll
         for (int o2 = 4; o2 < 32; o2 <<= 1) ls += __shfl_xor_sync(0xffffffffu, ls, o2);
-        l_run = l_run * al + ls;
+        l_run = __fmaf_rn(l_run, al, ls);
         m_run = mnew;
-#pragma unroll
-        for (int mt = 0; mt < 8; ++mt) {
-          o[mt][0] = ptx::fmul2(o[mt][0], f2(al, al));
-          o[mt][1] = ptx::fmul2(o[mt][1], f2(al, al));
-        }
+        // O *= al is fused into the PV update below (o = o al + t, one explicit FFMA2): a
+        // separate FMUL2 + FADD2 pair may or may not be contracted by ptxas depending on the
+        // surrounding code, which made the debug and production instantiations differ in ulps
+        const float2 al2 = f2(al, al);
 
         if (!tail_item) {
           // ---- (a6) P' per (row, page): RN 8-bit against fp32 (lo, s) of the unnormalized p~
@@ -609,7 +633,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
             }
             AP = f2(pA.s * 0.25f, pB.s * 0.25f);
             XP = f2(pA.s * ((float)spA - 127.5f * PI), pB.s * ((float)spB - 127.5f * PI));
-            MP = f2(pA.m + 127.5f * pA.s, pB.m + 127.5f * pB.s);
+            MP = f2(__fmaf_rn(127.5f, pA.s, pA.m), __fmaf_rn(127.5f, pB.s, pB.m));
             rcA = kMagic + (uint32_t)(-(2 * qkm * (int)spA - PI * 255 * qkm));
             rcB = kMagic + (uint32_t)(-(2 * qkm * (int)spB - PI * 255 * qkm));
           }
@@ -644,14 +668,25 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
               const float4* vsrc = ch < 64 ? vc_lo + 2 * ch : &ws.scr[ch - 64][0];
               const float4 v0 = vsrc[0], v1 = vsrc[1];
               const uint32_t e0 = (acc0[2 * hh] << 2) + acc1[2 * hh], e1 = (acc0[2 * hh + 1] << 2) + acc1[2 * hh + 1];
+              if (DBG && dbg.pv != nullptr && tig < G && dbg.hsel(s.hk * G + tig) >= 0) {  // 4 D' + RC, pages A, B
+                int32_t* dp = dbg.pv + (((int64_t)s.b * dbg.hdim(kc.Hq) + dbg.hsel(s.hk * G + tig)) * (dbg.astride / PI) +
+                                        jpA) * 128 + ch;
+                dp[0] = (int32_t)(e0 - kMagic);
+                if (hasB) dp[128] = (int32_t)(e1 - kMagic);
+              }
               const float2 e = ptx::fadd2(asf2(e0, e1), f2(v1.z, v1.w));
               const float2 t2 = ptx::ffma2(AP, ptx::fmul2(f2(v0.x, v0.y), e),
                                            ptx::ffma2(XP, f2(v0.z, v0.w), ptx::fmul2(MP, f2(v1.x, v1.y))));
-              o[mt][hh] = ptx::fadd2(o[mt][hh], t2);
+              o[mt][hh] = ptx::ffma2(o[mt][hh], al2, t2);
             }
           }
         } else {
           // ---- FP16 last V block (RQE): O^T += V_tail^T p~ in fp32
+#pragma unroll
+          for (int mt = 0; mt < 8; ++mt) {
+            o[mt][0] = ptx::fmul2(o[mt][0], al2);
+            o[mt][1] = ptx::fmul2(o[mt][1], al2);
+          }
           float* ptl = reinterpret_cast<float*>(pgA + PL.k_codes);  // [row 4][64]
 #pragma unroll
           for (int mt = 0; mt < 4; ++mt)
@@ -727,8 +762,9 @@ struct G8Smem {
 template <bool DBG>
 __global__ void __launch_bounds__(kThreads, kCtas8)
     decode_g8_kernel(const __half* __restrict__ q_new, const int32_t* __restrict__ slots, int batch, CacheView cv,
-                     KernelCfg kc, int* __restrict__ ws_meta, float* __restrict__ part,
-                     uint8_t* __restrict__ dbg_pcodes, int64_t dbg_stride) {
+                     KernelCfg kc, int* __restrict__ ws_meta, float* __restrict__ part, DecDbg dbg) {
+  uint8_t* const dbg_pcodes = dbg.pcodes;
+  const int64_t dbg_stride = dbg.pstride;
   constexpr int qkm = 3;
   extern __shared__ __align__(128) uint8_t smem_raw[];
   G8Smem& sm = *reinterpret_cast<G8Smem*>(smem_raw);
@@ -798,7 +834,7 @@ __global__ void __launch_bounds__(kThreads, kCtas8)
         if ((lane16 & 7) == 0) {
           qcf[beta] = ok ? cscale * sc * 0.25f : 0.f;
           qcf[2 + beta] = ok ? cscale * sc * ((float)sum - 127.5f * PI) : 0.f;
-          qcf[4 + beta] = ok ? cscale * (m + 127.5f * sc) : 0.f;
+          qcf[4 + beta] = ok ? cscale * __fmaf_rn(127.5f, sc, m) : 0.f;
           qcf[6 + beta] = __int_as_float(ok ? -(2 * qkm * sum - PI * 255 * qkm) : 0);
         }
       }
@@ -866,6 +902,12 @@ __global__ void __launch_bounds__(kThreads, kCtas8)
               const int t = hh ? t1 : t0;
               const float4 c0 = kcs[2 * t], c1 = kcs[2 * t + 1];
               const uint32_t e0 = (acc0[2 * hh] << 2) + acc1[2 * hh], e1 = (acc0[2 * hh + 1] << 2) + acc1[2 * hh + 1];
+              if (DBG && dbg.qk != nullptr && 4 * nt + tig < G && t < nk && dbg.hsel(s.hk * G + 4 * nt + tig) >= 0) {
+                int32_t* dq = dbg.qk + ((int64_t)s.b * dbg.hdim(kc.Hq) + dbg.hsel(s.hk * G + 4 * nt + tig)) * 2 * dbg.astride +
+                              jp * PI + t;  // raw 4 D_beta + RC
+                dq[0] = (int32_t)(e0 - kMagic);
+                dq[dbg.astride] = (int32_t)(e1 - kMagic);
+              }
               const float2 e = ptx::fadd2(asf2(e0, e1), f2(c1.z, c1.w));
               const float2 s2 = ptx::ffma2(QA[nt], ptx::fmul2(f2(c0.x, c0.y), e),
                                            ptx::ffma2(QX[nt], f2(c0.z, c0.w), ptx::fmul2(QM[nt], f2(c1.x, c1.y))));
@@ -899,7 +941,7 @@ __global__ void __launch_bounds__(kThreads, kCtas8)
             }
 #pragma unroll
           for (int o2 = 4; o2 < 32; o2 <<= 1) ls[nt] += __shfl_xor_sync(0xffffffffu, ls[nt], o2);
-          l_run[nt] = l_run[nt] * al[nt] + ls[nt];
+          l_run[nt] = __fmaf_rn(l_run[nt], al[nt], ls[nt]);
         }
         uint8_t* pcode = pg + PL.k_meta;                          // [row 8][64] in B-fragment order
         float* ptl = reinterpret_cast<float*>(pg + PL.k_codes);    // [row 8][64] p~ of a partial page
@@ -943,15 +985,10 @@ __global__ void __launch_bounds__(kThreads, kCtas8)
           __syncwarp();
           // PV lanes: rows n0, n1
           const float4 r0 = ws.rowinfo[n0], r1 = ws.rowinfo[n1];
-          const float2 alp = f2(r0.x, r1.x);
-#pragma unroll
-          for (int mt = 0; mt < 8; ++mt) {
-            o[mt][0] = ptx::fmul2(o[mt][0], alp);
-            o[mt][1] = ptx::fmul2(o[mt][1], alp);
-          }
+          const float2 alp = f2(r0.x, r1.x);  // O *= alp fused into the PV update (explicit FFMA2)
           const float2 AP = f2(r0.y * 0.25f, r1.y * 0.25f);
           const float2 XP = f2(r0.y * (r0.w - 127.5f * PI), r1.y * (r1.w - 127.5f * PI));
-          const float2 MP = f2(r0.z + 127.5f * r0.y, r1.z + 127.5f * r1.y);
+          const float2 MP = f2(__fmaf_rn(127.5f, r0.y, r0.z), __fmaf_rn(127.5f, r1.y, r1.z));
           const uint32_t rp0 = kMagic + (uint32_t)(-(2 * qkm * (int)r0.w - PI * 255 * qkm));
           const uint32_t rp1 = kMagic + (uint32_t)(-(2 * qkm * (int)r1.w - PI * 255 * qkm));
           // B fragments of P'^T: column n = g = row g; k-steps u: tokens 16 tig + 4 i + q(u, h)
@@ -969,10 +1006,18 @@ __global__ void __launch_bounds__(kThreads, kCtas8)
             for (int hh = 0; hh < 2; ++hh) {
               const float4 v4 = vcs[hh ? c1 : c0];
               const uint32_t e0 = (acc0[2 * hh] << 2) + acc1[2 * hh], e1 = (acc0[2 * hh + 1] << 2) + acc1[2 * hh + 1];
+              if (DBG && dbg.pv != nullptr) {  // raw 4 D'_page + RC_page, rows n0, n1
+                const int ch = hh ? c1 : c0;
+                const int64_t nbk = dbg.astride / PI;
+                const int hs0 = dbg.hsel(s.hk * G + n0), hs1 = dbg.hsel(s.hk * G + n1);
+                int32_t* dp = dbg.pv + (int64_t)s.b * dbg.hdim(kc.Hq) * nbk * 128 + (int64_t)jp * 128 + ch;
+                if (n0 < G && hs0 >= 0) dp[(int64_t)hs0 * nbk * 128] = (int32_t)(e0 - kMagic);
+                if (n1 < G && hs1 >= 0) dp[(int64_t)hs1 * nbk * 128] = (int32_t)(e1 - kMagic);
+              }
               const float2 e = ptx::fadd2(asf2(e0, e1), f2(v4.w, v4.w));
               const float2 t2 = ptx::ffma2(AP, ptx::fmul2(f2(v4.x, v4.x), e),
                                            ptx::ffma2(XP, f2(v4.y, v4.y), ptx::fmul2(MP, f2(v4.z, v4.z))));
-              o[mt][hh] = ptx::fadd2(o[mt][hh], t2);
+              o[mt][hh] = ptx::ffma2(o[mt][hh], alp, t2);
             }
           }
         } else {
@@ -1088,12 +1133,9 @@ __global__ void __launch_bounds__(128) decode_pair_combine(const int* __restrict
 }
 
 int grid_size(bool g8 = false) {
-  static int sms = 0;
-  if (!sms) {
-    int dev = 0;
-    sms = 148;
-    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  }
+  // per call and per current device (a process may drive several GPUs)
+  int dev = 0, sms = 148;
+  if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   if (const char* e = getenv("HACK_DECODE_GRID")) return atoi(e);
   return sms * (g8 ? kCtas8 : kCtasPerSm);
 }
@@ -1121,17 +1163,16 @@ cudaError_t launch_decode_pair(const KernelCfg& kc, const void* q_new, const int
   float* part = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(workspace) + meta_bytes(batch));
   const bool g8 = kc.G > 4;
   const size_t smem = g8 ? sizeof(G8Smem) : sizeof(PairSmem);
-  const bool with_dbg = dbg != nullptr && dbg->pcodes != nullptr;  // P-code dump: parity runs only
+  const bool with_dbg = dbg != nullptr && (dbg->pcodes != nullptr || dbg->qk_acc != nullptr ||
+                                           dbg->pv_acc != nullptr);  // dumps: parity runs only
   const bool no_se = !g8 && getenv("HACK_DECODE_NO_SE") != nullptr;  // f2 ablation only
   auto kern = g8 ? (with_dbg ? decode_g8_kernel<true> : decode_g8_kernel<false>)
                  : with_dbg ? (no_se ? decode_pair_kernel<true, false> : decode_pair_kernel<true, true>)
                             : (no_se ? decode_pair_kernel<false, false> : decode_pair_kernel<false, true>);
-  const int ki = (g8 ? 4 : 0) + (with_dbg ? 2 : 0) + (no_se ? 1 : 0);
-  static bool attr_set[8] = {false, false, false, false, false, false, false, false};  // once per process
-  if (!attr_set[ki]) {
+  // the attribute is per device / context: set it on every launch (cheap), no process-wide cache
+  {
     const cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    attr_set[ki] = true;
   }
   {
     // programmatic dependent launch: the grid launches (and its prologue runs) while the
@@ -1151,9 +1192,10 @@ cudaError_t launch_decode_pair(const KernelCfg& kc, const void* q_new, const int
 #else
     mc.numAttrs = 1;
 #endif
+    DecDbg dd = {nullptr, 0, nullptr, nullptr, 0, -1};
+    if (with_dbg) dd = {dbg->pcodes, dbg->pcodes_stride, dbg->qk_acc, dbg->pv_acc, dbg->acc_stride, dbg->acc_head};
     const cudaError_t e1 = cudaLaunchKernelEx(&mc, kern, reinterpret_cast<const __half*>(q_new), slots, batch, cv, kc,
-                                              meta, part, with_dbg ? dbg->pcodes : (uint8_t*)nullptr,
-                                              with_dbg ? dbg->pcodes_stride : (int64_t)0);
+                                              meta, part, dd);
     if (e1 != cudaSuccess) return e1;
   }
 #ifdef HACK_DEC_NOCOMBINE

@@ -4,9 +4,7 @@
 // (prefill_simt.cu).  Decode: the paired-page mma.sync kernel (decode_pair.cu) for b = 2,
 // Pi = 64, G <= 4; the general split-KV mma.sync kernel (decode_mma.cu) for Pi = 64,
 // G <= 8; else decode_simt.cu.  HACK_PREFILL_IMPL / HACK_DECODE_IMPL = "simt" force the
-// baseline kernels (parity cross-checks); HACK_DECODE_IMPL = "mma" skips the paired kernel.  csrc/experimental/decode_tc.cu (a tcgen05
-// decode with K/V operands unpacked into TMEM) is not built: it was slower than the
-// mma.sync kernel and hangs in some configurations (round-2 work).
+// baseline kernels (parity cross-checks); HACK_DECODE_IMPL = "mma" skips the paired kernel.
 #include <cstdlib>
 #include <cstring>
 
@@ -65,6 +63,12 @@ static bool use_decode_mma(const KernelCfg& kc) {
 
 static bool use_decode_pair(const KernelCfg& kc) {
   return decode_pair_supported(kc) && !env_is("HACK_DECODE_IMPL", "simt") && !env_is("HACK_DECODE_IMPL", "mma");
+}
+
+int debug_acc_form(const KernelCfg& kc, int op) {
+  if (op == 0) return prefill_tc_supported(kc) && !env_is("HACK_PREFILL_IMPL", "simt") ? HACK_ACC_S8_2B : HACK_ACC_NONE;
+  if (use_decode_pair(kc)) return HACK_ACC_CENTERED4;
+  return use_decode_mma(kc) ? HACK_ACC_PLAIN : HACK_ACC_NONE;
 }
 
 size_t decode_workspace_bytes(const KernelCfg& kc, int batch, int max_seqlen) {

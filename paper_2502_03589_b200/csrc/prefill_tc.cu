@@ -143,10 +143,13 @@ __host__ __device__ __forceinline__ int pack_heads(const KernelCfg& kc) {
   return (HACK_PRE_GP >= 4 && kc.G % 4 == 0) ? 4 : ((HACK_PRE_GP >= 2 && kc.G % 2 == 0) ? 2 : 1);
 }
 
-template <int BITS>
+// DBG: parity runs only (hack_debug_t): dumps the P codes and the raw QK / PV block
+// accumulators E = 2 D - 256 S_B (HACK_ACC_S8_2B); the production instantiation has none of it.
+template <int BITS, bool DBG>
 __global__ void __launch_bounds__(kThreads, 1) prefill_tc_kernel(
     const __half* __restrict__ q, const int32_t* __restrict__ cu_seqlens, const int32_t* __restrict__ slots,
-    CacheView cv, KernelCfg kc, void* __restrict__ out, uint8_t* __restrict__ dbg_pcodes, int64_t dbg_stride) {
+    CacheView cv, KernelCfg kc, void* __restrict__ out, uint8_t* __restrict__ dbg_pcodes, int64_t dbg_stride,
+    int32_t* __restrict__ dbg_qk, int32_t* __restrict__ dbg_pv, int64_t acc_stride, int acc_head) {
   using SM = TcSmem<BITS>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   SM& sm = *reinterpret_cast<SM*>(smem_raw);
@@ -481,9 +484,9 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_tc_kernel(
       }
       const int sqs = sum - 128 * PI;  // sum (q' - 128)
       sm.qconst[sw][r] =
-          make_float4(cscale * qm.s * 0.5f, cscale * qm.s * (float)sqs, cscale * (qm.m + 128.f * qm.s), 0.f);
+          make_float4(cscale * qm.s * 0.5f, cscale * qm.s * (float)sqs, cscale * __fmaf_rn(128.f, qm.s, qm.m), 0.f);
       {
-        const float X = cscale * qm.s * (float)sqs, M = cscale * (qm.m + 128.f * qm.s);
+        const float X = cscale * qm.s * (float)sqs, M = cscale * __fmaf_rn(128.f, qm.s, qm.m);
         float av[12];
         rank_a(X, av);
         rank_a(M, av + 6);
@@ -525,6 +528,15 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_tc_kernel(
           uint32_t d[16];
           ptx::tmem_ld16(tS + lane_base + 64 * beta + kb + 16 * h, d);
           ptx::tmem_wait_ld();
+          if (DBG && dbg_qk != nullptr && pos < L && (acc_head < 0 || hq == acc_head)) {  // E = 2 D - 256 SK
+            const int hs = acc_head < 0 ? hq : 0, hn = acc_head < 0 ? kc.Hq : 1;
+            int32_t* dq = dbg_qk + (((int64_t)(start + pos) * hn + hs) * 2 + beta) * acc_stride;
+#pragma unroll
+            for (int x = 0; x < 16; ++x) {
+              const int t = t0 + kb + 16 * h + x;
+              if (t < L) dq[t] = (int32_t)(d[x] - 0x4B400000u);
+            }
+          }
 #pragma unroll
           for (int g4 = 0; g4 < 4; ++g4) {
             const int kl = kb + 16 * h + 4 * g4;  // first of 4 keys
@@ -594,7 +606,7 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_tc_kernel(
 #endif
         ls2 = ptx::fadd2(ls2, make_float2(s[kk], s[kk + 1]));
       }
-      l_run = l_run * al + (ls2.x + ls2.y);
+      l_run = __fmaf_rn(l_run, al, ls2.x + ls2.y);
       // tile j-NB must be fully consumed by the O warps before its P / info slots are reused
       rwait<3>(&sm.o_done[bj], ph ^ 1);
       if (j < nfull) {
@@ -638,7 +650,7 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_tc_kernel(
           }
           *reinterpret_cast<uint4*>(sm.p[bj] + kmaj_off(r, kb + 16 * c16, 512)) =
               make_uint4(cw[0] ^ 0x80808080u, cw[1] ^ 0x80808080u, cw[2] ^ 0x80808080u, cw[3] ^ 0x80808080u);
-          if (dbg_pcodes != nullptr && pos < L) {
+          if (DBG && dbg_pcodes != nullptr && pos < L) {
             uint8_t* dp = dbg_pcodes + ((int64_t)(start + pos) * kc.Hq + hq) * dbg_stride + t0 + kb + 16 * c16;
 #pragma unroll
             for (int pos = 0; pos < 16; ++pos)
@@ -703,7 +715,7 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_tc_kernel(
           const int sps0 = sm.sp_part[bj][0][r] + sm.sp_part[bj][1][r] - 128 * PI;
           float av[16];
           rank_a(pi4.z * (float)sps0, av);
-          rank_a(pi4.w + 128.f * pi4.z, av + 6);
+          rank_a(__fmaf_rn(128.f, pi4.z, pi4.w), av + 6);
           av[12] = av[13] = av[14] = av[15] = 0.f;
           uint8_t* oar = reinterpret_cast<uint8_t*>(sm.ora);
 #pragma unroll
@@ -724,7 +736,8 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_tc_kernel(
         const int sps = sm.sp_part[bj][0][r] + sm.sp_part[bj][1][r] - 128 * PI;  // sum (p' - 128)
         const float2 ap2 = make_float2(0.5f * pi4.z, 0.5f * pi4.z);
         const float2 xp2 = make_float2(pi4.z * (float)sps, pi4.z * (float)sps);
-        const float2 mp2 = make_float2(pi4.w + 128.f * pi4.z, pi4.w + 128.f * pi4.z);
+        const float mp = __fmaf_rn(128.f, pi4.z, pi4.w);
+        const float2 mp2 = make_float2(mp, mp);
         rwait<4>(&sm.v_ready[bj], ph);
         rwait<4>(&sm.d_full[bd], (j / NDB) & 1);
         ptx::tc_fence_after();
@@ -733,6 +746,12 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_tc_kernel(
           uint32_t d[16];
           ptx::tmem_ld16(tD0 + 128 * bd + lane_base + cb + 16 * h, d);
           ptx::tmem_wait_ld();
+          if (DBG && dbg_pv != nullptr && pos < L && (acc_head < 0 || hq == acc_head)) {  // E' = 2 D' - 256 SV
+            const int hs = acc_head < 0 ? hq : 0, hn = acc_head < 0 ? kc.Hq : 1;
+            int32_t* dp = dbg_pv + (((int64_t)(start + pos) * hn + hs) * (acc_stride / PI) + j) * 128 + cb + 16 * h;
+#pragma unroll
+            for (int x = 0; x < 16; ++x) dp[x] = (int32_t)(d[x] - 0x4B400000u);
+          }
 #if HACK_ABL == 1
           if (d[0] == 0x12345u) o2[h].x += 1.f;  // (ablation: no PV Eq. 4 math)
 #else
@@ -834,13 +853,16 @@ template <int BITS>
 cudaError_t launch_t(const KernelCfg& kc, const void* q, const int32_t* cu, const int32_t* slots, int batch,
                      int max_seqlen, const CacheView& cv, void* out, const hack_debug_t* dbg, cudaStream_t st) {
   const size_t smem = sizeof(TcSmem<BITS>) + 1024;
-  auto kern = prefill_tc_kernel<BITS>;
+  const bool with_dbg = dbg != nullptr && (dbg->pcodes != nullptr || dbg->qk_acc != nullptr || dbg->pv_acc != nullptr);
+  auto kern = with_dbg ? prefill_tc_kernel<BITS, true> : prefill_tc_kernel<BITS, false>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   const int gp = pack_heads(kc);
   dim3 grid((max_seqlen + BM / gp - 1) / (BM / gp), kc.Hq / gp, batch);
   kern<<<grid, kThreads, smem, st>>>(reinterpret_cast<const __half*>(q), cu, slots, cv, kc, out,
-                                     dbg ? dbg->pcodes : nullptr, dbg ? dbg->pcodes_stride : 0);
+                                     dbg ? dbg->pcodes : nullptr, dbg ? dbg->pcodes_stride : 0,
+                                     dbg ? dbg->qk_acc : nullptr, dbg ? dbg->pv_acc : nullptr,
+                                     dbg ? dbg->acc_stride : 0, dbg ? dbg->acc_head : -1);
   note_launch();
   return cudaGetLastError();
 }

@@ -293,6 +293,11 @@ __global__ void __launch_bounds__(128) append_kernel(const __half* __restrict__ 
   const int H = kc.Hkv, Pi = kc.Pi;
   const int t = cv.seq_lens[slot];
   const int blk = t / Pi, row = t % Pi;
+  // capacity guard: a request whose next token needs a block beyond its block-table row is
+  // not appended (nothing written, seq_lens unchanged) rather than spilling into the next
+  // slot's row; uniform over the cluster (every CTA read the same t), so no barrier is skipped
+  // by only some of them.  hack_decode_attention rejects such a call on the host.
+  if (blk >= cv.max_pages_per_req) return;
   const uint32_t rng_id = cv.rng_ids[slot];
   const int c = threadIdx.x;
   const PageLayout& PL = kc.pl;

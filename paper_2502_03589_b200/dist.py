@@ -109,6 +109,14 @@ class WireHeader:
             raise ValueError("inconsistent header (HACK_ERR_PROTOCOL)")
         return h
 
+    def check(self, expect: "WireHeader"):
+        """The receiver's header check (libhack header_ok): dims, sizes, and the Philox seed
+        and head_base -- this rank's later appends continue the same streams (R3)."""
+        keys = ("num_layers", "num_kv_heads", "head_dim", "partition", "kv_bits", "prompt_len", "head_base", "seed")
+        bad = [k for k in keys if getattr(self, k) != getattr(expect, k)]
+        if bad:
+            raise ValueError(f"header mismatch in {bad} (HACK_ERR_PROTOCOL)")
+
 
 @dataclass
 class DecodeScheduler:

@@ -51,7 +51,13 @@ class CacheStruct(C.Structure):
 
 
 class DebugStruct(C.Structure):
-    _fields_ = [("pcodes", C.c_void_p), ("pcodes_stride", C.c_int64)]
+    _fields_ = [("pcodes", C.c_void_p), ("pcodes_stride", C.c_int64), ("qk_acc", C.c_void_p),
+                ("pv_acc", C.c_void_p), ("acc_stride", C.c_int64), ("acc_head", C.c_int32),
+                ("reserved", C.c_int32)]
+
+
+# hack_acc_form_t: affine form of the dumped MMA accumulators (include/hack.h)
+ACC_NONE, ACC_PLAIN, ACC_S8_2B, ACC_CENTERED4 = range(4)
 
 
 _S = C.c_int
@@ -65,6 +71,7 @@ _lib.hack_kv_transfer_bytes.restype = C.c_int64
 _lib.hack_prefill_workspace_size.restype = C.c_size_t
 _lib.hack_decode_workspace_size.restype = C.c_size_t
 _lib.hack_config_default.restype = None
+_lib.hack_debug_acc_form.restype = C.c_int32
 for _name in ("hack_config_validate", "hack_page_layout", "hack_quantize_pack", "hack_cache_ingest",
               "hack_prefill_attention", "hack_prefill_attention_cached", "hack_decode_append",
               "hack_decode_attention", "hack_decode_attention_cached", "hack_homomorphic_matmul",
@@ -94,6 +101,7 @@ _lib.hack_dequantize_cache.argtypes = [C.POINTER(Config), _P, C.c_int32, C.c_int
 _lib.hack_homomorphic_matmul.argtypes = [C.POINTER(Config), _P, _P, _P, _P, _P, _P, C.c_int32, C.c_int32,
                                          C.c_int32, _P, _P, _P]
 _lib.hack_prefill_workspace_size.argtypes = [C.POINTER(Config), C.c_int32, C.c_int32]
+_lib.hack_debug_acc_form.argtypes = [C.POINTER(Config), C.c_int32]
 _lib.hack_decode_workspace_size.argtypes = [C.POINTER(Config), C.c_int32, C.c_int32]
 _lib.hack_page_bytes.argtypes = [C.POINTER(Config)]
 _lib.hack_page_layout.argtypes = [C.POINTER(Config), C.POINTER(C.c_int64 * 12)]
@@ -234,13 +242,29 @@ class KVCache:
         return s
 
 
-def _dbg(pcodes: torch.Tensor | None):
-    if pcodes is None:
+def _dbg(pcodes: torch.Tensor | None, qk_acc: torch.Tensor | None = None, pv_acc: torch.Tensor | None = None,
+         acc_head: int = -1):
+    """hack_debug_t: pcodes u8 [rows, H_q, stride]; qk_acc int32 [rows, H_q, d/Pi, acc_stride];
+    pv_acc int32 [rows, H_q, acc_stride/Pi, d] (parity runs only).  acc_head >= 0 dumps only
+    that query head's accumulators, into [rows, 1, ...] arrays."""
+    if pcodes is None and qk_acc is None and pv_acc is None:
         return None
     d = DebugStruct()
-    d.pcodes = pcodes.data_ptr()
-    d.pcodes_stride = pcodes.shape[-1]
+    d.acc_head = acc_head
+    if pcodes is not None:
+        d.pcodes, d.pcodes_stride = pcodes.data_ptr(), pcodes.shape[-1]
+    if qk_acc is not None:
+        d.qk_acc, d.acc_stride = qk_acc.data_ptr(), qk_acc.shape[-1]
+    if pv_acc is not None:
+        if qk_acc is None:
+            raise ValueError("pv_acc needs qk_acc (the shared acc_stride comes from it)")
+        d.pv_acc = pv_acc.data_ptr()
     return C.byref(d)
+
+
+def debug_acc_form(cfg: Config, op: str) -> int:
+    """ACC_* form of the accumulator dump of the kernel the next prefill / decode call uses."""
+    return int(_lib.hack_debug_acc_form(C.byref(cfg), {"prefill": 0, "decode": 1}[op]))
 
 
 # --------------------------------------------------------------------------- calls
@@ -275,21 +299,22 @@ def _ws(workspace, nbytes, device):
 
 
 def prefill_attention(cfg: Config, q, k, v, cu_seqlens, slots, max_seqlen: int, cache: KVCache, out,
-                      workspace=None, debug_pcodes=None, stream=None):
+                      workspace=None, debug_pcodes=None, debug_qk=None, debug_pv=None, debug_head=-1, stream=None):
     cs = cache.struct()
     ws, nb = _ws(workspace, prefill_workspace_size(cfg, slots.shape[0], max_seqlen), q.device)
     _check(_lib.hack_prefill_attention(C.byref(cfg), _ptr(q), _ptr(k), _ptr(v), _ptr(cu_seqlens), _ptr(slots),
                                        slots.shape[0], max_seqlen, C.byref(cs), _ptr(out), _ptr(ws), nb,
-                                       _dbg(debug_pcodes), _stream(stream)), "prefill_attention")
+                                       _dbg(debug_pcodes, debug_qk, debug_pv, debug_head), _stream(stream)), "prefill_attention")
 
 
 def prefill_attention_cached(cfg: Config, q, cu_seqlens, slots, max_seqlen: int, cache: KVCache, out,
-                             workspace=None, debug_pcodes=None, stream=None):
+                             workspace=None, debug_pcodes=None, debug_qk=None, debug_pv=None, debug_head=-1, stream=None):
     cs = cache.struct()
     ws, nb = _ws(workspace, prefill_workspace_size(cfg, slots.shape[0], max_seqlen), q.device)
     _check(_lib.hack_prefill_attention_cached(C.byref(cfg), _ptr(q), _ptr(cu_seqlens), _ptr(slots),
                                               slots.shape[0], max_seqlen, C.byref(cs), _ptr(out), _ptr(ws), nb,
-                                              _dbg(debug_pcodes), _stream(stream)), "prefill_attention_cached")
+                                              _dbg(debug_pcodes, debug_qk, debug_pv, debug_head), _stream(stream)),
+           "prefill_attention_cached")
 
 
 def decode_append(cfg: Config, k_new, v_new, slots, cache: KVCache, stream=None):
@@ -299,20 +324,21 @@ def decode_append(cfg: Config, k_new, v_new, slots, cache: KVCache, stream=None)
 
 
 def decode_attention(cfg: Config, q_new, k_new, v_new, slots, max_seqlen: int, cache: KVCache, out,
-                     workspace=None, debug_pcodes=None, stream=None):
+                     workspace=None, debug_pcodes=None, debug_qk=None, debug_pv=None, debug_head=-1, stream=None):
     cs = cache.struct()
     ws, nb = _ws(workspace, decode_workspace_size(cfg, slots.shape[0], max_seqlen), q_new.device)
     _check(_lib.hack_decode_attention(C.byref(cfg), _ptr(q_new), _ptr(k_new), _ptr(v_new), _ptr(slots),
                                       slots.shape[0], max_seqlen, C.byref(cs), _ptr(out), _ptr(ws), nb,
-                                      _dbg(debug_pcodes), _stream(stream)), "decode_attention")
+                                      _dbg(debug_pcodes, debug_qk, debug_pv, debug_head), _stream(stream)), "decode_attention")
 
 
 def decode_attention_cached(cfg: Config, q_new, slots, max_seqlen: int, cache: KVCache, out, workspace=None,
-                            debug_pcodes=None, stream=None):
+                            debug_pcodes=None, debug_qk=None, debug_pv=None, debug_head=-1, stream=None):
     cs = cache.struct()
     ws, nb = _ws(workspace, decode_workspace_size(cfg, slots.shape[0], max_seqlen), q_new.device)
     _check(_lib.hack_decode_attention_cached(C.byref(cfg), _ptr(q_new), _ptr(slots), slots.shape[0], max_seqlen,
-                                             C.byref(cs), _ptr(out), _ptr(ws), nb, _dbg(debug_pcodes),
+                                             C.byref(cs), _ptr(out), _ptr(ws), nb,
+                                             _dbg(debug_pcodes, debug_qk, debug_pv, debug_head),
                                              _stream(stream)), "decode_attention_cached")
 
 

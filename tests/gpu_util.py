@@ -72,3 +72,62 @@ def compare_pages(cache, slot, state):
     if T:
         tail = cache.v_tail[slot, :, :T].cpu().numpy()              # [Hkv, T, d]
         assert np.array_equal(tail.transpose(1, 0, 2).view(np.uint16), a["tail"].view(np.uint16))
+
+
+# ---------------------------------------------------------------- MMA accumulator dumps
+# The hot kernels can dump their own int32 block accumulators (hack_debug_t.qk_acc /
+# pv_acc).  Each kernel's accumulator is an exact affine function of the paper's integer
+# block product D = sum_{z in block} a'_z b'_z (Eq. 4); the form is
+# reported by hack_debug_acc_form.  D comes from
+# oracle.homomm.int_blocks on the oracle's codes (QK) or on the GPU's own P codes with the
+# oracle's V codes (PV: P codes may differ from the oracle's at near-ties).
+
+def acc_expected(form, D, SA, SB, bits, Pi):
+    h = hk()
+    qkm = (1 << bits) - 1
+    D = np.asarray(D, np.int64)
+    if form == h.ACC_PLAIN:
+        return D
+    if form == h.ACC_S8_2B:                       # (a' - 128) x 2 b'
+        return 2 * D - 256 * np.asarray(SB, np.int64)
+    if form == h.ACC_CENTERED4:                   # 4 D - 2(2^b - 1) S_A + Pi 255 (2^b - 1)
+        return 4 * D - 2 * qkm * np.asarray(SA, np.int64) + Pi * 255 * qkm
+    raise AssertionError(f"no accumulator form {form}")
+
+
+def acc_buffers(rows, heads, ocfg, stride):
+    """Device int32 dump buffers: qk [rows, heads, d/Pi, stride], pv [rows, heads, stride/Pi, d]."""
+    qk = torch.full((rows, heads, ocfg.nbeta, stride), -7, dtype=torch.int32, device="cuda")
+    pv = torch.full((rows, heads, stride // ocfg.Pi, ocfg.d), -7, dtype=torch.int32, device="cuda")
+    return qk, pv
+
+
+def check_acc(form, ocfg, state, qc, qsum, pos, hq, got_qk, got_pv, gpu_pcodes):
+    """One query head hq (local index), query rows at positions `pos` (one row per entry):
+    got_qk [n, d/Pi, stride], got_pv [n, stride/Pi, d], gpu_pcodes [n, >= nfull*Pi].
+    QK: every key t <= pos; PV: every committed block j with j*Pi <= pos.  Bit-exact."""
+    from oracle import homomm
+    a = state.arrays()
+    Pi, b = ocfg.Pi, ocfg.bits
+    hkv = hq // ocfg.G
+    pos = np.asarray(pos)
+    L = a["kc"].shape[0]
+    D = homomm.int_blocks(qc[:, hq, :], a["kc"][:, hkv, :].T, Pi)           # [nb, n, L]
+    exp = acc_expected(form, D, qsum[:, hq, :].T[:, :, None], a["ksum"][:, hkv, :].T[:, None, :], b, Pi)
+    got = np.asarray(got_qk)[:, :, :L].transpose(1, 0, 2)
+    vis = np.arange(L)[None, :] <= pos[:, None]
+    bad = (got != exp) & vis[None]
+    assert not bad.any(), f"QK accumulator: {bad.sum()} of {vis.sum() * ocfg.nbeta} differ (first {np.argwhere(bad)[0]})"
+    nfull = a["vc"].shape[0]
+    nchk = 0
+    for j in range(nfull):
+        rows = pos >= j * Pi
+        if not rows.any():
+            continue
+        P = np.asarray(gpu_pcodes)[rows, j * Pi:(j + 1) * Pi]                # [n', Pi]
+        Dp = homomm.int_blocks(P, a["vc"][j, hkv].T, Pi)[0]                  # [n', d]
+        e = acc_expected(form, Dp, P.astype(np.int64).sum(1)[:, None], a["vsum"][j, hkv][None, :], b, Pi)
+        g = np.asarray(got_pv)[rows, j]
+        assert np.array_equal(g, e), f"PV accumulator block {j}: {(g != e).sum()} differ"
+        nchk += rows.sum()
+    return int(vis.sum()) * ocfg.nbeta, nchk * ocfg.d

@@ -43,7 +43,7 @@ def test_every_declared_symbol_is_exported(hk):
 
 
 def test_abi_version_and_default_config(hk):
-    assert hk.abi_version() == 1
+    assert hk.abi_version() == 2
     c = hk.config()
     assert (c.head_dim, c.partition, c.kv_bits, c.kv_round, c.q_round, c.p_round) == (128, 64, 2, 0, 0, 1)
     hk.config_validate(c)
@@ -114,3 +114,19 @@ def test_argument_errors_detected_before_launch(hk):
     assert st == hk.ERR_INVALID_ARG
     st = lib.hack_quantize_pack(ctypes.byref(c), hk.QMODE_V, 1, 65, 1, 0, 0, 0, 1, 1, 1, None)
     assert st == hk.ERR_SHAPE   # V rows must be a multiple of Pi
+
+
+def test_debug_acc_form_follows_dispatch(hk, monkeypatch):
+    """hack_debug_acc_form names the affine form of the accumulator dump of the kernel the
+    next call dispatches to (include/hack.h); host logic only, no GPU needed."""
+    c = hk.config(num_q_heads=4, num_kv_heads=1)
+    assert hk.debug_acc_form(c, "prefill") == hk.ACC_S8_2B          # prefill_tc (tcgen05)
+    assert hk.debug_acc_form(c, "decode") == hk.ACC_CENTERED4       # decode_pair (b = 2, Pi = 64)
+    assert hk.debug_acc_form(hk.config(num_q_heads=8, num_kv_heads=1), "decode") == hk.ACC_CENTERED4  # g8
+    assert hk.debug_acc_form(hk.config(kv_bits=4), "decode") == hk.ACC_PLAIN   # decode_mma
+    assert hk.debug_acc_form(hk.config(partition=32), "decode") == hk.ACC_PLAIN
+    assert hk.debug_acc_form(hk.config(num_q_heads=16, num_kv_heads=1), "decode") == hk.ACC_NONE  # simt
+    monkeypatch.setenv("HACK_DECODE_IMPL", "simt")
+    assert hk.debug_acc_form(c, "decode") == hk.ACC_NONE
+    monkeypatch.setenv("HACK_PREFILL_IMPL", "simt")
+    assert hk.debug_acc_form(c, "prefill") == hk.ACC_NONE

@@ -15,7 +15,7 @@ import hack_inputs
 from oracle import attention as att
 from oracle import pages as opages
 
-from .gpu_util import ROW_TOL, check_pcodes, gpu_cfg, hk, make_cache, row_rel_err
+from .gpu_util import ROW_TOL, acc_buffers, check_acc, check_pcodes, gpu_cfg, hk, make_cache, row_rel_err
 
 pytestmark = pytest.mark.gpu
 
@@ -63,18 +63,31 @@ def test_c4_long_prompt_one_kv_head(bits):
 
     qd, kd, vd = hack_inputs.decode_tokens(8, steps, 1, HQ, HKV)
     stride = (L + steps + 63) // 64 * 64
+    form = h.debug_acc_form(cfg, "decode")   # decode_g8_kernel (b = 2) / decode_mma_kernel (b = 4)
+    assert form != h.ACC_NONE
     for s in range(steps):
+        # production instantiation first, then the debug one (P codes + MMA accumulators)
         dout = torch.zeros((1, HQ, 128), dtype=torch.float32, device="cuda")
-        pc = torch.zeros((1, HQ, stride), dtype=torch.uint8, device="cuda")
         h.decode_attention(cfg, torch.from_numpy(qd[s]).cuda(), torch.from_numpy(kd[s]).cuda(),
-                           torch.from_numpy(vd[s]).cuda(), sl, L + steps, cache, dout, debug_pcodes=pc)
+                           torch.from_numpy(vd[s]).cuda(), sl, L + steps, cache, dout)
+        pc = torch.zeros((1, HQ, stride), dtype=torch.uint8, device="cuda")
+        qk, pv = acc_buffers(1, HQ, one, stride)
+        ddbg = torch.zeros_like(dout)
+        h.decode_attention_cached(cfg, torch.from_numpy(qd[s]).cuda(), sl, L + steps, cache, ddbg, debug_pcodes=pc,
+                                  debug_qk=qk, debug_pv=pv)
         torch.cuda.synchronize()
+        assert torch.equal(dout.view(torch.int32), ddbg.view(torch.int32)), "production and debug outputs differ"
         Od, diag = att.decode_step(state, qd[s, 0, heads], kd[s, 0, HSEL:HSEL + 1], vd[s, 0, HSEL:HSEL + 1],
                                    keep_diag=True)
         nf = state.nblocks * 64
         pcn = pc.cpu().numpy()[0, heads, :nf]
         for j in range(G):
             check_pcodes(pcn[j][None], diag[j]["pcodes"], diag[j]["py"])
+        pos = state.length - 1
+        qc, _, _, qsum = att.quantize_q(one, qd[s, 0, heads][None], np.array([pos]), rid)
+        qkn, pvn = qk.cpu().numpy()[0, heads], pv.cpu().numpy()[0, heads]
+        for j in range(G):
+            check_acc(form, one, state, qc, qsum, [pos], j, qkn[j][None], pvn[j][None], pcn[j][None])
         derr = row_rel_err(dout.cpu().numpy()[0, heads], Od).max()
         if derr > ROW_TOL:
             O2, _ = att.decode_attend(state, qd[s, 0, heads], pcodes_override={j: pcn[j][None] for j in range(G)})

@@ -10,7 +10,8 @@ import torch
 import hack_inputs
 from oracle import attention as att
 
-from .gpu_util import ROW_TOL, check_pcodes, compare_pages, gpu_cfg, hk, make_cache, row_rel_err
+from .gpu_util import (ROW_TOL, acc_buffers, check_acc, check_pcodes, compare_pages, gpu_cfg, hk, make_cache,
+                       row_rel_err)
 
 pytestmark = pytest.mark.gpu
 
@@ -23,6 +24,11 @@ def substituted_err(state, q, gpu_pcodes, O_gpu, Hq):
 
 
 def run_decode(ocfg, prompts, steps, seed=21, check_every=1, check_pages_at=()):
+    """Every step runs the PRODUCTION call (no debug pointers: even steps the combined
+    hack_decode_attention, odd steps hack_decode_append + hack_decode_attention_cached), then the
+    debug instantiation on the same cache (P codes + MMA accumulator dumps).  The two outputs
+    must be bit-identical; the production output is checked against the oracle; the dumped
+    accumulators bit-exactly through their affine form (acc_expected)."""
     h = hk()
     cfg = gpu_cfg(ocfg)
     B = len(prompts)
@@ -43,18 +49,31 @@ def run_decode(ocfg, prompts, steps, seed=21, check_every=1, check_pages_at=()):
         states.append(att.ingest_prompt(ocfg, k, v, rng_id=int(rid[i])))
     qd, kd, vd = hack_inputs.decode_tokens(seed, steps, B, ocfg.Hq, ocfg.Hkv)
     sl = torch.from_numpy(slots).cuda()
-    stride = (maxL + 63) // 64 * 64
-    worst, flips = 0.0, 0
+    stride = (maxL + ocfg.Pi - 1) // ocfg.Pi * ocfg.Pi
+    form = h.debug_acc_form(cfg, "decode")
+    worst, flips, nacc = 0.0, 0, 0
     for s in range(steps):
+        qs, ks, vs = (torch.from_numpy(x[s]).cuda() for x in (qd, kd, vd))
         out = torch.zeros((B, ocfg.Hq, 128), dtype=torch.float32, device="cuda")
+        if s % 2 == 0:
+            h.decode_attention(cfg, qs, ks, vs, sl, maxL, cache, out)
+        else:
+            h.decode_append(cfg, ks, vs, sl, cache)
+            h.decode_attention_cached(cfg, qs, sl, maxL, cache, out)
+        check = s % check_every == 0 or s == steps - 1
+        dout = torch.zeros_like(out)
         pc = torch.zeros((B, ocfg.Hq, stride), dtype=torch.uint8, device="cuda")
-        h.decode_attention(cfg, torch.from_numpy(qd[s]).cuda(), torch.from_numpy(kd[s]).cuda(),
-                           torch.from_numpy(vd[s]).cuda(), sl, maxL, cache, out, debug_pcodes=pc)
+        qk, pv = acc_buffers(B, ocfg.Hq, ocfg, stride) if check and form != h.ACC_NONE else (None, None)
+        h.decode_attention_cached(cfg, qs, sl, maxL, cache, dout, debug_pcodes=pc, debug_qk=qk, debug_pv=pv)
         torch.cuda.synchronize()
         og, pcn = out.cpu().numpy(), pc.cpu().numpy()
+        assert np.array_equal(og.view(np.uint32), dout.cpu().numpy().view(np.uint32)), \
+            f"step {s}: production and debug instantiations differ"
+        qkn = qk.cpu().numpy() if qk is not None else None
+        pvn = pv.cpu().numpy() if pv is not None else None
         for i in range(B):
             O, diag = att.decode_step(states[i], qd[s, i], kd[s, i], vd[s, i], keep_diag=True)
-            if s % check_every == 0 or s == steps - 1:
+            if check:
                 nf = states[i].nblocks * ocfg.Pi
                 for hq in range(ocfg.Hq):
                     if nf:
@@ -64,12 +83,22 @@ def run_decode(ocfg, prompts, steps, seed=21, check_every=1, check_pages_at=()):
                 if err > ROW_TOL and nf:
                     err = substituted_err(states[i], qd[s, i], pcn[i, :, :nf], og[i], ocfg.Hq)
                 assert err <= ROW_TOL, f"step {s} req {i}: row error {err:.3g}"
+                if qkn is not None:
+                    pos = states[i].length - 1
+                    qc, _, _, qsum = att.quantize_q(ocfg, qd[s, i][None], np.array([pos]), states[i].rng_id)
+                    for hq in range(ocfg.Hq):
+                        nq, npv = check_acc(form, ocfg, states[i], qc, qsum, [pos], hq, qkn[i, hq][None],
+                                            pvn[i, hq][None], pcn[i, hq][None])
+                        nacc += nq + npv
             assert int(cache.seq_lens[int(slots[i])]) == states[i].length
         if s in check_pages_at:
             for i in range(B):
                 compare_pages(cache, int(slots[i]), states[i])
     for i in range(B):
         compare_pages(cache, int(slots[i]), states[i])
+    if form != h.ACC_NONE:
+        assert nacc > 0
+    print(f"decode: worst row error {worst:.3g}, near-tie flips {flips}, accumulators checked {nacc}")
     return worst, flips
 
 
@@ -159,14 +188,23 @@ def test_c3_full_size_sampled_requests():
     qd, kd, vd = hack_inputs.decode_tokens(9, steps, B, ocfg.Hq, ocfg.Hkv)
     sl = torch.from_numpy(slots).cuda()
     stride = (maxL + 63) // 64 * 64
+    form = h.debug_acc_form(cfg, "decode")
+    assert form == h.ACC_CENTERED4          # the production decode_pair_kernel serves C3
     for s in range(steps):
         out = torch.zeros((B, ocfg.Hq, 128), dtype=torch.float32, device="cuda")
-        pc = torch.zeros((B, ocfg.Hq, stride), dtype=torch.uint8, device="cuda")
+        # production call first (no debug pointers), then the debug instantiation on the same cache
         h.decode_attention(cfg, torch.from_numpy(qd[s]).cuda(), torch.from_numpy(kd[s]).cuda(),
-                           torch.from_numpy(vd[s]).cuda(), sl, maxL, cache, out, debug_pcodes=pc)
+                           torch.from_numpy(vd[s]).cuda(), sl, maxL, cache, out)
+        dout = torch.zeros_like(out)
+        pc = torch.zeros((B, ocfg.Hq, stride), dtype=torch.uint8, device="cuda")
+        qk, pv = acc_buffers(B, ocfg.Hq, ocfg, stride)
+        h.decode_attention_cached(cfg, torch.from_numpy(qd[s]).cuda(), sl, maxL, cache, dout, debug_pcodes=pc,
+                                  debug_qk=qk, debug_pv=pv)
         torch.cuda.synchronize()
         og, pcn = out.cpu().numpy(), pc.cpu().numpy()
+        assert np.array_equal(og.view(np.uint32), dout.cpu().numpy().view(np.uint32))
         assert np.isfinite(og).all()
+        qkn, pvn = qk.cpu().numpy(), pv.cpu().numpy()
         for i in sampled:
             O, diag = att.decode_step(states[i], qd[s, i], kd[s, i], vd[s, i], keep_diag=True)
             nf = states[i].nblocks * ocfg.Pi
@@ -176,6 +214,11 @@ def test_c3_full_size_sampled_requests():
             if err > ROW_TOL:
                 err = substituted_err(states[i], qd[s, i], pcn[i, :, :nf], og[i], ocfg.Hq)
             assert err <= ROW_TOL, f"step {s} req {i}: row error {err:.3g}"
+            pos = states[i].length - 1
+            qc, _, _, qsum = att.quantize_q(ocfg, qd[s, i][None], np.array([pos]), states[i].rng_id)
+            for hq in range(ocfg.Hq):
+                check_acc(form, ocfg, states[i], qc, qsum, [pos], hq, qkn[i, hq][None], pvn[i, hq][None],
+                          pcn[i, hq][None])
     for i in sampled:
         compare_pages(cache, i, states[i])
 

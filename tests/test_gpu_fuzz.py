@@ -34,9 +34,9 @@ def draw(case):
 def test_random_prefill(case):
     ocfg, prompts, _ = draw(case)
     print(ocfg, prompts)
-    out, pc, cache, reqs, cu, slots, rid = run_prefill(ocfg, prompts, seed=100 + case)
+    res = run_prefill(ocfg, prompts, seed=100 + case)
     for i in range(len(prompts)):
-        check_request(ocfg, i, out, pc, cache, reqs, cu, slots, rid)
+        check_request(ocfg, i, *res)
 
 
 @pytest.mark.parametrize("case", range(24))

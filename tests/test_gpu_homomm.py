@@ -1,6 +1,9 @@
-"""GPU parity: hack_homomorphic_matmul (N9 test export: tcgen05 kind::i8 MMA core) vs the
-oracle.  Per-block int32 partials D_beta bit-exact; C = sum_beta Eq. 4 within 1e-3
-relative of the oracle's fp64 Eq. 4 and of dequantize-then-multiply."""
+"""GPU parity: hack_homomorphic_matmul (N9 test export: the prefill kernel's tcgen05 kind::i8
+configuration, s8 (a' - 128) x u8 (2 b')) vs the oracle.  Per-block int32 partials D_beta
+bit-exact at every Z (no CUDA-core fallback exists); C = sum_beta Eq. 4 per ELEMENT within
+1e-5 of sum_beta max|a_hat| sum|b_hat| (a bound of every term the fp32 epilogue adds) and
+per row within 1e-3
+(R18) of the oracle's fp64 Eq. 4 and of dequantize-then-multiply."""
 import numpy as np
 import pytest
 import torch
@@ -24,7 +27,8 @@ def make_operands(g, M, N, Z, Pi, bits):
 
 @pytest.mark.parametrize("M,N,Z,Pi,bits", [(128, 64, 128, 64, 2), (200, 100, 256, 64, 2), (77, 33, 128, 32, 2),
                                            (130, 70, 256, 128, 2), (128, 64, 512, 64, 4), (65, 129, 128, 32, 4),
-                                           (300, 200, 1024, 64, 2)])
+                                           (300, 200, 1024, 64, 2), (129, 65, 2048, 128, 4),
+                                           (64, 300, 4096, 32, 2)])
 def test_homomorphic_matmul_matches_oracle(M, N, Z, Pi, bits):
     h = hk()
     g = np.random.default_rng(M * 7 + N + Z + bits)
@@ -46,6 +50,13 @@ def test_homomorphic_matmul_matches_oracle(M, N, Z, Pi, bits):
     C_ref = homomm.homomorphic_matmul(ac, am, as_, bc.T, bm.T, bs.T, Pi)
     C_twin = homomm.dequant_matmul(ac, am, as_, bc.T, bm.T, bs.T, Pi)
     cg = c.cpu().numpy()
-    scale = np.abs(C_ref).max()
-    assert np.abs(cg - C_ref).max() <= 1e-3 * scale
-    assert np.abs(cg - C_twin).max() <= 1e-3 * scale
+    a_hat = np.repeat(as_, Pi, axis=1) * ac + np.repeat(am, Pi, axis=1)          # [M, Z]
+    b_hat = np.repeat(bs, Pi, axis=1) * bc + np.repeat(bm, Pi, axis=1)          # [N, Z]
+    # per-element scale bounding every Eq. 4 term: sum_beta max_z|a_hat| * sum_z |b_hat| over the block
+    amax = np.abs(a_hat).reshape(M, nb, Pi).max(-1)                             # [M, nb]
+    bsum = np.abs(b_hat).reshape(N, nb, Pi).sum(-1)                             # [N, nb]
+    mag = amax @ bsum.T
+    assert (np.abs(cg - C_ref) <= 1e-5 * mag + 1e-30).all()
+    for ref in (C_ref, C_twin):
+        row = np.abs(cg - ref).max(1) / np.maximum(np.abs(ref).max(1), 1e-6)
+        assert row.max() <= 1e-3

@@ -212,3 +212,76 @@ def test_kv_pull_cuda_ipc():
         pa, ta = request_bytes(c, 1, L)
         assert np.array_equal(pa, out["pages"][l])
         assert np.array_equal(ta.view(np.uint16), out["tails"][l].view(np.uint16))
+
+
+def _wire_header_spec(layers, Hkv, d, Pi, bits, prompt_len, first_token, rng_id, head_base, seed):
+    """The 64-byte header as include/hack.h documents it (S:350 fields), packed by the test
+    itself: magic "HACK", version 1, num_layers, H_kv, d, Pi, b, sum bytes, prompt_len,
+    tail_len, first_token, rng_id, page_bytes, head_base, payload_bytes, seed, 8 pad bytes."""
+    import struct
+    from oracle import pages as opages
+    lay = opages.layout(d, Pi, bits)
+    npages, T = (prompt_len + Pi - 1) // Pi, prompt_len % Pi
+    payload = layers * (npages * Hkv * lay["page_bytes"] + Hkv * T * d * 2)
+    return struct.pack("<IHHHHHBBIIiIIIQQ8x", 0x4B434148, 1, layers, Hkv, d, Pi, bits, lay["sum_bytes"], prompt_len,
+                       T, first_token, rng_id, lay["page_bytes"], head_base, payload, seed)
+
+
+def test_kv_pack_equals_oracle_wire_image():
+    """a10 against an image built without the GPU: the staging bytes of hack_kv_pack equal a
+    header packed from the documented field list, then per layer the oracle's packed pages
+    (oracle.pages; undefined bytes -- the partial last page's V section, padding -- masked)
+    and the oracle's FP16 tail rows (RQE)."""
+    from oracle import attention as att
+    from oracle import pages as opages
+    h, cfgs, src = setup(13)
+    slot, rid = 1, 4242
+    prefill_all(h, cfgs, src, slot=slot, rng_id=rid)
+    nbytes = h.kv_transfer_bytes(cfgs[0], LAYERS, L)
+    staging = torch.zeros(nbytes, dtype=torch.uint8, device="cuda")
+    h.kv_pack(cfgs[0], src, slot, L, first_token=31337, rng_id=rid, staging=staging)
+    got = staging.cpu().numpy()
+    hdr = _wire_header_spec(LAYERS, 2, 128, 64, 2, L, 31337, rid, 0, cfgs[0].seed)
+    assert bytes(got[:64]) == hdr
+    off = 64
+    for l in range(LAYERS):
+        _, k, v = hack_inputs.qkv(50 + l, L, 8, 2)
+        st = att.ingest_prompt(att.Config(Hq=8, Hkv=2, layer=l, seed=cfgs[0].seed), k, v, rng_id=rid)
+        ref, mask = opages.pack_request(st)                       # [npages, Hkv, page_bytes]
+        g = got[off:off + ref.size].reshape(ref.shape)
+        bad = (g != ref) & mask
+        assert not bad.any(), f"layer {l}: {bad.sum()} page bytes differ from the oracle image"
+        off += ref.size
+        tail = np.ascontiguousarray(st.arrays()["tail"].transpose(1, 0, 2)).view(np.uint8).reshape(-1)
+        assert np.array_equal(got[off:off + tail.size], tail), f"layer {l}: FP16 tail differs"
+        off += tail.size
+    assert off == nbytes
+
+
+def test_kv_transfer_rejects_foreign_streams():
+    """The header carries the cache's rng_id, seed and head_base: a caller rng_id that does
+    not match rng_ids[slot] poisons the header, and a receiver configured with another seed
+    or head_base (its appends would continue different Philox streams, R3) rejects it --
+    HACK_ERR_PROTOCOL on the device, cache untouched."""
+    h, cfgs, src = setup(14)
+    _, _, dst = setup(15)
+    prefill_all(h, cfgs, src, slot=0, rng_id=7)
+    nbytes = h.kv_transfer_bytes(cfgs[0], LAYERS, L)
+    before = dst[0].pages.clone()
+
+    def unpack_status(staging, cfg):
+        status = torch.zeros(2, dtype=torch.int32, device="cuda")
+        h.kv_unpack(cfg, dst, 0, L, staging, status=status)
+        torch.cuda.synchronize()
+        return int(status[0])
+
+    bad_rid = torch.zeros(nbytes, dtype=torch.uint8, device="cuda")
+    h.kv_pack(cfgs[0], src, 0, L, first_token=5, rng_id=8, staging=bad_rid)
+    assert unpack_status(bad_rid, cfgs[0]) == h.ERR_PROTOCOL
+    good = torch.zeros(nbytes, dtype=torch.uint8, device="cuda")
+    h.kv_pack(cfgs[0], src, 0, L, first_token=5, rng_id=7, staging=good)
+    for kw in (dict(seed=cfgs[0].seed + 1), dict(head_base=1)):
+        other = h.config(num_q_heads=8, num_kv_heads=2, out_fp32=True, **kw)
+        assert unpack_status(good, other) == h.ERR_PROTOCOL
+    assert torch.equal(before, dst[0].pages) and int(dst[0].seq_lens[0]) == 0
+    assert unpack_status(good, cfgs[0]) == h.OK

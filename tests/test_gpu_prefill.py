@@ -10,14 +10,19 @@ import torch
 import hack_inputs
 from oracle import attention as att
 
-from .gpu_util import ROW_TOL, check_pcodes, compare_pages, gpu_cfg, hk, make_cache, row_rel_err
+from .gpu_util import (ROW_TOL, acc_buffers, check_acc, check_pcodes, compare_pages, gpu_cfg, hk, make_cache,
+                       row_rel_err)
 
 pytestmark = pytest.mark.gpu
 
 
-def run_prefill(ocfg, prompts, dist="normal", seed=11, rng_ids=None, debug=True):
-    """prompts: list of lengths (one request each).  Returns GPU out [T,Hq,d],
-    pcodes, cache, and per-request inputs."""
+def run_prefill(ocfg, prompts, dist="normal", seed=11, rng_ids=None, debug=True, acc_head=-1):
+    """prompts: list of lengths (one request each).  Runs the PRODUCTION call
+    (hack_prefill_attention, no debug pointers), then -- with debug -- the debug
+    instantiation on the same cache (hack_prefill_attention_cached with P codes and MMA
+    accumulator dumps, all heads or only `acc_head`); the two outputs must be bit-identical.
+    Returns the production out [T,Hq,d], pcodes, cache, per-request inputs, cu, slots, rng
+    ids and the accumulator dumps (form, qk, pv) or None."""
     h = hk()
     cfg = gpu_cfg(ocfg)
     reqs = [hack_inputs.qkv(seed + i, L, ocfg.Hq, ocfg.Hkv, dist=dist, partition=ocfg.Pi, kv_bits=ocfg.bits)
@@ -32,24 +37,46 @@ def run_prefill(ocfg, prompts, dist="normal", seed=11, rng_ids=None, debug=True)
     rid = np.array(rng_ids if rng_ids is not None else [1000 + i for i in range(B)], np.uint32)
     cache.rng_ids[torch.from_numpy(slots).long()] = torch.from_numpy(rid.view(np.int32)).cuda()
     out = torch.zeros((q.shape[0], ocfg.Hq, 128), dtype=torch.float32, device="cuda")
-    stride = (maxL + 63) // 64 * 64
-    pc = torch.zeros((q.shape[0], ocfg.Hq, stride), dtype=torch.uint8, device="cuda") if debug else None
-    h.prefill_attention(cfg, torch.from_numpy(q).cuda(), torch.from_numpy(k).cuda(), torch.from_numpy(v).cuda(),
-                        torch.from_numpy(cu).cuda(), torch.from_numpy(slots).cuda(), maxL, cache, out,
-                        debug_pcodes=pc)
+    stride = (maxL + ocfg.Pi - 1) // ocfg.Pi * ocfg.Pi
+    qg, cug, slg = torch.from_numpy(q).cuda(), torch.from_numpy(cu).cuda(), torch.from_numpy(slots).cuda()
+    h.prefill_attention(cfg, qg, torch.from_numpy(k).cuda(), torch.from_numpy(v).cuda(), cug, slg, maxL, cache, out)
+    pc, acc = None, None
+    if debug:
+        pc = torch.zeros((q.shape[0], ocfg.Hq, stride), dtype=torch.uint8, device="cuda")
+        form = h.debug_acc_form(cfg, "prefill")
+        qk = pv = None
+        if form != h.ACC_NONE:
+            qk, pv = acc_buffers(q.shape[0], ocfg.Hq if acc_head < 0 else 1, ocfg, stride)
+        dout = torch.zeros_like(out)
+        h.prefill_attention_cached(cfg, qg, cug, slg, maxL, cache, dout, debug_pcodes=pc, debug_qk=qk,
+                                   debug_pv=pv, debug_head=acc_head)
+        torch.cuda.synchronize()
+        assert torch.equal(out.view(torch.int32), dout.view(torch.int32)), "production and debug outputs differ"
+        if qk is not None:
+            acc = (form, qk.cpu().numpy(), pv.cpu().numpy())
+        pc = pc.cpu().numpy()
     torch.cuda.synchronize()
-    return out.cpu().numpy(), (pc.cpu().numpy() if debug else None), cache, reqs, cu, slots, rid
+    return out.cpu().numpy(), pc, cache, reqs, cu, slots, rid, acc
 
 
-def check_request(ocfg, i, out, pc, cache, reqs, cu, slots, rid, rows=None, heads=None):
+def check_request(ocfg, i, out, pc, cache, reqs, cu, slots, rid, acc=None, rows=None, heads=None, acc_head=-1):
     """Parity protocol (DESIGN.md): pages bit-exact; every P-code mismatch a near-tie;
     plain row error <= 1e-3, else the oracle re-run with the GPU's P codes (which differ
-    from its own only at near-ties) must be within 1e-3."""
+    from its own only at near-ties) must be within 1e-3.  With `acc`, the kernel's QK / PV
+    accumulators of the checked rows (every head, or acc_head) are bit-exact."""
     q, k, v = reqs[i]
     O, state, diag = att.prefill(ocfg, q, k, v, rng_id=int(rid[i]), rows=rows, heads=heads, keep_diag=True)
     compare_pages(cache, int(slots[i]), state)
     assert int(cache.seq_lens[int(slots[i])]) == q.shape[0]
     rows = np.arange(q.shape[0]) if rows is None else np.asarray(rows)
+    if acc is not None:
+        form, qk, pv = acc
+        qc, _, _, qsum = att.quantize_q(ocfg, q[rows], rows, int(rid[i]))
+        for hq in (range(ocfg.Hq) if acc_head < 0 else [acc_head]):
+            hs = hq if acc_head < 0 else 0
+            nq, npv = check_acc(form, ocfg, state, qc, qsum, rows, hq, qk[cu[i] + rows, hs], pv[cu[i] + rows, hs],
+                                pc[cu[i] + rows, hq])
+        print(f"req {i}: accumulators bit-exact ({nq} QK + {npv} PV per head)")
     Og = out[cu[i]:cu[i + 1]]
     nfull = q.shape[0] // ocfg.Pi
     flips, worst_plain, override = 0, 0.0, {}
@@ -109,10 +136,10 @@ def test_c2_full_size_sampled_rows():
     """Mistral-7B shape (32 Q / 8 KV heads, 4K tokens) at BASELINE size: all page bytes
     bit-exact, sampled query rows of sampled heads within tolerance."""
     ocfg = att.Config(Hq=32, Hkv=8, Pi=64, bits=2)
-    res = run_prefill(ocfg, [4096], debug=True)
-    out, pc, cache, reqs, cu, slots, rid = res
+    res = run_prefill(ocfg, [4096], debug=True, acc_head=17)
+    out, pc, cache, reqs, cu, slots, rid, acc = res
     rows = np.array([0, 1, 63, 64, 777, 2048, 3000, 4031, 4095])
-    check_request(ocfg, 0, out, pc, cache, reqs, cu, slots, rid, rows=rows, heads=[0, 5, 17, 31])
+    check_request(ocfg, 0, out, pc, cache, reqs, cu, slots, rid, acc, rows=rows, heads=[0, 5, 17, 31], acc_head=17)
     assert np.isfinite(out).all()
 
 

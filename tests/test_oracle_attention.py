@@ -347,3 +347,50 @@ def test_pages_round_trip():
     vm = pg[1, 0, om:om + 512].view(np.float16).reshape(128, 2)
     assert np.array_equal(vm[:, 0].astype(np.float32), a["vm"][1, 0])
     assert not mk[2, 0, ov:ov + 16].any()        # partial page: V section undefined
+
+
+# ----------------------------------------------------------------- P-code substitution
+
+def test_pcodes_override_pins_the_near_tie_substitution():
+    """The near-tie protocol's step 3 re-runs the oracle with the GPU's P codes
+    (`pcodes_override`).  Pins: (1) substituting the oracle's own codes changes nothing;
+    (2) raising one code p'_{r,t} by 1 in committed block j changes exactly row r, by the
+    closed form s_p(r, j) * v_hat_t -- Eq. 4 with SP recomputed from the substituted codes
+    (sum_t (s_p p'_t + m_p)(s_v v'_t + m_v)); keeping the old SP would give
+    s_p s_v v'_t instead, an index mix-up would move another row or key; (3) the decode
+    entry point substitutes the same way."""
+    c = cfg(Hq=2, Hkv=1)
+    L = 150                                   # 2 committed V blocks + 22 FP16 tail tokens
+    q, k, v = hack_inputs.qkv(21, L, 2, 1)
+    O, st, diag = att.prefill(c, q, k, v, rng_id=9, keep_diag=True)
+    own = {hq: diag[hq]["pcodes"] for hq in diag}
+    O1, _, _ = att.prefill(c, q, k, v, rng_id=9, pcodes_override=own)
+    assert np.array_equal(O1, O)
+    hq, r, t = 1, 140, 70                     # key 70 lies in block j = 1, visible to row 140
+    j = t // c.Pi
+    P = diag[hq]["P"][r, j * c.Pi:(j + 1) * c.Pi]
+    s_p = (P.max() - P.min()) / 255.0
+    bumped = {h: own[h].copy() for h in own}
+    assert bumped[hq][r, t] < 255
+    bumped[hq][r, t] += 1
+    O2, _, _ = att.prefill(c, q, k, v, rng_id=9, pcodes_override=bumped)
+    dO = O2 - O
+    vh = v_hat(st, 0)[t]
+    assert np.allclose(dO[r, hq], s_p * vh, rtol=1e-9, atol=1e-14)
+    dO[r, hq] = 0
+    assert np.abs(dO).max() < 1e-15
+    a = st.arrays()
+    assert not np.allclose(s_p * vh, s_p * a["vs"][j, 0] * a["vc"][j, 0, :, t - j * c.Pi])   # the SP term matters
+    # decode: the last query row of a 150-token cache, same substitution
+    st2 = att.ingest_prompt(c, k, v, rng_id=9)
+    qn = hack_inputs.qkv(22, 1, 2, 1)[0][0]
+    Od, dg = att.decode_attend(st2, qn, keep_diag=True)
+    codes = {h: dg[h]["pcodes"].copy() for h in dg}
+    Od1, _ = att.decode_attend(st2, qn, pcodes_override=codes)
+    assert np.array_equal(Od1, Od)
+    Pd = dg[0]["P"][0, j * c.Pi:(j + 1) * c.Pi]
+    codes[0][0, t] = codes[0][0, t] + 1 if codes[0][0, t] < 255 else 254
+    sgn = 1 if dg[0]["pcodes"][0, t] < 255 else -1
+    Od2, _ = att.decode_attend(st2, qn, pcodes_override=codes)
+    assert np.allclose(Od2[0] - Od[0], sgn * (Pd.max() - Pd.min()) / 255.0 * v_hat(st2, 0)[t], rtol=1e-9, atol=1e-14)
+    assert np.array_equal(Od2[1], Od[1])
