@@ -76,7 +76,7 @@ struct TcSmem {
   alignas(128) float br[NB][BN * 24];     // rank-term B operand per key: m_k and y_k split 3 ways (kRankB)
   alignas(128) uint16_t pre_a[128 * 16];  // bf16 preset operands: A[:, 0] = 1, B[:, 0] = 1.5 * 2^23 (K-major,
   alignas(128) uint16_t pre_b[128 * 16];  //   SBO 256): one kind::f16 MMA writes the magic into D
-  alignas(16) float kcf[NB][2][3][BN];    // [buf][beta][field][key]: s_k, m_k, y_k
+  alignas(16) float kcf[NB][2][BN];       // [buf][beta][key]: s_k
   alignas(16) float vcf[NB][3][128];      // [buf][field][channel]: s_v, m_v, y_v
   float4 qconst[2][BM];                   // per (beta, row): cs s_q / 2, cs s_q SQ_s, cs mu_q
   int sp_part[NB][2][BM];                 // partial P-code sums (per S warpgroup)
@@ -354,7 +354,7 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_tc_kernel(
             c1 = m;
             c2 = fmaf(s2, (float)sum, PI * m);  // y_k = s_k SK + Pi m_k
           }
-          sm.kcf[bj][beta][0][key] = c0;
+          sm.kcf[bj][beta][key] = c0;
           float rv[12];
           rank_b(c1, rv);
           rank_b(c2, rv + 6);
@@ -429,27 +429,31 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_tc_kernel(
     {
       // (a3) quantize Q[i, 64 sw .. 64 sw + 63] (d-block beta = sw): 8-bit, fp32 meta, SR
       const uint4* qrow = reinterpret_cast<const uint4*>(q + ((int64_t)(start + i) * kc.Hq + hq) * 128 + 64 * sw);
-      float lo = INFINITY, hi = -INFINITY;
-#pragma unroll 1
-      for (int v8 = 0; v8 < 8; ++v8) {
-        const uint4 raw = qrow[v8];
-        const __half* hh = reinterpret_cast<const __half*>(&raw);
+      // all 8 loads of the 64-channel slice in flight at once (one memory latency per CTA,
+      // not eight), kept in registers for the quantization pass; min/max on packed halves
+      uint4 qr[8];
 #pragma unroll
-        for (int e = 0; e < 8; ++e) {
-          lo = fminf(lo, __half2float(hh[e]));
-          hi = fmaxf(hi, __half2float(hh[e]));
+      for (int v8 = 0; v8 < 8; ++v8) qr[v8] = __ldg(qrow + v8);
+      __half2 lo2 = *reinterpret_cast<const __half2*>(&qr[0].x), hi2 = lo2;
+#pragma unroll
+      for (int v8 = 0; v8 < 8; ++v8) {
+        const __half2* h2 = reinterpret_cast<const __half2*>(&qr[v8]);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          lo2 = __hmin2(lo2, h2[e]);
+          hi2 = __hmax2(hi2, h2[e]);
         }
       }
+      const float lo = fminf(__low2float(lo2), __high2float(lo2)), hi = fmaxf(__low2float(hi2), __high2float(hi2));
       const QMeta qm = meta_fp32(lo, hi, 255);
       const uint32_t c3 = stream_c3(kc.layer, kTagQ, kc.head_base * kc.G + hq);
       const uint32_t rng_id = cv.rng_ids[slot];
       int sum = 0;
-#pragma unroll 1
+#pragma unroll
       for (int g = 0; g < 4; ++g) {  // 16-channel groups
         float x[16];
-        const uint4 ra = qrow[2 * g], rb = qrow[2 * g + 1];
-        const __half* ha = reinterpret_cast<const __half*>(&ra);
-        const __half* hb = reinterpret_cast<const __half*>(&rb);
+        const __half* ha = reinterpret_cast<const __half*>(&qr[2 * g]);
+        const __half* hb = reinterpret_cast<const __half*>(&qr[2 * g + 1]);
 #pragma unroll
         for (int e = 0; e < 8; ++e) {
           x[e] = __half2float(ha[e]);
@@ -540,7 +544,7 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_tc_kernel(
 #pragma unroll
           for (int g4 = 0; g4 < 4; ++g4) {
             const int kl = kb + 16 * h + 4 * g4;  // first of 4 keys
-            const float4 sk4 = *reinterpret_cast<const float4*>(&sm.kcf[bj][beta][0][kl]);
+            const float4 sk4 = *reinterpret_cast<const float4*>(&sm.kcf[bj][beta][kl]);
 #pragma unroll
             for (int pr = 0; pr < 2; ++pr) {
               const int k2 = 4 * g4 + 2 * pr, ks = 16 * h + k2;
@@ -614,7 +618,12 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_tc_kernel(
         // y = (p - lo) / s rounded with the 1.5*2^23 magic number (y in [0, 255])
         const float plo = any_masked ? 0.f : ex2(mn - m_run);
         const float phi = ex2(mx - m_run);
-        QMeta pm = meta_fp32(plo, phi, 255);
+        // transient P meta (never stored; the codes only need to agree up to near-ties, DESIGN
+        // "Parity protocol"): multiply and a fast reciprocal instead of IEEE division
+        QMeta pm;
+        pm.m = plo;
+        pm.s = (phi - plo) * (1.f / 255.f);
+        pm.inv = __fdividef(255.f, phi - plo);
         if (!(pm.s > 1e-30f)) {
           pm.s = 0.f;
           pm.inv = 0.f;
