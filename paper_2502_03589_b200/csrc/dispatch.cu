@@ -16,6 +16,7 @@ cudaError_t launch_prefill_simt(const KernelCfg& kc, const void* q, const int32_
                                 int batch, int max_seqlen, const CacheView& cv, void* out,
                                 const hack_debug_t* dbg, cudaStream_t st);
 bool prefill_tc_supported(const KernelCfg& kc);
+
 cudaError_t launch_prefill_tc(const KernelCfg& kc, const void* q, const int32_t* cu, const int32_t* slots, int batch,
                               int max_seqlen, const CacheView& cv, void* out, const hack_debug_t* dbg,
                               cudaStream_t st);
@@ -52,8 +53,9 @@ cudaError_t launch_prefill_attention(const KernelCfg& kc, const void* q, const i
                                      const int32_t* slots, int batch, int max_seqlen, const CacheView& cv,
                                      void* out, void* workspace, const hack_debug_t* dbg, cudaStream_t st) {
   (void)workspace;
-  if (prefill_tc_supported(kc) && !env_is("HACK_PREFILL_IMPL", "simt"))
+  if (prefill_tc_supported(kc) && !env_is("HACK_PREFILL_IMPL", "simt")) {
     return launch_prefill_tc(kc, q, cu_seqlens, slots, batch, max_seqlen, cv, out, dbg, st);
+  }
   return launch_prefill_simt(kc, q, cu_seqlens, slots, batch, max_seqlen, cv, out, dbg, st);
 }
 

@@ -62,6 +62,13 @@ constexpr int NSW = 256;       // S-warpgroup threads
 constexpr int NOW = 256;       // O-warpgroup threads
 constexpr float kMagic = 12582912.f;           // 1.5 * 2^23 (P' rounding)
 constexpr float kRescaleTh = 8.f;             // lazy-rescale threshold (log2 units)
+#ifndef HACK_PRE_PBAR
+#define HACK_PRE_PBAR 1  // S -> O handoff of tile j on named barrier kPBar0 + j % NB (0: the mbarrier, polled)
+#endif
+// Named barriers: 0 = __syncthreads, 3..6 = the S warp pairs' row exchange, 7..9 = S -> O.
+// Generations of barrier kPBar0 + b alternate strictly: the S warps arrive for tile j only
+// after the O warps finished tile j - NB (o_done), which they synced on for tile j - NB.
+constexpr uint32_t kPBar0 = 7;
 
 template <int BITS>
 struct TcSmem {
@@ -98,13 +105,19 @@ struct TcSmem {
 // B = 1.5*2^23 e_0) before the kind::i8 MMAs accumulate onto them, so the float view of an
 // accumulated integer E (|E| < 2^22) is 1.5*2^23 + E and one FADD2 converts two exactly.
 #ifndef HACK_ABL
-#define HACK_ABL 0  // timing ablations only (scripts/ablate_pre.sh); results are wrong for != 0
+#define HACK_ABL 0  // timing ablations only, bit flags (1 O math, 2 P-quant math, 4 Eq. 4, 8 exp2); wrong results
 #endif
 // Waits per role: bit set in HACK_PRE_SLEEP -> that role waits with a suspend hint
 // (NANOSLEEP.SYNCS, wakes on the phase flip) instead of a polling loop that takes issue
 // slots from the epilogue warps.  Bits: 0 producer, 1 MMA issuer, 2 unpack, 3 S, 4 O.
 #ifndef HACK_PRE_SLEEP
 #define HACK_PRE_SLEEP 0
+#endif
+#ifndef HACK_PRE_SREG_S
+#define HACK_PRE_SREG_S "88"  // S-warpgroup registers (setmaxnreg)
+#endif
+#ifndef HACK_PRE_SREG_SVC
+#define HACK_PRE_SREG_SVC "40"  // service warps; 128 x 40 + 256 x 88 + 256 x 128 <= the launch's 96 x 640
 #endif
 template <int ROLE>
 HACK_DEV void rwait(uint64_t* bar, uint32_t parity) {
@@ -216,8 +229,8 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_tc_kernel(
 #endif
 
   if (warp < 4) {
-    // register budget (launch: 96 x 640): service 40, S 88, O 128 -> 9216 freed >= 8192 taken
-    asm volatile("setmaxnreg.dec.sync.aligned.u32 40;");
+    // register budget (launch: 96 x 640 = 61440): service 40, S HACK_PRE_SREG_S, O 128
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 " HACK_PRE_SREG_SVC ";");
     if (warp == 0) {
       // ---------------------------------------------------------------- producer
       if (lane == 0) {
@@ -325,7 +338,7 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_tc_kernel(
         rwait<2>(&sm.k_free[bj], ph ^ 1);
         const uint8_t* pg = sm.stage[s];
         const int nk = min(BN, L - j * BN);
-        {  // K' codes: thread = key; 8 consecutive keys fill one 128-byte core matrix per store
+        if (!(HACK_ABL & 16)) {  // K' codes: thread = key; 8 consecutive keys fill one 128-byte core matrix per store
           const int key = ut;
           const uint4* src = reinterpret_cast<const uint4*>(pg + PL.k_codes + key * (128 * BITS / 8));
 #pragma unroll
@@ -343,7 +356,7 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_tc_kernel(
           }
         }
 #pragma unroll
-        for (int beta = 0; beta < 2; ++beta) {  // per-(key, beta) Eq. 4 coefficients
+        for (int beta = 0; beta < 2 && !(HACK_ABL & 16); ++beta) {  // per-(key, beta) Eq. 4 coefficients
           const int key = ut, e = 2 * key + beta;
           float c0 = 0.f, c1 = 0.f, c2 = 0.f;
           if (key < nk) {
@@ -367,7 +380,7 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_tc_kernel(
         ptx::fence_proxy_async_smem();
         ptx::mbar_arrive(&sm.k_ready[bj]);
         rwait<2>(&sm.o_done[bj], ph ^ 1);  // O warps done with tile j - NB
-        if (j < nfull) {
+        if (j < nfull && !(HACK_ABL & 16)) {
 #if HACK_PRE_ORANK
           if (j > 0) rwait<2>(&sm.or_done, (j - 1) & 1);  // the single B operand buffer is free
 #endif
@@ -417,7 +430,7 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_tc_kernel(
   } else if (warp < 12) {
     // ------------------------------------------------------------------ S warpgroups (2)
     // thread = query row r = TMEM lane; SW s owns keys 32s..32s+31 of every tile
-    asm volatile("setmaxnreg.dec.sync.aligned.u32 88;");
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 " HACK_PRE_SREG_S ";");
     const int sw = (warp - 4) >> 2;
     const int r = (tid - 128) & (BM - 1);
     const int pos = i0 + (r & (pbp - 1)), hq = hq0 + r / pbp;  // this row's position and head
@@ -525,7 +538,7 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_tc_kernel(
         for (int x = 0; x < 16; ++x) s[16 * h + x] = __uint_as_float(d[x]);
       }
 #pragma unroll
-      for (int beta = 0; beta < 2 && HACK_ABL != 3; ++beta) {
+      for (int beta = 0; beta < 2 && !(HACK_ABL & 4); ++beta) {
         const float2 A = beta ? qa1 : qa0;
 #pragma unroll
         for (int h = 0; h < 2; ++h) {  // 16 keys per TMEM load (register pressure)
@@ -601,7 +614,7 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_tc_kernel(
 #pragma unroll
       for (int kk = 0; kk < 32; kk += 2) {
         const float2 a2 = ptx::fadd2(make_float2(s[kk], s[kk + 1]), mneg);
-#if HACK_ABL == 4
+#if (HACK_ABL & 8)
         s[kk] = a2.x;
         s[kk + 1] = a2.y;
 #else
@@ -634,7 +647,7 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_tc_kernel(
 #pragma unroll
         for (int c16 = 0; c16 < 2; ++c16) {
           uint32_t bits[16];
-#if HACK_ABL == 2
+#if (HACK_ABL & 2)
 #pragma unroll
           for (int kk = 0; kk < 16; ++kk) bits[kk] = __float_as_uint(s[16 * c16 + kk]);
           if (false)
@@ -674,7 +687,10 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_tc_kernel(
         for (int kk = 0; kk < 32; ++kk) sm.ptail[r][kb + kk] = s[kk];
         if (sw == 0) sm.pinfo[bj][r] = make_float4(al, resc ? 1.f : 0.f, 0.f, 0.f);
       }
-      ptx::mbar_arrive(&sm.p_ready[bj]);
+      ptx::mbar_arrive(&sm.p_ready[bj]);  // for the MMA warp (PV)
+#if HACK_PRE_PBAR
+      ptx::named_bar_arrive(kPBar0 + bj, NSW + NOW);  // for the O warps (hardware barrier: no polling)
+#endif
     }
     sm.lpart[sw][r] = l_run;
     ptx::mbar_arrive(&sm.l_ready);
@@ -694,7 +710,12 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_tc_kernel(
     for (int j = 0; j < nkt; ++j) {
       const int bj = j % NB, bd = j % NDB;
       const uint32_t ph = (j / NB) & 1;
+#if HACK_PRE_PBAR
+      ptx::named_bar_sync(kPBar0 + bj, NSW + NOW);  // S warps' P' and row info of tile j
+      (void)ph;
+#else
       rwait<4>(&sm.p_ready[bj], ph);
+#endif
       const float4 pi4 = sm.pinfo[bj][r];
       if (pi4.y != 0.f) {  // warp-uniform (lazy rescaling decided per S warp = same 32 rows)
         const float2 al2 = make_float2(pi4.x, pi4.x);
@@ -761,7 +782,7 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_tc_kernel(
 #pragma unroll
             for (int x = 0; x < 16; ++x) dp[x] = (int32_t)(d[x] - 0x4B400000u);
           }
-#if HACK_ABL == 1
+#if (HACK_ABL & 1)
           if (d[0] == 0x12345u) o2[h].x += 1.f;  // (ablation: no PV Eq. 4 math)
 #else
 #pragma unroll

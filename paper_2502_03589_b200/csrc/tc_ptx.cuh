@@ -78,6 +78,11 @@ HACK_DEV void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared:
 HACK_DEV void named_bar_sync(uint32_t id, uint32_t nthreads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
+// producer side of a named-barrier handoff: no wait; the consumers' bar.sync blocks (no issue
+// slots spent polling) until every producer thread arrived
+HACK_DEV void named_bar_arrive(uint32_t id, uint32_t nthreads) {
+  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
 HACK_DEV void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 HACK_DEV void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 
