@@ -76,7 +76,9 @@ typedef struct {
   int32_t kv_bits;       /* b for K/V codes: 2 or 4; Q and P are fixed at 8 */
   int32_t kv_round;      /* hack_round_t for K/V codes (default STOCHASTIC) */
   int32_t q_round;       /* hack_round_t for Q codes (default STOCHASTIC, R6) */
-  int32_t p_round;       /* must be NEAREST_EVEN (R6) */
+  int32_t p_round;       /* hack_round_t for P codes: NEAREST_EVEN (default, R6) or STOCHASTIC (the paper's
+                            P:575-578 rounding; prefill at Pi = 64 and decode with G <= 8, else
+                            HACK_ERR_UNSUPPORTED at the attention call) */
   uint64_t seed;         /* Philox4x32-10 key (R3) */
   int32_t layer;         /* layer index folded into the Philox counter (R3) */
   int32_t head_base;     /* global index of local KV head 0 (head sharding keeps codes identical, SURVEY e) */
@@ -146,7 +148,7 @@ typedef enum {
 int32_t hack_debug_acc_form(const hack_config_t* cfg, int32_t op);
 
 /* ---- configuration and layout ------------------------------------------ */
-void hack_config_default(hack_config_t* cfg);          /* H=1/1, d=128, Pi=64, b=2, SR/SR/RN, fp16 out */
+void hack_config_default(hack_config_t* cfg);          /* H=1/1, d=128, Pi=64, b=2, SR/SR/RN (K-V/Q/P), fp16 out */
 hack_status_t hack_config_validate(const hack_config_t* cfg);
 int64_t hack_page_bytes(const hack_config_t* cfg);     /* 5376 at (d=128, Pi=64, b=2); -1 if invalid */
 /* offsets_out[12] = {off, size} x {K_CODES, K_META, K_SUMS, V_CODES, V_META, V_SUMS} (bytes) */

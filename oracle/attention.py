@@ -41,7 +41,7 @@ class Config:
     layer: int = 0
     kv_round: str = "sr"
     q_round: str = "sr"
-    p_round: str = "rn"         # reading R6
+    p_round: str = "rn"         # reading R6 ("sr": the paper's stochastic rounding, selectable)
     head_base: int = 0          # global index of local KV head 0 (sharding)
 
     @property
@@ -107,11 +107,13 @@ def quantize_v_block(cfg: Config, v_blk: np.ndarray, start: int, rng_id: int):
     return quant.quantize(x, cfg.bits, "fp16", cfg.kv_round, u)
 
 
-def quantize_p(p_blk: np.ndarray, rnd: str = "rn"):
+def quantize_p(p_blk: np.ndarray, rnd: str = "rn", u: np.ndarray | None = None):
     """P partition = one row's Pi keys of one V block, 8-bit,
     transient fp64 meta.  Masked entries are exact zeros inside the partition
-    (R8).  Returns codes, m, s, sums, y (pre-rounding value, for the near-tie
-    parity protocol)."""
+    (R8).  rnd: 'rn' round-to-nearest-even (the default reading R6) or 'sr' the
+    paper's stochastic rounding (R1: floor(y) + [u < frac(y)]) with
+    uniforms u of p_blk's shape.  Returns codes, m, s, sums, y (pre-rounding value,
+    for the near-tie parity protocol)."""
     p = np.asarray(p_blk, np.float64)
     lo = p.min(-1)
     hi = p.max(-1)
@@ -119,9 +121,16 @@ def quantize_p(p_blk: np.ndarray, rnd: str = "rn"):
     with np.errstate(divide="ignore", invalid="ignore"):
         y = (p - lo[..., None]) / s[..., None]
     y = np.where((s == 0)[..., None], 0.0, y)
-    if rnd != "rn":
-        raise NotImplementedError("P uses round-to-nearest-even (reading R6)")
-    c = np.clip(np.rint(y), 0, 255).astype(np.uint8)
+    if rnd == "rn":
+        c = np.rint(y)
+    elif rnd == "sr":
+        if u is None or np.shape(u) != p.shape:
+            raise ValueError("stochastic rounding of P needs u with the partition's shape")
+        fl = np.floor(y)
+        c = fl + (np.asarray(u, np.float64) < (y - fl))
+    else:
+        raise ValueError(rnd)
+    c = np.clip(c, 0, 255).astype(np.uint8)
     return c, lo, s, c.astype(np.int64).sum(-1), y
 
 
@@ -199,7 +208,7 @@ def ingest_prompt(cfg: Config, k: np.ndarray, v: np.ndarray, rng_id: int = 0) ->
 
 # ---------------------------------------------------------------- attention core
 
-def _attend(cfg: Config, st: dict, qc, qm, qs, qsum, pos, hq, pcodes_override=None):
+def _attend(cfg: Config, st: dict, qc, qm, qs, qsum, pos, hq, pcodes_override=None, rng_id: int = 0):
     """Rows of one query head hq against the state's keys 0..L-1, each row i
     seeing keys t <= pos[i].  Returns O [n, d] fp64 and diagnostics."""
     d, Pi, nb = cfg.d, cfg.Pi, cfg.nbeta
@@ -231,9 +240,12 @@ def _attend(cfg: Config, st: dict, qc, qm, qs, qsum, pos, hq, pcodes_override=No
     nfull = st["vc"].shape[0]
     py = np.zeros((n, nfull * Pi))
     pcodes = np.zeros((n, nfull * Pi), np.uint8)
+    pu = None
+    if cfg.p_round == "sr" and nfull:   # position-keyed P stream of this query head (R3)
+        pu = philox.uniforms_p(cfg.seed, rng_id, cfg.layer, cfg.head_base * cfg.G + hq, pos, np.arange(nfull * Pi))
     for j in range(nfull):
         sl = slice(j * Pi, (j + 1) * Pi)
-        c, m_p, s_p, SP, y = quantize_p(P[:, sl], cfg.p_round)
+        c, m_p, s_p, SP, y = quantize_p(P[:, sl], cfg.p_round, None if pu is None else pu[:, sl])
         if pcodes_override is not None:
             c = np.asarray(pcodes_override[:, sl], np.uint8)
             SP = c.astype(np.int64).sum(-1)
@@ -250,7 +262,7 @@ def _attend(cfg: Config, st: dict, qc, qm, qs, qsum, pos, hq, pcodes_override=No
     T = L - nfull * Pi
     if T:
         O += P[:, nfull * Pi:] @ st["tail"][:T, hk, :].astype(np.float64)
-    return O, dict(P=P, pcodes=pcodes, py=py)
+    return O, dict(P=P, pcodes=pcodes, py=py, pu=pu)
 
 
 def prefill(cfg: Config, q: np.ndarray, k: np.ndarray, v: np.ndarray, rng_id: int = 0,
@@ -269,7 +281,7 @@ def prefill(cfg: Config, q: np.ndarray, k: np.ndarray, v: np.ndarray, rng_id: in
     diag = {}
     for hq in heads:
         ov = None if pcodes_override is None else pcodes_override[hq]
-        o, dg = _attend(cfg, st, qc[:, hq], qm[:, hq], qs[:, hq], qsum[:, hq], rows, hq, ov)
+        o, dg = _attend(cfg, st, qc[:, hq], qm[:, hq], qs[:, hq], qsum[:, hq], rows, hq, ov, rng_id)
         O[rows, hq] = o
         if keep_diag:
             diag[hq] = dg
@@ -299,7 +311,7 @@ def decode_attend(state: KVState, q_new: np.ndarray, pcodes_override=None, keep_
     diag = {}
     for hq in range(cfg.Hq):
         ov = None if pcodes_override is None else pcodes_override.get(hq)
-        o, dg = _attend(cfg, st, qc[:, hq], qm[:, hq], qs[:, hq], qsum[:, hq], [pos], hq, ov)
+        o, dg = _attend(cfg, st, qc[:, hq], qm[:, hq], qs[:, hq], qsum[:, hq], [pos], hq, ov, state.rng_id)
         O[hq] = o[0]
         if keep_diag:
             diag[hq] = dg

@@ -14,6 +14,8 @@ shape, sharding, or on whether a token was quantized by prefill or decode:
 with tag Q=0, K=1, V=2, P=3 and, for an element at position t, channel c:
     K, Q : n = (t*d + c) >> 2,   w = c & 3      (4 consecutive channels / call)
     V    : n = (t >> 2)*d + c,   w = t & 3      (4 consecutive tokens / call)
+    P    : n = (i << 30) | (t >> 2), w = t & 3  (query position i, key position t < 2^32;
+                                                4 consecutive keys / call; head = query head)
 """
 from __future__ import annotations
 
@@ -87,3 +89,14 @@ def uniforms_colwise(seed, rng_id, layer, head, positions, d) -> np.ndarray:
     c = np.arange(d, dtype=np.uint64)[None, :]
     n = (t >> np.uint64(2)) * np.uint64(d) + c
     return uniforms(seed, rng_id, layer, TAG_V, head, n, (t & np.uint64(3)).astype(np.int64))
+
+
+def uniforms_p(seed, rng_id, layer, head, qpos, keys) -> np.ndarray:
+    """P stream (stochastic rounding of P, reading R6's selectable mode): u[r, t] for query
+    rows at positions `qpos` (1-D) and key positions `keys` (1-D); `head` = the global
+    query head.  Position-keyed like K/Q/V, so codes do not depend on tiling or on whether
+    a row is a prefill row or a decode step."""
+    i = np.asarray(qpos, dtype=np.uint64)[:, None]
+    t = np.asarray(keys, dtype=np.uint64)[None, :]
+    n = (i << np.uint64(30)) | (t >> np.uint64(2))
+    return uniforms(seed, rng_id, layer, TAG_P, head, n, (t & np.uint64(3)).astype(np.int64))

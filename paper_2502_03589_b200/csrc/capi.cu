@@ -122,7 +122,8 @@ hack_status_t hack_config_validate(const hack_config_t* c) {
   if (c->head_dim % c->partition) return fail(HACK_ERR_UNSUPPORTED, "head_dim %% partition != 0");
   if ((c->kv_round != 0 && c->kv_round != 1) || (c->q_round != 0 && c->q_round != 1))
     return fail(HACK_ERR_INVALID_ARG, "bad rounding mode");
-  if (c->p_round != HACK_ROUND_NEAREST_EVEN) return fail(HACK_ERR_UNSUPPORTED, "P rounding must be NEAREST_EVEN (R6)");
+  if (c->p_round != HACK_ROUND_NEAREST_EVEN && c->p_round != HACK_ROUND_STOCHASTIC)
+    return fail(HACK_ERR_INVALID_ARG, "bad P rounding mode");
   if (c->out_dtype != 0 && c->out_dtype != 1) return fail(HACK_ERR_INVALID_ARG, "out_dtype must be 0 or 1");
   if (c->layer < 0 || c->layer > 0xFFFF || c->head_base < 0 || c->head_base > 0xFFF)
     return fail(HACK_ERR_INVALID_ARG, "layer/head_base out of counter range");
@@ -213,6 +214,8 @@ hack_status_t check_prefill(const KernelCfg& kc, const hack_kv_cache_t* cache, c
     return fail(HACK_ERR_CAPACITY, "prefill: max_seqlen needs more pages than max_pages_per_req");
   const size_t need = prefill_workspace_bytes(kc, batch, max_seqlen);
   if (ws_bytes < need || (need && !ws)) return fail(HACK_ERR_CAPACITY, "prefill: workspace %zu < %zu", ws_bytes, need);
+  if (kc.p_round == HACK_ROUND_STOCHASTIC && !p_sr_supported(kc, 0))
+    return fail(HACK_ERR_UNSUPPORTED, "prefill: P stochastic rounding needs the tcgen05 kernel (Pi = 64)");
   return check_debug(kc, dbg, max_seqlen, 0, "prefill");
 }
 
@@ -233,6 +236,8 @@ hack_status_t check_decode(const KernelCfg& kc, const hack_kv_cache_t* cache, co
     return fail(HACK_ERR_CAPACITY, "decode: max_seqlen needs more pages than max_pages_per_req");
   const size_t need = decode_workspace_bytes(kc, batch, max_seqlen);
   if (ws_bytes < need || (need && !ws)) return fail(HACK_ERR_CAPACITY, "decode: workspace %zu < %zu", ws_bytes, need);
+  if (kc.p_round == HACK_ROUND_STOCHASTIC && !p_sr_supported(kc, 1))
+    return fail(HACK_ERR_UNSUPPORTED, "decode: P stochastic rounding needs decode_mma_kernel (G <= 8)");
   return check_debug(kc, dbg, max_seqlen, 1, "decode");
 }
 

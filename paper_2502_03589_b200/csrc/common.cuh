@@ -57,6 +57,19 @@ HACK_DEV uint32_t pick(const Philox4& p, int w) {
   return w == 0 ? p.x : (w == 1 ? p.y : (w == 2 ? p.z : p.w));
 }
 
+// P stream (stochastic rounding of P, R6 selectable): the uniform of element (query
+// position i, key position t) of global query head `ghead`; Philox block n = (i << 30) |
+// (t >> 2), word t & 3 (oracle/philox.py uniforms_p).
+HACK_DEV float p_uniform(uint64_t seed, uint32_t rng_id, int layer, int ghead, int64_t i, int t) {
+  const Philox4 r = philox_block(seed, rng_id, stream_c3(layer, kTagP, ghead), ((uint64_t)i << 30) | (uint64_t)(t >> 2));
+  return u24(pick(r, t & 3));
+}
+// SR of one P value y = (p - lo) / s (R1): floor(y) + [u < frac(y)], clamped to 255.
+HACK_DEV uint32_t p_code_sr(float y, float u) {
+  const float fl = floorf(y);
+  return (uint32_t)min(255, max(0, (int)fl + (u < y - fl ? 1 : 0)));
+}
+
 // ---------------------------------------------------------------- quantizer
 // Partition meta: K/V store fp16 (m, s) and compute codes against the stored
 // values (R4); Q/P keep fp32 meta.  scale = fp32(fp32(hi - lo) / (2^b - 1)).

@@ -372,8 +372,17 @@ __global__ void __launch_bounds__(kThreads, dmma_ctas<BITS, PI_>()) decode_mma_k
 #pragma unroll
           for (int hh = 0; hh < 2; ++hh) {
             const int t = 16 * mt + g + 8 * hh;
-            const float2 y = ptx::fadd2(ptx::ffma2(sv2[mt][hh], inv2, nlo2), make_float2(12582912.f, 12582912.f));
-            const uint32_t c0 = __float_as_uint(y.x) & 0xFFu, c1 = __float_as_uint(y.y) & 0xFFu;
+            uint32_t c0, c1;
+            if (kc.p_round == HACK_ROUND_NEAREST_EVEN) {
+              const float2 y = ptx::fadd2(ptx::ffma2(sv2[mt][hh], inv2, nlo2), make_float2(12582912.f, 12582912.f));
+              c0 = __float_as_uint(y.x) & 0xFFu;
+              c1 = __float_as_uint(y.y) & 0xFFu;
+            } else {  // the paper's stochastic rounding of P (R6, selectable)
+              const float2 y = ptx::ffma2(sv2[mt][hh], inv2, nlo2);
+              const int ta = jp * PI + t, gh = (kc.head_base * G + hk * G);
+              c0 = n0 < G ? p_code_sr(y.x, p_uniform(kc.seed, rng_id, kc.layer, gh + n0, pos, ta)) : 0u;
+              c1 = n1 < G ? p_code_sr(y.y, p_uniform(kc.seed, rng_id, kc.layer, gh + n1, pos, ta)) : 0u;
+            }
             sp0 += c0;
             sp1 += c1;
             // B-fragment position of token t: t' = t mod 16 = 4i + tig' -> 4 tig' + i (b=2)

@@ -64,7 +64,14 @@ static bool use_decode_mma(const KernelCfg& kc) {
 }
 
 static bool use_decode_pair(const KernelCfg& kc) {
-  return decode_pair_supported(kc) && !env_is("HACK_DECODE_IMPL", "simt") && !env_is("HACK_DECODE_IMPL", "mma");
+  // P stochastic rounding (R6, selectable) runs on decode_mma_kernel
+  return decode_pair_supported(kc) && kc.p_round == HACK_ROUND_NEAREST_EVEN && !env_is("HACK_DECODE_IMPL", "simt") &&
+         !env_is("HACK_DECODE_IMPL", "mma");
+}
+
+bool p_sr_supported(const KernelCfg& kc, int op) {
+  if (op == 0) return prefill_tc_supported(kc) && !env_is("HACK_PREFILL_IMPL", "simt");
+  return use_decode_mma(kc);
 }
 
 int debug_acc_form(const KernelCfg& kc, int op) {

@@ -48,6 +48,8 @@ cudaError_t launch_prefill_attention(const KernelCfg& kc, const void* q, const i
 size_t decode_workspace_bytes(const KernelCfg& kc, int batch, int max_seqlen);
 // hack_acc_form_t of the kernel the next prefill (op 0) / decode (op 1) call dispatches to
 int debug_acc_form(const KernelCfg& kc, int op);
+// whether the kernel serving op (0 prefill, 1 decode) implements P stochastic rounding
+bool p_sr_supported(const KernelCfg& kc, int op);
 cudaError_t launch_decode_attention(const KernelCfg& kc, const void* q_new, const int32_t* slots, int batch,
                                     int max_seqlen, const CacheView& cv, void* out, void* workspace,
                                     const hack_debug_t* dbg, cudaStream_t st);

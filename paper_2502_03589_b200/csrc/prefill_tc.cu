@@ -158,7 +158,8 @@ __host__ __device__ __forceinline__ int pack_heads(const KernelCfg& kc) {
 
 // DBG: parity runs only (hack_debug_t): dumps the P codes and the raw QK / PV block
 // accumulators E = 2 D - 256 S_B (HACK_ACC_S8_2B); the production instantiation has none of it.
-template <int BITS, bool DBG>
+// PSR: P codes by the paper's stochastic rounding (R6, selectable) instead of RN.
+template <int BITS, bool DBG, bool PSR>
 __global__ void __launch_bounds__(kThreads, 1) prefill_tc_kernel(
     const __half* __restrict__ q, const int32_t* __restrict__ cu_seqlens, const int32_t* __restrict__ slots,
     CacheView cv, KernelCfg kc, void* __restrict__ out, uint8_t* __restrict__ dbg_pcodes, int64_t dbg_stride,
@@ -652,12 +653,31 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_tc_kernel(
           for (int kk = 0; kk < 16; ++kk) bits[kk] = __float_as_uint(s[16 * c16 + kk]);
           if (false)
 #endif
+          if (!PSR) {
 #pragma unroll
-          for (int kk = 0; kk < 16; kk += 2) {
-            const float2 y =
-                ptx::fadd2(ptx::ffma2(make_float2(s[16 * c16 + kk], s[16 * c16 + kk + 1]), inv2, nlo2), magic);
-            bits[kk] = __float_as_uint(y.x);
-            bits[kk + 1] = __float_as_uint(y.y);
+            for (int kk = 0; kk < 16; kk += 2) {
+              const float2 y =
+                  ptx::fadd2(ptx::ffma2(make_float2(s[16 * c16 + kk], s[16 * c16 + kk + 1]), inv2, nlo2), magic);
+              bits[kk] = __float_as_uint(y.x);
+              bits[kk + 1] = __float_as_uint(y.y);
+            }
+          } else {
+            // the paper's stochastic rounding for P (R6, selectable): floor(y) + [u < frac(y)],
+            // u from the position-keyed P stream (query position i, key t, global query head)
+            const uint32_t c3 = stream_c3(kc.layer, kTagP, kc.head_base * kc.G + hq);
+            const uint32_t rid = cv.rng_ids[slot];
+#pragma unroll
+            for (int k4 = 0; k4 < 16; k4 += 4) {
+              const int t = t0 + kb + 16 * c16 + k4;
+              const Philox4 rr = philox_block(kc.seed, rid, c3, ((uint64_t)i << 30) | (uint64_t)(t >> 2));
+              const float u4[4] = {u24(rr.x), u24(rr.y), u24(rr.z), u24(rr.w)};
+#pragma unroll
+              for (int e = 0; e < 4; ++e) {
+                const float y = fmaf(s[16 * c16 + k4 + e], pm.inv, nlo2.x);
+                const float fl = floorf(y);
+                bits[k4 + e] = (uint32_t)min(255, (int)fl + (u4[e] < y - fl ? 1 : 0));
+              }
+            }
           }
           uint32_t cw[4];
 #pragma unroll
@@ -884,7 +904,9 @@ cudaError_t launch_t(const KernelCfg& kc, const void* q, const int32_t* cu, cons
                      int max_seqlen, const CacheView& cv, void* out, const hack_debug_t* dbg, cudaStream_t st) {
   const size_t smem = sizeof(TcSmem<BITS>) + 1024;
   const bool with_dbg = dbg != nullptr && (dbg->pcodes != nullptr || dbg->qk_acc != nullptr || dbg->pv_acc != nullptr);
-  auto kern = with_dbg ? prefill_tc_kernel<BITS, true> : prefill_tc_kernel<BITS, false>;
+  const bool psr = kc.p_round == HACK_ROUND_STOCHASTIC;
+  auto kern = with_dbg ? (psr ? prefill_tc_kernel<BITS, true, true> : prefill_tc_kernel<BITS, true, false>)
+                       : (psr ? prefill_tc_kernel<BITS, false, true> : prefill_tc_kernel<BITS, false, false>);
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   const int gp = pack_heads(kc);

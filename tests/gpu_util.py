@@ -21,6 +21,7 @@ def gpu_cfg(ocfg: att.Config, out_fp32=True):
     h = hk()
     return h.config(num_q_heads=ocfg.Hq, num_kv_heads=ocfg.Hkv, partition=ocfg.Pi, kv_bits=ocfg.bits,
                     kv_round=0 if ocfg.kv_round == "sr" else 1, q_round=0 if ocfg.q_round == "sr" else 1,
+                    p_round=0 if ocfg.p_round == "sr" else 1,
                     seed=ocfg.seed, layer=ocfg.layer, head_base=ocfg.head_base, out_fp32=out_fp32)
 
 
@@ -31,13 +32,18 @@ def row_rel_err(O_gpu: np.ndarray, O_ref: np.ndarray) -> np.ndarray:
     return num / den
 
 
-def check_pcodes(gpu_codes: np.ndarray, ora_codes: np.ndarray, ora_y: np.ndarray):
-    """Every P-code mismatch must be a near-tie of the oracle's fp64 y (RN boundary
-    k + 1/2) and off by one.  Returns the number of mismatches."""
+def check_pcodes(gpu_codes: np.ndarray, ora_codes: np.ndarray, ora_y: np.ndarray, ora_u: np.ndarray | None = None):
+    """Every P-code mismatch must be a near-tie of the oracle's fp64 y and off by one: the
+    RN boundary is k + 1/2; under stochastic rounding (ora_u given) c = ceil(y - u), so the
+    boundary is y - u integer.  Returns the number of mismatches."""
     mism = gpu_codes != ora_codes
     if mism.any():
         y = ora_y[mism]
-        dist = np.abs(y - (np.floor(y) + 0.5))
+        if ora_u is None:
+            dist = np.abs(y - (np.floor(y) + 0.5))
+        else:
+            z = y - np.asarray(ora_u, np.float64)[mism]
+            dist = np.abs(z - np.rint(z))
         bad = (dist >= NEAR_TIE) | (np.abs(gpu_codes[mism].astype(int) - ora_codes[mism].astype(int)) > 1)
         assert not bad.any(), f"{bad.sum()} non-near-tie P-code mismatches (max dist {dist.max():.3g})"
     return int(mism.sum())

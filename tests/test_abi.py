@@ -56,7 +56,7 @@ def test_abi_version_and_default_config(hk):
     (dict(head_dim=64), 2),
     (dict(num_q_heads=6, num_kv_heads=4), 3),   # H_q % H_kv != 0 -> SHAPE
     (dict(num_q_heads=34, num_kv_heads=2), 2),  # G = 17 > 16
-    (dict(p_round=0), 2),                       # P rounding is RN (R6)
+    (dict(p_round=5), 1),                       # P rounding: RN (R6 default) or SR
     (dict(kv_round=5), 1),
 ])
 def test_config_validation_errors(hk, kw, status):

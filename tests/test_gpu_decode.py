@@ -44,8 +44,11 @@ def run_decode(ocfg, prompts, steps, seed=21, check_every=1, check_pages_at=()):
         cu = torch.tensor([0, L], dtype=torch.int32, device="cuda")
         sl = torch.tensor([slots[i]], dtype=torch.int32, device="cuda")
         out = torch.zeros((L, ocfg.Hq, 128), dtype=torch.float32, device="cuda")
-        h.prefill_attention(cfg, torch.from_numpy(q).cuda(), torch.from_numpy(k).cuda(),
-                            torch.from_numpy(v).cuda(), cu, sl, L, cache, out)
+        if ocfg.p_round == "sr" and ocfg.Pi != 64:   # P-SR prefill runs at Pi = 64 only: ingest the prompt
+            h.cache_ingest(cfg, torch.from_numpy(k).cuda(), torch.from_numpy(v).cuda(), cu, sl, L, cache)
+        else:
+            h.prefill_attention(cfg, torch.from_numpy(q).cuda(), torch.from_numpy(k).cuda(),
+                                torch.from_numpy(v).cuda(), cu, sl, L, cache, out)
         states.append(att.ingest_prompt(ocfg, k, v, rng_id=int(rid[i])))
     qd, kd, vd = hack_inputs.decode_tokens(seed, steps, B, ocfg.Hq, ocfg.Hkv)
     sl = torch.from_numpy(slots).cuda()
@@ -77,7 +80,8 @@ def run_decode(ocfg, prompts, steps, seed=21, check_every=1, check_pages_at=()):
                 nf = states[i].nblocks * ocfg.Pi
                 for hq in range(ocfg.Hq):
                     if nf:
-                        flips += check_pcodes(pcn[i, hq, :nf][None], diag[hq]["pcodes"], diag[hq]["py"])
+                        flips += check_pcodes(pcn[i, hq, :nf][None], diag[hq]["pcodes"], diag[hq]["py"],
+                                              diag[hq]["pu"])
                 err = row_rel_err(og[i], O).max()
                 worst = max(worst, float(err))
                 if err > ROW_TOL and nf:
@@ -269,3 +273,11 @@ def test_decode_group8_paired_kernel(Hq):
 def test_decode_general_mma_kernel_g8(monkeypatch):
     monkeypatch.setenv("HACK_DECODE_IMPL", "mma")
     run_decode(att.Config(Hq=16, Hkv=2, Pi=64, bits=2, seed=15), [300, 129], 20, check_every=7)
+
+
+@pytest.mark.parametrize("Pi,bits,Hq", [(64, 2, 4), (64, 4, 8), (32, 2, 2), (128, 4, 4)])
+def test_decode_p_stochastic_rounding(Pi, bits, Hq):
+    """R6 selectable: P stochastic rounding on decode_mma_kernel (the paired kernels keep RN),
+    across flushes; near-ties judged against the SR boundary."""
+    run_decode(att.Config(Hq=Hq, Hkv=2 if Hq < 8 else 1, Pi=Pi, bits=bits, p_round="sr", seed=19), [130, 64],
+               Pi + 3, check_every=7)

@@ -85,7 +85,7 @@ def check_request(ocfg, i, out, pc, cache, reqs, cu, slots, rid, acc=None, rows=
         worst_plain = max(worst_plain, float(err.max()))
         if pc is not None and nfull:
             g = pc[cu[i] + rows, hq, :nfull * ocfg.Pi]
-            flips += check_pcodes(g, diag[hq]["pcodes"], diag[hq]["py"])
+            flips += check_pcodes(g, diag[hq]["pcodes"], diag[hq]["py"], diag[hq]["pu"])
             override[hq] = g          # rows of `rows`, the order att.prefill computes them
     worst = worst_plain
     if worst_plain > ROW_TOL:
@@ -150,3 +150,26 @@ def test_prefill_simt_baseline_kernel(monkeypatch):
     res = run_prefill(ocfg, [300, 77])
     for i in range(2):
         check_request(ocfg, i, *res)
+
+
+@pytest.mark.parametrize("L,Hq,Hkv,bits", [(300, 4, 2, 2), (513, 8, 2, 4), (64, 2, 1, 2)])
+def test_prefill_p_stochastic_rounding(L, Hq, Hkv, bits):
+    """R6 selectable: the paper's stochastic rounding for P with the
+    position-keyed P stream; near-ties are judged against the SR boundary y - u integer."""
+    ocfg = att.Config(Hq=Hq, Hkv=Hkv, Pi=64, bits=bits, p_round="sr", seed=77)
+    res = run_prefill(ocfg, [L])
+    check_request(ocfg, 0, *res)
+
+
+def test_prefill_p_sr_unsupported_on_the_cuda_core_kernel():
+    h = hk()
+    cfg = gpu_cfg(att.Config(Hq=2, Hkv=1, Pi=32, bits=2, p_round="sr"))
+    cache = make_cache(cfg, 1, 64)
+    q = torch.zeros((64, 2, 128), dtype=torch.float16, device="cuda")
+    k = torch.zeros((64, 1, 128), dtype=torch.float16, device="cuda")
+    cu = torch.tensor([0, 64], dtype=torch.int32, device="cuda")
+    sl = torch.zeros(1, dtype=torch.int32, device="cuda")
+    with pytest.raises(h.HackError) as e:
+        h.prefill_attention(cfg, q, k, k, cu, sl, 64, cache, torch.zeros_like(q))
+    assert e.value.status == h.ERR_UNSUPPORTED
+    assert int(cache.seq_lens[0]) == 0                 # rejected before the ingest launch

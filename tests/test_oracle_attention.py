@@ -394,3 +394,64 @@ def test_pcodes_override_pins_the_near_tie_substitution():
     Od2, _ = att.decode_attend(st2, qn, pcodes_override=codes)
     assert np.allclose(Od2[0] - Od[0], sgn * (Pd.max() - Pd.min()) / 255.0 * v_hat(st2, 0)[t], rtol=1e-9, atol=1e-14)
     assert np.array_equal(Od2[1], Od[1])
+
+
+# ----------------------------------------------------------------- P stochastic rounding (R6, selectable)
+
+def test_p_sr_extremes_and_rn_default():
+    """quantize_p 'sr' is floor(y) + [u < frac(y)] (R1): u = 0 gives ceil(y) off the grid and
+    y on it; u -> 1 gives floor(y); the default stays round-to-nearest-even."""
+    g = np.random.default_rng(3)
+    p = np.concatenate([[0.0, 1.0], g.random(62)])[None]               # lo = 0, hi = 1: y = 255 p
+    y = 255.0 * p
+    c0, *_ = att.quantize_p(p, "sr", np.zeros_like(p, np.float32))
+    c1, *_ = att.quantize_p(p, "sr", np.full_like(p, 1 - 2.0 ** -24, np.float32))
+    assert np.array_equal(c0, np.ceil(y).astype(np.uint8))
+    assert np.array_equal(c1, np.floor(y).astype(np.uint8))
+    crn, *_ = att.quantize_p(p)
+    assert np.array_equal(crn, np.rint(y).astype(np.uint8))
+    with pytest.raises(ValueError):
+        att.quantize_p(p, "sr")
+
+
+def test_p_sr_unbiased_over_streams():
+    """E[p_hat] = p under SR: dequantized P averaged over 4000 independent
+    position-keyed streams (rng ids) is within 4 sigma of p for every key."""
+    from oracle import philox
+    g = np.random.default_rng(4)
+    p = g.random(64)
+    n = 4000
+    u = np.stack([philox.uniforms_p(7, rid, 0, 3, [100], np.arange(64))[0] for rid in range(n)])
+    c, lo, s, _, y = att.quantize_p(np.broadcast_to(p, (n, 64)), "sr", u)
+    phat = lo[:, None] + s[:, None] * c
+    frac = y[0] - np.floor(y[0])
+    sigma = s[0] * np.sqrt(frac * (1 - frac) / n) + 1e-15
+    assert (np.abs(phat.mean(0) - p) <= 4 * sigma + 1e-12).all()
+
+
+def test_p_sr_counter_map_is_position_keyed():
+    """u(i, t) depends only on (query position, key position, head, request, layer): the
+    same element drawn through different key ranges agrees; distinct elements differ."""
+    from oracle import philox
+    a = philox.uniforms_p(9, 5, 2, 1, [7, 300], np.arange(0, 128))
+    b = philox.uniforms_p(9, 5, 2, 1, [300], np.arange(64, 192))
+    assert np.array_equal(a[1, 64:], b[0, :64])
+    grid = philox.uniforms_p(9, 5, 2, 1, np.arange(64), np.arange(256))
+    assert len(np.unique(grid)) > 0.999 * grid.size
+    assert not np.array_equal(philox.uniforms_p(9, 5, 2, 2, [7], np.arange(8)), a[:1, :8])
+
+
+def test_p_sr_decode_row_equals_prefill_row():
+    """With P stochastic rounding, the decode step's P codes are the last prefill row's
+    (position-keyed counters), and the outputs agree (SR pins the same code choices)."""
+    c = cfg(Hq=4, Hkv=2, p_round="sr")
+    L = 200
+    q, k, v = hack_inputs.qkv(41, L, 4, 2)
+    O, _, dg = att.prefill(c, q, k, v, rng_id=3, rows=[L - 1], keep_diag=True)
+    st = att.ingest_prompt(c, k[:L - 1], v[:L - 1], rng_id=3)
+    o, dd = att.decode_step(st, q[L - 1], k[L - 1], v[L - 1], keep_diag=True)
+    for hq in range(4):
+        assert np.array_equal(dd[hq]["pcodes"], dg[hq]["pcodes"])
+    assert np.allclose(o, O[L - 1], rtol=1e-12, atol=1e-14)
+    Orn, _, _ = att.prefill(cfg(Hq=4, Hkv=2), q, k, v, rng_id=3, rows=[L - 1])
+    assert not np.array_equal(O[L - 1], Orn[L - 1])                    # the mode changes the codes
