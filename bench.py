@@ -641,7 +641,7 @@ def run_sweep(args, h, dev, seed, flush):
             dec_bytes = B * Hkv * (n // Pi) * pb + B * Hq * 128 * 2 * 2
             res["points"].append({
                 "Pi": Pi, "bits": bits,
-                "prefill_kernel": "prefill_tc_kernel (tcgen05)" if Pi == 64 else "prefill_simt (CUDA cores)",
+                "prefill_kernel": f"prefill_tc_kernel<{Pi}, {bits}> (tcgen05)",
                 "decode_kernel": "decode_pair_kernel (mma.sync)" if Pi == 64 and bits == 2
                 else f"decode_mma_kernel<{bits}, {Pi}> (mma.sync)",
                 "prefill_tops": ops / (pre_ms * 1e-3) / 1e12, "prefill_ms": pre_ms,

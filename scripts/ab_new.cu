@@ -79,9 +79,9 @@ struct Geo {
   static constexpr int KR = NBETA * 12 < 16 ? 16 : NBETA * 12;  // rank-term K (tf32), 12 per block
   static constexpr int SBO_R = KR * 32;                 // K-major SBO of the rank operands
   static constexpr int SBO_T = BN * 8;                  // K-major SBO of the P and V tiles (K = BN)
-  static constexpr int TR = 128;                        // TMEM: rank-term columns
-  static constexpr int TD = (128 + BN + 31) / 32 * 32;  // TMEM: first D' column
-  static_assert(TD + NDB * 128 <= 512, "TMEM budget");
+  static constexpr int TR = BN <= 64 ? 384 : 128;      // TMEM: rank-term columns
+  static constexpr int TD = BN <= 64 ? 128 : 256;       // TMEM: first D' column
+  static_assert(TD + NDB * 128 <= 512 && TR + BN <= 512, "TMEM budget");
 };
 
 template <int PI_, int BITS>
@@ -136,26 +136,6 @@ HACK_DEV void rank_b(float y, float* v) {
 // Query heads packed per CTA (they share the KV head): HACK_PRE_GP if it divides the GQA group.
 __host__ __device__ __forceinline__ int pack_heads(const KernelCfg& kc) {
   return (HACK_PRE_GP >= 4 && kc.G % 4 == 0) ? 4 : ((HACK_PRE_GP >= 2 && kc.G % 2 == 0) ? 2 : 1);
-}
-
-// Causal mask (R8) of n scores at keys t0.. for the row at position i, and the running max /
-// min over the visible keys.
-template <int N>
-HACK_DEV void mask_minmax_t(float* s, int t0, int i, bool full, bool& masked, float& mx, float& mn) {
-  if (!full) {
-#pragma unroll
-    for (int x = 0; x < N; ++x) {
-      const bool vis = (t0 + x) <= i;
-      masked |= !vis;
-      mn = fminf(mn, vis ? s[x] : INFINITY);  // min over the visible keys only
-      s[x] = vis ? s[x] : -INFINITY;
-    }
-  } else {
-#pragma unroll
-    for (int x = 0; x < N; ++x) mn = fminf(mn, s[x]);
-  }
-#pragma unroll
-  for (int x = 0; x < N; ++x) mx = fmaxf(mx, s[x]);
 }
 
 // 16 P values -> 16 code bytes (RN by the 1.5*2^23 magic number, or SR) packed in the
@@ -626,20 +606,31 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_tc_kernel(
             }
           }
         }
-        if (WB) {  // mask, max / min of this chunk, then keep it in TMEM (over its consumed D_0)
-          mask_minmax_t<16>(s + so, t0 + kb + 16 * c, i, full, masked, mx, mn);
+        if (!full) {
+#pragma unroll
+          for (int x = 0; x < 16; ++x) {
+            const bool vis = (t0 + kb + 16 * c + x) <= i;  // causal mask (R8)
+            masked |= !vis;
+            mn = fminf(mn, vis ? s[so + x] : INFINITY);  // min over the visible keys only
+            s[so + x] = vis ? s[so + x] : -INFINITY;
+          }
+        } else {
+#pragma unroll
+          for (int x = 0; x < 16; ++x) mn = fminf(mn, s[so + x]);
+        }
+#pragma unroll
+        for (int x = 0; x < 16; ++x) mx = fmaxf(mx, s[so + x]);
+        if (WB) {  // keep the scores in TMEM (over D_0 of these keys, already consumed)
           uint32_t su[16];
 #pragma unroll
           for (int x = 0; x < 16; ++x) su[x] = __float_as_uint(s[so + x]);
           ptx::tmem_st16(tS + lane_base + kb + 16 * c, su);
         }
       }
-      if (WB) {
-        ptx::tmem_wait_st();
-      } else {
+      if (WB) ptx::tmem_wait_st();
+      if (!WB) {
         ptx::tc_fence_before();
         ptx::mbar_arrive(&sm.s_free);  // S columns may now be overwritten by QK(j+1)
-        mask_minmax_t<KPT>(s, t0 + kb, i, full, masked, mx, mn);
       }
       ptx::mbar_arrive(&sm.k_free[bj]);  // K' tile + key coefficients may be refilled
       sm.xch[j & 1][sw][r] = make_float2(mx, masked ? -INFINITY : mn);
@@ -672,12 +663,20 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_tc_kernel(
         if (!(ps > 1e-30f)) ps = pinv = 0.f;
         pnlo = -plo * pinv;
       }
-      // ---- pass 2: p~ = 2^(S - m), row sum, P' codes (or the FP16 tail tile's p~ -> TMEM),
-      // 16 keys at a time (issuing all exp2 first measured 2 % slower at Pi = 64)
+      // ---- pass 2: p~ = 2^(S - m), row sum, P' codes (or the FP16 tail tile's p~ -> TMEM)
       float2 ls2 = make_float2(0.f, 0.f);
       const float2 mneg = make_float2(-m_run, -m_run);
       uint32_t psum = 0;
-      auto exp_chunk = [&](int so) {
+#pragma unroll
+      for (int c = 0; c < KPT / 16; ++c) {
+        const int so = WB ? 0 : 16 * c;  // this chunk's scores: s[so .. so + 15]
+        if (WB) {
+          uint32_t su[16];
+          ptx::tmem_ld16(tS + lane_base + kb + 16 * c, su);
+          ptx::tmem_wait_ld();
+#pragma unroll
+          for (int x = 0; x < 16; ++x) s[so + x] = __uint_as_float(su[x]);
+        }
 #pragma unroll
         for (int kk = 0; kk < 16; kk += 2) {
           const float2 a2 = ptx::fadd2(make_float2(s[so + kk], s[so + kk + 1]), mneg);
@@ -690,8 +689,6 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_tc_kernel(
 #endif
           ls2 = ptx::fadd2(ls2, make_float2(s[so + kk], s[so + kk + 1]));
         }
-      };
-      auto out_chunk = [&](int so, int c) {
         if (committed) {
           const uint4 cw = p_codes16<BITS, PSR>(s + so, pinv, pnlo, kc.seed, p_rid, p_c3, i, t0 + kb + 16 * c, psum);
           *reinterpret_cast<uint4*>(sm.p[bj] + kmaj_off(r, kb + 16 * c, SBO_T)) =
@@ -707,24 +704,6 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_tc_kernel(
 #pragma unroll
           for (int x = 0; x < 16; ++x) su[x] = __float_as_uint(s[so + x]);
           ptx::tmem_st16(tS + lane_base + kb + 16 * c, su);
-        }
-      };
-      if (WB) {
-#pragma unroll
-        for (int c = 0; c < KPT / 16; ++c) {
-          uint32_t su[16];
-          ptx::tmem_ld16(tS + lane_base + kb + 16 * c, su);
-          ptx::tmem_wait_ld();
-#pragma unroll
-          for (int x = 0; x < 16; ++x) s[x] = __uint_as_float(su[x]);
-          exp_chunk(0);
-          out_chunk(0, c);
-        }
-      } else {
-#pragma unroll
-        for (int c = 0; c < KPT / 16; ++c) {
-          exp_chunk(16 * c);
-          out_chunk(16 * c, c);
         }
       }
       l_run = __fmaf_rn(l_run, al, ls2.x + ls2.y);

@@ -1,0 +1,933 @@
+// prefill_tc.cu -- homomorphic prefill attention on the 5th-gen tensor cores (a3-a7).
+//
+// One CTA = 128 query rows of one query head, warp-specialised (20 warps):
+//   warp 0      producer: whole packed pages (K' + V' codes, fp16 meta, cached sums;
+//               DESIGN.md "HBM layout") -> 4-stage smem ring via cp.async.bulk (TMA)
+//   warp 1      MMA issuer: tcgen05.mma kind::i8, accumulators in TMEM
+//                 QK: per d-block beta D_beta[128 x 64] = (Q'-128)_beta K'_beta^T
+//                 PV: D'[128 x 128] = (P'-128) V'^T per 64-token V block
+//               (A operands are stored as signed s8 = code - 128, B as u8 codes)
+//   warps 2-3   unpack: 2/4-bit codes c -> doubled codes 2c (u8) in K-major UMMA tiles
+//               (tc_common.cuh) + per-key / per-channel Eq. 4 coefficients from the page
+//               meta and CACHED sums (SE)
+//   warps 4-11  two S warpgroups; thread = query row = TMEM lane; SW s owns keys
+//               32s..32s+31 of every tile:
+//                 (a3) Q quantization, 8-bit SR (SW s: d-block s)
+//                 (a4) S = centered Eq. 4 x log2e/sqrt(d)
+//                 (a5) causal online softmax, row max/min combined through smem (2 warps)
+//                 (a6) P' 8-bit RN per (row, V block) -> smem A tile + row info
+//   warps 12-19 two O warpgroups; thread = row; OW o owns output channels 64o..64o+63:
+//                 (a7) O = alpha O + centered Eq. 4 on D' (TMEM, double-buffered, so the
+//                      S warps run up to NB tiles ahead); FP16 last V block (RQE)
+//                      in fp32; O / l.
+// Centering: with s8 A codes a' - 128 and B = 2c the MMA gives
+// E = 2 D_s = 2 sum (a'-128) c exactly (|E| < 2^18, so its fp32 conversion is exact).  The
+// remaining Eq. 4 terms are a rank-2 update per block:
+//   S  = cs [ (s_q/2) s_k 2D_s + s_q SQ_s m_k + mu_q y_k ],  y_k = s_k SK + Pi m_k
+//   O += (s_p/2) s_v 2D_s + s_p SP_s m_v + mu_p y_v,         y_v = s_v SV + Pi m_v
+// (mu = m + 128 s for the 8-bit side; m_k, m_v the stored fp16 minima).
+// Online softmax with lazy rescaling: the running max only moves when a row's tile max
+// exceeds it by more than 8 (log2 units; p~ <= 256), warp-uniformly, so most tiles skip the
+// O *= alpha pass.  P' codes are invariant to the row scale (R13).
+// TMEM (512 columns): S (D_0 | D_1, 128) | D'[2] (2 x 128).  Pi = 64; other partitions
+// use prefill_simt.cu.
+#include "common.cuh"
+#include "internal.h"
+#include "tc_common.cuh"
+
+namespace hack {
+
+namespace {
+
+constexpr int PI = 64;
+constexpr int BM = 128;
+constexpr int BN = 64;
+#ifndef HACK_PRE_ORANK
+#define HACK_PRE_ORANK 0  // O-side Eq. 4 rank terms on the tensor pipe (experiment: correct, 17 % slower)
+#endif
+#ifndef HACK_PRE_GP
+#define HACK_PRE_GP 2  // query heads of one KV head packed into a CTA's 128 rows (1: one head x 128 positions)
+#endif
+#ifndef HACK_PRE_NS
+#define HACK_PRE_NS (HACK_PRE_ORANK ? 2 : 4)
+#endif
+constexpr int NS = HACK_PRE_NS;  // page stages
+constexpr int NB = 3;          // K/V/P tile buffer sets
+#ifndef HACK_PRE_NDB
+#define HACK_PRE_NDB (HACK_PRE_ORANK ? 1 : 2)
+#endif
+constexpr int NDB = HACK_PRE_NDB;  // D' (PV accumulator) TMEM buffers
+constexpr int kThreads = 640;  // 4 service warps + 2 S warpgroups + 2 O warpgroups
+constexpr int NSW = 256;       // S-warpgroup threads
+constexpr int NOW = 256;       // O-warpgroup threads
+constexpr float kMagic = 12582912.f;           // 1.5 * 2^23 (P' rounding)
+constexpr float kRescaleTh = 8.f;             // lazy-rescale threshold (log2 units)
+#ifndef HACK_PRE_PBAR
+#define HACK_PRE_PBAR 1  // S -> O handoff of tile j on named barrier kPBar0 + j % NB (0: the mbarrier, polled)
+#endif
+// Named barriers: 0 = __syncthreads, 3..6 = the S warp pairs' row exchange, 7..9 = S -> O.
+// Generations of barrier kPBar0 + b alternate strictly: the S warps arrive for tile j only
+// after the O warps finished tile j - NB (o_done), which they synced on for tile j - NB.
+constexpr uint32_t kPBar0 = 7;
+
+template <int BITS>
+struct TcSmem {
+  static constexpr int PB = BITS == 2 ? 5376 : 9728;  // page bytes (d=128, Pi=64)
+  uint8_t stage[NS][PB];
+  alignas(128) uint8_t q[BM * 128];       // Q' - 128 (s8), K-major, SBO 1024
+  alignas(128) uint8_t k[NB][BN * 128];   // K' (u8), K-major, SBO 1024
+  alignas(128) uint8_t v[NB][128 * BN];   // V' (u8), K-major (keys = K), SBO 512
+  alignas(128) uint8_t p[NB][BM * BN];    // P' - 128 (s8), K-major, SBO 512
+  alignas(128) float ar[BM * 24];         // rank-term A operand (tf32, K-major, SBO 768): per row, per beta
+                                          //   X and M split 3 ways (kRankA)
+  alignas(128) float br[NB][BN * 24];     // rank-term B operand per key: m_k and y_k split 3 ways (kRankB)
+  alignas(128) uint16_t pre_a[128 * 16];  // bf16 preset operands: A[:, 0] = 1, B[:, 0] = 1.5 * 2^23 (K-major,
+  alignas(128) uint16_t pre_b[128 * 16];  //   SBO 256): one kind::f16 MMA writes the magic into D
+  alignas(16) float kcf[NB][2][BN];       // [buf][beta][key]: s_k
+  alignas(16) float vcf[NB][3][128];      // [buf][field][channel]: s_v, m_v, y_v
+  float4 qconst[2][BM];                   // per (beta, row): cs s_q / 2, cs s_q SQ_s, cs mu_q
+  int sp_part[NB][2][BM];                 // partial P-code sums (per S warpgroup)
+  float4 pinfo[NB][BM];                   // per (tile, row): alpha, rescaled?, s_p, m_p
+  float2 xch[2][2][BM];                   // partial (max, min | -inf if masked)
+  float ptail[BM][BN + 1];                // p~ of the FP16 tail tile
+  float lpart[2][BM];
+#if HACK_PRE_ORANK
+  alignas(128) float ora[BM * 16];        // O-rank A operand (tf32, K-major, SBO 512): x_p, mu_p split 3 ways
+  alignas(128) float orb[128 * 16];       // O-rank B operand per channel: m_v, y_v split 3 ways
+  uint64_t a_ready, or_done;
+#endif
+  uint64_t full[NS], empty[NS], k_ready[NB], k_free[NB], v_ready[NB], o_done[NB], p_ready[NB],
+      d_full[2], d_free[2], s_full, s_free, q_ready, l_ready;
+  uint32_t tmem_base;
+};
+
+// Integer accumulators are preset to the fp32 bits of 1.5*2^23 by one bf16 MMA (A = e_0,
+// B = 1.5*2^23 e_0) before the kind::i8 MMAs accumulate onto them, so the float view of an
+// accumulated integer E (|E| < 2^22) is 1.5*2^23 + E and one FADD2 converts two exactly.
+#ifndef HACK_ABL
+#define HACK_ABL 0  // timing ablations only, bit flags (1 O math, 2 P-quant math, 4 Eq. 4, 8 exp2); wrong results
+#endif
+// Waits per role: bit set in HACK_PRE_SLEEP -> that role waits with a suspend hint
+// (NANOSLEEP.SYNCS, wakes on the phase flip) instead of a polling loop that takes issue
+// slots from the epilogue warps.  Bits: 0 producer, 1 MMA issuer, 2 unpack, 3 S, 4 O.
+#ifndef HACK_PRE_SLEEP
+#define HACK_PRE_SLEEP 0
+#endif
+#ifndef HACK_PRE_SREG_S
+#define HACK_PRE_SREG_S "88"  // S-warpgroup registers (setmaxnreg)
+#endif
+#ifndef HACK_PRE_SREG_SVC
+#define HACK_PRE_SREG_SVC "40"  // service warps; 128 x 40 + 256 x 88 + 256 x 128 <= the launch's 96 x 640
+#endif
+template <int ROLE>
+HACK_DEV void rwait(uint64_t* bar, uint32_t parity) {
+  if ((HACK_PRE_SLEEP >> ROLE) & 1)
+    ptx::mbar_wait_sleep(bar, parity);
+  else
+    ptx::mbar_wait(bar, parity);
+}
+
+HACK_DEV float2 acc2f(uint32_t a, uint32_t b) {
+  return ptx::fadd2(make_float2(__uint_as_float(a), __uint_as_float(b)), make_float2(-kMagic, -kMagic));
+}
+
+// Exact 3-way tf32 split x = h + m + l (11 + 11 + <= 2 significant bits); a product x y is
+// then hh' + hm' + mh' + hl' + lh' + mm' up to ~2^-33 relative (the dropped ml', lm', ll').
+// A-side (row constant) and B-side (key coefficient) orders pair up those six terms.
+HACK_DEV void split3(float x, float& h, float& m, float& l) {
+  h = ptx::tf32_hi(x);
+  const float r = x - h;
+  m = ptx::tf32_hi(r);
+  l = r - m;
+}
+HACK_DEV void rank_a(float x, float* v) {
+  float h, m, l;
+  split3(x, h, m, l);
+  v[0] = h; v[1] = h; v[2] = m; v[3] = h; v[4] = l; v[5] = m;
+}
+HACK_DEV void rank_b(float y, float* v) {
+  float h, m, l;
+  split3(y, h, m, l);
+  v[0] = h; v[1] = m; v[2] = h; v[3] = l; v[4] = h; v[5] = m;
+}
+
+// Query heads packed per CTA (they share the KV head): HACK_PRE_GP if it divides the GQA group.
+__host__ __device__ __forceinline__ int pack_heads(const KernelCfg& kc) {
+  return (HACK_PRE_GP >= 4 && kc.G % 4 == 0) ? 4 : ((HACK_PRE_GP >= 2 && kc.G % 2 == 0) ? 2 : 1);
+}
+
+// DBG: parity runs only (hack_debug_t): dumps the P codes and the raw QK / PV block
+// accumulators E = 2 D - 256 S_B (HACK_ACC_S8_2B); the production instantiation has none of it.
+// PSR: P codes by the paper's stochastic rounding (R6, selectable) instead of RN.
+template <int BITS, bool DBG, bool PSR>
+__global__ void __launch_bounds__(kThreads, 1) prefill_tc_kernel(
+    const __half* __restrict__ q, const int32_t* __restrict__ cu_seqlens, const int32_t* __restrict__ slots,
+    CacheView cv, KernelCfg kc, void* __restrict__ out, uint8_t* __restrict__ dbg_pcodes, int64_t dbg_stride,
+    int32_t* __restrict__ dbg_qk, int32_t* __restrict__ dbg_pv, int64_t acc_stride, int acc_head) {
+  using SM = TcSmem<BITS>;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  SM& sm = *reinterpret_cast<SM*>(smem_raw);
+
+  // Block order: linear id -> (rank, head) with the head fastest, so the whole grid runs
+  // heaviest-first (longest causal rows of every head before any lighter tile): greedy
+  // block scheduling then balances the SMs (LPT), ~15% shorter than per-head ordering.
+  const int b = blockIdx.z;
+  // GQA row packing: the 128 MMA rows are gp query heads (of one KV head) x pbp positions,
+  // so the K'/V' tiles a CTA unpacks serve gp heads and the causal diagonal is pbp wide.
+  const int gp = pack_heads(kc), pbp = BM / gp;
+  const int lin = blockIdx.x + gridDim.x * blockIdx.y;
+  const int npk = kc.Hq / gp;
+  const int rank = lin / npk, hq0 = (lin % npk) * gp;  // heads hq0 .. hq0 + gp - 1
+  const int start = cu_seqlens[b], L = cu_seqlens[b + 1] - start;
+  const int nqt = (L + pbp - 1) / pbp;
+  if (rank >= nqt) return;
+  const int qt = nqt - 1 - rank;  // heavy (long causal rows) tiles first
+  const int i0 = qt * pbp;        // first position of the CTA
+  const int slot = slots[b];
+  const int hk = hq0 / kc.G;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int nkt = min((i0 + pbp - 1) / BN, (L - 1) / BN) + 1;  // key tiles (causal)
+  const int nfull = L / PI;                                    // committed V blocks
+  const PageLayout PL = kc.pl;
+
+  if (tid == 0) {
+    for (int s = 0; s < NS; ++s) {
+      ptx::mbar_init(&sm.full[s], 1);
+      ptx::mbar_init(&sm.empty[s], 64);
+    }
+    for (int x = 0; x < NB; ++x) {
+      ptx::mbar_init(&sm.k_ready[x], 64);
+      ptx::mbar_init(&sm.k_free[x], NSW);
+      ptx::mbar_init(&sm.v_ready[x], 64);
+      ptx::mbar_init(&sm.o_done[x], NOW);
+      ptx::mbar_init(&sm.p_ready[x], NSW);
+    }
+    for (int x = 0; x < 2; ++x) {
+      ptx::mbar_init(&sm.d_full[x], 1);
+      ptx::mbar_init(&sm.d_free[x], NOW);
+    }
+    ptx::mbar_init(&sm.s_full, 1);
+    ptx::mbar_init(&sm.s_free, NSW);
+#if HACK_PRE_ORANK
+    ptx::mbar_init(&sm.a_ready, NOW);
+    ptx::mbar_init(&sm.or_done, 1);
+#endif
+    ptx::mbar_init(&sm.q_ready, NSW);
+    ptx::mbar_init(&sm.l_ready, NSW);
+    ptx::fence_mbar_init();
+  }
+  if (warp == 1) ptx::tmem_alloc(&sm.tmem_base, 512);
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem = sm.tmem_base;
+  const uint32_t tS = tmem;         // columns 0..127: D_0 | D_1
+  const uint32_t tD0 = tmem + 128;  // D'[0] columns 128..255, D'[1] 256..383
+  const uint32_t tR = tmem + 384;   // rank terms of S (64 columns): sum_beta X m_k + M y_k (3xTF32 MMA)
+#if HACK_PRE_ORANK
+  static_assert(NDB == 1, "the O-rank accumulator takes the second D' buffer's columns");
+  const uint32_t tOR = tmem + 256;  // O-side rank terms, all tiles: sum_j x_p m_v + mu_p y_v (3xTF32 MMA)
+#endif
+
+  if (warp < 4) {
+    // register budget (launch: 96 x 640 = 61440): service 40, S HACK_PRE_SREG_S, O 128
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 " HACK_PRE_SREG_SVC ";");
+    if (warp == 0) {
+      // ---------------------------------------------------------------- producer
+      if (lane == 0) {
+        const int32_t* bt = cv.block_table + (int64_t)slot * cv.max_pages_per_req;
+        for (int j = 0; j < nkt; ++j) {
+          const int s = j % NS;
+          rwait<0>(&sm.empty[s], ((j / NS) & 1) ^ 1);
+          ptx::mbar_arrive_expect_tx(&sm.full[s], SM::PB);
+          const uint8_t* pg = cv.pages + ((int64_t)bt[j] * cv.num_kv_heads + hk) * cv.page_bytes;
+          ptx::bulk_g2s(sm.stage[s], pg, SM::PB, &sm.full[s]);
+        }
+      }
+    } else if (warp == 1) {
+      // ---------------------------------------------------------------- MMA issuer
+      const uint32_t idesc_qk = ptx::idesc_s8u8(BM, BN), idesc_pv = ptx::idesc_s8u8(BM, 128);
+      const uint32_t qa = ptx::smem_u32(sm.q);
+      const uint64_t pre_a = ptx::smem_desc_kmajor(ptx::smem_u32(sm.pre_a), 128, 256);
+      const uint64_t pre_b = ptx::smem_desc_kmajor(ptx::smem_u32(sm.pre_b), 128, 256);
+      const uint32_t idesc_pre = ptx::idesc_bf16(BM, 128);
+      rwait<1>(&sm.q_ready, 0);
+      for (int j = 0; j <= nkt; ++j) {
+        if (j < nkt) {
+          const int bq = j % NB;
+          rwait<1>(&sm.k_ready[bq], (j / NB) & 1);
+          rwait<1>(&sm.s_free, (j & 1) ^ 1);
+          ptx::tc_fence_after();
+          if (lane == 0) {
+            const uint32_t ka = ptx::smem_u32(sm.k[bq]);
+            ptx::mma_bf16(tS, pre_a, pre_b, idesc_pre, 0u);  // D_0 | D_1 := 1.5 * 2^23
+#pragma unroll
+            for (int beta = 0; beta < 2; ++beta)
+#pragma unroll
+              for (int ks = 0; ks < PI / 32; ++ks) {
+                const uint32_t koff = (uint32_t)(beta * 4 + ks * 2) * 128;  // 16-byte K chunks
+                ptx::mma_u8(tS + 64 * beta, ptx::smem_desc_kmajor(qa + koff, 128, 1024),
+                            ptx::smem_desc_kmajor(ka + koff, 128, 1024), idesc_qk, 1u);
+              }
+            // rank-2-per-block terms of Eq. 4 on the tensor pipe: R = [X | M] [m_k ; y_k]
+            // with both sides split 3 ways (exact tf32 parts, fp32-level product), so the S
+            // epilogue keeps one FMUL2 + FFMA2 per key pair and block
+            const uint32_t ra = ptx::smem_u32(sm.ar), rb = ptx::smem_u32(sm.br[bq]);
+#pragma unroll
+            for (int ks = 0; ks < 3; ++ks)
+              ptx::mma_tf32(tR, ptx::smem_desc_kmajor(ra + ks * 256, 128, 768),
+                            ptx::smem_desc_kmajor(rb + ks * 256, 128, 768), ptx::idesc_tf32(BM, BN), ks > 0);
+            ptx::mma_commit(&sm.s_full);
+          }
+          __syncwarp();
+        }
+        const int jj = j - 1;  // PV of the previous tile, after QK of this one (overlap)
+        if (jj >= 0 && jj < nfull) {
+          const int bd = jj % NDB, bq = jj % NB;
+          const uint32_t ph = (jj / NB) & 1;
+          rwait<1>(&sm.p_ready[bq], ph);
+          rwait<1>(&sm.v_ready[bq], ph);
+          rwait<1>(&sm.d_free[bd], ((jj / NDB) & 1) ^ 1);
+          ptx::tc_fence_after();
+          if (lane == 0) {
+            const uint32_t pa = ptx::smem_u32(sm.p[bq]), va = ptx::smem_u32(sm.v[bq]);
+            ptx::mma_bf16(tD0 + 128 * bd, pre_a, pre_b, idesc_pre, 0u);  // D' := 1.5 * 2^23
+#pragma unroll
+            for (int ks = 0; ks < BN / 32; ++ks)
+              ptx::mma_u8(tD0 + 128 * bd, ptx::smem_desc_kmajor(pa + ks * 256, 128, 512),
+                          ptx::smem_desc_kmajor(va + ks * 256, 128, 512), idesc_pv, 1u);
+            ptx::mma_commit(&sm.d_full[bd]);
+          }
+          __syncwarp();
+#if HACK_PRE_ORANK
+          // O-side rank-2 terms of tile jj into the persistent fp32 accumulator (the O warps
+          // wrote A after reading tile jj's P meta and rescaled the accumulator if needed)
+          rwait<1>(&sm.a_ready, jj & 1);
+          ptx::tc_fence_after();
+          if (lane == 0) {
+            const uint32_t oa = ptx::smem_u32(sm.ora), ob = ptx::smem_u32(sm.orb);
+#pragma unroll
+            for (int ks = 0; ks < 2; ++ks)
+              ptx::mma_tf32(tOR, ptx::smem_desc_kmajor(oa + ks * 256, 128, 512),
+                            ptx::smem_desc_kmajor(ob + ks * 256, 128, 512), ptx::idesc_tf32(BM, 128),
+                            (jj > 0 || ks > 0) ? 1u : 0u);
+            ptx::mma_commit(&sm.or_done);
+          }
+          __syncwarp();
+#endif
+        }
+      }
+    } else {
+      // ---------------------------------------------------------------- unpack (64 threads)
+      const int ut = tid - 64;
+      // bf16 preset operands (visible to the MMA through the proxy fence before k_ready)
+#pragma unroll
+      for (int rr = 0; rr < 2; ++rr) {
+        const int row = ut + 64 * rr;
+        *reinterpret_cast<uint4*>(reinterpret_cast<uint8_t*>(sm.pre_a) + kmaj_off(row, 0, 256)) =
+            make_uint4(0x3F80u, 0u, 0u, 0u);  // bf16 1.0 at k = 0
+        *reinterpret_cast<uint4*>(reinterpret_cast<uint8_t*>(sm.pre_a) + kmaj_off(row, 16, 256)) = make_uint4(0u, 0u, 0u, 0u);
+        *reinterpret_cast<uint4*>(reinterpret_cast<uint8_t*>(sm.pre_b) + kmaj_off(row, 0, 256)) =
+            make_uint4(0x4B40u, 0u, 0u, 0u);  // bf16 1.5 * 2^23 at k = 0
+        *reinterpret_cast<uint4*>(reinterpret_cast<uint8_t*>(sm.pre_b) + kmaj_off(row, 16, 256)) = make_uint4(0u, 0u, 0u, 0u);
+      }
+#pragma unroll 1
+      for (int j = 0; j < nkt; ++j) {
+        const int s = j % NS, bj = j % NB;
+        const uint32_t ph = (j / NB) & 1;
+        rwait<2>(&sm.full[s], (j / NS) & 1);
+        rwait<2>(&sm.k_free[bj], ph ^ 1);
+        const uint8_t* pg = sm.stage[s];
+        const int nk = min(BN, L - j * BN);
+        if (!(HACK_ABL & 16)) {  // K' codes: thread = key; 8 consecutive keys fill one 128-byte core matrix per store
+          const int key = ut;
+          const uint4* src = reinterpret_cast<const uint4*>(pg + PL.k_codes + key * (128 * BITS / 8));
+#pragma unroll
+          for (int h = 0; h < BITS; ++h) {  // 16-byte pieces of the packed row
+            const uint4 pw = src[h];
+            const uint32_t w4[4] = {pw.x, pw.y, pw.z, pw.w};
+#pragma unroll
+            for (int x = 0; x < 4; ++x) {
+              const int wi = 4 * h + x;
+              if (BITS == 2)
+                *reinterpret_cast<uint4*>(sm.k[bj] + kmaj_off(key, 16 * wi, 1024)) = unpack16_2b_x2(w4[x]);
+              else
+                *reinterpret_cast<uint2*>(sm.k[bj] + kmaj_off(key, 8 * wi, 1024)) = unpack8_4b_x2(w4[x]);
+            }
+          }
+        }
+#pragma unroll
+        for (int beta = 0; beta < 2 && !(HACK_ABL & 16); ++beta) {  // per-(key, beta) Eq. 4 coefficients
+          const int key = ut, e = 2 * key + beta;
+          float c0 = 0.f, c1 = 0.f, c2 = 0.f;
+          if (key < nk) {
+            const __half2 mh = reinterpret_cast<const __half2*>(pg + PL.k_meta)[e];
+            const float m = __low2float(mh), s2 = __high2float(mh);
+            const int sum = load_sum(pg + PL.k_sums, e, PL.sum_bytes);  // cached sum (SE)
+            c0 = s2;
+            c1 = m;
+            c2 = fmaf(s2, (float)sum, PI * m);  // y_k = s_k SK + Pi m_k
+          }
+          sm.kcf[bj][beta][key] = c0;
+          float rv[12];
+          rank_b(c1, rv);
+          rank_b(c2, rv + 6);
+          uint8_t* brk = reinterpret_cast<uint8_t*>(sm.br[bj]);
+#pragma unroll
+          for (int x = 0; x < 12; x += 4)
+            *reinterpret_cast<float4*>(brk + kmaj_off(key, 4 * (12 * beta + x), 768)) =
+                make_float4(rv[x], rv[x + 1], rv[x + 2], rv[x + 3]);
+        }
+        ptx::fence_proxy_async_smem();
+        ptx::mbar_arrive(&sm.k_ready[bj]);
+        rwait<2>(&sm.o_done[bj], ph ^ 1);  // O warps done with tile j - NB
+        if (j < nfull && !(HACK_ABL & 16)) {
+#if HACK_PRE_ORANK
+          if (j > 0) rwait<2>(&sm.or_done, (j - 1) & 1);  // the single B operand buffer is free
+#endif
+#pragma unroll
+          for (int c2 = 0; c2 < 2; ++c2) {
+            const int ch = ut + 64 * c2;
+            const uint4* src = reinterpret_cast<const uint4*>(pg + PL.v_codes + ch * (BN * BITS / 8));
+#pragma unroll
+            for (int h = 0; h < BITS / 2; ++h) {
+              const uint4 pw = src[h];
+              const uint32_t w4[4] = {pw.x, pw.y, pw.z, pw.w};
+#pragma unroll
+              for (int x = 0; x < 4; ++x) {
+                const int wi = 4 * h + x;
+                if (BITS == 2)
+                  *reinterpret_cast<uint4*>(sm.v[bj] + kmaj_off(ch, 16 * wi, 512)) = unpack16_2b_x2(w4[x]);
+                else
+                  *reinterpret_cast<uint2*>(sm.v[bj] + kmaj_off(ch, 8 * wi, 512)) = unpack8_4b_x2(w4[x]);
+              }
+            }
+            const __half2 mh = reinterpret_cast<const __half2*>(pg + PL.v_meta)[ch];
+            const float m = __low2float(mh), s2 = __high2float(mh);
+            const int sum = load_sum(pg + PL.v_sums, ch, PL.sum_bytes);  // cached sum (SE)
+            sm.vcf[bj][0][ch] = s2;
+            sm.vcf[bj][1][ch] = m;
+            sm.vcf[bj][2][ch] = fmaf(s2, (float)sum, PI * m);  // y_v = s_v SV + Pi m_v
+#if HACK_PRE_ORANK
+            {
+              float bv[16];
+              rank_b(m, bv);
+              rank_b(fmaf(s2, (float)sum, PI * m), bv + 6);
+              bv[12] = bv[13] = bv[14] = bv[15] = 0.f;
+              uint8_t* obr = reinterpret_cast<uint8_t*>(sm.orb);
+#pragma unroll
+              for (int x = 0; x < 16; x += 4)
+                *reinterpret_cast<float4*>(obr + kmaj_off(ch, 4 * x, 512)) =
+                    make_float4(bv[x], bv[x + 1], bv[x + 2], bv[x + 3]);
+            }
+#endif
+          }
+        }
+        ptx::fence_proxy_async_smem();
+        ptx::mbar_arrive(&sm.v_ready[bj]);
+        ptx::mbar_arrive(&sm.empty[s]);
+      }
+    }
+  } else if (warp < 12) {
+    // ------------------------------------------------------------------ S warpgroups (2)
+    // thread = query row r = TMEM lane; SW s owns keys 32s..32s+31 of every tile
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 " HACK_PRE_SREG_S ";");
+    const int sw = (warp - 4) >> 2;
+    const int r = (tid - 128) & (BM - 1);
+    const int pos = i0 + (r & (pbp - 1)), hq = hq0 + r / pbp;  // this row's position and head
+    const int i = min(pos, L - 1);  // this thread's query position (padding rows clamp)
+    const uint32_t lane_base = (uint32_t)(32 * (warp & 3)) << 16;
+    const uint32_t qbar = 3 + (warp & 3);  // the 2 S warps sharing these 32 rows
+    const float cscale = 1.4426950408889634f / sqrtf(128.f);
+    const int kb = 32 * sw;
+    {
+      // (a3) quantize Q[i, 64 sw .. 64 sw + 63] (d-block beta = sw): 8-bit, fp32 meta, SR
+      const uint4* qrow = reinterpret_cast<const uint4*>(q + ((int64_t)(start + i) * kc.Hq + hq) * 128 + 64 * sw);
+      // all 8 loads of the 64-channel slice in flight at once (one memory latency per CTA,
+      // not eight), kept in registers for the quantization pass; min/max on packed halves
+      uint4 qr[8];
+#pragma unroll
+      for (int v8 = 0; v8 < 8; ++v8) qr[v8] = __ldg(qrow + v8);
+      __half2 lo2 = *reinterpret_cast<const __half2*>(&qr[0].x), hi2 = lo2;
+#pragma unroll
+      for (int v8 = 0; v8 < 8; ++v8) {
+        const __half2* h2 = reinterpret_cast<const __half2*>(&qr[v8]);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          lo2 = __hmin2(lo2, h2[e]);
+          hi2 = __hmax2(hi2, h2[e]);
+        }
+      }
+      const float lo = fminf(__low2float(lo2), __high2float(lo2)), hi = fmaxf(__low2float(hi2), __high2float(hi2));
+      const QMeta qm = meta_fp32(lo, hi, 255);
+      const uint32_t c3 = stream_c3(kc.layer, kTagQ, kc.head_base * kc.G + hq);
+      const uint32_t rng_id = cv.rng_ids[slot];
+      int sum = 0;
+#pragma unroll
+      for (int g = 0; g < 4; ++g) {  // 16-channel groups
+        float x[16];
+        const __half* ha = reinterpret_cast<const __half*>(&qr[2 * g]);
+        const __half* hb = reinterpret_cast<const __half*>(&qr[2 * g + 1]);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          x[e] = __half2float(ha[e]);
+          x[8 + e] = __half2float(hb[e]);
+        }
+        int cc[16];
+        if (kc.q_round == HACK_ROUND_STOCHASTIC) {
+#pragma unroll
+          for (int k4 = 0; k4 < 4; ++k4) {
+            const uint64_t n = ((uint64_t)i * 128u + (uint64_t)(64 * sw + 16 * g + 4 * k4)) >> 2;
+            const Philox4 rr = philox_block(kc.seed, rng_id, c3, n);
+            cc[4 * k4 + 0] = quant_sr(x[4 * k4 + 0], qm, u24(rr.x), 255);
+            cc[4 * k4 + 1] = quant_sr(x[4 * k4 + 1], qm, u24(rr.y), 255);
+            cc[4 * k4 + 2] = quant_sr(x[4 * k4 + 2], qm, u24(rr.z), 255);
+            cc[4 * k4 + 3] = quant_sr(x[4 * k4 + 3], qm, u24(rr.w), 255);
+          }
+        } else {
+#pragma unroll
+          for (int e = 0; e < 16; ++e) cc[e] = quant_rn(x[e], qm, 255);
+        }
+        uint32_t wv[4];
+#pragma unroll
+        for (int x4 = 0; x4 < 4; ++x4) {
+          uint32_t wd = 0;
+#pragma unroll
+          for (int e = 0; e < 4; ++e) wd |= (uint32_t)cc[perm_src<BITS>(4 * x4 + e)] << (8 * e);
+          wv[x4] = wd ^ 0x80808080u;  // s8 operand: code - 128
+        }
+#pragma unroll
+        for (int e = 0; e < 16; ++e) sum += cc[e];
+        *reinterpret_cast<uint4*>(sm.q + kmaj_off(r, 64 * sw + 16 * g, 1024)) = make_uint4(wv[0], wv[1], wv[2], wv[3]);
+      }
+      const int sqs = sum - 128 * PI;  // sum (q' - 128)
+      sm.qconst[sw][r] =
+          make_float4(cscale * qm.s * 0.5f, cscale * qm.s * (float)sqs, cscale * __fmaf_rn(128.f, qm.s, qm.m), 0.f);
+      {
+        const float X = cscale * qm.s * (float)sqs, M = cscale * __fmaf_rn(128.f, qm.s, qm.m);
+        float av[12];
+        rank_a(X, av);
+        rank_a(M, av + 6);
+        uint8_t* arr = reinterpret_cast<uint8_t*>(sm.ar);
+#pragma unroll
+        for (int x = 0; x < 12; x += 4)
+          *reinterpret_cast<float4*>(arr + kmaj_off(r, 4 * (12 * sw + x), 768)) =
+              make_float4(av[x], av[x + 1], av[x + 2], av[x + 3]);
+      }
+      ptx::fence_proxy_async_smem();
+      ptx::mbar_arrive(&sm.q_ready);
+    }
+    ptx::named_bar_sync(qbar, 64);  // both halves of the Q row constants visible
+    const float4 qc0 = sm.qconst[0][r], qc1 = sm.qconst[1][r];
+    const float2 qa0 = make_float2(qc0.x, qc0.x), qa1 = make_float2(qc1.x, qc1.x);
+    float m_run = -INFINITY, l_run = 0.f;
+
+#pragma unroll 1
+    for (int j = 0; j < nkt; ++j) {
+      const int bj = j % NB, t0 = j * BN;
+      const uint32_t ph = (j / NB) & 1;
+      const bool full = (t0 + BN - 1) <= i0;  // every key visible to every row of the CTA
+      rwait<3>(&sm.s_full, j & 1);
+      ptx::tc_fence_after();
+      float s[32];
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {  // rank terms (tensor pipe) seed the accumulation
+        uint32_t d[16];
+        ptx::tmem_ld16(tR + lane_base + kb + 16 * h, d);
+        ptx::tmem_wait_ld();
+#pragma unroll
+        for (int x = 0; x < 16; ++x) s[16 * h + x] = __uint_as_float(d[x]);
+      }
+#pragma unroll
+      for (int beta = 0; beta < 2 && !(HACK_ABL & 4); ++beta) {
+        const float2 A = beta ? qa1 : qa0;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {  // 16 keys per TMEM load (register pressure)
+          uint32_t d[16];
+          ptx::tmem_ld16(tS + lane_base + 64 * beta + kb + 16 * h, d);
+          ptx::tmem_wait_ld();
+          if (DBG && dbg_qk != nullptr && pos < L && (acc_head < 0 || hq == acc_head)) {  // E = 2 D - 256 SK
+            const int hs = acc_head < 0 ? hq : 0, hn = acc_head < 0 ? kc.Hq : 1;
+            int32_t* dq = dbg_qk + (((int64_t)(start + pos) * hn + hs) * 2 + beta) * acc_stride;
+#pragma unroll
+            for (int x = 0; x < 16; ++x) {
+              const int t = t0 + kb + 16 * h + x;
+              if (t < L) dq[t] = (int32_t)(d[x] - 0x4B400000u);
+            }
+          }
+#pragma unroll
+          for (int g4 = 0; g4 < 4; ++g4) {
+            const int kl = kb + 16 * h + 4 * g4;  // first of 4 keys
+            const float4 sk4 = *reinterpret_cast<const float4*>(&sm.kcf[bj][beta][kl]);
+#pragma unroll
+            for (int pr = 0; pr < 2; ++pr) {
+              const int k2 = 4 * g4 + 2 * pr, ks = 16 * h + k2;
+              const float2 E = acc2f(d[k2], d[k2 + 1]);
+              const float2 skp = pr ? make_float2(sk4.z, sk4.w) : make_float2(sk4.x, sk4.y);
+              const float2 t = ptx::fmul2(skp, E);  // s_k 2D_s
+              const float2 a = ptx::ffma2(A, t, make_float2(s[ks], s[ks + 1]));
+              s[ks] = a.x;
+              s[ks + 1] = a.y;
+            }
+          }
+        }
+      }
+      ptx::tc_fence_before();
+      ptx::mbar_arrive(&sm.s_free);      // S columns may now be overwritten by QK(j+1)
+      ptx::mbar_arrive(&sm.k_free[bj]);  // K' tile + key coefficients may be refilled
+      bool masked = false;
+      if (!full) {
+#pragma unroll
+        for (int kk = 0; kk < 32; ++kk) {
+          const bool vis = (t0 + kb + kk) <= i;  // causal mask (R8)
+          masked |= !vis;
+          s[kk] = vis ? s[kk] : -INFINITY;
+        }
+      }
+      float mx = s[0], mn = s[0];
+#pragma unroll
+      for (int kk = 1; kk < 32; ++kk) {
+        mx = fmaxf(mx, s[kk]);
+        mn = fminf(mn, s[kk]);
+      }
+      if (masked) {  // min over the visible keys only
+        mn = INFINITY;
+#pragma unroll
+        for (int kk = 0; kk < 32; ++kk) mn = fminf(mn, s[kk] == -INFINITY ? INFINITY : s[kk]);
+      }
+      sm.xch[j & 1][sw][r] = make_float2(mx, masked ? -INFINITY : mn);
+      ptx::named_bar_sync(qbar, 64);
+      const float2 o = sm.xch[j & 1][sw ^ 1][r];
+      mx = fmaxf(mx, o.x);
+      const bool any_masked = masked || (o.y == -INFINITY);
+      mn = fminf(masked ? INFINITY : mn, o.y == -INFINITY ? INFINITY : o.y);
+      // lazy rescaling: move the running max only when some row of this warp outgrew it by
+      // more than kRescaleTh (identical decision in both S warps sharing these rows)
+      float al = 1.f;
+      const bool resc = __any_sync(0xffffffffu, mx > m_run + kRescaleTh);
+      if (resc) {
+        const float m_new = fmaxf(m_run, mx);
+        al = (m_run == -INFINITY) ? 0.f : ex2(m_run - m_new);
+        m_run = m_new;
+      }
+      float2 ls2 = make_float2(0.f, 0.f);
+      const float2 mneg = make_float2(-m_run, -m_run);
+#pragma unroll
+      for (int kk = 0; kk < 32; kk += 2) {
+        const float2 a2 = ptx::fadd2(make_float2(s[kk], s[kk + 1]), mneg);
+#if (HACK_ABL & 8)
+        s[kk] = a2.x;
+        s[kk + 1] = a2.y;
+#else
+        s[kk] = ex2(a2.x);  // ex2(-inf) = +0 for masked keys
+        s[kk + 1] = ex2(a2.y);
+#endif
+        ls2 = ptx::fadd2(ls2, make_float2(s[kk], s[kk + 1]));
+      }
+      l_run = __fmaf_rn(l_run, al, ls2.x + ls2.y);
+      // tile j-NB must be fully consumed by the O warps before its P / info slots are reused
+      rwait<3>(&sm.o_done[bj], ph ^ 1);
+      if (j < nfull) {
+        // (a6) P' per (row, V block): 8-bit RN on p~ (codes invariant to the row scale);
+        // y = (p - lo) / s rounded with the 1.5*2^23 magic number (y in [0, 255])
+        const float plo = any_masked ? 0.f : ex2(mn - m_run);
+        const float phi = ex2(mx - m_run);
+        // transient P meta (never stored; the codes only need to agree up to near-ties, DESIGN
+        // "Parity protocol"): multiply and a fast reciprocal instead of IEEE division
+        QMeta pm;
+        pm.m = plo;
+        pm.s = (phi - plo) * (1.f / 255.f);
+        pm.inv = __fdividef(255.f, phi - plo);
+        if (!(pm.s > 1e-30f)) {
+          pm.s = 0.f;
+          pm.inv = 0.f;
+        }
+        const float2 inv2 = make_float2(pm.inv, pm.inv), nlo2 = make_float2(-plo * pm.inv, -plo * pm.inv);
+        const float2 magic = make_float2(kMagic, kMagic);
+        uint32_t sum = 0;
+#pragma unroll
+        for (int c16 = 0; c16 < 2; ++c16) {
+          uint32_t bits[16];
+#if (HACK_ABL & 2)
+#pragma unroll
+          for (int kk = 0; kk < 16; ++kk) bits[kk] = __float_as_uint(s[16 * c16 + kk]);
+          if (false)
+#endif
+          if (!PSR) {
+#pragma unroll
+            for (int kk = 0; kk < 16; kk += 2) {
+              const float2 y =
+                  ptx::fadd2(ptx::ffma2(make_float2(s[16 * c16 + kk], s[16 * c16 + kk + 1]), inv2, nlo2), magic);
+              bits[kk] = __float_as_uint(y.x);
+              bits[kk + 1] = __float_as_uint(y.y);
+            }
+          } else {
+            // the paper's stochastic rounding for P (R6, selectable): floor(y) + [u < frac(y)],
+            // u from the position-keyed P stream (query position i, key t, global query head)
+            const uint32_t c3 = stream_c3(kc.layer, kTagP, kc.head_base * kc.G + hq);
+            const uint32_t rid = cv.rng_ids[slot];
+#pragma unroll
+            for (int k4 = 0; k4 < 16; k4 += 4) {
+              const int t = t0 + kb + 16 * c16 + k4;
+              const Philox4 rr = philox_block(kc.seed, rid, c3, ((uint64_t)i << 30) | (uint64_t)(t >> 2));
+              const float u4[4] = {u24(rr.x), u24(rr.y), u24(rr.z), u24(rr.w)};
+#pragma unroll
+              for (int e = 0; e < 4; ++e) {
+                const float y = fmaf(s[16 * c16 + k4 + e], pm.inv, nlo2.x);
+                const float fl = floorf(y);
+                bits[k4 + e] = (uint32_t)min(255, (int)fl + (u4[e] < y - fl ? 1 : 0));
+              }
+            }
+          }
+          uint32_t cw[4];
+#pragma unroll
+          for (int x4 = 0; x4 < 4; ++x4) {
+            // byte position p of this 16-key chunk holds local key perm_src(p)
+            const uint32_t lo2 =
+                ptx::prmt(bits[perm_src<BITS>(4 * x4 + 0)], bits[perm_src<BITS>(4 * x4 + 1)], 0x0040u);
+            const uint32_t hi2 =
+                ptx::prmt(bits[perm_src<BITS>(4 * x4 + 2)], bits[perm_src<BITS>(4 * x4 + 3)], 0x0040u);
+            cw[x4] = ptx::prmt(lo2, hi2, 0x5410u);
+            sum = __dp4a(cw[x4], 0x01010101u, sum);
+          }
+          *reinterpret_cast<uint4*>(sm.p[bj] + kmaj_off(r, kb + 16 * c16, 512)) =
+              make_uint4(cw[0] ^ 0x80808080u, cw[1] ^ 0x80808080u, cw[2] ^ 0x80808080u, cw[3] ^ 0x80808080u);
+          if (DBG && dbg_pcodes != nullptr && pos < L) {
+            uint8_t* dp = dbg_pcodes + ((int64_t)(start + pos) * kc.Hq + hq) * dbg_stride + t0 + kb + 16 * c16;
+#pragma unroll
+            for (int pos = 0; pos < 16; ++pos)
+              dp[perm_src<BITS>(pos)] = (uint8_t)((cw[pos >> 2] >> (8 * (pos & 3))) & 0xFF);
+          }
+        }
+        sm.sp_part[bj][sw][r] = (int)sum;
+        if (sw == 0) sm.pinfo[bj][r] = make_float4(al, resc ? 1.f : 0.f, pm.s, pm.m);
+        ptx::fence_proxy_async_smem();
+      } else {
+#pragma unroll
+        for (int kk = 0; kk < 32; ++kk) sm.ptail[r][kb + kk] = s[kk];
+        if (sw == 0) sm.pinfo[bj][r] = make_float4(al, resc ? 1.f : 0.f, 0.f, 0.f);
+      }
+      ptx::mbar_arrive(&sm.p_ready[bj]);  // for the MMA warp (PV)
+#if HACK_PRE_PBAR
+      ptx::named_bar_arrive(kPBar0 + bj, NSW + NOW);  // for the O warps (hardware barrier: no polling)
+#endif
+    }
+    sm.lpart[sw][r] = l_run;
+    ptx::mbar_arrive(&sm.l_ready);
+  } else {
+    // ------------------------------------------------------------------ O warpgroups (2)
+    // thread = query row r = TMEM lane; OW o owns output channels 64o..64o+63
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 128;");
+    const int ow = (warp - 12) >> 2;
+    const int r = (tid - 384) & (BM - 1);
+    const int pos = i0 + (r & (pbp - 1)), hq = hq0 + r / pbp;
+    const uint32_t lane_base = (uint32_t)(32 * (warp & 3)) << 16;
+    const int cb = 64 * ow;
+    float2 o2[32];  // channels cb + 2x, cb + 2x + 1
+#pragma unroll
+    for (int x = 0; x < 32; ++x) o2[x] = make_float2(0.f, 0.f);
+#pragma unroll 1
+    for (int j = 0; j < nkt; ++j) {
+      const int bj = j % NB, bd = j % NDB;
+      const uint32_t ph = (j / NB) & 1;
+#if HACK_PRE_PBAR
+      ptx::named_bar_sync(kPBar0 + bj, NSW + NOW);  // S warps' P' and row info of tile j
+      (void)ph;
+#else
+      rwait<4>(&sm.p_ready[bj], ph);
+#endif
+      const float4 pi4 = sm.pinfo[bj][r];
+      if (pi4.y != 0.f) {  // warp-uniform (lazy rescaling decided per S warp = same 32 rows)
+        const float2 al2 = make_float2(pi4.x, pi4.x);
+#pragma unroll
+        for (int x = 0; x < 32; ++x) o2[x] = ptx::fmul2(o2[x], al2);
+#if HACK_PRE_ORANK
+        if (j > 0 && j - 1 < nfull) {  // the O-rank accumulator (tiles < j) rescales too
+          rwait<4>(&sm.or_done, (j - 1) & 1);
+          ptx::tc_fence_after();
+#pragma unroll
+          for (int h = 0; h < 4; ++h) {
+            uint32_t d[16];
+            ptx::tmem_ld16(tOR + lane_base + cb + 16 * h, d);
+            ptx::tmem_wait_ld();
+#pragma unroll
+            for (int x = 0; x < 16; ++x) d[x] = __float_as_uint(__uint_as_float(d[x]) * pi4.x);
+            ptx::tmem_st16(tOR + lane_base + cb + 16 * h, d);
+          }
+          ptx::tmem_wait_st();
+        }
+#endif
+      }
+#if HACK_PRE_ORANK
+      if (j < nfull) {
+        if (ow == 0) {  // A operand row r of tile j: x_p and mu_p (Eq. 4 P side), split 3 ways
+          if (j > 0) rwait<4>(&sm.or_done, (j - 1) & 1);  // A of tile j - 1 consumed
+          const int sps0 = sm.sp_part[bj][0][r] + sm.sp_part[bj][1][r] - 128 * PI;
+          float av[16];
+          rank_a(pi4.z * (float)sps0, av);
+          rank_a(__fmaf_rn(128.f, pi4.z, pi4.w), av + 6);
+          av[12] = av[13] = av[14] = av[15] = 0.f;
+          uint8_t* oar = reinterpret_cast<uint8_t*>(sm.ora);
+#pragma unroll
+          for (int x = 0; x < 16; x += 4)
+            *reinterpret_cast<float4*>(oar + kmaj_off(r, 4 * x, 512)) =
+                make_float4(av[x], av[x + 1], av[x + 2], av[x + 3]);
+          ptx::fence_proxy_async_smem();
+        }
+        ptx::tc_fence_before();
+        // FIXME(experiment): one 256-count barrier for both O warpgroups lets warpgroup 1
+        // arrive for tile j + 1 before warpgroup 0 arrived for tile j (not observed in the
+        // tests); use one barrier per warpgroup before enabling this path
+        ptx::mbar_arrive(&sm.a_ready);
+      }
+#endif
+      if (j < nfull) {
+        // (a7) O += (s_p/2) s_v E + s_p SP_s m_v + mu_p y_v on D' of this tile
+        const int sps = sm.sp_part[bj][0][r] + sm.sp_part[bj][1][r] - 128 * PI;  // sum (p' - 128)
+        const float2 ap2 = make_float2(0.5f * pi4.z, 0.5f * pi4.z);
+        const float2 xp2 = make_float2(pi4.z * (float)sps, pi4.z * (float)sps);
+        const float mp = __fmaf_rn(128.f, pi4.z, pi4.w);
+        const float2 mp2 = make_float2(mp, mp);
+        rwait<4>(&sm.v_ready[bj], ph);
+        rwait<4>(&sm.d_full[bd], (j / NDB) & 1);
+        ptx::tc_fence_after();
+#pragma unroll
+        for (int h = 0; h < 4; ++h) {
+          uint32_t d[16];
+          ptx::tmem_ld16(tD0 + 128 * bd + lane_base + cb + 16 * h, d);
+          ptx::tmem_wait_ld();
+          if (DBG && dbg_pv != nullptr && pos < L && (acc_head < 0 || hq == acc_head)) {  // E' = 2 D' - 256 SV
+            const int hs = acc_head < 0 ? hq : 0, hn = acc_head < 0 ? kc.Hq : 1;
+            int32_t* dp = dbg_pv + (((int64_t)(start + pos) * hn + hs) * (acc_stride / PI) + j) * 128 + cb + 16 * h;
+#pragma unroll
+            for (int x = 0; x < 16; ++x) dp[x] = (int32_t)(d[x] - 0x4B400000u);
+          }
+#if (HACK_ABL & 1)
+          if (d[0] == 0x12345u) o2[h].x += 1.f;  // (ablation: no PV Eq. 4 math)
+#else
+#pragma unroll
+          for (int x4 = 0; x4 < 4; ++x4) {
+            const int c0 = cb + 16 * h + 4 * x4;
+            const float4 sv4 = *reinterpret_cast<const float4*>(&sm.vcf[bj][0][c0]);
+#if !HACK_PRE_ORANK
+            const float4 mv4 = *reinterpret_cast<const float4*>(&sm.vcf[bj][1][c0]);
+            const float4 y4 = *reinterpret_cast<const float4*>(&sm.vcf[bj][2][c0]);
+#endif
+#pragma unroll
+            for (int pr = 0; pr < 2; ++pr) {
+              const int xo = 4 * x4 + 2 * pr;
+              const int oi = 8 * h + 2 * x4 + pr;
+              const float2 E = acc2f(d[xo], d[xo + 1]);
+              const float2 svp = pr ? make_float2(sv4.z, sv4.w) : make_float2(sv4.x, sv4.y);
+              const float2 t = ptx::fmul2(svp, E);  // s_v 2D_s
+#if HACK_PRE_ORANK
+              o2[oi] = ptx::ffma2(ap2, t, o2[oi]);  // rank terms: TMEM accumulator (tensor pipe)
+#else
+              const float2 mvp = pr ? make_float2(mv4.z, mv4.w) : make_float2(mv4.x, mv4.y);
+              const float2 yp = pr ? make_float2(y4.z, y4.w) : make_float2(y4.x, y4.y);
+              float2 a = ptx::ffma2(ap2, t, o2[oi]);
+              a = ptx::ffma2(xp2, mvp, a);
+              o2[oi] = ptx::ffma2(mp2, yp, a);
+#endif
+            }
+          }
+#endif
+        }
+        ptx::tc_fence_before();
+        ptx::mbar_arrive(&sm.d_free[bd]);
+      } else {
+        // FP16 last V block (RQE): O += sum_t p~_t v_t in fp32
+        const int T = L - nfull * PI;
+        const __half* tail =
+            reinterpret_cast<const __half*>(cv.v_tail) + ((int64_t)slot * kc.Hkv + hk) * PI * 128 + cb;
+#pragma unroll 1
+        for (int t = 0; t < T; ++t) {
+          const float pt = sm.ptail[r][t];
+          const uint4* vr = reinterpret_cast<const uint4*>(tail + t * 128);
+#pragma unroll
+          for (int c8 = 0; c8 < 8; ++c8) {
+            const uint4 raw = vr[c8];
+            const __half2* h2 = reinterpret_cast<const __half2*>(&raw);
+#pragma unroll
+            for (int e = 0; e < 4; ++e)
+              o2[c8 * 4 + e] = ptx::ffma2(make_float2(pt, pt), __half22float2(h2[e]), o2[c8 * 4 + e]);
+          }
+        }
+      }
+      ptx::mbar_arrive(&sm.o_done[bj]);
+    }
+#if HACK_PRE_ORANK
+    const int nor = min(nkt, nfull);  // O-rank tiles of this CTA (its key tiles that are committed)
+    if (nor > 0) {  // add the O-side rank terms accumulated on the tensor pipe
+      rwait<4>(&sm.or_done, (nor - 1) & 1);
+      ptx::tc_fence_after();
+#pragma unroll
+      for (int h = 0; h < 4; ++h) {
+        uint32_t d[16];
+        ptx::tmem_ld16(tOR + lane_base + cb + 16 * h, d);
+        ptx::tmem_wait_ld();
+#pragma unroll
+        for (int x = 0; x < 8; ++x)
+          o2[8 * h + x] = ptx::fadd2(o2[8 * h + x], make_float2(__uint_as_float(d[2 * x]), __uint_as_float(d[2 * x + 1])));
+      }
+    }
+#endif
+    rwait<4>(&sm.l_ready, 0);
+    if (pos < L) {
+      const float inv_l = 1.f / (sm.lpart[0][r] + sm.lpart[1][r]);
+      const int64_t base = ((int64_t)(start + pos) * kc.Hq + hq) * 128 + cb;
+      if (kc.out_fp32) {
+        float4* op = reinterpret_cast<float4*>(reinterpret_cast<float*>(out) + base);
+#pragma unroll
+        for (int c4 = 0; c4 < 16; ++c4)
+          op[c4] = make_float4(o2[2 * c4].x * inv_l, o2[2 * c4].y * inv_l, o2[2 * c4 + 1].x * inv_l,
+                               o2[2 * c4 + 1].y * inv_l);
+      } else {
+        uint4* op = reinterpret_cast<uint4*>(reinterpret_cast<__half*>(out) + base);
+#pragma unroll
+        for (int c8 = 0; c8 < 8; ++c8) {
+          __half2 hh[4];
+#pragma unroll
+          for (int e = 0; e < 4; ++e) hh[e] = __floats2half2_rn(o2[4 * c8 + e].x * inv_l, o2[4 * c8 + e].y * inv_l);
+          op[c8] = *reinterpret_cast<uint4*>(hh);
+        }
+      }
+    }
+  }
+  ptx::tc_fence_before();
+  __syncthreads();
+  if (warp == 1) ptx::tmem_dealloc(tmem, 512);
+}
+
+template <int BITS>
+cudaError_t launch_t(const KernelCfg& kc, const void* q, const int32_t* cu, const int32_t* slots, int batch,
+                     int max_seqlen, const CacheView& cv, void* out, const hack_debug_t* dbg, cudaStream_t st) {
+  const size_t smem = sizeof(TcSmem<BITS>) + 1024;
+  const bool with_dbg = dbg != nullptr && (dbg->pcodes != nullptr || dbg->qk_acc != nullptr || dbg->pv_acc != nullptr);
+  const bool psr = kc.p_round == HACK_ROUND_STOCHASTIC;
+  auto kern = with_dbg ? (psr ? prefill_tc_kernel<BITS, true, true> : prefill_tc_kernel<BITS, true, false>)
+                       : (psr ? prefill_tc_kernel<BITS, false, true> : prefill_tc_kernel<BITS, false, false>);
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  const int gp = pack_heads(kc);
+  dim3 grid((max_seqlen + BM / gp - 1) / (BM / gp), kc.Hq / gp, batch);
+  kern<<<grid, kThreads, smem, st>>>(reinterpret_cast<const __half*>(q), cu, slots, cv, kc, out,
+                                     dbg ? dbg->pcodes : nullptr, dbg ? dbg->pcodes_stride : 0,
+                                     dbg ? dbg->qk_acc : nullptr, dbg ? dbg->pv_acc : nullptr,
+                                     dbg ? dbg->acc_stride : 0, dbg ? dbg->acc_head : -1);
+  note_launch();
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+bool prefill_tc_supported(const KernelCfg& kc) { return kc.Pi == 64 && kc.d == 128; }
+
+cudaError_t launch_prefill_tc(const KernelCfg& kc, const void* q, const int32_t* cu, const int32_t* slots, int batch,
+                              int max_seqlen, const CacheView& cv, void* out, const hack_debug_t* dbg,
+                              cudaStream_t st) {
+  if (kc.bits == 2) return launch_t<2>(kc, q, cu, slots, batch, max_seqlen, cv, out, dbg, st);
+  return launch_t<4>(kc, q, cu, slots, batch, max_seqlen, cv, out, dbg, st);
+}
+
+}  // namespace hack

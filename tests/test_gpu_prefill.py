@@ -152,17 +152,19 @@ def test_prefill_simt_baseline_kernel(monkeypatch):
         check_request(ocfg, i, *res)
 
 
-@pytest.mark.parametrize("L,Hq,Hkv,bits", [(300, 4, 2, 2), (513, 8, 2, 4), (64, 2, 1, 2)])
-def test_prefill_p_stochastic_rounding(L, Hq, Hkv, bits):
+@pytest.mark.parametrize("L,Hq,Hkv,bits,Pi", [(300, 4, 2, 2, 64), (513, 8, 2, 4, 64), (64, 2, 1, 2, 64),
+                                             (200, 4, 1, 2, 32), (300, 2, 1, 4, 128)])
+def test_prefill_p_stochastic_rounding(L, Hq, Hkv, bits, Pi):
     """R6 selectable: the paper's stochastic rounding for P with the
     position-keyed P stream; near-ties are judged against the SR boundary y - u integer."""
-    ocfg = att.Config(Hq=Hq, Hkv=Hkv, Pi=64, bits=bits, p_round="sr", seed=77)
+    ocfg = att.Config(Hq=Hq, Hkv=Hkv, Pi=Pi, bits=bits, p_round="sr", seed=77)
     res = run_prefill(ocfg, [L])
     check_request(ocfg, 0, *res)
 
 
-def test_prefill_p_sr_unsupported_on_the_cuda_core_kernel():
+def test_prefill_p_sr_unsupported_on_the_cuda_core_kernel(monkeypatch):
     h = hk()
+    monkeypatch.setenv("HACK_PREFILL_IMPL", "simt")   # the CUDA-core baseline has RN P only
     cfg = gpu_cfg(att.Config(Hq=2, Hkv=1, Pi=32, bits=2, p_round="sr"))
     cache = make_cache(cfg, 1, 64)
     q = torch.zeros((64, 2, 128), dtype=torch.float16, device="cuda")
