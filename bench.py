@@ -330,7 +330,7 @@ def run_disagg(args, rank, local_rank, world):
         vd = dev_normal((C5["dec_steps"], B, Hkv, 128), 702 + pair, dev)
         dout = torch.empty((B, Hq, 128), dtype=torch.float16, device=dev)
         slots = torch.arange(B, dtype=torch.int32, device=dev)
-        ws = torch.empty(max(h.decode_workspace_size(cfgs[0], B, maxL), 1), dtype=torch.uint8, device=dev)
+        ws = torch.zeros(max(h.decode_workspace_size(cfgs[0], B, maxL), 1), dtype=torch.uint8, device=dev)
         barrier(world)
         ev[0].record(stream)
         for i, L in enumerate(lens):
@@ -619,7 +619,7 @@ def run_sweep(args, h, dev, seed, flush):
             kn = dev_normal((n_dec, B, Hkv, 128), seed + 57, dev)
             vn = dev_normal((n_dec, B, Hkv, 128), seed + 58, dev)
             dout = torch.empty((B, Hq, 128), dtype=torch.float16, device=dev)
-            ws = torch.empty(max(h.decode_workspace_size(cfg, B, ctx + n_dec + 2), 1), dtype=torch.uint8,
+            ws = torch.zeros(max(h.decode_workspace_size(cfg, B, ctx + n_dec + 2), 1), dtype=torch.uint8,
                              device=dev)
             h.decode_append(cfg, kn[0], vn[0], slots, cache)
             h.decode_attention_cached(cfg, qn[0], slots, ctx + n_dec + 2, cache, dout, workspace=ws)
@@ -694,7 +694,7 @@ def run_c4(args, h, dev, world, seed, flush):
         kn = dev_normal((n_dec, B, Hkv, 128), seed + 45, dev)
         vn = dev_normal((n_dec, B, Hkv, 128), seed + 46, dev)
         dout = torch.empty((B, Hq, 128), dtype=torch.float16, device=dev)
-        ws = torch.empty(max(h.decode_workspace_size(cfg, B, L + n_dec + 2), 1), dtype=torch.uint8, device=dev)
+        ws = torch.zeros(max(h.decode_workspace_size(cfg, B, L + n_dec + 2), 1), dtype=torch.uint8, device=dev)
         h.decode_append(cfg, kn[0], vn[0], slots, cache)      # warm-up step
         h.decode_attention_cached(cfg, qn[0], slots, L + n_dec + 2, cache, dout, workspace=ws)
         torch.cuda.synchronize()
@@ -761,7 +761,7 @@ def run_decode(args, h, dev, rank, world, peaks, traffic, seed, flush):
     vn = dev_normal((nsteps, B, Hkv, 128), seed + 302, dev)
     out = torch.empty((B, Hq, 128), dtype=torch.float16, device=dev)
     ws_bytes = h.decode_workspace_size(cfg, B, max_len)
-    ws = torch.empty(max(ws_bytes, 1), dtype=torch.uint8, device=dev)
+    ws = torch.zeros(max(ws_bytes, 1), dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream()
     it = [0]
 

@@ -24,7 +24,7 @@ for _ in range(nl):
 qn = torch.randn((steps * 3, B, Hkv * G, 128), device="cuda").half()
 kn = torch.randn((steps * 3, B, Hkv, 128), device="cuda").half()
 out = torch.empty((B, Hkv * G, 128), dtype=torch.float16, device="cuda")
-ws = torch.empty(h.decode_workspace_size(cfg, B, ctx + steps * 4 + Pi), dtype=torch.uint8, device="cuda")
+ws = torch.zeros(h.decode_workspace_size(cfg, B, ctx + steps * 4 + Pi), dtype=torch.uint8, device="cuda")
 ML = ctx + steps * 4 + Pi
 for i in range(3):
     h.decode_append(cfg, kn[i], kn[i], slots, caches[i % nl])
