@@ -36,9 +36,6 @@ import numpy as np  # noqa: E402
 C2 = dict(Hq=32, Hkv=8, L=4096, Pi=64, bits=2)
 C3 = dict(Hq=32, Hkv=8, B=64, ctx=8192, Pi=64, bits=2)
 C4 = dict(Hq=64, Hkv=8, L=32768, B=16, Pi=64)
-# C5 (BASELINE configs[4]): disaggregated prefill -> decode over NVLink, mixed-length trace;
-# per prefill/decode pair: `reqs` requests of a `layers`-layer Mistral-shaped model
-C5 = dict(Hq=32, Hkv=8, Pi=64, bits=2, layers=4, reqs=8, lmin=512, lmax=8192, dec_steps=16)
 WORKLOAD = ("C2: Mistral-7B-shaped homomorphic prefill attention (32 Q / 8 KV heads, d=128), "
             "one 4096-token causal prompt, 2-bit K/V, Pi=64, Q/P 8-bit")
 DECODE_WORKLOAD = ("C3: Llama-3.1-8B-shaped decode attention (32 Q / 8 KV heads, d=128), batch 64, "
@@ -231,167 +228,6 @@ def run_reference(args, rank):
 
 
 # ----------------------------------------------------------------------------- HACK arm
-
-def c5_trace(pair):
-    """Seeded mixed-length prompt lengths of one prefill -> decode pair (ragged tails)."""
-    import numpy as np
-    rng = np.random.default_rng(5000 + pair)
-    blocks = rng.integers(C5["lmin"] // 64, C5["lmax"] // 64 + 1, C5["reqs"])
-    return [int(b * 64 - t) for b, t in zip(blocks, rng.integers(0, 64, C5["reqs"]))]
-
-
-def run_disagg(args, rank, local_rank, world):
-    """C5: ranks 0..N/2-1 prefill, ranks N/2..N-1 decode; rank p sends its requests' packed
-    KV (all layers, hack_kv_send: pages + meta + cached sums + FP16 tail + header) to rank
-    p + N/2 (hack_kv_recv validates the header on the device and scatters into that rank's
-    paged cache), which then runs C5["dec_steps"] batched decode steps over all layers.
-    The trace (prompt lengths, inputs) is seeded per pair, so both sides know every length.
-    Transport: the library's NCCL comm (kv_send / kv_recv) with --dist-backend nccl; with
-    gloo (several ranks on one GPU, tests) hack_kv_pack -> host send/recv -> hack_kv_unpack.
-    Timed from a common barrier with CUDA events; JCT = max over ranks."""
-    import numpy as np
-    import torch
-    import torch.distributed as dist
-
-    from paper_2502_03589_b200 import hack as h
-
-    if world < 2 or world % 2:
-        raise SystemExit("--mode disagg needs an even number of ranks >= 2")
-    dev = torch.device("cuda", local_rank)
-    P = world // 2
-    prefill = rank < P
-    pair = rank % P
-    peer = rank + P if prefill else rank - P
-    Hq, Hkv, Pi, layers, R = C5["Hq"], C5["Hkv"], C5["Pi"], C5["layers"], C5["reqs"]
-    lens = c5_trace(pair)
-    maxL = max(lens) + C5["dec_steps"] + 1
-    mp = (maxL + Pi - 1) // Pi
-    cfgs = [h.config(num_q_heads=Hq, num_kv_heads=Hkv, partition=Pi, kv_bits=C5["bits"], out_fp32=False, layer=l)
-            for l in range(layers)]
-    first = h.KVCache.allocate(cfgs[0], R, mp, device=dev)
-    caches = [first] + [h.KVCache.allocate(cfgs[l], R, mp, num_pages=first.pages.shape[0], shared_tables=first,
-                                           device=dev) for l in range(1, layers)]
-    rids = [7 * pair + i for i in range(R)]
-    nccl = args.dist_backend == "nccl"
-    pull = args.transport == "pull"
-    comm = None
-    if pull:  # the decode rank maps the prefill rank's caches through CUDA IPC (peer memory)
-        from torch.multiprocessing.reductions import reduce_tensor
-        mine = ([[reduce_tensor(t) for t in (c.pages, c.v_tail, c.block_table, c.seq_lens, c.rng_ids)]
-                 for c in caches] if prefill else None)
-        shared = [None] * world
-        dist.all_gather_object(shared, mine)
-        if not prefill:
-            remote = [h.KVCache(cfgs[l], *[fn(*a) for fn, a in shared[peer][l]]) for l in range(layers)]
-    elif nccl:  # one 2-rank NCCL communicator per prefill/decode pair, ids exchanged over the group
-        uid = h.comm_unique_id() if prefill else None
-        ids = [None] * world
-        dist.all_gather_object(ids, uid)
-        comm = h.comm_init(2, 0 if prefill else 1, ids[pair])
-    stream = torch.cuda.current_stream()
-    staging = [torch.empty(h.kv_transfer_bytes(cfgs[0], layers, L), dtype=torch.uint8, device=dev) for L in lens]
-    ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
-    res = {}
-    if prefill:
-        qkv = [[(dev_normal((L, Hq, 128), 900 + 97 * pair + 13 * i + l, dev),
-                 dev_normal((L, Hkv, 128), 901 + 97 * pair + 13 * i + l, dev),
-                 dev_normal((L, Hkv, 128), 902 + 97 * pair + 13 * i + l, dev)) for l in range(layers)]
-               for i, L in enumerate(lens)]
-        out = torch.empty((max(lens), Hq, 128), dtype=torch.float16, device=dev)
-        first.rng_ids.copy_(torch.tensor(rids, dtype=torch.int32, device=dev))
-        barrier(world)
-        ev[0].record(stream)
-        for i, L in enumerate(lens):
-            cu = torch.tensor([0, L], dtype=torch.int32, device=dev)
-            sl = torch.tensor([i], dtype=torch.int32, device=dev)
-            for l in range(layers):
-                q, k, v = qkv[i][l]
-                h.prefill_attention(cfgs[l], q, k, v, cu, sl, L, caches[l], out[:L])
-            if pull:  # tell the decode rank that request i is complete (its pull reads our memory)
-                torch.cuda.synchronize()
-                dist.send(torch.tensor([i], dtype=torch.int32, device=dev if nccl else "cpu"), dst=peer)
-            elif nccl:
-                h.kv_send(comm, 1, cfgs[0], caches, i, L, first_token=i, rng_id=rids[i], staging=staging[i])
-            else:
-                h.kv_pack(cfgs[0], caches, i, L, first_token=i, rng_id=rids[i], staging=staging[i])
-                dist.send(staging[i].cpu(), dst=peer)
-        ev[1].record(stream)
-        torch.cuda.synchronize()
-        pre_ms = ev[0].elapsed_time(ev[1])
-        ops = sum(prefill_ops(L, Hq) for L in lens) * layers
-        res = {"role": "prefill", "ms": pre_ms, "prefill_tops_incl_send": ops / (pre_ms * 1e-3) / 1e12,
-               "wire_bytes": sum(int(b.numel()) for b in staging)}
-        jct = pre_ms
-    else:
-        status = torch.zeros((R, 2), dtype=torch.int32, device=dev)
-        B = R
-        qd = dev_normal((C5["dec_steps"], B, Hq, 128), 700 + pair, dev)
-        kd = dev_normal((C5["dec_steps"], B, Hkv, 128), 701 + pair, dev)
-        vd = dev_normal((C5["dec_steps"], B, Hkv, 128), 702 + pair, dev)
-        dout = torch.empty((B, Hq, 128), dtype=torch.float16, device=dev)
-        slots = torch.arange(B, dtype=torch.int32, device=dev)
-        ws = torch.zeros(max(h.decode_workspace_size(cfgs[0], B, maxL), 1), dtype=torch.uint8, device=dev)
-        barrier(world)
-        ev[0].record(stream)
-        for i, L in enumerate(lens):
-            if pull:
-                t = torch.zeros(1, dtype=torch.int32, device=dev if nccl else "cpu")
-                dist.recv(t, src=peer)
-                h.kv_pull(cfgs[0], remote, caches, i, i, L)
-                status[i, 1] = i
-            elif nccl:
-                h.kv_recv(comm, 0, cfgs[0], caches, i, L, staging[i], status=status[i])
-            else:
-                buf = torch.empty(staging[i].numel(), dtype=torch.uint8)
-                dist.recv(buf, src=peer)
-                staging[i].copy_(buf)
-                h.kv_unpack(cfgs[0], caches, i, L, staging[i], status=status[i])
-        ev[1].record(stream)
-        # every append advances seq_lens: each layer decodes on its own copy (hack.h, a8)
-        import dataclasses
-        dcaches = [dataclasses.replace(c_, seq_lens=first.seq_lens.clone()) for c_ in caches]
-        for s in range(C5["dec_steps"]):
-            for l in range(layers):
-                h.decode_attention(cfgs[l], qd[s], kd[s], vd[s], slots, maxL, dcaches[l], dout, workspace=ws)
-        ev[2].record(stream)
-        torch.cuda.synchronize()
-        st = status.cpu().tolist()
-        if any(x[0] != 0 or x[1] != i for i, x in enumerate(st)):
-            raise RuntimeError(f"C5: kv_recv status {st}")
-        recv_ms, dec_ms = ev[0].elapsed_time(ev[1]), ev[1].elapsed_time(ev[2])
-        res = {"role": "decode", "recv_ms": recv_ms, "decode_ms": dec_ms,
-               "decode_tokens_per_s": B * C5["dec_steps"] / (dec_ms * 1e-3)}
-        jct = recv_ms + dec_ms
-    if pull:
-        dist.barrier()  # the prefill ranks keep their caches mapped until every pull finished
-        if not prefill:
-            del remote
-    all_res = [None] * world
-    dist.all_gather_object(all_res, res)
-    jct_max = max_over_ranks(jct, world)
-    if comm is not None:
-        h.comm_destroy(comm)
-    if rank == 0:
-        pre = [r for r in all_res if r["role"] == "prefill"]
-        dec = [r for r in all_res if r["role"] == "decode"]
-        tokens = world // 2 * R * C5["dec_steps"]
-        line = {"metric": "C5 disaggregated trace: generated tokens/s", "value": tokens / (jct_max * 1e-3),
-                "unit": "tokens/s", "n_gpus": world, "higher_is_better": True, "scaling": "weak",
-                "vs_baseline": None, "dtype": "u8", "data": "synthetic",
-                "config": {"workload": f"C5: {P} prefill + {P} decode ranks, {R} mixed-length requests per pair "
-                                       f"({C5['lmin']}-{C5['lmax']} tokens), {layers} layers x {Hq}/{Hkv} heads, "
-                                       f"2-bit, {C5['dec_steps']} decode steps",
-                           "transport": ("hack_kv_pull over CUDA IPC peer memory (fused, no staging)" if pull else
-                                         "hack_kv_send/recv (NCCL p2p)" if nccl else "kv_pack + gloo host send/recv"),
-                           "lengths_pair0": c5_trace(0)},
-                "jct_ms": jct_max,
-                "prefill_tops_incl_send": sum(r["prefill_tops_incl_send"] for r in pre),
-                "wire_bytes": sum(r["wire_bytes"] for r in pre),
-                "transfer_wait_ms_max": max(r["recv_ms"] for r in dec),
-                "decode_tokens_per_s": sum(r["decode_tokens_per_s"] for r in dec),
-                "per_rank": all_res}
-        print(json.dumps(line), flush=True)
-
 
 def run_hack(args, rank, local_rank, world):
     import torch
@@ -1001,8 +837,12 @@ def main():
                     help="decode: launch eagerly instead of replaying a CUDA graph of the K timed steps")
     ap.add_argument("--mode", default="flagship", choices=["flagship", "disagg"],
                     help="disagg: the C5 disaggregated prefill -> decode trace (needs an even N >= 2)")
-    ap.add_argument("--transport", default="nccl", choices=["nccl", "pull"],
-                    help="disagg: packed KV over the library's NCCL send/recv, or hack_kv_pull on CUDA IPC peer memory")
+    ap.add_argument("--c5-reqs", type=int, default=32, help="disagg: requests in the trace")
+    ap.add_argument("--c5-layers", type=int, default=4, help="disagg: layers of the attention stack")
+    ap.add_argument("--c5-load", type=float, default=0.9, help="disagg: arrival rate / calibrated prefill capacity")
+    ap.add_argument("--c5-max-prompt", type=int, default=16384, help="disagg: prompt length cap")
+    ap.add_argument("--c5-max-output", type=int, default=256, help="disagg: output length cap")
+    ap.add_argument("--c5-seed", type=int, default=20250205)
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                     help="process-group backend for barriers / max-over-ranks (gloo: several ranks on one GPU, tests)")
     args = ap.parse_args()
@@ -1032,7 +872,8 @@ def main():
         local_rank = local_dev
     try:
         if args.mode == "disagg":
-            run_disagg(args, rank, local_rank, world)
+            import bench_c5
+            bench_c5.run(args, rank, local_rank, world, barrier, dev_normal)
         else:
             run_hack(args, rank, local_rank, world)
     finally:
