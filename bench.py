@@ -5,10 +5,11 @@
     torchrun --nproc-per-node N bench.py --gpus N ...    (one rank per GPU)
 
 Workload (BASELINE.json configs[1], "C2"): Mistral-7B-shaped homomorphic prefill --
-32 Q / 8 KV heads, d=128, one 4096-token prompt, 2-bit K/V, Pi=64.  One step =
-hack_cache_ingest (a1, a2: quantize K/V into pages + FP16 tail) +
-hack_prefill_attention_cached (a3-a7: Q quant, Eq. 4 Q'K'^T, online softmax, P quant,
-Eq. 4 P'V' + FP tail).  The decode rows (a8, a9) are timed in the same run on
+32 Q / 8 KV heads, d=128, one 4096-token prompt, 2-bit K/V, Pi=64.  One step = one
+hack_prefill_attention call: the ingest (a1, a2: quantize K/V into pages + FP16 tail), then
+the attention kernel (a3-a7: Q quant, Eq. 4 Q'K'^T, online softmax, P quant, Eq. 4 P'V' + FP
+tail) launched as a programmatic dependent of the ingest.  The roofline times the attention
+kernel alone (hack_prefill_attention_cached, separate launches).  The decode rows (a8, a9) are timed in the same run on
 configs[2] ("C3": Llama-3.1-8B-shaped decode, batch 64, context 8192) and reported
 under "decode".  Headline: algorithmic int8 ops (2 matmuls x 2*d*L(L+1)/2 x H_q,
 causal triangle) / step time, in TOPS.  Multi-GPU: weak scaling, every rank runs its
@@ -258,30 +259,40 @@ def run_hack(args, rank, local_rank, world):
     ops = prefill_ops(L, Hq)
 
     def prefill_step(evs=None):
+        # one hack_prefill_attention call: ingest (a1, a2) + attention (a3-a7), the attention
+        # kernel a programmatic dependent of the ingest (its Q quantization overlaps it)
         if evs:
             evs[0].record(stream)
-        h.cache_ingest(cfg, k, v, cu, slots, L, cache)
+        h.prefill_attention(cfg, q, k, v, cu, slots, L, cache, out, workspace=ws)
         if evs:
             evs[1].record(stream)
+
+    def attn_only(evs):
+        # the attention kernel alone (the roofline's kernel), on the ingested cache
+        evs[0].record(stream)
         h.prefill_attention_cached(cfg, q, cu, slots, L, cache, out, workspace=ws)
-        if evs:
-            evs[2].record(stream)
+        evs[1].record(stream)
 
     for _ in range(args.warmup):
         flush.fill_(1)
         prefill_step()
     barrier(world)
     n0 = h.kernel_launches()
-    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in range(args.steps)]
+    evk = [[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in range(args.steps)]
     with ClockSampler(local_rank) as clk:
         barrier(world)
         for i in range(args.steps):
             flush.fill_(1)                      # L2 flush, outside the events
             prefill_step(evs[i])
         barrier(world)
-    launches = h.kernel_launches() - n0
-    step_ms = [e[0].elapsed_time(e[2]) for e in evs]
-    attn_ms = [e[1].elapsed_time(e[2]) for e in evs]
+        launches = h.kernel_launches() - n0
+        for i in range(args.steps):
+            flush.fill_(1)
+            attn_only(evk[i])
+        barrier(world)
+    step_ms = [e[0].elapsed_time(e[1]) for e in evs]
+    attn_ms = [e[0].elapsed_time(e[1]) for e in evk]
     ms = max_over_ranks(sum(step_ms) / len(step_ms), world)
     attn_avg = max_over_ranks(sum(attn_ms) / len(attn_ms), world)
     value = ops * world / (ms * 1e-3) / 1e12

@@ -303,7 +303,7 @@ hack_status_t hack_prefill_attention(const hack_config_t* cfg, const void* q, co
       HACK_OK)
     return st;
   return cuda_status(launch_prefill_attention(kc, q, cu, slots, batch, max_seqlen, cv, out, ws, dbg,
-                                              (cudaStream_t)stream),
+                                              (cudaStream_t)stream, /*pdl=*/true),
                      "prefill_attention");
 }
 

@@ -19,7 +19,7 @@ bool prefill_tc_supported(const KernelCfg& kc);
 
 cudaError_t launch_prefill_tc(const KernelCfg& kc, const void* q, const int32_t* cu, const int32_t* slots, int batch,
                               int max_seqlen, const CacheView& cv, void* out, const hack_debug_t* dbg,
-                              cudaStream_t st);
+                              cudaStream_t st, bool pdl);
 cudaError_t launch_decode_simt(const KernelCfg& kc, const void* q_new, const int32_t* slots, int batch,
                                const CacheView& cv, void* out, const hack_debug_t* dbg, cudaStream_t st);
 
@@ -51,10 +51,10 @@ size_t prefill_workspace_bytes(const KernelCfg& kc, int batch, int max_seqlen) {
 
 cudaError_t launch_prefill_attention(const KernelCfg& kc, const void* q, const int32_t* cu_seqlens,
                                      const int32_t* slots, int batch, int max_seqlen, const CacheView& cv,
-                                     void* out, void* workspace, const hack_debug_t* dbg, cudaStream_t st) {
+                                     void* out, void* workspace, const hack_debug_t* dbg, cudaStream_t st, bool pdl) {
   (void)workspace;
   if (prefill_tc_supported(kc) && !env_is("HACK_PREFILL_IMPL", "simt")) {
-    return launch_prefill_tc(kc, q, cu_seqlens, slots, batch, max_seqlen, cv, out, dbg, st);
+    return launch_prefill_tc(kc, q, cu_seqlens, slots, batch, max_seqlen, cv, out, dbg, st, pdl);
   }
   return launch_prefill_simt(kc, q, cu_seqlens, slots, batch, max_seqlen, cv, out, dbg, st);
 }

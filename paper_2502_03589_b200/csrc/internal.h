@@ -41,9 +41,11 @@ cudaError_t launch_append(const KernelCfg& kc, const void* k_new, const void* v_
                           int batch, const CacheView& cv, cudaStream_t st);
 
 size_t prefill_workspace_bytes(const KernelCfg& kc, int batch, int max_seqlen);
+// pdl: launched right after this call's ingest on the same stream (programmatic dependent)
 cudaError_t launch_prefill_attention(const KernelCfg& kc, const void* q, const int32_t* cu_seqlens,
                                      const int32_t* slots, int batch, int max_seqlen, const CacheView& cv,
-                                     void* out, void* workspace, const hack_debug_t* dbg, cudaStream_t st);
+                                     void* out, void* workspace, const hack_debug_t* dbg, cudaStream_t st,
+                                     bool pdl = false);
 
 size_t decode_workspace_bytes(const KernelCfg& kc, int batch, int max_seqlen);
 // hack_acc_form_t of the kernel the next prefill (op 0) / decode (op 1) call dispatches to

@@ -273,6 +273,9 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_tc_kernel(
     asm volatile("setmaxnreg.dec.sync.aligned.u32 40;");
     if (warp == 0) {
       // ---------------------------------------------------------------- producer
+      // launched as a programmatic dependent of the ingest (hack_prefill_attention): the
+      // pages are read only after that grid completed
+      asm volatile("griddepcontrol.wait;" ::: "memory");
       if (lane == 0) {
         const int32_t* bt = cv.block_table + (int64_t)slot * cv.max_pages_per_req;
         for (int j = 0; j < nkt; ++j) {
@@ -743,6 +746,7 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_tc_kernel(
     // ------------------------------------------------------------------ O warpgroups (2)
     // thread = query row r = TMEM lane; OW o owns output channels 64o..64o+63
     asm volatile("setmaxnreg.inc.sync.aligned.u32 128;");
+    asm volatile("griddepcontrol.wait;" ::: "memory");  // the FP16 tail is the ingest's output too
     const int ow = (warp - 12) >> 2;
     const int r = (tid - 384) & (BM - 1);
     const int pos = i0 + (r & (pbp - 1)), hq = hq0 + r / pbp;
@@ -869,7 +873,8 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_tc_kernel(
 
 template <int PI_, int BITS>
 cudaError_t launch_t(const KernelCfg& kc, const void* q, const int32_t* cu, const int32_t* slots, int batch,
-                     int max_seqlen, const CacheView& cv, void* out, const hack_debug_t* dbg, cudaStream_t st) {
+                     int max_seqlen, const CacheView& cv, void* out, const hack_debug_t* dbg, cudaStream_t st,
+                     bool pdl) {
   if (kc.pl.page_bytes != Geo<PI_, BITS>::PB) return cudaErrorInvalidValue;  // layout drift guard
   const size_t smem = sizeof(TcSmem<PI_, BITS>) + 1024;
   const bool with_dbg = dbg != nullptr && (dbg->pcodes != nullptr || dbg->qk_acc != nullptr || dbg->pv_acc != nullptr);
@@ -879,11 +884,25 @@ cudaError_t launch_t(const KernelCfg& kc, const void* q, const int32_t* cu, cons
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   const int gp = pack_heads(kc);
-  dim3 grid((max_seqlen + BM / gp - 1) / (BM / gp), kc.Hq / gp, batch);
-  kern<<<grid, kThreads, smem, st>>>(reinterpret_cast<const __half*>(q), cu, slots, cv, kc, out,
-                                     dbg ? dbg->pcodes : nullptr, dbg ? dbg->pcodes_stride : 0,
-                                     dbg ? dbg->qk_acc : nullptr, dbg ? dbg->pv_acc : nullptr,
-                                     dbg ? dbg->acc_stride : 0, dbg ? dbg->acc_head : -1);
+  cudaLaunchConfig_t lc = {};
+  lc.gridDim = dim3((max_seqlen + BM / gp - 1) / (BM / gp), kc.Hq / gp, batch);
+  lc.blockDim = dim3(kThreads);
+  lc.dynamicSmemBytes = smem;
+  lc.stream = st;
+  // pdl: a programmatic dependent of the ingest just launched on `st` (hack_prefill_attention):
+  // the Q quantization prologue (which reads only q and rng_ids) overlaps the ingest; the
+  // producer and O warps wait in griddepcontrol.wait before they read pages or the FP16 tail.
+  // Without pdl griddepcontrol.wait returns at once (the stream order already holds).
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  lc.attrs = at;
+  lc.numAttrs = pdl ? 1 : 0;
+  e = cudaLaunchKernelEx(&lc, kern, reinterpret_cast<const __half*>(q), cu, slots, cv, kc, out,
+                         dbg ? dbg->pcodes : (uint8_t*)nullptr, dbg ? dbg->pcodes_stride : (int64_t)0,
+                         dbg ? dbg->qk_acc : (int32_t*)nullptr, dbg ? dbg->pv_acc : (int32_t*)nullptr,
+                         dbg ? dbg->acc_stride : (int64_t)0, dbg ? dbg->acc_head : -1);
+  if (e != cudaSuccess) return e;
   note_launch();
   return cudaGetLastError();
 }
@@ -896,14 +915,14 @@ bool prefill_tc_supported(const KernelCfg& kc) {
 
 cudaError_t launch_prefill_tc(const KernelCfg& kc, const void* q, const int32_t* cu, const int32_t* slots, int batch,
                               int max_seqlen, const CacheView& cv, void* out, const hack_debug_t* dbg,
-                              cudaStream_t st) {
+                              cudaStream_t st, bool pdl) {
   switch (kc.Pi * 8 + kc.bits) {
-    case 32 * 8 + 2: return launch_t<32, 2>(kc, q, cu, slots, batch, max_seqlen, cv, out, dbg, st);
-    case 32 * 8 + 4: return launch_t<32, 4>(kc, q, cu, slots, batch, max_seqlen, cv, out, dbg, st);
-    case 64 * 8 + 2: return launch_t<64, 2>(kc, q, cu, slots, batch, max_seqlen, cv, out, dbg, st);
-    case 64 * 8 + 4: return launch_t<64, 4>(kc, q, cu, slots, batch, max_seqlen, cv, out, dbg, st);
-    case 128 * 8 + 2: return launch_t<128, 2>(kc, q, cu, slots, batch, max_seqlen, cv, out, dbg, st);
-    case 128 * 8 + 4: return launch_t<128, 4>(kc, q, cu, slots, batch, max_seqlen, cv, out, dbg, st);
+    case 32 * 8 + 2: return launch_t<32, 2>(kc, q, cu, slots, batch, max_seqlen, cv, out, dbg, st, pdl);
+    case 32 * 8 + 4: return launch_t<32, 4>(kc, q, cu, slots, batch, max_seqlen, cv, out, dbg, st, pdl);
+    case 64 * 8 + 2: return launch_t<64, 2>(kc, q, cu, slots, batch, max_seqlen, cv, out, dbg, st, pdl);
+    case 64 * 8 + 4: return launch_t<64, 4>(kc, q, cu, slots, batch, max_seqlen, cv, out, dbg, st, pdl);
+    case 128 * 8 + 2: return launch_t<128, 2>(kc, q, cu, slots, batch, max_seqlen, cv, out, dbg, st, pdl);
+    case 128 * 8 + 4: return launch_t<128, 4>(kc, q, cu, slots, batch, max_seqlen, cv, out, dbg, st, pdl);
     default: return cudaErrorInvalidValue;
   }
 }

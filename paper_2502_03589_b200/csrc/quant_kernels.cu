@@ -130,6 +130,7 @@ __global__ void __launch_bounds__(128) ingest_v_kernel(const __half* __restrict_
                                                        const int32_t* __restrict__ cu_seqlens,
                                                        const int32_t* __restrict__ slots, CacheView cv,
                                                        KernelCfg kc) {
+  asm volatile("griddepcontrol.launch_dependents;");  // (prefill attention, see ingest_kv64_kernel)
   const int b = blockIdx.y;
   const int start = cu_seqlens[b], L = cu_seqlens[b + 1] - start;
   const int slot = slots[b];
@@ -255,6 +256,7 @@ __global__ void __launch_bounds__(128) ingest_v64_kernel(const __half* __restric
                                                          const int32_t* __restrict__ cu_seqlens,
                                                          const int32_t* __restrict__ slots, CacheView cv,
                                                          KernelCfg kc) {
+  asm volatile("griddepcontrol.launch_dependents;");
   __shared__ V64Red red;
   ingest_v64_body<BITS>(v, cu_seqlens, slots, cv, kc, blockIdx.x, blockIdx.y, threadIdx.x, 0, red);
 }
@@ -267,6 +269,10 @@ __global__ void __launch_bounds__(256) ingest_kv64_kernel(const __half* __restri
                                                           const int32_t* __restrict__ cu_seqlens,
                                                           const int32_t* __restrict__ slots, CacheView cv,
                                                           KernelCfg kc, int nk, int nv) {
+  // the prefill attention kernel is launched as a programmatic dependent of the ingest
+  // (hack_prefill_attention): let it start its Q quantization now; it reads the cache only
+  // after griddepcontrol.wait, i.e. after this grid completed
+  asm volatile("griddepcontrol.launch_dependents;");
   __shared__ V64Red red[2];
   if ((int)blockIdx.x < nk) {
     ingest_k_body<BITS>(k, cu_seqlens, slots, cv, kc, blockIdx.x, blockIdx.y, threadIdx.x);
