@@ -34,6 +34,7 @@
 // exceeds it by more than 8 (log2 units; p~ <= 256), warp-uniformly, so most tiles skip the
 // O *= alpha pass.  P' codes are invariant to the row scale (R13).
 // TMEM (512 columns): S (d/Pi x BN = 128) | R (BN) | D'[2] (2 x 128).
+#include <cstdlib>
 #include "common.cuh"
 #include "internal.h"
 #include "tc_common.cuh"
@@ -105,7 +106,7 @@ struct TcSmem {
   float2 xch[2][2][BM];                      // partial (max, min | -inf if masked); Q meta at Pi = 128
   float lpart[2][BM];
   uint64_t full[NS], empty[NS], k_ready[NB], k_free[NB], v_ready[NB], o_done[NB], p_ready[NB], d_full[2],
-      d_free[2], s_full, s_free, q_ready, l_ready;
+      d_free[2], s_full, s_free, q_ready, l_ready, l_free;
   uint32_t tmem_base;
 };
 
@@ -206,7 +207,7 @@ template <int PI_, int BITS, bool DBG, bool PSR>
 __global__ void __launch_bounds__(kThreads, 1) prefill_tc_kernel(
     const __half* __restrict__ q, const int32_t* __restrict__ cu_seqlens, const int32_t* __restrict__ slots,
     CacheView cv, KernelCfg kc, void* __restrict__ out, uint8_t* __restrict__ dbg_pcodes, int64_t dbg_stride,
-    int32_t* __restrict__ dbg_qk, int32_t* __restrict__ dbg_pv, int64_t acc_stride, int acc_head) {
+    int32_t* __restrict__ dbg_qk, int32_t* __restrict__ dbg_pv, int64_t acc_stride, int acc_head, int nitems) {
   using Gm = Geo<PI_, BITS>;
   using SM = TcSmem<PI_, BITS>;
   constexpr int PI = Gm::PI, BN = Gm::BN, NBETA = Gm::NBETA, KPT = Gm::KPT, NS = Gm::NS, NB = Gm::NB;
@@ -215,27 +216,50 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_tc_kernel(
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   SM& sm = *reinterpret_cast<SM*>(smem_raw);
 
-  // Block order: linear id -> (rank, head) with the head fastest, so the whole grid runs
-  // heaviest-first (longest causal rows of every head before any lighter tile): greedy
-  // block scheduling then balances the SMs (LPT), ~15% shorter than per-head ordering.
-  const int b = blockIdx.z;
-  // GQA row packing: the 128 MMA rows are gp query heads (of one KV head) x pbp positions,
-  // so the K'/V' tiles a CTA unpacks serve gp heads and the causal diagonal is pbp wide.
+  // Work items: (request, query-tile rank, head pair); rank 0 = the heaviest (longest causal
+  // rows).  GQA row packing: the 128 MMA rows are gp query heads (of one KV head) x pbp
+  // positions, so the K'/V' tiles a CTA unpacks serve gp heads and the causal diagonal is pbp
+  // wide.  Persistent launch (nitems > 0, one request): CTA c runs items c, 2G-1-c, 2G+c, ...
+  // of the heaviest-first order (a snake over the G CTAs balances the causal triangle), the
+  // next item's pages, Q quantization and first tiles overlapping the previous item's drain
+  // (no per-CTA launch, TMEM allocation and pipeline fill per item).  Otherwise one item per
+  // CTA from the grid (head pair fastest, heaviest first).
   const int gp = pack_heads(kc), pbp = BM / gp;
-  const int lin = blockIdx.x + gridDim.x * blockIdx.y;
   const int npk = kc.Hq / gp;
-  const int rank = lin / npk, hq0 = (lin % npk) * gp;  // heads hq0 .. hq0 + gp - 1
-  const int start = cu_seqlens[b], L = cu_seqlens[b + 1] - start;
-  const int nqt = (L + pbp - 1) / pbp;
-  if (rank >= nqt) return;
-  const int qt = nqt - 1 - rank;  // heavy (long causal rows) tiles first
-  const int i0 = qt * pbp;        // first position of the CTA
-  const int slot = slots[b];
-  const int hk = hq0 / kc.G;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int nkt = min((i0 + pbp - 1) / BN, (L - 1) / BN) + 1;  // key tiles (causal)
-  const int nfull = L / PI;                                    // committed V blocks
   const PageLayout PL = kc.pl;
+  struct Item {
+    int start, L, i0, hq0, hk, slot, nkt, nfull;
+  };
+  auto get_item = [&](int it, Item& w) -> bool {
+    int b, lin;
+    if (nitems > 0) {
+      const int G = gridDim.x, c = blockIdx.x;
+      lin = it * G + ((it & 1) ? G - 1 - c : c);
+      if (lin >= nitems) return false;
+      b = 0;
+    } else {
+      if (it > 0) return false;
+      b = blockIdx.z;
+      lin = blockIdx.x + gridDim.x * blockIdx.y;
+    }
+    const int rank = lin / npk;
+    w.hq0 = (lin % npk) * gp;  // heads hq0 .. hq0 + gp - 1
+    w.start = cu_seqlens[b];
+    w.L = cu_seqlens[b + 1] - w.start;
+    const int nqt = (w.L + pbp - 1) / pbp;
+    if (rank >= nqt) return false;
+    w.i0 = (nqt - 1 - rank) * pbp;  // first position of the item
+    w.slot = slots[b];
+    w.hk = w.hq0 / kc.G;
+    w.nkt = min((w.i0 + pbp - 1) / BN, (w.L - 1) / BN) + 1;  // key tiles (causal)
+    w.nfull = w.L / PI;                                      // committed V blocks
+    return true;
+  };
+  {
+    Item w0;
+    if (!get_item(0, w0)) return;
+  }
 
   if (tid == 0) {
     for (int s = 0; s < NS; ++s) {
@@ -257,6 +281,7 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_tc_kernel(
     ptx::mbar_init(&sm.s_free, NSW);
     ptx::mbar_init(&sm.q_ready, NSW);
     ptx::mbar_init(&sm.l_ready, NSW);
+    ptx::mbar_init(&sm.l_free, NOW);
     ptx::fence_mbar_init();
   }
   if (warp == 1) ptx::tmem_alloc(&sm.tmem_base, 512);
@@ -277,13 +302,17 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_tc_kernel(
       // pages are read only after that grid completed
       asm volatile("griddepcontrol.wait;" ::: "memory");
       if (lane == 0) {
-        const int32_t* bt = cv.block_table + (int64_t)slot * cv.max_pages_per_req;
-        for (int j = 0; j < nkt; ++j) {
-          const int s = j % NS;
-          ptx::mbar_wait(&sm.empty[s], ((j / NS) & 1) ^ 1);
-          ptx::mbar_arrive_expect_tx(&sm.full[s], Gm::PB);
-          const uint8_t* pg = cv.pages + ((int64_t)bt[j] * cv.num_kv_heads + hk) * cv.page_bytes;
-          ptx::bulk_g2s(sm.stage[s], pg, Gm::PB, &sm.full[s]);
+        int jg = 0;  // tiles of all items so far (ring phases)
+        Item w;
+        for (int it = 0; get_item(it, w); ++it) {
+          const int32_t* bt = cv.block_table + (int64_t)w.slot * cv.max_pages_per_req;
+          for (int j = 0; j < w.nkt; ++j, ++jg) {
+            const int s = jg % NS;
+            ptx::mbar_wait(&sm.empty[s], ((jg / NS) & 1) ^ 1);
+            ptx::mbar_arrive_expect_tx(&sm.full[s], Gm::PB);
+            const uint8_t* pg = cv.pages + ((int64_t)bt[j] * cv.num_kv_heads + w.hk) * cv.page_bytes;
+            ptx::bulk_g2s(sm.stage[s], pg, Gm::PB, &sm.full[s]);
+          }
         }
       }
     } else if (warp == 1) {
@@ -293,12 +322,20 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_tc_kernel(
       const uint64_t pre_a = ptx::smem_desc_kmajor(ptx::smem_u32(sm.pre_a), 128, 256);
       const uint64_t pre_b = ptx::smem_desc_kmajor(ptx::smem_u32(sm.pre_b), 128, 256);
       const uint32_t idesc_pre = ptx::idesc_bf16(BM, 128);
-      ptx::mbar_wait(&sm.q_ready, 0);
-      for (int j = 0; j <= nkt; ++j) {
-        if (j < nkt) {
-          const int bq = j % NB;
-          ptx::mbar_wait(&sm.k_ready[bq], (j / NB) & 1);
-          ptx::mbar_wait(&sm.s_free, (j & 1) ^ 1);
+      int jg = 0, jpv = 0;  // tiles / PV tiles of all items so far (ring phases)
+      bool prev_tail = false;
+      Item w;
+#pragma unroll 1
+      for (int it = 0; get_item(it, w); ++it) {
+      ptx::mbar_wait(&sm.q_ready, it & 1);  // this item's Q' and rank-term rows in smem
+#pragma unroll 1
+      for (int j = 0; j <= w.nkt; ++j) {
+        if (j < w.nkt) {
+          const int g = jg + j, bq = g % NB;
+          ptx::mbar_wait(&sm.k_ready[bq], (g / NB) & 1);
+          ptx::mbar_wait(&sm.s_free, (g & 1) ^ 1);
+          // the previous item's FP16 tail p~ sits in the S columns: the O warps must be done
+          if (j == 0 && prev_tail) ptx::mbar_wait(&sm.o_done[(g - 1) % NB], ((g - 1) / NB) & 1);
           ptx::tc_fence_after();
           if (lane == 0) {
             const uint32_t ka = ptx::smem_u32(sm.k[bq]);
@@ -324,12 +361,13 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_tc_kernel(
           __syncwarp();
         }
         const int jj = j - 1;  // PV of the previous tile, after QK of this one (overlap)
-        if (jj >= 0 && jj < nfull) {
-          const int bd = jj % NDB, bq = jj % NB;
-          const uint32_t ph = (jj / NB) & 1;
+        if (jj >= 0 && jj < w.nfull) {
+          const int g = jg + jj, bd = jpv % NDB, bq = g % NB;
+          const uint32_t ph = (g / NB) & 1;
           ptx::mbar_wait(&sm.p_ready[bq], ph);
           ptx::mbar_wait(&sm.v_ready[bq], ph);
-          ptx::mbar_wait(&sm.d_free[bd], ((jj / NDB) & 1) ^ 1);
+          ptx::mbar_wait(&sm.d_free[bd], ((jpv / NDB) & 1) ^ 1);
+          ++jpv;
           ptx::tc_fence_after();
           if (lane == 0) {
             const uint32_t pa = ptx::smem_u32(sm.p[bq]), va = ptx::smem_u32(sm.v[bq]);
@@ -342,6 +380,9 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_tc_kernel(
           }
           __syncwarp();
         }
+      }
+      prev_tail = w.nfull < w.nkt;  // the last tile was the FP16 tail
+      jg += w.nkt;
       }
     } else {
       // ---------------------------------------------------------------- unpack (64 threads)
@@ -357,14 +398,18 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_tc_kernel(
             make_uint4(0x4B40u, 0u, 0u, 0u);  // bf16 1.5 * 2^23 at k = 0
         *reinterpret_cast<uint4*>(reinterpret_cast<uint8_t*>(sm.pre_b) + kmaj_off(row, 16, 256)) = make_uint4(0u, 0u, 0u, 0u);
       }
+      int jg = 0;
+      Item w;
 #pragma unroll 1
-      for (int j = 0; j < nkt; ++j) {
-        const int s = j % NS, bj = j % NB;
-        const uint32_t ph = (j / NB) & 1;
-        ptx::mbar_wait(&sm.full[s], (j / NS) & 1);
+      for (int it = 0; get_item(it, w); ++it) {
+#pragma unroll 1
+      for (int j = 0; j < w.nkt; ++j, ++jg) {
+        const int s = jg % NS, bj = jg % NB;
+        const uint32_t ph = (jg / NB) & 1;
+        ptx::mbar_wait(&sm.full[s], (jg / NS) & 1);
         ptx::mbar_wait(&sm.k_free[bj], ph ^ 1);
         const uint8_t* pg = sm.stage[s];
-        const int nk = min(BN, L - j * BN);
+        const int nk = min(BN, w.L - j * BN);
         if (!(HACK_ABL & 16)) {
           // K' codes: thread = key; 8 consecutive keys fill one 128-byte core matrix per store
 #pragma unroll
@@ -415,7 +460,7 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_tc_kernel(
         ptx::fence_proxy_async_smem();
         ptx::mbar_arrive(&sm.k_ready[bj]);
         ptx::mbar_wait(&sm.o_done[bj], ph ^ 1);  // O warps done with tile j - NB
-        if (j < nfull && !(HACK_ABL & 16)) {
+        if (j < w.nfull && !(HACK_ABL & 16)) {
           constexpr int WPC = BN * BITS / 32;  // packed 32-bit words per V channel row
 #pragma unroll
           for (int c2 = 0; c2 < 2; ++c2) {
@@ -453,6 +498,7 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_tc_kernel(
         ptx::mbar_arrive(&sm.v_ready[bj]);
         ptx::mbar_arrive(&sm.empty[s]);
       }
+      }
     }
   } else if (warp < 12) {
     // ------------------------------------------------------------------ S warpgroups (2)
@@ -460,13 +506,20 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_tc_kernel(
     asm volatile("setmaxnreg.dec.sync.aligned.u32 88;");
     const int sw = (warp - 4) >> 2;
     const int r = (tid - 128) & (BM - 1);
-    const int pos = i0 + (r & (pbp - 1)), hq = hq0 + r / pbp;  // this row's position and head
-    const int i = min(pos, L - 1);  // this thread's query position (padding rows clamp)
     const uint32_t lane_base = (uint32_t)(32 * (warp & 3)) << 16;
     const uint32_t qbar = 3 + (warp & 3);  // the 2 S warps sharing these 32 rows
     const float cscale = 1.4426950408889634f / sqrtf(128.f);
     const int kb = KPT * sw;
+    int jg = 0;  // tiles of all items so far
+    Item w;
+#pragma unroll 1
+    for (int it = 0; get_item(it, w); ++it) {
+    const int pos = w.i0 + (r & (pbp - 1)), hq = w.hq0 + r / pbp;  // this row's position and head
+    const int L = w.L, start = w.start;
+    const int i = min(pos, L - 1);  // this thread's query position (padding rows clamp)
     {
+      // (QK of the previous item complete: this thread waited its last s_full)
+      if (PI == 128 && it > 0) ptx::named_bar_sync(qbar, 64);  // partner done with the last xch
       // (a3) quantize Q[i, 64 sw .. 64 sw + 63]: 8-bit, fp32 meta, SR, partitions of Pi
       // channels (a 128-channel partition spans both warpgroups: min/max and sums exchanged)
       const uint4* qrow = reinterpret_cast<const uint4*>(q + ((int64_t)(start + i) * kc.Hq + hq) * 128 + 64 * sw);
@@ -501,7 +554,7 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_tc_kernel(
         qm[pp] = meta_fp32(lo, hi, 255);
       }
       const uint32_t c3 = stream_c3(kc.layer, kTagQ, kc.head_base * kc.G + hq);
-      const uint32_t rng_id = cv.rng_ids[slot];
+      const uint32_t rng_id = cv.rng_ids[w.slot];
       int sum[NPL];
 #pragma unroll
       for (int pp = 0; pp < NPL; ++pp) sum[pp] = 0;
@@ -575,14 +628,14 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_tc_kernel(
     for (int beta = 0; beta < NBETA; ++beta) qa[beta] = sm.qa[beta][r];
     float m_run = -INFINITY, l_run = 0.f;
     const uint32_t p_c3 = PSR ? stream_c3(kc.layer, kTagP, kc.head_base * kc.G + hq) : 0u;
-    const uint32_t p_rid = PSR ? cv.rng_ids[slot] : 0u;
+    const uint32_t p_rid = PSR ? cv.rng_ids[w.slot] : 0u;
 
 #pragma unroll 1
-    for (int j = 0; j < nkt; ++j) {
-      const int bj = j % NB, t0 = j * BN;
-      const uint32_t ph = (j / NB) & 1;
-      const bool full = (t0 + BN - 1) <= i0;  // every key visible to every row of the CTA
-      ptx::mbar_wait(&sm.s_full, j & 1);
+    for (int j = 0; j < w.nkt; ++j, ++jg) {
+      const int bj = jg % NB, t0 = j * BN;
+      const uint32_t ph = (jg / NB) & 1;
+      const bool full = (t0 + BN - 1) <= w.i0;  // every key visible to every row of the item
+      ptx::mbar_wait(&sm.s_full, jg & 1);
       ptx::tc_fence_after();
       // ---- pass 1: S = R + sum_beta (s_q/2) s_k E_beta (centered Eq. 4) x log2(e)/sqrt(d),
       // causal mask, row max / min; 16 keys per TMEM load (register pressure)
@@ -645,9 +698,9 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_tc_kernel(
         mask_minmax_t<KPT>(s, t0 + kb, i, full, masked, mx, mn);
       }
       ptx::mbar_arrive(&sm.k_free[bj]);  // K' tile + key coefficients may be refilled
-      sm.xch[j & 1][sw][r] = make_float2(mx, masked ? -INFINITY : mn);
+      sm.xch[jg & 1][sw][r] = make_float2(mx, masked ? -INFINITY : mn);
       ptx::named_bar_sync(qbar, 64);
-      const float2 o = sm.xch[j & 1][sw ^ 1][r];
+      const float2 o = sm.xch[jg & 1][sw ^ 1][r];
       mx = fmaxf(mx, o.x);
       const bool any_masked = masked || (o.y == -INFINITY);
       mn = fminf(masked ? INFINITY : mn, o.y == -INFINITY ? INFINITY : o.y);
@@ -662,7 +715,7 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_tc_kernel(
       }
       // tile j-NB must be fully consumed by the O warps before its P / info slots are reused
       ptx::mbar_wait(&sm.o_done[bj], ph ^ 1);
-      const bool committed = j < nfull;
+      const bool committed = j < w.nfull;
       float pinv = 0.f, pnlo = 0.f, ps = 0.f, plo = 0.f;
       if (committed) {
         // (a6) P' per (row, V block): 8-bit on p~ (codes invariant to the row scale);
@@ -740,8 +793,10 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_tc_kernel(
       ptx::mbar_arrive(&sm.p_ready[bj]);              // for the MMA warp (PV)
       ptx::named_bar_arrive(kPBar0 + bj, NSW + NOW);  // for the O warps (hardware barrier: no polling)
     }
+    ptx::mbar_wait(&sm.l_free, (it & 1) ^ 1);  // the O warps read the previous item's sums
     sm.lpart[sw][r] = l_run;
     ptx::mbar_arrive(&sm.l_ready);
+    }
   } else {
     // ------------------------------------------------------------------ O warpgroups (2)
     // thread = query row r = TMEM lane; OW o owns output channels 64o..64o+63
@@ -749,16 +804,21 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_tc_kernel(
     asm volatile("griddepcontrol.wait;" ::: "memory");  // the FP16 tail is the ingest's output too
     const int ow = (warp - 12) >> 2;
     const int r = (tid - 384) & (BM - 1);
-    const int pos = i0 + (r & (pbp - 1)), hq = hq0 + r / pbp;
     const uint32_t lane_base = (uint32_t)(32 * (warp & 3)) << 16;
     const int cb = 64 * ow;
+    int jg = 0, jpv = 0;  // tiles / PV tiles of all items so far
+    Item w;
+#pragma unroll 1
+    for (int it = 0; get_item(it, w); ++it) {
+    const int pos = w.i0 + (r & (pbp - 1)), hq = w.hq0 + r / pbp;
+    const int L = w.L, start = w.start;
     float2 o2[32];  // channels cb + 2x, cb + 2x + 1
 #pragma unroll
     for (int x = 0; x < 32; ++x) o2[x] = make_float2(0.f, 0.f);
 #pragma unroll 1
-    for (int j = 0; j < nkt; ++j) {
-      const int bj = j % NB, bd = j % NDB;
-      const uint32_t ph = (j / NB) & 1;
+    for (int j = 0; j < w.nkt; ++j, ++jg) {
+      const int bj = jg % NB;
+      const uint32_t ph = (jg / NB) & 1;
       ptx::named_bar_sync(kPBar0 + bj, NSW + NOW);  // S warps' P' and row info of tile j
       const float4 pi4 = sm.pinfo[bj][r];
       if (pi4.y != 0.f) {  // warp-uniform (lazy rescaling decided per S warp = same 32 rows)
@@ -766,7 +826,10 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_tc_kernel(
 #pragma unroll
         for (int x = 0; x < 32; ++x) o2[x] = ptx::fmul2(o2[x], al2);
       }
-      if (j < nfull) {
+      if (j < w.nfull) {
+        const int bd = jpv % NDB;
+        const uint32_t dph = (jpv / NDB) & 1;
+        ++jpv;
         // (a7) O += (s_p/2) s_v E + s_p SP_s m_v + mu_p y_v on D' of this tile
         const int sps = sm.sp_part[bj][0][r] + sm.sp_part[bj][1][r] - 128 * PI;  // sum (p' - 128)
         const float2 ap2 = make_float2(0.5f * pi4.z, 0.5f * pi4.z);
@@ -774,7 +837,7 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_tc_kernel(
         const float mp = __fmaf_rn(128.f, pi4.z, pi4.w);
         const float2 mp2 = make_float2(mp, mp);
         ptx::mbar_wait(&sm.v_ready[bj], ph);
-        ptx::mbar_wait(&sm.d_full[bd], (j / NDB) & 1);
+        ptx::mbar_wait(&sm.d_full[bd], dph);
         ptx::tc_fence_after();
 #pragma unroll
         for (int h = 0; h < 4; ++h) {
@@ -818,9 +881,9 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_tc_kernel(
         // FP16 last V block (RQE): O += sum_t p~_t v_t in fp32, p~ from the S warps
         // through TMEM (columns = the tile's local keys)
         ptx::tc_fence_after();
-        const int T = L - nfull * PI;
+        const int T = L - w.nfull * PI;
         const __half* tail =
-            reinterpret_cast<const __half*>(cv.v_tail) + ((int64_t)slot * kc.Hkv + hk) * PI * 128 + cb;
+            reinterpret_cast<const __half*>(cv.v_tail) + ((int64_t)w.slot * kc.Hkv + w.hk) * PI * 128 + cb;
 #pragma unroll 1
         for (int c = 0; 16 * c < T; ++c) {
           uint32_t pt16[16];
@@ -844,9 +907,10 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_tc_kernel(
       }
       ptx::mbar_arrive(&sm.o_done[bj]);
     }
-    ptx::mbar_wait(&sm.l_ready, 0);
+    ptx::mbar_wait(&sm.l_ready, it & 1);
+    const float inv_l = 1.f / (sm.lpart[0][r] + sm.lpart[1][r]);
+    ptx::mbar_arrive(&sm.l_free);
     if (pos < L) {
-      const float inv_l = 1.f / (sm.lpart[0][r] + sm.lpart[1][r]);
       const int64_t base = ((int64_t)(start + pos) * kc.Hq + hq) * 128 + cb;
       if (kc.out_fp32) {
         float4* op = reinterpret_cast<float4*>(reinterpret_cast<float*>(out) + base);
@@ -865,10 +929,20 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_tc_kernel(
         }
       }
     }
+    }
   }
   ptx::tc_fence_before();
   __syncthreads();
   if (warp == 1) ptx::tmem_dealloc(tmem, 512);
+}
+
+// HACK_PREFILL_PERSIST=0 forces one CTA per item (A/B runs); default persistent for batch 1.
+bool persistent_enabled() {
+  static const bool on = [] {
+    const char* v = getenv("HACK_PREFILL_PERSIST");
+    return v == nullptr || v[0] != '0';
+  }();
+  return on;
 }
 
 template <int PI_, int BITS>
@@ -885,7 +959,17 @@ cudaError_t launch_t(const KernelCfg& kc, const void* q, const int32_t* cu, cons
   if (e != cudaSuccess) return e;
   const int gp = pack_heads(kc);
   cudaLaunchConfig_t lc = {};
-  lc.gridDim = dim3((max_seqlen + BM / gp - 1) / (BM / gp), kc.Hq / gp, batch);
+  const int nqt = (max_seqlen + BM / gp - 1) / (BM / gp);
+  int nitems = 0;  // persistent launch: one request, at most one CTA per SM looping over items
+  if (batch == 1 && persistent_enabled()) {
+    int dev = 0, nsm = 0;
+    if ((e = cudaGetDevice(&dev)) != cudaSuccess) return e;
+    if ((e = cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev)) != cudaSuccess) return e;
+    nitems = nqt * (kc.Hq / gp);
+    lc.gridDim = dim3(min(nitems, nsm), 1, 1);
+  } else {
+    lc.gridDim = dim3(nqt, kc.Hq / gp, batch);
+  }
   lc.blockDim = dim3(kThreads);
   lc.dynamicSmemBytes = smem;
   lc.stream = st;
@@ -901,7 +985,7 @@ cudaError_t launch_t(const KernelCfg& kc, const void* q, const int32_t* cu, cons
   e = cudaLaunchKernelEx(&lc, kern, reinterpret_cast<const __half*>(q), cu, slots, cv, kc, out,
                          dbg ? dbg->pcodes : (uint8_t*)nullptr, dbg ? dbg->pcodes_stride : (int64_t)0,
                          dbg ? dbg->qk_acc : (int32_t*)nullptr, dbg ? dbg->pv_acc : (int32_t*)nullptr,
-                         dbg ? dbg->acc_stride : (int64_t)0, dbg ? dbg->acc_head : -1);
+                         dbg ? dbg->acc_stride : (int64_t)0, dbg ? dbg->acc_head : -1, nitems);
   if (e != cudaSuccess) return e;
   note_launch();
   return cudaGetLastError();
