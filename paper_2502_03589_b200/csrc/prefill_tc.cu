@@ -47,12 +47,11 @@ constexpr int BM = 128;
 #ifndef HACK_PRE_GP
 #define HACK_PRE_GP 2  // query heads of one KV head packed into a CTA's 128 rows (1: one head x 128 positions)
 #endif
-constexpr int kThreads = 640;  // 4 service warps + 2 S warpgroups + 2 O warpgroups
-constexpr int NSW = 256;       // S-warpgroup threads
 constexpr int NOW = 256;       // O-warpgroup threads
 constexpr float kMagic = 12582912.f;  // 1.5 * 2^23 (P' rounding)
 constexpr float kRescaleTh = 8.f;     // lazy-rescale threshold (log2 units)
-// Named barriers: 0 = __syncthreads, 3..6 = the S warp pairs' row exchange, 7..9 = S -> O.
+// Named barriers: 0 = __syncthreads, 3..6 = the row exchange of the NSG S warps sharing 32
+// rows, 7..9 = S -> O.
 // Generations of barrier kPBar0 + b alternate strictly: the S warps arrive for tile j only
 // after the O warps finished tile j - NB (o_done), which they synced on for tile j - NB.
 constexpr uint32_t kPBar0 = 7;
@@ -64,12 +63,34 @@ constexpr uint32_t kPBar0 = 7;
 #define HACK_ABL 0  // timing ablations only, bit flags (1 O math, 2 P-quant math, 4 Eq. 4, 8 exp2, 16 unpack)
 #endif
 
+#ifndef HACK_PRE_NSG
+#define HACK_PRE_NSG 2  // S warpgroups at Pi >= 64 (4: 16 keys per thread at Pi = 64, measured 6 % slower)
+#endif
+// service / S / O registers per thread with 4 S warpgroups (setmaxnreg shares of 64K)
+#ifndef HACK_PRE_RSVC
+#define HACK_PRE_RSVC 40
+#endif
+#ifndef HACK_PRE_RS
+#define HACK_PRE_RS 56
+#endif
+#ifndef HACK_PRE_RO
+#define HACK_PRE_RO 112
+#endif
+
 // Shapes per partition size: one key tile = one V block (BN = Pi keys); d/Pi d-blocks.
 template <int PI_, int BITS>
 struct Geo {
   static constexpr int PI = PI_, BN = PI_, NBETA = 128 / PI_;
-  static constexpr int KPT = BN / 2;                    // keys per S thread per tile
-  static constexpr bool WB = KPT > 32;                  // scores written back to TMEM between passes
+  // S warpgroups: each owns BN / NSG keys of every tile (more, shorter S warps hide the
+  // latency of the per-key epilogue chain; the S side is the kernel's critical path)
+  static constexpr int NSG = PI_ == 32 ? 2 : HACK_PRE_NSG;
+  static constexpr int THREADS = 128 + 128 * NSG + 256;  // service WG + S WGs + 2 O WGs
+  static constexpr int REG_SVC = NSG == 2 ? 40 : HACK_PRE_RSVC;
+  static constexpr int REG_S = NSG == 2 ? 88 : HACK_PRE_RS;
+  static constexpr int REG_O = NSG == 2 ? 128 : HACK_PRE_RO;
+  static_assert(REG_SVC * 128 + REG_S * 128 * NSG + REG_O * 256 <= 65536, "register file");
+  static constexpr int KPT = BN / NSG;                  // keys per S thread per tile
+  static constexpr bool WB = KPT > (NSG == 2 ? 32 : 16);  // scores written back to TMEM between passes
   static constexpr int SB = (BITS + (PI_ == 32 ? 5 : PI_ == 64 ? 6 : 7)) <= 8 ? 1 : 2;  // sum bytes (R13)
   static constexpr int up16(int x) { return (x + 15) / 16 * 16; }
   static constexpr int PB = up16(PI_ * 128 * BITS / 8) + up16(PI_ * NBETA * 4) + up16(PI_ * NBETA * SB) +
@@ -101,10 +122,12 @@ struct TcSmem {
   alignas(16) float kcf[NB][Gm::NBETA][BN];  // [buf][beta][key]: s_k
   alignas(16) float vcf[NB][3][128];         // [buf][field][channel]: s_v, m_v, y_v
   float qa[Gm::NBETA][BM];                   // per (beta, row): cs s_q / 2
-  int sp_part[NB][2][BM];                    // partial P-code sums (per S warpgroup)
+  int sp_part[NB][Gm::NSG][BM];              // partial P-code sums (per S warpgroup)
   float4 pinfo[NB][BM];                      // per (tile, row): alpha, rescaled?, s_p, m_p
-  float2 xch[2][2][BM];                      // partial (max, min | -inf if masked); Q meta at Pi = 128
-  float lpart[2][BM];
+  float2 xch[2][Gm::NSG][BM];                // partial (max, min | -inf if masked) per tile
+  float2 xq[Gm::NSG][BM];                    // Q prologue: partial (min, max) of a partition
+  int xs[Gm::NSG][BM];                       // Q prologue: partial code sums of a partition
+  float lpart[Gm::NSG][BM];
   uint64_t full[NS], empty[NS], k_ready[NB], k_free[NB], v_ready[NB], o_done[NB], p_ready[NB], d_full[2],
       d_free[2], s_full, s_free, q_ready, l_ready, l_free;
   uint32_t tmem_base;
@@ -204,7 +227,7 @@ HACK_DEV uint4 p_codes16(const float* s, float inv, float nlo, uint64_t seed, ui
 // accumulators E = 2 D - 256 S_B (HACK_ACC_S8_2B); the production instantiation has none of it.
 // PSR: P codes by the paper's stochastic rounding (R6, selectable) instead of RN.
 template <int PI_, int BITS, bool DBG, bool PSR>
-__global__ void __launch_bounds__(kThreads, 1) prefill_tc_kernel(
+__global__ void __launch_bounds__(Geo<PI_, BITS>::THREADS, 1) prefill_tc_kernel(
     const __half* __restrict__ q, const int32_t* __restrict__ cu_seqlens, const int32_t* __restrict__ slots,
     CacheView cv, KernelCfg kc, void* __restrict__ out, uint8_t* __restrict__ dbg_pcodes, int64_t dbg_stride,
     int32_t* __restrict__ dbg_qk, int32_t* __restrict__ dbg_pv, int64_t acc_stride, int acc_head, int nitems) {
@@ -213,6 +236,8 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_tc_kernel(
   constexpr int PI = Gm::PI, BN = Gm::BN, NBETA = Gm::NBETA, KPT = Gm::KPT, NS = Gm::NS, NB = Gm::NB;
   constexpr int NDB = Gm::NDB, KR = Gm::KR, SBO_R = Gm::SBO_R, SBO_T = Gm::SBO_T;
   constexpr bool WB = Gm::WB;
+  constexpr int NSG = Gm::NSG, NSW = 128 * NSG;  // S warpgroups, S threads
+  constexpr int OBASE = 128 + NSW;              // first O thread
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   SM& sm = *reinterpret_cast<SM*>(smem_raw);
 
@@ -294,8 +319,8 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_tc_kernel(
   const uint32_t tD0 = tmem + Gm::TD;    // D'[0], D'[1] (128 columns each)
 
   if (warp < 4) {
-    // register budget (launch: 96 x 640 = 61440): service 40, S 88, O 128
-    asm volatile("setmaxnreg.dec.sync.aligned.u32 40;");
+    // register budget (launch: THREADS x the launch-bound cap): service, S and O shares (Geo)
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(Gm::REG_SVC));
     if (warp == 0) {
       // ---------------------------------------------------------------- producer
       // launched as a programmatic dependent of the ingest (hack_prefill_attention): the
@@ -500,16 +525,25 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_tc_kernel(
       }
       }
     }
-  } else if (warp < 12) {
-    // ------------------------------------------------------------------ S warpgroups (2)
+  } else if (warp < 4 + 4 * NSG) {
+    // ------------------------------------------------------------------ S warpgroups (NSG)
     // thread = query row r = TMEM lane; SW s owns keys KPT s .. KPT s + KPT - 1 of every tile
-    asm volatile("setmaxnreg.dec.sync.aligned.u32 88;");
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(Gm::REG_S));
     const int sw = (warp - 4) >> 2;
     const int r = (tid - 128) & (BM - 1);
     const uint32_t lane_base = (uint32_t)(32 * (warp & 3)) << 16;
-    const uint32_t qbar = 3 + (warp & 3);  // the 2 S warps sharing these 32 rows
+    const uint32_t qbar = 3 + (warp & 3);  // the NSG S warps sharing these 32 rows
+    constexpr uint32_t QBN = 32 * NSG;      // ... their thread count
     const float cscale = 1.4426950408889634f / sqrtf(128.f);
     const int kb = KPT * sw;
+    // Q prologue geometry: this thread quantizes CW channels of its row; a partition of Pi
+    // channels is NPL partitions of one thread or spans PW warpgroups (min/max and code
+    // sums exchanged through xq / xs)
+    constexpr int CW = 128 / NSG, NQV = CW / 8;
+    constexpr int NPL = PI >= CW ? 1 : CW / PI;
+    constexpr int PW = PI > CW ? PI / CW : 1;
+    constexpr int VPP = NQV / NPL;  // 16-byte pieces per (local) partition
+    const int g0 = sw - sw % PW;    // first warpgroup of this thread's partition
     int jg = 0;  // tiles of all items so far
     Item w;
 #pragma unroll 1
@@ -519,17 +553,15 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_tc_kernel(
     const int i = min(pos, L - 1);  // this thread's query position (padding rows clamp)
     {
       // (QK of the previous item complete: this thread waited its last s_full)
-      if (PI == 128 && it > 0) ptx::named_bar_sync(qbar, 64);  // partner done with the last xch
-      // (a3) quantize Q[i, 64 sw .. 64 sw + 63]: 8-bit, fp32 meta, SR, partitions of Pi
-      // channels (a 128-channel partition spans both warpgroups: min/max and sums exchanged)
-      const uint4* qrow = reinterpret_cast<const uint4*>(q + ((int64_t)(start + i) * kc.Hq + hq) * 128 + 64 * sw);
-      // all 8 loads of the 64-channel slice in flight at once (one memory latency per CTA,
-      // not eight), kept in registers for the quantization pass; min/max on packed halves
-      uint4 qr[8];
+      // (a3) quantize Q[i, CW sw .. CW sw + CW - 1]: 8-bit, fp32 meta, SR, partitions of Pi
+      // channels.  xq / xs reuse across items: a warpgroup writes them again only after the
+      // tile barriers of this item, which its partners pass after their reads.
+      const uint4* qrow = reinterpret_cast<const uint4*>(q + ((int64_t)(start + i) * kc.Hq + hq) * 128 + CW * sw);
+      // all loads of the slice in flight at once (one memory latency per CTA), kept in
+      // registers for the quantization pass; min/max on packed halves
+      uint4 qr[NQV];
 #pragma unroll
-      for (int v8 = 0; v8 < 8; ++v8) qr[v8] = __ldg(qrow + v8);
-      constexpr int NPL = PI >= 64 ? 1 : 64 / PI;  // partitions in this thread's 64 channels
-      constexpr int VPP = 8 / NPL;                 // 16-byte pieces per (local) partition
+      for (int v8 = 0; v8 < NQV; ++v8) qr[v8] = __ldg(qrow + v8);
       QMeta qm[NPL];
 #pragma unroll
       for (int pp = 0; pp < NPL; ++pp) {
@@ -544,12 +576,15 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_tc_kernel(
           }
         }
         float lo = fminf(__low2float(lo2), __high2float(lo2)), hi = fmaxf(__low2float(hi2), __high2float(hi2));
-        if (PI == 128) {  // the other half of the partition lives in the partner warpgroup
-          sm.xch[0][sw][r] = make_float2(lo, hi);
-          ptx::named_bar_sync(qbar, 64);
-          const float2 o = sm.xch[0][sw ^ 1][r];
-          lo = fminf(lo, o.x);
-          hi = fmaxf(hi, o.y);
+        if (PW > 1) {  // the rest of the partition lives in the partner warpgroups
+          sm.xq[sw][r] = make_float2(lo, hi);
+          ptx::named_bar_sync(qbar, QBN);
+#pragma unroll
+          for (int w2 = 0; w2 < PW; ++w2) {
+            const float2 o = sm.xq[g0 + w2][r];
+            lo = fminf(lo, o.x);
+            hi = fmaxf(hi, o.y);
+          }
         }
         qm[pp] = meta_fp32(lo, hi, 255);
       }
@@ -559,8 +594,8 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_tc_kernel(
 #pragma unroll
       for (int pp = 0; pp < NPL; ++pp) sum[pp] = 0;
 #pragma unroll
-      for (int g = 0; g < 4; ++g) {  // 16-channel groups
-        const int pp = PI >= 64 ? 0 : (16 * g) / PI;
+      for (int g = 0; g < CW / 16; ++g) {  // 16-channel groups
+        const int pp = PI >= CW ? 0 : (16 * g) / PI;
         float x[16];
         const __half* ha = reinterpret_cast<const __half*>(&qr[2 * g]);
         const __half* hb = reinterpret_cast<const __half*>(&qr[2 * g + 1]);
@@ -573,7 +608,7 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_tc_kernel(
         if (kc.q_round == HACK_ROUND_STOCHASTIC) {
 #pragma unroll
           for (int k4 = 0; k4 < 4; ++k4) {
-            const uint64_t n = ((uint64_t)i * 128u + (uint64_t)(64 * sw + 16 * g + 4 * k4)) >> 2;
+            const uint64_t n = ((uint64_t)i * 128u + (uint64_t)(CW * sw + 16 * g + 4 * k4)) >> 2;
             const Philox4 rr = philox_block(kc.seed, rng_id, c3, n);
             cc[4 * k4 + 0] = quant_sr(x[4 * k4 + 0], qm[pp], u24(rr.x), 255);
             cc[4 * k4 + 1] = quant_sr(x[4 * k4 + 1], qm[pp], u24(rr.y), 255);
@@ -594,35 +629,38 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_tc_kernel(
         }
 #pragma unroll
         for (int e = 0; e < 16; ++e) sum[pp] += cc[e];
-        *reinterpret_cast<uint4*>(sm.q + kmaj_off(r, 64 * sw + 16 * g, 1024)) = make_uint4(wv[0], wv[1], wv[2], wv[3]);
+        *reinterpret_cast<uint4*>(sm.q + kmaj_off(r, CW * sw + 16 * g, 1024)) = make_uint4(wv[0], wv[1], wv[2], wv[3]);
       }
-      if (PI == 128) {  // code sum over both halves of the partition
-        reinterpret_cast<int*>(&sm.xch[1][sw][r])[0] = sum[0];
-        ptx::named_bar_sync(qbar, 64);
-        sum[0] += reinterpret_cast<const int*>(&sm.xch[1][sw ^ 1][r])[0];
+      if (PW > 1) {  // code sum over the whole partition
+        sm.xs[sw][r] = sum[0];
+        ptx::named_bar_sync(qbar, QBN);
+        sum[0] = 0;
+#pragma unroll
+        for (int w2 = 0; w2 < PW; ++w2) sum[0] += sm.xs[g0 + w2][r];
       }
+      if (sw == g0) {  // the partition's constants: written once
 #pragma unroll
-      for (int pp = 0; pp < NPL; ++pp) {
-        const int beta = PI == 128 ? 0 : sw * NPL + pp;
-        if (PI == 128 && sw == 1) break;  // the single block's constants: written once
-        const int sqs = sum[pp] - 128 * PI;  // sum (q' - 128)
-        sm.qa[beta][r] = cscale * qm[pp].s * 0.5f;
-        const float X = cscale * qm[pp].s * (float)sqs, M = cscale * __fmaf_rn(128.f, qm[pp].s, qm[pp].m);
-        float av[12];
-        rank_a(X, av);
-        rank_a(M, av + 6);
-        uint8_t* arr = reinterpret_cast<uint8_t*>(sm.ar);
+        for (int pp = 0; pp < NPL; ++pp) {
+          const int beta = (CW * sw) / PI + pp;
+          const int sqs = sum[pp] - 128 * PI;  // sum (q' - 128)
+          sm.qa[beta][r] = cscale * qm[pp].s * 0.5f;
+          const float X = cscale * qm[pp].s * (float)sqs, M = cscale * __fmaf_rn(128.f, qm[pp].s, qm[pp].m);
+          float av[12];
+          rank_a(X, av);
+          rank_a(M, av + 6);
+          uint8_t* arr = reinterpret_cast<uint8_t*>(sm.ar);
 #pragma unroll
-        for (int x = 0; x < 12; x += 4)
-          *reinterpret_cast<float4*>(arr + kmaj_off(r, 4 * (12 * beta + x), SBO_R)) =
-              make_float4(av[x], av[x + 1], av[x + 2], av[x + 3]);
-        if (KR > 12 * NBETA)
-          *reinterpret_cast<float4*>(arr + kmaj_off(r, 4 * 12 * NBETA, SBO_R)) = make_float4(0.f, 0.f, 0.f, 0.f);
+          for (int x = 0; x < 12; x += 4)
+            *reinterpret_cast<float4*>(arr + kmaj_off(r, 4 * (12 * beta + x), SBO_R)) =
+                make_float4(av[x], av[x + 1], av[x + 2], av[x + 3]);
+          if (KR > 12 * NBETA && beta == 0)
+            *reinterpret_cast<float4*>(arr + kmaj_off(r, 4 * 12 * NBETA, SBO_R)) = make_float4(0.f, 0.f, 0.f, 0.f);
+        }
       }
       ptx::fence_proxy_async_smem();
       ptx::mbar_arrive(&sm.q_ready);
     }
-    ptx::named_bar_sync(qbar, 64);  // both halves of the Q row constants visible
+    ptx::named_bar_sync(qbar, QBN);  // the row's Q constants (all partitions) visible
     float qa[NBETA];
 #pragma unroll
     for (int beta = 0; beta < NBETA; ++beta) qa[beta] = sm.qa[beta][r];
@@ -699,11 +737,16 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_tc_kernel(
       }
       ptx::mbar_arrive(&sm.k_free[bj]);  // K' tile + key coefficients may be refilled
       sm.xch[jg & 1][sw][r] = make_float2(mx, masked ? -INFINITY : mn);
-      ptx::named_bar_sync(qbar, 64);
-      const float2 o = sm.xch[jg & 1][sw ^ 1][r];
-      mx = fmaxf(mx, o.x);
-      const bool any_masked = masked || (o.y == -INFINITY);
-      mn = fminf(masked ? INFINITY : mn, o.y == -INFINITY ? INFINITY : o.y);
+      ptx::named_bar_sync(qbar, QBN);
+      bool any_masked = masked;
+      if (masked) mn = INFINITY;
+#pragma unroll
+      for (int w2 = 1; w2 < NSG; ++w2) {  // the other warpgroups' keys of these rows
+        const float2 o = sm.xch[jg & 1][(sw + w2) % NSG][r];
+        mx = fmaxf(mx, o.x);
+        any_masked |= o.y == -INFINITY;
+        mn = fminf(mn, o.y == -INFINITY ? INFINITY : o.y);
+      }
       // lazy rescaling: move the running max only when some row of this warp outgrew it by
       // more than kRescaleTh (identical decision in both S warps sharing these rows)
       float al = 1.f;
@@ -800,10 +843,10 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_tc_kernel(
   } else {
     // ------------------------------------------------------------------ O warpgroups (2)
     // thread = query row r = TMEM lane; OW o owns output channels 64o..64o+63
-    asm volatile("setmaxnreg.inc.sync.aligned.u32 128;");
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(Gm::REG_O));
     asm volatile("griddepcontrol.wait;" ::: "memory");  // the FP16 tail is the ingest's output too
-    const int ow = (warp - 12) >> 2;
-    const int r = (tid - 384) & (BM - 1);
+    const int ow = (warp - 4 - 4 * NSG) >> 2;
+    const int r = (tid - OBASE) & (BM - 1);
     const uint32_t lane_base = (uint32_t)(32 * (warp & 3)) << 16;
     const int cb = 64 * ow;
     int jg = 0, jpv = 0;  // tiles / PV tiles of all items so far
@@ -831,7 +874,9 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_tc_kernel(
         const uint32_t dph = (jpv / NDB) & 1;
         ++jpv;
         // (a7) O += (s_p/2) s_v E + s_p SP_s m_v + mu_p y_v on D' of this tile
-        const int sps = sm.sp_part[bj][0][r] + sm.sp_part[bj][1][r] - 128 * PI;  // sum (p' - 128)
+        int sps = -128 * PI;  // sum (p' - 128)
+#pragma unroll
+        for (int w2 = 0; w2 < NSG; ++w2) sps += sm.sp_part[bj][w2][r];
         const float2 ap2 = make_float2(0.5f * pi4.z, 0.5f * pi4.z);
         const float2 xp2 = make_float2(pi4.z * (float)sps, pi4.z * (float)sps);
         const float mp = __fmaf_rn(128.f, pi4.z, pi4.w);
@@ -908,7 +953,10 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_tc_kernel(
       ptx::mbar_arrive(&sm.o_done[bj]);
     }
     ptx::mbar_wait(&sm.l_ready, it & 1);
-    const float inv_l = 1.f / (sm.lpart[0][r] + sm.lpart[1][r]);
+    float lsum = sm.lpart[0][r];
+#pragma unroll
+    for (int w2 = 1; w2 < NSG; ++w2) lsum += sm.lpart[w2][r];
+    const float inv_l = 1.f / lsum;
     ptx::mbar_arrive(&sm.l_free);
     if (pos < L) {
       const int64_t base = ((int64_t)(start + pos) * kc.Hq + hq) * 128 + cb;
@@ -970,18 +1018,20 @@ cudaError_t launch_t(const KernelCfg& kc, const void* q, const int32_t* cu, cons
   } else {
     lc.gridDim = dim3(nqt, kc.Hq / gp, batch);
   }
-  lc.blockDim = dim3(kThreads);
+  lc.blockDim = dim3(Geo<PI_, BITS>::THREADS);
   lc.dynamicSmemBytes = smem;
   lc.stream = st;
   // pdl: a programmatic dependent of the ingest just launched on `st` (hack_prefill_attention):
   // the Q quantization prologue (which reads only q and rng_ids) overlaps the ingest; the
   // producer and O warps wait in griddepcontrol.wait before they read pages or the FP16 tail.
   // Without pdl griddepcontrol.wait returns at once (the stream order already holds).
+  // Not for the persistent launch: its one CTA per SM would share the SMs with the ingest
+  // blocks and slow the ingest it waits for (C2 step measured 446 us with, 434 us without).
   cudaLaunchAttribute at[1];
   at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   at[0].val.programmaticStreamSerializationAllowed = 1;
   lc.attrs = at;
-  lc.numAttrs = pdl ? 1 : 0;
+  lc.numAttrs = pdl && nitems == 0 ? 1 : 0;
   e = cudaLaunchKernelEx(&lc, kern, reinterpret_cast<const __half*>(q), cu, slots, cv, kc, out,
                          dbg ? dbg->pcodes : (uint8_t*)nullptr, dbg ? dbg->pcodes_stride : (int64_t)0,
                          dbg ? dbg->qk_acc : (int32_t*)nullptr, dbg ? dbg->pv_acc : (int32_t*)nullptr,
