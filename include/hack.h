@@ -214,8 +214,9 @@ hack_status_t hack_decode_append(const hack_config_t* cfg, const void* k_new, co
                                  void* stream);
 /* Append (a8) then attend (a9) with L_Q = 1: q_new device fp16 [batch][H_q][d];
  * out [batch][H_q][d].  max_seqlen: host upper bound of seq_lens after the append.
- * workspace: device, >= hack_decode_workspace_size() bytes (split partials; any contents),
- * one workspace per stream. */
+ * workspace: device, >= hack_decode_workspace_size() bytes (split partials and per-unit
+ * merge counters): zero-filled before its first use; every launch leaves the counters zero
+ * again, so it is reused without clearing.  One workspace per stream. */
 size_t hack_decode_workspace_size(const hack_config_t* cfg, int32_t batch, int32_t max_seqlen);
 hack_status_t hack_decode_attention(const hack_config_t* cfg, const void* q_new, const void* k_new,
                                     const void* v_new, const int32_t* slots, int32_t batch,

@@ -25,7 +25,8 @@
 //     pages in order (cp.async.bulk into a 9-slot ring), the 3 compute warps take page
 //     pairs round-robin and flush one (m, l, O) partial per (segment, warp) to global
 //     memory.  Partial slot of (unit u, CTA c) = u + c (injective: units and CTA ranges
-//     are both monotone along the flattened order).  decode_pair_combine merges them.
+//     are both monotone along the flattened order).  The CTA completing a unit merges its
+//     partials (merge_units), no second kernel.
 #include <cstdlib>
 
 #include "common.cuh"
@@ -73,6 +74,7 @@ struct PairSmem {
   int R, P;
   uint64_t full[NSTG], fullv[NSTG], empty[NSTG];  // fullv: the V half of a split page copy
   int tag[NSTG];  // page index of the slot's latest issued fill (see wait_fill)
+  int mflag;      // merge_units: this CTA completes the unit
 };
 
 HACK_DEV void mma16832(uint32_t (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3, uint32_t b0,
@@ -113,6 +115,7 @@ HACK_DEV int npages_of(const CacheView& cv, const int32_t* slots, int b) {
 // One unit segment of a CTA's page range.
 struct Seg {
   int b, hk, p0, p1;  // request, KV head, page range [p0, p1) of the unit
+  int uoff, npg;      // flattened offset of the unit's first page, its page count
 };
 
 // Walks the unit segments of the flattened page range [pos, end).
@@ -131,6 +134,8 @@ struct SegWalker {
     s.hk = rel / npg;
     s.p0 = rel - s.hk * npg;
     s.p1 = min(npg, s.p0 + (end - pos));
+    s.uoff = base + s.hk * npg;
+    s.npg = npg;
     pos += s.p1 - s.p0;
     return true;
   }
@@ -367,6 +372,89 @@ HACK_DEV void produce_pages(SMT& sm, SegWalker walk, const CacheView& cv, const 
   }
 }
 
+// In-kernel merge of the split partials (flash-decoding combine, no second kernel): after its
+// last segment a CTA counts itself in on every unit it contributed to (one counter per unit
+// in the workspace); the CTA that completes a unit's count merges the unit's partials (NW
+// warps x contributing CTAs) into the output rows and resets the counter to zero for the
+// next launch.  A partial covers slot (u + c, warp): CTA c of the unit's CTA span
+// [uoff / R, (uoff + npg - 1) / R].  Writers fence their partial stores before the count;
+// the merging CTA fences after it and reads the partials through L2 (ld.cg).
+// All 4 warps (3 compute + the producer) of the CTA run it: thread = output channel.
+template <int NWp>
+HACK_DEV void merge_units(SegWalker walk, int R, const CacheView& cv, const int32_t* __restrict__ slots,
+                          const KernelCfg& kc, int* __restrict__ cnt, const float* __restrict__ part,
+                          void* __restrict__ out, int* flag_smem, int tid) {
+  static_assert((NWp + 1) * 32 == 128, "thread = channel");
+  __threadfence();  // this thread's partial stores precede the CTA's count below
+  __syncthreads();
+  const int G = kc.G;
+  Seg s;
+  while (walk.next(cv, slots, kc.Hkv, s)) {
+    const int u = s.b * kc.Hkv + s.hk;
+    const int cf = s.uoff / R, cl = (s.uoff + s.npg - 1) / R;
+    if (tid == 0) {
+      const int n = atomicAdd(cnt + u, 1) + 1;
+      const bool last = n == cl - cf + 1;
+      if (last) cnt[u] = 0;  // no other CTA touches it again in this launch
+      *flag_smem = last;
+    }
+    __syncthreads();
+    const bool last = *flag_smem != 0;
+    __syncthreads();  // (flag reused by the next segment)
+    if (!last) continue;
+    __threadfence();
+    const int np = (cl - cf + 1) * NWp;
+    const int64_t stride = (int64_t)G * kPart;  // partial k at base + k * stride
+    const float* base = part + ((int64_t)(u + cf) * NWp) * stride;
+    // warp w merges row n0 + w, lane = 4 channels: every partial load of the row in flight
+    // at once (one L2 round trip per 8 partials)
+    const int w = tid >> 5, lane = tid & 31;
+    for (int n = w; n < G; n += NWp + 1) {
+      float M = -INFINITY, L = 0.f;
+      float4 O = make_float4(0.f, 0.f, 0.f, 0.f);
+      for (int k0 = 0; k0 < np; k0 += 8) {
+        float ms[8], ls[8];
+        float4 os[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const bool ok = k0 + k < np;
+          const float* src = base + (k0 + k) * stride + n * kPart;
+          ms[k] = ok ? __ldcg(src) : -INFINITY;
+          ls[k] = ok ? __ldcg(src + 1) : 0.f;
+          os[k] = ok ? make_float4(__ldcg(src + 2 + 4 * lane), __ldcg(src + 3 + 4 * lane), __ldcg(src + 4 + 4 * lane),
+                                   __ldcg(src + 5 + 4 * lane))
+                     : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+        float Mn = M;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) Mn = fmaxf(Mn, ms[k]);
+        if (Mn == -INFINITY) continue;
+        const float r = ex2(M - Mn);  // 0 when M = -inf
+        L *= r;
+        O.x *= r; O.y *= r; O.z *= r; O.w *= r;
+        M = Mn;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const float f = ex2(ms[k] - M);  // ex2(-inf) = 0 for empty partials
+          L = fmaf(f, ls[k], L);
+          O.x = fmaf(f, os[k].x, O.x);
+          O.y = fmaf(f, os[k].y, O.y);
+          O.z = fmaf(f, os[k].z, O.z);
+          O.w = fmaf(f, os[k].w, O.w);
+        }
+      }
+      const float il = 1.f / L;
+      const int64_t idx = ((int64_t)s.b * kc.Hq + s.hk * G + n) * 128 + 4 * lane;
+      if (kc.out_fp32) {
+        *reinterpret_cast<float4*>(reinterpret_cast<float*>(out) + idx) = make_float4(O.x * il, O.y * il, O.z * il, O.w * il);
+      } else {
+        __half2 hv[2] = {__floats2half2_rn(O.x * il, O.y * il), __floats2half2_rn(O.z * il, O.w * il)};
+        *reinterpret_cast<uint2*>(reinterpret_cast<__half*>(out) + idx) = *reinterpret_cast<uint2*>(hv);
+      }
+    }
+  }
+}
+
 // DBG: parity runs only (hack_debug_t): P-code and raw QK / PV accumulator dumps.
 struct DecDbg {
   uint8_t* pcodes;
@@ -383,7 +471,8 @@ struct DecDbg {
 template <bool DBG, bool SE>
 __global__ void __launch_bounds__(kThreads, kCtasPerSm)
     decode_pair_kernel(const __half* __restrict__ q_new, const int32_t* __restrict__ slots, int batch, CacheView cv,
-                       KernelCfg kc, int* __restrict__ ws_meta, float* __restrict__ part, DecDbg dbg) {
+                       KernelCfg kc, int* __restrict__ ws_meta, int* __restrict__ cnt, float* __restrict__ part,
+                       void* __restrict__ out, int merge, DecDbg dbg) {
   uint8_t* const dbg_pcodes = dbg.pcodes;
   const int64_t dbg_stride = dbg.pstride;
   constexpr int qkm = 3;
@@ -416,8 +505,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
 
   if (warp == NW) {
     produce_pages<NSTG>(sm, walk, cv, slots, Hkv, kc, lane);
-    return;
-  }
+  } else {
 
   // -------------------------------------------------------------------- compute warps
   typename PairSmem::Warp& ws = sm.w[warp];
@@ -727,6 +815,10 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
     it_base += nitems;
     k_base += s.p1 - s.p0;
   }
+  }  // compute warps
+  if (merge)
+    merge_units<NW>(SegWalker{sm.range_b0, sm.range_base, min(c * sm.R, sm.P), min(c * sm.R + sm.R, sm.P)}, sm.R, cv,
+                    slots, kc, cnt, part, out, &sm.mflag, tid);
 }
 
 // ============================================================================ G in (4, 8]
@@ -757,12 +849,14 @@ struct G8Smem {
   int R, P;
   uint64_t full[NSTG8], fullv[NSTG8], empty[NSTG8];
   int tag[NSTG8];
+  int mflag;
 };
 
 template <bool DBG>
 __global__ void __launch_bounds__(kThreads, kCtas8)
     decode_g8_kernel(const __half* __restrict__ q_new, const int32_t* __restrict__ slots, int batch, CacheView cv,
-                     KernelCfg kc, int* __restrict__ ws_meta, float* __restrict__ part, DecDbg dbg) {
+                     KernelCfg kc, int* __restrict__ ws_meta, int* __restrict__ cnt, float* __restrict__ part,
+                     void* __restrict__ out, int merge, DecDbg dbg) {
   uint8_t* const dbg_pcodes = dbg.pcodes;
   const int64_t dbg_stride = dbg.pstride;
   constexpr int qkm = 3;
@@ -793,8 +887,7 @@ __global__ void __launch_bounds__(kThreads, kCtas8)
   SegWalker walk{sm.range_b0, sm.range_base, min(c * R, P), min(c * R + R, P)};
   if (warp == NW) {
     produce_pages<NSTG8>(sm, walk, cv, slots, Hkv, kc, lane);
-    return;
-  }
+  } else {
 
   typename G8Smem::Warp& ws = sm.w[warp];
   const float cscale = 1.4426950408889634f / sqrtf(128.f);
@@ -1077,6 +1170,10 @@ __global__ void __launch_bounds__(kThreads, kCtas8)
     it_base += nitems;
     k_base += s.p1 - s.p0;
   }
+  }  // compute warps
+  if (merge)
+    merge_units<NW>(SegWalker{sm.range_b0, sm.range_base, min(c * sm.R, sm.P), min(c * sm.R + sm.R, sm.P)}, sm.R, cv,
+                    slots, kc, cnt, part, out, &sm.mflag, tid);
 }
 
 // out[b][hk*G + n][c] = sum_parts e^(m - M) O / sum_parts e^(m - M) l over the partials of
@@ -1141,6 +1238,9 @@ int grid_size(bool g8 = false) {
 }
 
 size_t meta_bytes(int batch) { return ((size_t)(kMetaInts + 2 * batch) * sizeof(int) + 255) / 256 * 256; }
+// merge counters, one per (request, KV head) unit: zero before the first launch, and every
+// launch leaves them zero (merge_units)
+size_t cnt_bytes(const KernelCfg& kc, int batch) { return ((size_t)batch * kc.Hkv * sizeof(int) + 255) / 256 * 256; }
 
 }  // namespace
 
@@ -1152,20 +1252,30 @@ bool decode_pair_supported(const KernelCfg& kc) {
 size_t decode_pair_workspace(const KernelCfg& kc, int batch, int max_seqlen) {
   (void)max_seqlen;
   const size_t slots = (size_t)batch * kc.Hkv + grid_size(kc.G > 4);
-  return meta_bytes(batch) + slots * NW * kc.G * kPart * sizeof(float);
+  return meta_bytes(batch) + cnt_bytes(kc, batch) + slots * NW * kc.G * kPart * sizeof(float);
 }
 
 cudaError_t launch_decode_pair(const KernelCfg& kc, const void* q_new, const int32_t* slots, int batch,
                                int max_seqlen, const CacheView& cv, void* out, void* workspace,
                                const hack_debug_t* dbg, cudaStream_t st) {
-  (void)max_seqlen;
   int* meta = reinterpret_cast<int*>(workspace);
-  float* part = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(workspace) + meta_bytes(batch));
+  int* cnt = reinterpret_cast<int*>(reinterpret_cast<uint8_t*>(workspace) + meta_bytes(batch));
+  float* part = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(workspace) + meta_bytes(batch) + cnt_bytes(kc, batch));
   const bool g8 = kc.G > 4;
   const size_t smem = g8 ? sizeof(G8Smem) : sizeof(PairSmem);
   const bool with_dbg = dbg != nullptr && (dbg->pcodes != nullptr || dbg->qk_acc != nullptr ||
                                            dbg->pv_acc != nullptr);  // dumps: parity runs only
   const bool no_se = !g8 && getenv("HACK_DECODE_NO_SE") != nullptr;  // f2 ablation only
+  // where the split partials are merged: in the main kernel by the CTA completing a unit
+  // (merge_units) when units span few CTAs -- the merging CTA's few L2 round trips beat a
+  // second launch -- else by decode_pair_combine, whose B x H_q CTAs merge in parallel
+  // (long units over many CTAs, e.g. head-sharded decode).  Estimated from the host bound
+  // max_seqlen: CTAs per unit ~ pages per unit / pages per CTA.
+  const int grid = grid_size(g8);
+  const double npg = (double)((max_seqlen + PI - 1) / PI);
+  const double per_cta = npg * batch * kc.Hkv / grid;
+  bool merge = npg <= 1.5 * per_cta;  // (C3: 1.2 -> in-kernel; head-sharded N = 2: 2.3 measured 5 % slower in-kernel)
+  if (const char* e = getenv("HACK_DECODE_MERGE")) merge = e[0] == '1';  // A/B timing knob
   auto kern = g8 ? (with_dbg ? decode_g8_kernel<true> : decode_g8_kernel<false>)
                  : with_dbg ? (no_se ? decode_pair_kernel<true, false> : decode_pair_kernel<true, true>)
                             : (no_se ? decode_pair_kernel<false, false> : decode_pair_kernel<false, true>);
@@ -1179,7 +1289,7 @@ cudaError_t launch_decode_pair(const KernelCfg& kc, const void* q_new, const int
     // preceding kernel on the stream (the append) drains; griddepcontrol.wait in the
     // kernel orders its global reads after that kernel's writes
     cudaLaunchConfig_t mc = {};
-    mc.gridDim = dim3(grid_size(g8));
+    mc.gridDim = dim3(grid);
     mc.blockDim = dim3(kThreads);
     mc.dynamicSmemBytes = smem;
     mc.stream = st;
@@ -1195,17 +1305,15 @@ cudaError_t launch_decode_pair(const KernelCfg& kc, const void* q_new, const int
     DecDbg dd = {nullptr, 0, nullptr, nullptr, 0, -1};
     if (with_dbg) dd = {dbg->pcodes, dbg->pcodes_stride, dbg->qk_acc, dbg->pv_acc, dbg->acc_stride, dbg->acc_head};
     const cudaError_t e1 = cudaLaunchKernelEx(&mc, kern, reinterpret_cast<const __half*>(q_new), slots, batch, cv, kc,
-                                              meta, part, dd);
+                                              meta, cnt, part, out, merge ? 1 : 0, dd);
     if (e1 != cudaSuccess) return e1;
   }
-#ifdef HACK_DEC_NOCOMBINE
-  note_launch();  // timing experiment only (the merge costs ~9.7 us of 117 on C3): no outputs
-  return cudaGetLastError();
-#endif
-  // the merge is launched as a programmatic dependent of the main kernel (PDL): its CTAs can
-  // be resident before the main grid drains and wait in griddepcontrol.wait.  (Computing the
-  // page geometry from seq_lens before the wait, with an early launch_dependents trigger in
-  // the main grid, measured 2 us slower.)
+  note_launch();
+  if (merge) return cudaGetLastError();
+  // the merge kernel is launched as a programmatic dependent of the main kernel (PDL): its CTAs
+  // can be resident before the main grid drains and wait in griddepcontrol.wait.  (Computing
+  // the page geometry from seq_lens before the wait, with an early launch_dependents trigger
+  // in the main grid, measured 2 us slower.)
   cudaLaunchConfig_t lc = {};
   lc.gridDim = dim3(batch, kc.Hq);
   lc.blockDim = dim3(128);
@@ -1217,7 +1325,7 @@ cudaError_t launch_decode_pair(const KernelCfg& kc, const void* q_new, const int
   lc.numAttrs = 1;
   const cudaError_t e2 = cudaLaunchKernelEx(&lc, decode_pair_combine, (const int*)meta, (const float*)part, kc, out);
   if (e2 != cudaSuccess) return e2;
-  note_launch(2);
+  note_launch();
   return cudaGetLastError();
 }
 

@@ -294,7 +294,9 @@ def _ws(workspace, nbytes, device):
     if nbytes == 0:
         return None, 0
     if workspace is None:
-        workspace = torch.empty(nbytes, dtype=torch.uint8, device=device)
+        # zero-filled: the decode workspace holds merge counters that must start at zero
+        # (hack.h); the library leaves them zero after every launch
+        workspace = torch.zeros(nbytes, dtype=torch.uint8, device=device)
     return workspace, workspace.numel()
 
 

@@ -116,7 +116,12 @@ def test_decode_crosses_flush(L):
     run_decode(att.Config(Hq=4, Hkv=1, Pi=64, bits=2), [L], 70, check_every=7, check_pages_at=(5, 40))
 
 
-def test_decode_batch_gqa_mixed_lengths():
+@pytest.mark.parametrize("merge", ["auto", "1", "0"])
+def test_decode_batch_gqa_mixed_lengths(merge, monkeypatch):
+    # merge: where the split partials are merged (decode_pair.cu): chosen by the launch, in
+    # the main kernel (merge_units), or by decode_pair_combine
+    if merge != "auto":
+        monkeypatch.setenv("HACK_DECODE_MERGE", merge)
     run_decode(att.Config(Hq=8, Hkv=2, Pi=64, bits=2, seed=99, layer=1), [100, 1, 64, 255], 40, check_every=5)
 
 
@@ -264,9 +269,11 @@ def test_decode_long_context_tiny_cta_ranges():
     run_decode(att.Config(Hq=4, Hkv=1, Pi=64, bits=2, seed=31), [96000], 2)
 
 
-@pytest.mark.parametrize("Hq", [8, 6])
-def test_decode_group8_paired_kernel(Hq):
+@pytest.mark.parametrize("Hq,merge", [(8, "auto"), (6, "auto"), (8, "1")])
+def test_decode_group8_paired_kernel(Hq, merge, monkeypatch):
     # decode_g8_kernel: G in (4, 8] (C4 70B shape has G = 8), flushes, tails, mixed lengths
+    if merge != "auto":
+        monkeypatch.setenv("HACK_DECODE_MERGE", merge)
     run_decode(att.Config(Hq=Hq, Hkv=1, Pi=64, bits=2, seed=14), [300, 64, 1000, 1], 70, check_every=9)
 
 
@@ -281,3 +288,37 @@ def test_decode_p_stochastic_rounding(Pi, bits, Hq):
     across flushes; near-ties judged against the SR boundary."""
     run_decode(att.Config(Hq=Hq, Hkv=2 if Hq < 8 else 1, Pi=Pi, bits=bits, p_round="sr", seed=19), [130, 64],
                Pi + 3, check_every=7)
+
+
+@pytest.mark.parametrize("Hq,merge", [(8, "1"), (16, "1"), (8, "0")])
+def test_decode_workspace_reuse_merge_counters(Hq, merge, monkeypatch):
+    """The in-kernel merge counts CTAs per unit in the workspace and leaves the counters zero:
+    one zero-filled workspace reused for many launches (mixed lengths, units split over many
+    CTAs, G = 4 pair kernel and G = 8 kernel) gives bit-identical outputs to a fresh
+    workspace per launch, and the counter region is zero afterwards."""
+    monkeypatch.setenv("HACK_DECODE_MERGE", merge)
+    h = hk()
+    ocfg = att.Config(Hq=Hq, Hkv=2, Pi=64, bits=2, seed=5)
+    cfg = gpu_cfg(ocfg)
+    lens = [5000, 1, 64, 700, 129, 3000]
+    B = len(lens)
+    cache = make_cache(cfg, max_reqs=B, max_len=max(lens) + 4, seed=5)
+    for i, n in enumerate(lens):
+        _, k, v = hack_inputs.qkv(60 + i, n, 1, ocfg.Hkv)
+        h.cache_ingest(cfg, torch.from_numpy(k).cuda(), torch.from_numpy(v).cuda(),
+                       torch.tensor([0, n], dtype=torch.int32, device="cuda"),
+                       torch.tensor([i], dtype=torch.int32, device="cuda"), n, cache)
+    sl = torch.arange(B, dtype=torch.int32, device="cuda")
+    nb = h.decode_workspace_size(cfg, B, max(lens) + 4)
+    ws = torch.zeros(nb, dtype=torch.uint8, device="cuda")
+    qd, _, _ = hack_inputs.decode_tokens(9, 6, B, ocfg.Hq, ocfg.Hkv)
+    for s in range(6):
+        q = torch.from_numpy(qd[s]).cuda()
+        o1 = torch.zeros((B, ocfg.Hq, 128), dtype=torch.float32, device="cuda")
+        o2 = torch.zeros_like(o1)
+        h.decode_attention_cached(cfg, q, sl, max(lens) + 4, cache, o1, workspace=ws)
+        h.decode_attention_cached(cfg, q, sl, max(lens) + 4, cache, o2)   # fresh zero workspace
+        assert np.array_equal(o1.cpu().numpy().view(np.uint32), o2.cpu().numpy().view(np.uint32)), f"launch {s}"
+    # counter region: after the header of (16 + 2 B) ints rounded to 256 B, B * H_kv ints
+    off = ((16 + 2 * B) * 4 + 255) // 256 * 256
+    assert int(ws[off:off + 4 * B * ocfg.Hkv].view(torch.int32).abs().sum()) == 0
