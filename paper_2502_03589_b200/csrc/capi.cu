@@ -353,11 +353,8 @@ hack_status_t hack_decode_attention(const hack_config_t* cfg, const void* q_new,
   if ((st = check_append(cache, k_new, v_new, slots, batch)) != HACK_OK) return st;
   if ((st = check_decode(kc, cache, q_new, slots, batch, max_seqlen, out, ws, ws_bytes, dbg)) != HACK_OK) return st;
   if ((st = check_device()) != HACK_OK) return st;
-  if ((st = cuda_status(launch_append(kc, k_new, v_new, slots, batch, cv, (cudaStream_t)stream), "decode_append")) !=
-      HACK_OK)
-    return st;
-  return cuda_status(launch_decode_attention(kc, q_new, slots, batch, max_seqlen, cv, out, ws, dbg,
-                                             (cudaStream_t)stream),
+  return cuda_status(launch_decode_step(kc, q_new, k_new, v_new, slots, batch, max_seqlen, cv, out, ws, dbg,
+                                        (cudaStream_t)stream),
                      "decode_attention");
 }
 

@@ -29,6 +29,7 @@
 //     partials (merge_units), no second kernel.
 #include <cstdlib>
 
+#include "append.cuh"
 #include "common.cuh"
 #include "internal.h"
 #include "tc_ptx.cuh"
@@ -108,8 +109,15 @@ HACK_DEV Planes planes2(uint32_t w) {
 HACK_DEV float2 f2(float a, float b) { return make_float2(a, b); }
 HACK_DEV float2 asf2(uint32_t a, uint32_t b) { return make_float2(__uint_as_float(a), __uint_as_float(b)); }
 
-HACK_DEV int npages_of(const CacheView& cv, const int32_t* slots, int b) {
-  return (cv.seq_lens[slots[b]] + PI - 1) / PI;
+// The request's length this step: seq_lens, + 1 in the fused decode step (its append runs in
+// the kernel and seq_lens is bumped only when every CTA is done reading it), unless the
+// capacity guard of the append (append_kernel) skips the request.
+HACK_DEV int len_of(const CacheView& cv, int slot, int add) {
+  const int t = cv.seq_lens[slot];
+  return t + (add && t / PI < cv.max_pages_per_req ? 1 : 0);
+}
+HACK_DEV int npages_of(const CacheView& cv, const int32_t* slots, int b, int add) {
+  return (len_of(cv, slots[b], add) + PI - 1) / PI;
 }
 
 // One unit segment of a CTA's page range.
@@ -121,13 +129,15 @@ struct Seg {
 // Walks the unit segments of the flattened page range [pos, end).
 struct SegWalker {
   int b, base, pos, end;  // current request, flattened offset of its first unit, cursor, range end
-  HACK_DEV bool next(const CacheView& cv, const int32_t* slots, int Hkv, Seg& s) {
+  // add: fused append, lengths + 1 (len_of); from the kernel parameter at each call (no register
+  // held across the attention loop)
+  HACK_DEV bool next(const CacheView& cv, const int32_t* slots, int Hkv, Seg& s, int add) {
     if (pos >= end) return false;
-    int npg = npages_of(cv, slots, b);
+    int npg = npages_of(cv, slots, b, add);
     while (pos >= base + npg * Hkv) {  // (only when the cursor sits exactly on a request boundary)
       base += npg * Hkv;
       ++b;
-      npg = npages_of(cv, slots, b);
+      npg = npages_of(cv, slots, b, add);
     }
     const int rel = pos - base;
     s.b = b;
@@ -234,13 +244,13 @@ HACK_DEV void qk_page(const uint8_t* pg, const PageLayout& PL, const float4* kcs
 // CTA 0 also publishes the per-request offsets and page counts for the merge kernel.
 template <class SMT>
 HACK_DEV void locate_range(SMT& sm, const CacheView& cv, const int32_t* __restrict__ slots, int batch, int Hkv,
-                           int* __restrict__ ws_meta, int warp, int lane) {
+                           int* __restrict__ ws_meta, int warp, int lane, int add) {
   const int c = blockIdx.x;
   if (warp == 0) {
     int P = 0;
     for (int b0 = 0; b0 < batch; b0 += 32) {
       const int b = b0 + lane;
-      const int n = b < batch ? npages_of(cv, slots, b) * Hkv : 0;
+      const int n = b < batch ? npages_of(cv, slots, b, add) * Hkv : 0;
       int v = n;
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {  // inclusive scan
@@ -259,7 +269,7 @@ HACK_DEV void locate_range(SMT& sm, const CacheView& cv, const int32_t* __restri
     int base = 0, bsel = batch, basesel = P;
     for (int b0 = 0; b0 < batch && bsel == batch; b0 += 32) {
       const int b = b0 + lane;
-      const int n = b < batch ? npages_of(cv, slots, b) * Hkv : 0;
+      const int n = b < batch ? npages_of(cv, slots, b, add) * Hkv : 0;
       int v = n;
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
@@ -312,17 +322,49 @@ HACK_DEV void wait_fill(SMT& sm, int k) {
   ptx::mbar_wait(&sm.full[s], (k / N) & 1);
 }
 
+// Fused decode step (hack_decode_attention): k_new / v_new of the step and the grid-wide
+// completion counter (workspace, zero between launches).
+struct StepIO {
+  const __half* k_new;
+  const __half* v_new;
+  int* done;
+};
+
+// The append (a8) of every unit whose last page (at the new length) lies in this CTA's range,
+// run by the producer warp (32 lanes) once the page ring is full or, before that, right
+// before it issues such a page: the appended page (K row, and the V block of a flush) and the
+// unit's FP16 tail are read by this CTA only, after that page's copy.  Generic-proxy stores,
+// then a proxy fence, so the bulk copies (async proxy) see them; the compute warps see the tail
+// through the page's full barrier (release by the producer's arrive, acquire by their wait).
+// (Inlined: as a call, its ABI cost the attention loop registers and spills.)
+HACK_DEV void producer_append(const StepIO& io, SegWalker walk, const CacheView& cv,
+                                             const int32_t* __restrict__ slots, const KernelCfg& kc, int lane) {
+  Seg s;
+  while (walk.next(cv, slots, kc.Hkv, s, 1)) {
+    if (s.p1 != s.npg) continue;  // the unit's last page is another CTA's
+    const int slot = slots[s.b];
+    const int t = cv.seq_lens[slot];
+    if (t / PI >= cv.max_pages_per_req) continue;  // capacity guard (append_kernel)
+    append_unit<2, true, 32>(io.k_new, io.v_new, s.b, slot, t, s.hk, cv, kc, lane, [] { __syncwarp(); });
+  }
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+  __threadfence_block();
+  __syncwarp();
+}
+
 // Producer warp: streams the CTA's pages in order into an N-slot ring (cp.async.bulk).
-template <int N, class SMT>
+template <int N, bool FUSED, class SMT>
 HACK_DEV void produce_pages(SMT& sm, SegWalker walk, const CacheView& cv, const int32_t* __restrict__ slots,
-                            int Hkv, const KernelCfg& kc, int lane) {
+                            int Hkv, const KernelCfg& kc, int lane, const StepIO& io) {
+  const SegWalker walk0 = walk;
+  bool appended = false;
     // ------------------------------------------------------------------ producer
   // The whole warp walks the segments; block-table entries are fetched 32 pages at a
   // time with one coalesced load, so the issuing lane never waits on a dependent global
   // load between two page copies (one such wait per page capped the issue rate).
   Seg s;
   int k = 0;
-  while (walk.next(cv, slots, Hkv, s)) {
+  while (walk.next(cv, slots, Hkv, s, FUSED)) {
     const int32_t* bt = cv.block_table + (int64_t)slots[s.b] * cv.max_pages_per_req;
     for (int p0 = s.p0; p0 < s.p1; p0 += 32) {
       const int n = min(32, s.p1 - p0);
@@ -335,6 +377,12 @@ HACK_DEV void produce_pages(SMT& sm, SegWalker walk, const CacheView& cv, const 
         const int pid = __shfl_sync(0xffffffffu, ent, x);
         const int xf = x + HACK_DEC_PF;
         const int pfa = __shfl_sync(0xffffffffu, ent, xf & 31), pfb = __shfl_sync(0xffffffffu, ent2, xf & 31);
+        // fused step: the appends of the CTA's units run once the ring is full (the producer
+        // would wait for a slot anyway) or before the first page that receives a new token
+        if (FUSED && !appended && (k == N || (s.p1 == s.npg && p0 + x == s.p1 - 1))) {
+          producer_append(io, walk0, cv, slots, kc, lane);
+          appended = true;
+        }
         if (lane == 0) {
           const int st = k % N;
 #ifdef HACK_DEC_SPIN
@@ -383,13 +431,13 @@ HACK_DEV void produce_pages(SMT& sm, SegWalker walk, const CacheView& cv, const 
 template <int NWp>
 HACK_DEV void merge_units(SegWalker walk, int R, const CacheView& cv, const int32_t* __restrict__ slots,
                           const KernelCfg& kc, int* __restrict__ cnt, const float* __restrict__ part,
-                          void* __restrict__ out, int* flag_smem, int tid) {
+                          void* __restrict__ out, int* flag_smem, int tid, int add) {
   static_assert((NWp + 1) * 32 == 128, "thread = channel");
   __threadfence();  // this thread's partial stores precede the CTA's count below
   __syncthreads();
   const int G = kc.G;
   Seg s;
-  while (walk.next(cv, slots, kc.Hkv, s)) {
+  while (walk.next(cv, slots, kc.Hkv, s, add)) {
     const int u = s.b * kc.Hkv + s.hk;
     const int cf = s.uoff / R, cl = (s.uoff + s.npg - 1) / R;
     if (tid == 0) {
@@ -455,6 +503,26 @@ HACK_DEV void merge_units(SegWalker walk, int R, const CacheView& cv, const int3
   }
 }
 
+// seq_lens += 1 for the step's requests, by the last CTA to finish: every CTA has read the old
+// lengths (range geometry, walks, merge) before it counts itself done.
+HACK_DEV void bump_lengths(const StepIO& io, const CacheView& cv, const int32_t* __restrict__ slots, int batch,
+                           int* flag_smem, int tid) {
+  __syncthreads();
+  if (tid == 0) {
+    __threadfence();
+    *flag_smem = atomicAdd(io.done, 1) == (int)gridDim.x - 1;
+  }
+  __syncthreads();
+  if (*flag_smem == 0) return;
+  __threadfence();
+  for (int b = tid; b < batch; b += blockDim.x) {
+    const int slot = slots[b];
+    const int t = __ldcg(cv.seq_lens + slot);
+    if (t / PI < cv.max_pages_per_req) cv.seq_lens[slot] = t + 1;  // capacity guard (append_kernel)
+  }
+  if (tid == 0) *io.done = 0;
+}
+
 // DBG: parity runs only (hack_debug_t): P-code and raw QK / PV accumulator dumps.
 struct DecDbg {
   uint8_t* pcodes;
@@ -468,11 +536,11 @@ struct DecDbg {
   HACK_DEV int hdim(int Hq) const { return head < 0 ? Hq : 1; }
 };
 
-template <bool DBG, bool SE>
+template <bool DBG, bool SE, bool FUSED>
 __global__ void __launch_bounds__(kThreads, kCtasPerSm)
     decode_pair_kernel(const __half* __restrict__ q_new, const int32_t* __restrict__ slots, int batch, CacheView cv,
                        KernelCfg kc, int* __restrict__ ws_meta, int* __restrict__ cnt, float* __restrict__ part,
-                       void* __restrict__ out, int merge, DecDbg dbg) {
+                       void* __restrict__ out, int merge, StepIO io, DecDbg dbg) {
   uint8_t* const dbg_pcodes = dbg.pcodes;
   const int64_t dbg_stride = dbg.pstride;
   constexpr int qkm = 3;
@@ -498,13 +566,13 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
   // only shared memory; seq_lens, pages and the FP16 tail are read after this wait
   asm volatile("griddepcontrol.wait;" ::: "memory");
 #endif
-  locate_range(sm, cv, slots, batch, Hkv, ws_meta, warp, lane);
+  locate_range(sm, cv, slots, batch, Hkv, ws_meta, warp, lane, FUSED);
   __syncthreads();
   const int R = sm.R, P = sm.P;
   SegWalker walk{sm.range_b0, sm.range_base, min(c * R, P), min(c * R + R, P)};
 
   if (warp == NW) {
-    produce_pages<NSTG>(sm, walk, cv, slots, Hkv, kc, lane);
+    produce_pages<NSTG, FUSED>(sm, walk, cv, slots, Hkv, kc, lane, io);
   } else {
 
   // -------------------------------------------------------------------- compute warps
@@ -512,9 +580,9 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
   const float cscale = 1.4426950408889634f / sqrtf(128.f);
   Seg s;
   int it_base = 0, k_base = 0;
-  while (walk.next(cv, slots, Hkv, s)) {
+  while (walk.next(cv, slots, Hkv, s, FUSED)) {
     const int slot = slots[s.b];
-    const int len = cv.seq_lens[slot];
+    const int len = len_of(cv, slot, FUSED);
     const int nfull = len / PI;
     const int nc = max(0, min(s.p1, nfull) - s.p0);  // committed pages of the segment
     const bool has_tail = s.p1 > nfull;              // the segment ends with the partial last page
@@ -818,7 +886,8 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
   }  // compute warps
   if (merge)
     merge_units<NW>(SegWalker{sm.range_b0, sm.range_base, min(c * sm.R, sm.P), min(c * sm.R + sm.R, sm.P)}, sm.R, cv,
-                    slots, kc, cnt, part, out, &sm.mflag, tid);
+                    slots, kc, cnt, part, out, &sm.mflag, tid, FUSED);
+  if (FUSED && merge) bump_lengths(io, cv, slots, batch, &sm.mflag, tid);  // (else decode_pair_combine)
 }
 
 // ============================================================================ G in (4, 8]
@@ -852,11 +921,11 @@ struct G8Smem {
   int mflag;
 };
 
-template <bool DBG>
+template <bool DBG, bool FUSED>
 __global__ void __launch_bounds__(kThreads, kCtas8)
     decode_g8_kernel(const __half* __restrict__ q_new, const int32_t* __restrict__ slots, int batch, CacheView cv,
                      KernelCfg kc, int* __restrict__ ws_meta, int* __restrict__ cnt, float* __restrict__ part,
-                     void* __restrict__ out, int merge, DecDbg dbg) {
+                     void* __restrict__ out, int merge, StepIO io, DecDbg dbg) {
   uint8_t* const dbg_pcodes = dbg.pcodes;
   const int64_t dbg_stride = dbg.pstride;
   constexpr int qkm = 3;
@@ -881,12 +950,12 @@ __global__ void __launch_bounds__(kThreads, kCtas8)
   // only shared memory; seq_lens, pages and the FP16 tail are read after this wait
   asm volatile("griddepcontrol.wait;" ::: "memory");
 #endif
-  locate_range(sm, cv, slots, batch, Hkv, ws_meta, warp, lane);
+  locate_range(sm, cv, slots, batch, Hkv, ws_meta, warp, lane, FUSED);
   __syncthreads();
   const int R = sm.R, P = sm.P;
   SegWalker walk{sm.range_b0, sm.range_base, min(c * R, P), min(c * R + R, P)};
   if (warp == NW) {
-    produce_pages<NSTG8>(sm, walk, cv, slots, Hkv, kc, lane);
+    produce_pages<NSTG8, FUSED>(sm, walk, cv, slots, Hkv, kc, lane, io);
   } else {
 
   typename G8Smem::Warp& ws = sm.w[warp];
@@ -894,9 +963,9 @@ __global__ void __launch_bounds__(kThreads, kCtas8)
   const int n0 = 2 * tig, n1 = 2 * tig + 1;  // rows of this lane in the PV fragments
   Seg s;
   int it_base = 0, k_base = 0;
-  while (walk.next(cv, slots, Hkv, s)) {
+  while (walk.next(cv, slots, Hkv, s, FUSED)) {
     const int slot = slots[s.b];
-    const int len = cv.seq_lens[slot];
+    const int len = len_of(cv, slot, FUSED);
     const int nfull = len / PI;
     const int nitems = s.p1 - s.p0;  // single pages
     const int my0 = ((warp - it_base) % NW + NW) % NW;
@@ -1173,18 +1242,27 @@ __global__ void __launch_bounds__(kThreads, kCtas8)
   }  // compute warps
   if (merge)
     merge_units<NW>(SegWalker{sm.range_b0, sm.range_base, min(c * sm.R, sm.P), min(c * sm.R + sm.R, sm.P)}, sm.R, cv,
-                    slots, kc, cnt, part, out, &sm.mflag, tid);
+                    slots, kc, cnt, part, out, &sm.mflag, tid, FUSED);
+  if (FUSED && merge) bump_lengths(io, cv, slots, batch, &sm.mflag, tid);  // (else decode_pair_combine)
 }
 
 // out[b][hk*G + n][c] = sum_parts e^(m - M) O / sum_parts e^(m - M) l over the partials of
 // unit u = b*Hkv + hk: CTAs c_first..c_last of its flattened page range, NW warps each.
+// Fused step (bump != 0): seq_lens += 1 here, after the main grid (every read of the old
+// lengths) completed.
 __global__ void __launch_bounds__(128) decode_pair_combine(const int* __restrict__ ws_meta,
                                                            const float* __restrict__ part, KernelCfg kc,
-                                                           void* __restrict__ out) {
+                                                           void* __restrict__ out, CacheView cv,
+                                                           const int32_t* __restrict__ slots, int bump) {
   const int b = blockIdx.x, hq = blockIdx.y, c = threadIdx.x, batch = gridDim.x;
   const int hk = hq / kc.G, n = hq % kc.G;
   // launched with programmatic stream serialization: wait for the main kernel's results
   asm volatile("griddepcontrol.wait;" ::: "memory");
+  if (bump && hq == 0 && c == 0) {
+    const int slot = slots[b];
+    const int t = cv.seq_lens[slot];
+    if (t / PI < cv.max_pages_per_req) cv.seq_lens[slot] = t + 1;  // capacity guard (append_kernel)
+  }
   const int R = ws_meta[0];
   const int npg = ws_meta[kMetaInts + batch + b];
   const int off = ws_meta[kMetaInts + b] + hk * npg;
@@ -1241,6 +1319,7 @@ size_t meta_bytes(int batch) { return ((size_t)(kMetaInts + 2 * batch) * sizeof(
 // merge counters, one per (request, KV head) unit: zero before the first launch, and every
 // launch leaves them zero (merge_units)
 size_t cnt_bytes(const KernelCfg& kc, int batch) { return ((size_t)batch * kc.Hkv * sizeof(int) + 255) / 256 * 256; }
+// workspace: meta | merge counters | fused-step completion counter (256 B) | partials
 
 }  // namespace
 
@@ -1252,15 +1331,18 @@ bool decode_pair_supported(const KernelCfg& kc) {
 size_t decode_pair_workspace(const KernelCfg& kc, int batch, int max_seqlen) {
   (void)max_seqlen;
   const size_t slots = (size_t)batch * kc.Hkv + grid_size(kc.G > 4);
-  return meta_bytes(batch) + cnt_bytes(kc, batch) + slots * NW * kc.G * kPart * sizeof(float);
+  return meta_bytes(batch) + cnt_bytes(kc, batch) + 256 + slots * NW * kc.G * kPart * sizeof(float);
 }
 
 cudaError_t launch_decode_pair(const KernelCfg& kc, const void* q_new, const int32_t* slots, int batch,
                                int max_seqlen, const CacheView& cv, void* out, void* workspace,
-                               const hack_debug_t* dbg, cudaStream_t st) {
+                               const hack_debug_t* dbg, cudaStream_t st, const void* k_new, const void* v_new) {
   int* meta = reinterpret_cast<int*>(workspace);
   int* cnt = reinterpret_cast<int*>(reinterpret_cast<uint8_t*>(workspace) + meta_bytes(batch));
-  float* part = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(workspace) + meta_bytes(batch) + cnt_bytes(kc, batch));
+  int* done = reinterpret_cast<int*>(reinterpret_cast<uint8_t*>(workspace) + meta_bytes(batch) + cnt_bytes(kc, batch));
+  float* part = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(workspace) + meta_bytes(batch) + cnt_bytes(kc, batch) + 256);
+  // fused decode step (k_new given): the append runs inside the attention kernel
+  const StepIO io = {reinterpret_cast<const __half*>(k_new), reinterpret_cast<const __half*>(v_new), done};
   const bool g8 = kc.G > 4;
   const size_t smem = g8 ? sizeof(G8Smem) : sizeof(PairSmem);
   const bool with_dbg = dbg != nullptr && (dbg->pcodes != nullptr || dbg->qk_acc != nullptr ||
@@ -1276,9 +1358,13 @@ cudaError_t launch_decode_pair(const KernelCfg& kc, const void* q_new, const int
   const double per_cta = npg * batch * kc.Hkv / grid;
   bool merge = npg <= 1.5 * per_cta;  // (C3: 1.2 -> in-kernel; head-sharded N = 2: 2.3 measured 5 % slower in-kernel)
   if (const char* e = getenv("HACK_DECODE_MERGE")) merge = e[0] == '1';  // A/B timing knob
-  auto kern = g8 ? (with_dbg ? decode_g8_kernel<true> : decode_g8_kernel<false>)
-                 : with_dbg ? (no_se ? decode_pair_kernel<true, false> : decode_pair_kernel<true, true>)
-                            : (no_se ? decode_pair_kernel<false, false> : decode_pair_kernel<false, true>);
+  const bool fused = k_new != nullptr;  // (the SE ablation never runs fused: launch_decode_step)
+  auto kern = g8 ? (with_dbg ? (fused ? decode_g8_kernel<true, true> : decode_g8_kernel<true, false>)
+                             : (fused ? decode_g8_kernel<false, true> : decode_g8_kernel<false, false>))
+          : with_dbg ? (no_se ? decode_pair_kernel<true, false, false>
+                              : (fused ? decode_pair_kernel<true, true, true> : decode_pair_kernel<true, true, false>))
+                     : (no_se ? decode_pair_kernel<false, false, false>
+                              : (fused ? decode_pair_kernel<false, true, true> : decode_pair_kernel<false, true, false>));
   // the attribute is per device / context: set it on every launch (cheap), no process-wide cache
   {
     const cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -1305,7 +1391,7 @@ cudaError_t launch_decode_pair(const KernelCfg& kc, const void* q_new, const int
     DecDbg dd = {nullptr, 0, nullptr, nullptr, 0, -1};
     if (with_dbg) dd = {dbg->pcodes, dbg->pcodes_stride, dbg->qk_acc, dbg->pv_acc, dbg->acc_stride, dbg->acc_head};
     const cudaError_t e1 = cudaLaunchKernelEx(&mc, kern, reinterpret_cast<const __half*>(q_new), slots, batch, cv, kc,
-                                              meta, cnt, part, out, merge ? 1 : 0, dd);
+                                              meta, cnt, part, out, merge ? 1 : 0, io, dd);
     if (e1 != cudaSuccess) return e1;
   }
   note_launch();
@@ -1323,7 +1409,8 @@ cudaError_t launch_decode_pair(const KernelCfg& kc, const void* q_new, const int
   at[0].val.programmaticStreamSerializationAllowed = 1;
   lc.attrs = at;
   lc.numAttrs = 1;
-  const cudaError_t e2 = cudaLaunchKernelEx(&lc, decode_pair_combine, (const int*)meta, (const float*)part, kc, out);
+  const cudaError_t e2 = cudaLaunchKernelEx(&lc, decode_pair_combine, (const int*)meta, (const float*)part, kc, out, cv,
+                                            slots, k_new != nullptr ? 1 : 0);
   if (e2 != cudaSuccess) return e2;
   note_launch();
   return cudaGetLastError();

@@ -52,6 +52,9 @@ size_t decode_workspace_bytes(const KernelCfg& kc, int batch, int max_seqlen);
 int debug_acc_form(const KernelCfg& kc, int op);
 // whether the kernel serving op (0 prefill, 1 decode) implements P stochastic rounding
 bool p_sr_supported(const KernelCfg& kc, int op);
+cudaError_t launch_decode_step(const KernelCfg& kc, const void* q_new, const void* k_new, const void* v_new,
+                               const int32_t* slots, int batch, int max_seqlen, const CacheView& cv, void* out,
+                               void* workspace, const hack_debug_t* dbg, cudaStream_t st);
 cudaError_t launch_decode_attention(const KernelCfg& kc, const void* q_new, const int32_t* slots, int batch,
                                     int max_seqlen, const CacheView& cv, void* out, void* workspace,
                                     const hack_debug_t* dbg, cudaStream_t st);

@@ -10,4 +10,4 @@ l = json.loads(open("gpurun_out/b_dq.json").read().strip().splitlines()[-1]); d 
 print("prefill step %.1f kernel %.1f | decode attn ms %.4f GB/s %.0f step ms %.4f" % (
     l["value"], l["roofline"]["achieved"], d["attn_ms"], d["kv_gbs"], d["ms_per_step"]))
 PY
-for n in 2 4 8; do python scripts/dec_shard_probe.py $n; done
+for n in 1 2 4 8; do python scripts/dec_shard_probe.py $n; done; PROBE_SEPARATE=1 python scripts/dec_shard_probe.py 8

@@ -26,15 +26,24 @@ kn = torch.randn((steps * 3, B, Hkv, 128), device="cuda").half()
 out = torch.empty((B, Hkv * G, 128), dtype=torch.float16, device="cuda")
 ws = torch.zeros(h.decode_workspace_size(cfg, B, ctx + steps * 4 + Pi), dtype=torch.uint8, device="cuda")
 ML = ctx + steps * 4 + Pi
+SEP = os.environ.get("PROBE_SEPARATE") == "1"   # append + attention as two calls (round-1 step)
+
+
+def step(i):
+    if SEP:
+        h.decode_append(cfg, kn[i], kn[i], slots, caches[i % nl])
+        h.decode_attention_cached(cfg, qn[i], slots, ML, caches[i % nl], out, workspace=ws)
+    else:
+        h.decode_attention(cfg, qn[i], kn[i], kn[i], slots, ML, caches[i % nl], out, workspace=ws)
+
+
 for i in range(3):
-    h.decode_append(cfg, kn[i], kn[i], slots, caches[i % nl])
-    h.decode_attention_cached(cfg, qn[i], slots, ML, caches[i % nl], out, workspace=ws)
+    step(i)
 torch.cuda.synchronize()
 g1, g2 = torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()
 with torch.cuda.graph(g1):
     for i in range(steps):
-        h.decode_append(cfg, kn[3 + i], kn[3 + i], slots, caches[i % nl])
-        h.decode_attention_cached(cfg, qn[3 + i], slots, ML, caches[i % nl], out, workspace=ws)
+        step(3 + i)
 with torch.cuda.graph(g2):
     for i in range(steps):
         h.decode_attention_cached(cfg, qn[3 + i], slots, ML, caches[i % nl], out, workspace=ws)
@@ -43,5 +52,5 @@ e[0].record(); g1.replay(); e[1].record(); e[2].record(); g2.replay(); e[3].reco
 torch.cuda.synchronize()
 step, attn = e[0].elapsed_time(e[1]) / steps, e[2].elapsed_time(e[3]) / steps
 gb = B * Hkv * ctx * 84 / (attn * 1e-3) / 1e9
-print(json.dumps({"N": N, "grid": os.environ.get("HACK_DECODE_GRID", "default"), "step_us": round(step * 1e3, 1),
+print(json.dumps({"N": N, "step": "separate" if SEP else "fused", "grid": os.environ.get("HACK_DECODE_GRID", "default"), "step_us": round(step * 1e3, 1),
                   "attn_us": round(attn * 1e3, 1), "kv_gbs": round(gb, 1), "layers": nl}))

@@ -10,7 +10,7 @@ import torch
 import hack_inputs
 from oracle import attention as att
 
-from .gpu_util import (ROW_TOL, acc_buffers, check_acc, check_pcodes, compare_pages, gpu_cfg, hk, make_cache,
+from .gpu_util import (ROW_TOL, acc_buffers, check_acc, check_pcodes, compare_pages, gpu_cfg, gpu_pages_of, hk, make_cache,
                        row_rel_err)
 
 pytestmark = pytest.mark.gpu
@@ -322,3 +322,48 @@ def test_decode_workspace_reuse_merge_counters(Hq, merge, monkeypatch):
     # counter region: after the header of (16 + 2 B) ints rounded to 256 B, B * H_kv ints
     off = ((16 + 2 * B) * 4 + 255) // 256 * 256
     assert int(ws[off:off + 4 * B * ocfg.Hkv].view(torch.int32).abs().sum()) == 0
+
+
+@pytest.mark.parametrize("Hq,merge", [(8, "1"), (8, "0"), (16, "1"), (16, "0")])
+def test_fused_decode_step_equals_separate(Hq, merge, monkeypatch):
+    """hack_decode_attention fuses the append (a8) into the paired decode kernel (the CTA
+    owning a unit's last page appends before loading it; seq_lens bumped after every CTA
+    read it, by the last CTA or by the combine kernel).  Over 70 steps (every request
+    crosses a flush) it must produce bit-identical outputs, pages, FP16 tails and lengths to
+    the separate append kernel + attention (HACK_DECODE_FUSED=0), on both merge paths; the
+    oracle comparison of the fused path is run_decode's even steps."""
+    h = hk()
+    monkeypatch.setenv("HACK_DECODE_MERGE", merge)
+    ocfg = att.Config(Hq=Hq, Hkv=2, Pi=64, bits=2, seed=8)
+    cfg = gpu_cfg(ocfg)
+    lens = [1000, 1, 64, 63, 300]
+    B, steps = len(lens), 70
+    caches = [make_cache(cfg, max_reqs=B, max_len=max(lens) + steps, seed=8) for _ in range(2)]
+    for c in caches:
+        c.rng_ids.copy_(torch.arange(100, 100 + B, dtype=torch.int32, device="cuda"))
+        for i, n in enumerate(lens):
+            _, k, v = hack_inputs.qkv(80 + i, n, 1, ocfg.Hkv)
+            h.cache_ingest(cfg, torch.from_numpy(k).cuda(), torch.from_numpy(v).cuda(),
+                           torch.tensor([0, n], dtype=torch.int32, device="cuda"),
+                           torch.tensor([i], dtype=torch.int32, device="cuda"), n, c)
+    sl = torch.arange(B, dtype=torch.int32, device="cuda")
+    qd, kd, vd = hack_inputs.decode_tokens(12, steps, B, ocfg.Hq, ocfg.Hkv)
+    ML = max(lens) + steps
+    ws = [torch.zeros(h.decode_workspace_size(cfg, B, ML), dtype=torch.uint8, device="cuda") for _ in range(2)]
+    for s in range(steps):
+        q, k, v = (torch.from_numpy(x[s]).cuda() for x in (qd, kd, vd))
+        outs = []
+        for j, fused in enumerate(("1", "0")):
+            monkeypatch.setenv("HACK_DECODE_FUSED", fused)
+            o = torch.zeros((B, ocfg.Hq, 128), dtype=torch.float32, device="cuda")
+            h.decode_attention(cfg, q, k, v, sl, ML, caches[j], o, workspace=ws[j])
+            outs.append(o.cpu().numpy())
+        assert np.array_equal(outs[0].view(np.uint32), outs[1].view(np.uint32)), f"step {s}"
+    a, b = caches
+    assert torch.equal(a.seq_lens, b.seq_lens)
+    assert [int(x) for x in a.seq_lens[:B].cpu()] == [n + steps for n in lens]
+    for i in range(B):
+        npg = (lens[i] + steps + ocfg.Pi - 1) // ocfg.Pi
+        assert np.array_equal(gpu_pages_of(a, i, npg), gpu_pages_of(b, i, npg)), f"request {i} pages"
+        T = (lens[i] + steps) % ocfg.Pi  # valid FP16 tail rows
+        assert torch.equal(a.v_tail[i, :, :T], b.v_tail[i, :, :T]), f"request {i} tail"
