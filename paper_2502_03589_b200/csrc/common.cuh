@@ -82,7 +82,7 @@ HACK_DEV QMeta meta_fp16(float lo, float hi, int qmax) {
   QMeta q;
   q.m = __half2float(__float2half_rn(lo));
   q.s = __half2float(__float2half_rn(s32));
-  q.inv = __frcp_rn(q.s);
+  q.inv = q.s > 0.f ? __frcp_rn(q.s) : 0.f;  // scale 0: y = 0, every code 0 (R5)
   return q;
 }
 
@@ -90,25 +90,24 @@ HACK_DEV QMeta meta_fp32(float lo, float hi, int qmax) {
   QMeta q;
   q.m = lo;
   q.s = __fdiv_rn(__fsub_rn(hi, lo), (float)qmax);
-  q.inv = __frcp_rn(q.s);
+  q.inv = q.s > 0.f ? __frcp_rn(q.s) : 0.f;  // scale 0: y = 0, every code 0 (R5)
   return q;
 }
 
 // One code: y = fp32(fp32(x - m) * inv); SR: floor(y) + [u < y - floor(y)] (R1);
-// RN: rint half-even (R17); scale 0 -> 0 (R5); clamp to [0, qmax].
+// RN: rint half-even (R17); scale 0 -> 0 (R5, inv = 0 gives y = 0); clamp to [0, qmax].
+// Branch-free: y is clamped to [0, qmax] first, which gives the same code as clamping the
+// result (y < 0: floor(y) + [u < frac] <= 0; y > qmax: >= qmax; and u >= 0 so a clamped
+// y adds nothing), and the integer part is read off the 1.5 * 2^23 magic sum (|y| < 2^22).
 HACK_DEV int quant_sr(float x, const QMeta& q, float u, int qmax) {
-  if (!(q.s > 0.f)) return 0;
-  const float y = __fmul_rn(__fsub_rn(x, q.m), q.inv);
+  const float y = fminf(fmaxf(__fmul_rn(__fsub_rn(x, q.m), q.inv), 0.f), (float)qmax);
   const float fl = floorf(y);
-  int c = (int)fl + (u < __fsub_rn(y, fl) ? 1 : 0);
-  return c < 0 ? 0 : (c > qmax ? qmax : c);
+  return (__float_as_int(__fadd_rn(fl, 12582912.f)) - 0x4B400000) + (u < __fsub_rn(y, fl) ? 1 : 0);
 }
 
 HACK_DEV int quant_rn(float x, const QMeta& q, int qmax) {
-  if (!(q.s > 0.f)) return 0;
-  const float y = __fmul_rn(__fsub_rn(x, q.m), q.inv);
-  int c = __float2int_rn(y);
-  return c < 0 ? 0 : (c > qmax ? qmax : c);
+  const float y = fminf(fmaxf(__fmul_rn(__fsub_rn(x, q.m), q.inv), 0.f), (float)qmax);
+  return __float_as_int(__fadd_rn(y, 12582912.f)) - 0x4B400000;  // round half to even
 }
 
 // -------------------------------------------------------------------------- K / Q rows
