@@ -1315,6 +1315,19 @@ int grid_size(bool g8 = false) {
   return sms * (g8 ? kCtas8 : kCtasPerSm);
 }
 
+// Where the split partials are merged: in the main kernel by the CTA completing a unit
+// (merge_units) when units span few CTAs -- the merging CTA's few L2 round trips beat a
+// second launch -- else by decode_pair_combine, whose B x H_q CTAs merge in parallel (long
+// units over many CTAs, e.g. head-sharded decode).  Estimated from the host bound
+// max_seqlen: CTAs per unit ~ pages per unit / pages per CTA.  (C3: 1.2 -> in the kernel;
+// head-sharded N = 2: 2.3, measured 5 % slower in the kernel.)
+bool merge_in_kernel(const KernelCfg& kc, int batch, int max_seqlen) {
+  if (const char* e = getenv("HACK_DECODE_MERGE")) return e[0] == '1';  // A/B timing knob
+  const double npg = (double)((max_seqlen + PI - 1) / PI);
+  const double per_cta = npg * batch * kc.Hkv / grid_size(kc.G > 4);
+  return npg <= 1.5 * per_cta;
+}
+
 size_t meta_bytes(int batch) { return ((size_t)(kMetaInts + 2 * batch) * sizeof(int) + 255) / 256 * 256; }
 // merge counters, one per (request, KV head) unit: zero before the first launch, and every
 // launch leaves them zero (merge_units)
@@ -1322,6 +1335,15 @@ size_t cnt_bytes(const KernelCfg& kc, int batch) { return ((size_t)batch * kc.Hk
 // workspace: meta | merge counters | fused-step completion counter (256 B) | partials
 
 }  // namespace
+
+// The decode step (hack_decode_attention) fuses the append into this kernel when the merge
+// runs in decode_pair_combine, which then bumps seq_lens.  With the merge in the kernel the
+// bump needs a grid-wide completion count, and the fused step measured 1.5 % slower than the
+// append kernel + attention (C3: 122.0 vs 120.2 us); HACK_DECODE_FUSED=1 / 0 forces a path.
+bool decode_pair_fuse_step(const KernelCfg& kc, int batch, int max_seqlen) {
+  if (const char* e = getenv("HACK_DECODE_FUSED")) return e[0] == '1';
+  return !merge_in_kernel(kc, batch, max_seqlen);
+}
 
 bool decode_pair_supported(const KernelCfg& kc) {
   return kc.Pi == 64 && kc.d == 128 && kc.bits == 2 && kc.G <= 8 && kc.pl.page_bytes == PB &&
@@ -1348,16 +1370,8 @@ cudaError_t launch_decode_pair(const KernelCfg& kc, const void* q_new, const int
   const bool with_dbg = dbg != nullptr && (dbg->pcodes != nullptr || dbg->qk_acc != nullptr ||
                                            dbg->pv_acc != nullptr);  // dumps: parity runs only
   const bool no_se = !g8 && getenv("HACK_DECODE_NO_SE") != nullptr;  // f2 ablation only
-  // where the split partials are merged: in the main kernel by the CTA completing a unit
-  // (merge_units) when units span few CTAs -- the merging CTA's few L2 round trips beat a
-  // second launch -- else by decode_pair_combine, whose B x H_q CTAs merge in parallel
-  // (long units over many CTAs, e.g. head-sharded decode).  Estimated from the host bound
-  // max_seqlen: CTAs per unit ~ pages per unit / pages per CTA.
   const int grid = grid_size(g8);
-  const double npg = (double)((max_seqlen + PI - 1) / PI);
-  const double per_cta = npg * batch * kc.Hkv / grid;
-  bool merge = npg <= 1.5 * per_cta;  // (C3: 1.2 -> in-kernel; head-sharded N = 2: 2.3 measured 5 % slower in-kernel)
-  if (const char* e = getenv("HACK_DECODE_MERGE")) merge = e[0] == '1';  // A/B timing knob
+  const bool merge = merge_in_kernel(kc, batch, max_seqlen);
   const bool fused = k_new != nullptr;  // (the SE ablation never runs fused: launch_decode_step)
   auto kern = g8 ? (with_dbg ? (fused ? decode_g8_kernel<true, true> : decode_g8_kernel<true, false>)
                              : (fused ? decode_g8_kernel<false, true> : decode_g8_kernel<false, false>))

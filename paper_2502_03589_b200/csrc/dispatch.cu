@@ -30,6 +30,7 @@ cudaError_t launch_decode_mma(const KernelCfg& kc, const void* q_new, const int3
                               const hack_debug_t* dbg, cudaStream_t st);
 
 bool decode_pair_supported(const KernelCfg& kc);
+bool decode_pair_fuse_step(const KernelCfg& kc, int batch, int max_seqlen);
 size_t decode_pair_workspace(const KernelCfg& kc, int batch, int max_seqlen);
 cudaError_t launch_decode_pair(const KernelCfg& kc, const void* q_new, const int32_t* slots, int batch,
                                int max_seqlen, const CacheView& cv, void* out, void* workspace,
@@ -96,13 +97,13 @@ cudaError_t launch_decode_attention(const KernelCfg& kc, const void* q_new, cons
 }
 
 // One decode step (hack_decode_attention): the append (a8) fused into the paired decode
-// kernel (one launch per step; HACK_DECODE_FUSED=0 or the SE / RQE ablations keep the separate
-// append kernel), else the append kernel followed by the attention.
+// kernel when decode_pair_fuse_step says so (one launch per step; the SE / RQE ablations keep
+// the separate append kernel), else the append kernel followed by the attention.
 cudaError_t launch_decode_step(const KernelCfg& kc, const void* q_new, const void* k_new, const void* v_new,
                                const int32_t* slots, int batch, int max_seqlen, const CacheView& cv, void* out,
                                void* workspace, const hack_debug_t* dbg, cudaStream_t st) {
   if (use_decode_pair(kc) && !getenv("HACK_DECODE_NO_RQE") && !getenv("HACK_DECODE_NO_SE") &&
-      !env_is("HACK_DECODE_FUSED", "0"))
+      decode_pair_fuse_step(kc, batch, max_seqlen))
     return launch_decode_pair(kc, q_new, slots, batch, max_seqlen, cv, out, workspace, dbg, st, k_new, v_new);
   const cudaError_t e = launch_append(kc, k_new, v_new, slots, batch, cv, st);
   if (e != cudaSuccess) return e;
