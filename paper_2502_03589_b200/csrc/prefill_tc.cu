@@ -33,7 +33,8 @@
 // Online softmax with lazy rescaling: the running max only moves when a row's tile max
 // exceeds it by more than 8 (log2 units; p~ <= 256), warp-uniformly, so most tiles skip the
 // O *= alpha pass.  P' codes are invariant to the row scale (R13).
-// TMEM (512 columns): S (d/Pi x BN = 128) | R (BN) | D'[2] (2 x 128).
+// TMEM (512 columns): S buffers [NSB] (d/Pi x BN = 128 | R (BN)) | D'[NDB] (128 each); NSB = 1,
+// NDB = 2 (HACK_PRE_NSB=2 double-buffers S with one D' at Pi <= 64, measured slower).
 #include <cstdlib>
 #include "common.cuh"
 #include "internal.h"
@@ -63,6 +64,9 @@ constexpr uint32_t kPBar0 = 7;
 #define HACK_ABL 0  // timing ablations only, bit flags (1 O math, 2 P-quant math, 4 Eq. 4, 8 exp2, 16 unpack)
 #endif
 
+#ifndef HACK_PRE_NSB
+#define HACK_PRE_NSB 1  // S accumulator buffers in TMEM (Geo::NSB)
+#endif
 #ifndef HACK_PRE_NSG
 #define HACK_PRE_NSG 2  // S warpgroups at Pi >= 64 (4: 16 keys per thread at Pi = 64, measured 6 % slower)
 #endif
@@ -97,12 +101,18 @@ struct Geo {
                             up16(128 * PI_ * BITS / 8) + up16(128 * 4) + up16(128 * SB);  // page bytes
   static constexpr int NS = PI_ == 128 ? 2 : 4;         // page stages
   static constexpr int NB = PI_ == 128 ? 2 : 3;         // K/V/P tile buffer sets
-  static constexpr int NDB = 2;                         // D' (PV accumulator) TMEM buffers
+  // S accumulator buffers in TMEM (d/Pi x BN accumulator columns + BN rank-term columns
+  // each).  HACK_PRE_NSB=2 (where two fit beside one D' buffer): the MMA warp issues
+  // QK(j + 1) while the S warps still read tile j, at the price of a single D' buffer --
+  // measured 1.4 % slower on C2 (401 vs 395 us), so one S buffer and two D' buffers.
+  static constexpr int SBC = (128 + BN + 31) / 32 * 32;  // columns of one S buffer
+  static constexpr int NSB = HACK_PRE_NSB == 2 && 2 * SBC + 128 <= 512 ? 2 : 1;
+  static constexpr int NDB = NSB == 2 ? 1 : 2;          // D' (PV accumulator) TMEM buffers
   static constexpr int KR = NBETA * 12 < 16 ? 16 : NBETA * 12;  // rank-term K (tf32), 12 per block
   static constexpr int SBO_R = KR * 32;                 // K-major SBO of the rank operands
   static constexpr int SBO_T = BN * 8;                  // K-major SBO of the P and V tiles (K = BN)
-  static constexpr int TR = 128;                        // TMEM: rank-term columns
-  static constexpr int TD = (128 + BN + 31) / 32 * 32;  // TMEM: first D' column
+  static constexpr int TR = 128;                        // TMEM: rank-term columns (in an S buffer)
+  static constexpr int TD = NSB * SBC;                  // TMEM: first D' column
   static_assert(TD + NDB * 128 <= 512, "TMEM budget");
 };
 
@@ -129,7 +139,7 @@ struct TcSmem {
   int xs[Gm::NSG][BM];                       // Q prologue: partial code sums of a partition
   float lpart[Gm::NSG][BM];
   uint64_t full[NS], empty[NS], k_ready[NB], k_free[NB], v_ready[NB], o_done[NB], p_ready[NB], d_full[2],
-      d_free[2], s_full, s_free, q_ready, l_ready, l_free;
+      d_free[2], s_full[2], s_free[2], q_ready, l_ready, l_free;
   uint32_t tmem_base;
 };
 
@@ -302,8 +312,10 @@ __global__ void __launch_bounds__(Geo<PI_, BITS>::THREADS, 1) prefill_tc_kernel(
       ptx::mbar_init(&sm.d_full[x], 1);
       ptx::mbar_init(&sm.d_free[x], NOW);
     }
-    ptx::mbar_init(&sm.s_full, 1);
-    ptx::mbar_init(&sm.s_free, NSW);
+    for (int x = 0; x < 2; ++x) {
+      ptx::mbar_init(&sm.s_full[x], 1);
+      ptx::mbar_init(&sm.s_free[x], NSW);
+    }
     ptx::mbar_init(&sm.q_ready, NSW);
     ptx::mbar_init(&sm.l_ready, NSW);
     ptx::mbar_init(&sm.l_free, NOW);
@@ -314,9 +326,12 @@ __global__ void __launch_bounds__(Geo<PI_, BITS>::THREADS, 1) prefill_tc_kernel(
   __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem = sm.tmem_base;
-  const uint32_t tS = tmem;              // columns 0..127: D_beta (BN each); scores / tail p~ (WB)
-  const uint32_t tR = tmem + Gm::TR;     // rank terms of S (BN columns): sum_beta X m_k + M y_k (3xTF32)
-  const uint32_t tD0 = tmem + Gm::TD;    // D'[0], D'[1] (128 columns each)
+  // S buffer b at columns b SBC: D_beta (BN each; scores / tail p~ in WB), then at + TR the
+  // rank terms of S (BN columns): sum_beta X m_k + M y_k (3xTF32).  Tile g uses buffer g % NSB.
+  const uint32_t tS = tmem;
+  const uint32_t tR = tmem + Gm::TR;
+  const uint32_t tD0 = tmem + Gm::TD;    // D'[0 .. NDB) (128 columns each)
+  constexpr int NSB = Gm::NSB, SBC = Gm::SBC;
 
   if (warp < 4) {
     // register budget (launch: THREADS x the launch-bound cap): service, S and O shares (Geo)
@@ -348,7 +363,7 @@ __global__ void __launch_bounds__(Geo<PI_, BITS>::THREADS, 1) prefill_tc_kernel(
       const uint64_t pre_b = ptx::smem_desc_kmajor(ptx::smem_u32(sm.pre_b), 128, 256);
       const uint32_t idesc_pre = ptx::idesc_bf16(BM, 128);
       int jg = 0, jpv = 0;  // tiles / PV tiles of all items so far (ring phases)
-      bool prev_tail = false;
+      int last_tail = -1 - NSB;  // global index of the latest FP16-tail tile (its p~ sits in its S buffer)
       Item w;
 #pragma unroll 1
       for (int it = 0; get_item(it, w); ++it) {
@@ -358,19 +373,20 @@ __global__ void __launch_bounds__(Geo<PI_, BITS>::THREADS, 1) prefill_tc_kernel(
         if (j < w.nkt) {
           const int g = jg + j, bq = g % NB;
           ptx::mbar_wait(&sm.k_ready[bq], (g / NB) & 1);
-          ptx::mbar_wait(&sm.s_free, (g & 1) ^ 1);
-          // the previous item's FP16 tail p~ sits in the S columns: the O warps must be done
-          if (j == 0 && prev_tail) ptx::mbar_wait(&sm.o_done[(g - 1) % NB], ((g - 1) / NB) & 1);
+          const uint32_t sbo = (uint32_t)(SBC * (g % NSB));
+          ptx::mbar_wait(&sm.s_free[g % NSB], ((g / NSB) & 1) ^ 1);
+          // an earlier item's FP16 tail p~ sits in this S buffer: the O warps must be done
+          if (last_tail == g - NSB) ptx::mbar_wait(&sm.o_done[(g - NSB) % NB], ((g - NSB) / NB) & 1);
           ptx::tc_fence_after();
           if (lane == 0) {
             const uint32_t ka = ptx::smem_u32(sm.k[bq]);
-            ptx::mma_bf16(tS, pre_a, pre_b, idesc_pre, 0u);  // D_beta := 1.5 * 2^23 (all 128 columns)
+            ptx::mma_bf16(tS + sbo, pre_a, pre_b, idesc_pre, 0u);  // D_beta := 1.5 * 2^23 (all 128 columns)
 #pragma unroll
             for (int beta = 0; beta < NBETA; ++beta)
 #pragma unroll
               for (int ks = 0; ks < PI / 32; ++ks) {
                 const uint32_t koff = (uint32_t)(beta * PI / 16 + ks * 2) * 128;  // 16-byte K chunks
-                ptx::mma_u8(tS + BN * beta, ptx::smem_desc_kmajor(qa + koff, 128, 1024),
+                ptx::mma_u8(tS + sbo + BN * beta, ptx::smem_desc_kmajor(qa + koff, 128, 1024),
                             ptx::smem_desc_kmajor(ka + koff, 128, 1024), idesc_qk, 1u);
               }
             // rank-2-per-block terms of Eq. 4 on the tensor pipe: R = [X | M] [m_k ; y_k]
@@ -379,9 +395,9 @@ __global__ void __launch_bounds__(Geo<PI_, BITS>::THREADS, 1) prefill_tc_kernel(
             const uint32_t ra = ptx::smem_u32(sm.ar), rb = ptx::smem_u32(sm.br[bq]);
 #pragma unroll
             for (int ks = 0; ks < KR / 8; ++ks)
-              ptx::mma_tf32(tR, ptx::smem_desc_kmajor(ra + ks * 256, 128, SBO_R),
+              ptx::mma_tf32(tR + sbo, ptx::smem_desc_kmajor(ra + ks * 256, 128, SBO_R),
                             ptx::smem_desc_kmajor(rb + ks * 256, 128, SBO_R), ptx::idesc_tf32(BM, BN), ks > 0);
-            ptx::mma_commit(&sm.s_full);
+            ptx::mma_commit(&sm.s_full[g % NSB]);
           }
           __syncwarp();
         }
@@ -406,7 +422,7 @@ __global__ void __launch_bounds__(Geo<PI_, BITS>::THREADS, 1) prefill_tc_kernel(
           __syncwarp();
         }
       }
-      prev_tail = w.nfull < w.nkt;  // the last tile was the FP16 tail
+      if (w.nfull < w.nkt) last_tail = jg + w.nkt - 1;  // the item's last tile is the FP16 tail
       jg += w.nkt;
       }
     } else {
@@ -673,7 +689,8 @@ __global__ void __launch_bounds__(Geo<PI_, BITS>::THREADS, 1) prefill_tc_kernel(
       const int bj = jg % NB, t0 = j * BN;
       const uint32_t ph = (jg / NB) & 1;
       const bool full = (t0 + BN - 1) <= w.i0;  // every key visible to every row of the item
-      ptx::mbar_wait(&sm.s_full, jg & 1);
+      const uint32_t sbo = (uint32_t)(SBC * (jg % NSB));  // this tile's S buffer
+      ptx::mbar_wait(&sm.s_full[jg % NSB], (jg / NSB) & 1);
       ptx::tc_fence_after();
       // ---- pass 1: S = R + sum_beta (s_q/2) s_k E_beta (centered Eq. 4) x log2(e)/sqrt(d),
       // causal mask, row max / min; 16 keys per TMEM load (register pressure)
@@ -685,7 +702,7 @@ __global__ void __launch_bounds__(Geo<PI_, BITS>::THREADS, 1) prefill_tc_kernel(
         const int so = WB ? 0 : 16 * c;  // this chunk's scores: s[so .. so + 15]
         {
           uint32_t d[16];
-          ptx::tmem_ld16(tR + lane_base + kb + 16 * c, d);  // rank terms (tensor pipe) seed S
+          ptx::tmem_ld16(tR + sbo + lane_base + kb + 16 * c, d);  // rank terms (tensor pipe) seed S
           ptx::tmem_wait_ld();
 #pragma unroll
           for (int x = 0; x < 16; ++x) s[so + x] = __uint_as_float(d[x]);
@@ -694,7 +711,7 @@ __global__ void __launch_bounds__(Geo<PI_, BITS>::THREADS, 1) prefill_tc_kernel(
         for (int beta = 0; beta < NBETA && !(HACK_ABL & 4); ++beta) {
           const float2 A = make_float2(qa[beta], qa[beta]);
           uint32_t d[16];
-          ptx::tmem_ld16(tS + lane_base + BN * beta + kb + 16 * c, d);
+          ptx::tmem_ld16(tS + sbo + lane_base + BN * beta + kb + 16 * c, d);
           ptx::tmem_wait_ld();
           if (DBG && dbg_qk != nullptr && pos < L && (acc_head < 0 || hq == acc_head)) {  // E = 2 D - 256 SK
             const int hs = acc_head < 0 ? hq : 0, hn = acc_head < 0 ? kc.Hq : 1;
@@ -725,14 +742,14 @@ __global__ void __launch_bounds__(Geo<PI_, BITS>::THREADS, 1) prefill_tc_kernel(
           uint32_t su[16];
 #pragma unroll
           for (int x = 0; x < 16; ++x) su[x] = __float_as_uint(s[so + x]);
-          ptx::tmem_st16(tS + lane_base + kb + 16 * c, su);
+          ptx::tmem_st16(tS + sbo + lane_base + kb + 16 * c, su);
         }
       }
       if (WB) {
         ptx::tmem_wait_st();
       } else {
         ptx::tc_fence_before();
-        ptx::mbar_arrive(&sm.s_free);  // S columns may now be overwritten by QK(j+1)
+        ptx::mbar_arrive(&sm.s_free[jg % NSB]);  // S columns may now be overwritten by QK(j+1)
         mask_minmax_t<KPT>(s, t0 + kb, i, full, masked, mx, mn);
       }
       ptx::mbar_arrive(&sm.k_free[bj]);  // K' tile + key coefficients may be refilled
@@ -805,14 +822,14 @@ __global__ void __launch_bounds__(Geo<PI_, BITS>::THREADS, 1) prefill_tc_kernel(
           uint32_t su[16];
 #pragma unroll
           for (int x = 0; x < 16; ++x) su[x] = __float_as_uint(s[so + x]);
-          ptx::tmem_st16(tS + lane_base + kb + 16 * c, su);
+          ptx::tmem_st16(tS + sbo + lane_base + kb + 16 * c, su);
         }
       };
       if (WB) {
 #pragma unroll
         for (int c = 0; c < KPT / 16; ++c) {
           uint32_t su[16];
-          ptx::tmem_ld16(tS + lane_base + kb + 16 * c, su);
+          ptx::tmem_ld16(tS + sbo + lane_base + kb + 16 * c, su);
           ptx::tmem_wait_ld();
 #pragma unroll
           for (int x = 0; x < 16; ++x) s[x] = __uint_as_float(su[x]);
@@ -829,7 +846,7 @@ __global__ void __launch_bounds__(Geo<PI_, BITS>::THREADS, 1) prefill_tc_kernel(
       l_run = __fmaf_rn(l_run, al, ls2.x + ls2.y);
       if (!committed) ptx::tmem_wait_st();
       if (WB || !committed) ptx::tc_fence_before();
-      if (WB) ptx::mbar_arrive(&sm.s_free);  // scores consumed: S may be overwritten by QK(j+1)
+      if (WB) ptx::mbar_arrive(&sm.s_free[jg % NSB]);  // scores consumed: S may be overwritten by QK(j+1)
       sm.sp_part[bj][sw][r] = (int)psum;
       if (sw == 0) sm.pinfo[bj][r] = make_float4(al, resc ? 1.f : 0.f, ps, plo);
       if (committed) ptx::fence_proxy_async_smem();
@@ -932,7 +949,7 @@ __global__ void __launch_bounds__(Geo<PI_, BITS>::THREADS, 1) prefill_tc_kernel(
 #pragma unroll 1
         for (int c = 0; 16 * c < T; ++c) {
           uint32_t pt16[16];
-          ptx::tmem_ld16(tS + lane_base + 16 * c, pt16);
+          ptx::tmem_ld16(tS + (uint32_t)(SBC * (jg % NSB)) + lane_base + 16 * c, pt16);
           ptx::tmem_wait_ld();
 #pragma unroll
           for (int x = 0; x < 16; ++x) {
