@@ -64,6 +64,9 @@ constexpr uint32_t kPBar0 = 7;
 #define HACK_ABL 0  // timing ablations only, bit flags (1 O math, 2 P-quant math, 4 Eq. 4, 8 exp2, 16 unpack)
 #endif
 
+#ifndef HACK_PRE_TMEMP
+#define HACK_PRE_TMEMP 0  // P' tiles in TMEM where they fit (Geo::TP); measured 3.5 % slower on C2
+#endif
 #ifndef HACK_PRE_NSB
 #define HACK_PRE_NSB 1  // S accumulator buffers in TMEM (Geo::NSB)
 #endif
@@ -113,6 +116,13 @@ struct Geo {
   static constexpr int SBO_T = BN * 8;                  // K-major SBO of the P and V tiles (K = BN)
   static constexpr int TR = 128;                        // TMEM: rank-term columns (in an S buffer)
   static constexpr int TD = NSB * SBC;                  // TMEM: first D' column
+  // HACK_PRE_TMEMP=1: P' tiles in TMEM (the PV MMA's A operand from tensor memory, 4 codes
+  // per column) where NB of them fit after the D' buffers, written by the S warps with
+  // tcgen05.st instead of STS + a generic->async proxy fence per tile.  Parity-clean, but the
+  // C2 kernel measured 411 vs 397 us (the proxy fence is cheaper than it looked in the stall
+  // samples), so P' stays in smem.
+  static constexpr int TPC = TD + NDB * 128;            // TMEM: first P' column
+  static constexpr bool TP = HACK_PRE_TMEMP && TPC + NB * (BN / 4) <= 512;
   static_assert(TD + NDB * 128 <= 512, "TMEM budget");
 };
 
@@ -124,7 +134,7 @@ struct TcSmem {
   alignas(128) uint8_t q[BM * 128];          // Q' - 128 (s8), K-major, SBO 1024
   alignas(128) uint8_t k[NB][BN * 128];      // K' (u8, doubled), K-major, SBO 1024
   alignas(128) uint8_t v[NB][128 * BN];      // V' (u8, doubled), K-major (keys = K), SBO 8 BN
-  alignas(128) uint8_t p[NB][BM * BN];       // P' - 128 (s8), K-major, SBO 8 BN
+  alignas(128) uint8_t p[NB][Gm::TP ? 128 : BM * BN];  // P' - 128 (s8), K-major, SBO 8 BN (unless in TMEM)
   alignas(128) float ar[BM * Gm::KR];        // rank-term A operand (tf32): per row, per beta X, M split 3 ways
   alignas(128) float br[NB][BN * Gm::KR];    // rank-term B operand per key: m_k, y_k split 3 ways
   alignas(128) uint16_t pre_a[128 * 16];     // bf16 preset operands: A[:, 0] = 1, B[:, 0] = 1.5 * 2^23 (K-major,
@@ -414,9 +424,14 @@ __global__ void __launch_bounds__(Geo<PI_, BITS>::THREADS, 1) prefill_tc_kernel(
             const uint32_t pa = ptx::smem_u32(sm.p[bq]), va = ptx::smem_u32(sm.v[bq]);
             ptx::mma_bf16(tD0 + 128 * bd, pre_a, pre_b, idesc_pre, 0u);  // D' := 1.5 * 2^23
 #pragma unroll
-            for (int ks = 0; ks < BN / 32; ++ks)
-              ptx::mma_u8(tD0 + 128 * bd, ptx::smem_desc_kmajor(pa + ks * 256, 128, SBO_T),
-                          ptx::smem_desc_kmajor(va + ks * 256, 128, SBO_T), idesc_pv, 1u);
+            for (int ks = 0; ks < BN / 32; ++ks) {
+              if (Gm::TP)  // A = P' from TMEM: lane = row, 8 columns per 32-key step
+                ptx::mma_u8_ts(tD0 + 128 * bd, tmem + Gm::TPC + bq * (BN / 4) + 8 * ks,
+                               ptx::smem_desc_kmajor(va + ks * 256, 128, SBO_T), idesc_pv, 1u);
+              else
+                ptx::mma_u8(tD0 + 128 * bd, ptx::smem_desc_kmajor(pa + ks * 256, 128, SBO_T),
+                            ptx::smem_desc_kmajor(va + ks * 256, 128, SBO_T), idesc_pv, 1u);
+            }
             ptx::mma_commit(&sm.d_full[bd]);
           }
           __syncwarp();
@@ -810,8 +825,12 @@ __global__ void __launch_bounds__(Geo<PI_, BITS>::THREADS, 1) prefill_tc_kernel(
       auto out_chunk = [&](int so, int c) {
         if (committed) {
           const uint4 cw = p_codes16<BITS, PSR>(s + so, pinv, pnlo, kc.seed, p_rid, p_c3, i, t0 + kb + 16 * c, psum);
-          *reinterpret_cast<uint4*>(sm.p[bj] + kmaj_off(r, kb + 16 * c, SBO_T)) =
-              make_uint4(cw.x ^ 0x80808080u, cw.y ^ 0x80808080u, cw.z ^ 0x80808080u, cw.w ^ 0x80808080u);
+          if (Gm::TP)
+            ptx::tmem_st4(tmem + lane_base + Gm::TPC + bj * (BN / 4) + (kb + 16 * c) / 4, cw.x ^ 0x80808080u,
+                          cw.y ^ 0x80808080u, cw.z ^ 0x80808080u, cw.w ^ 0x80808080u);
+          else
+            *reinterpret_cast<uint4*>(sm.p[bj] + kmaj_off(r, kb + 16 * c, SBO_T)) =
+                make_uint4(cw.x ^ 0x80808080u, cw.y ^ 0x80808080u, cw.z ^ 0x80808080u, cw.w ^ 0x80808080u);
           if (DBG && dbg_pcodes != nullptr && pos < L) {
             uint8_t* dp = dbg_pcodes + ((int64_t)(start + pos) * kc.Hq + hq) * dbg_stride + t0 + kb + 16 * c;
             const uint32_t cwa[4] = {cw.x, cw.y, cw.z, cw.w};
@@ -844,12 +863,12 @@ __global__ void __launch_bounds__(Geo<PI_, BITS>::THREADS, 1) prefill_tc_kernel(
         }
       }
       l_run = __fmaf_rn(l_run, al, ls2.x + ls2.y);
-      if (!committed) ptx::tmem_wait_st();
-      if (WB || !committed) ptx::tc_fence_before();
+      if (Gm::TP || !committed) ptx::tmem_wait_st();
+      if (Gm::TP || WB || !committed) ptx::tc_fence_before();
       if (WB) ptx::mbar_arrive(&sm.s_free[jg % NSB]);  // scores consumed: S may be overwritten by QK(j+1)
       sm.sp_part[bj][sw][r] = (int)psum;
       if (sw == 0) sm.pinfo[bj][r] = make_float4(al, resc ? 1.f : 0.f, ps, plo);
-      if (committed) ptx::fence_proxy_async_smem();
+      if (committed && !Gm::TP) ptx::fence_proxy_async_smem();
       ptx::mbar_arrive(&sm.p_ready[bj]);              // for the MMA warp (PV)
       ptx::named_bar_arrive(kPBar0 + bj, NSW + NOW);  // for the O warps (hardware barrier: no polling)
     }

@@ -146,6 +146,11 @@ HACK_DEV void tmem_st32_const(uint32_t taddr, uint32_t v) {
       "r"(v)
       : "memory");
 }
+HACK_DEV void tmem_st4(uint32_t taddr, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1,%2,%3,%4};" ::"r"(taddr), "r"(a), "r"(b), "r"(c),
+               "r"(d)
+               : "memory");
+}
 HACK_DEV void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 
 // warp-wide reductions (sm_100a CREDUX / REDUX)
