@@ -202,6 +202,22 @@ hack_status_t hack_prefill_attention_cached(const hack_config_t* cfg, const void
                                             size_t workspace_bytes, const hack_debug_t* debug,
                                             void* stream);
 
+/* The same call with HOST buffers (e2e path): q, k, v, out and cu_seqlens / slots are host
+ * pointers (page-locked for copy/compute overlap; pageable works, serialised), total tokens
+ * = cu_seqlens[batch].  The library stages them through `workspace` (device, >=
+ * hack_prefill_host_workspace_size() bytes, any contents) and pipelines: K/V up -> ingest;
+ * then per query-head chunk (head_chunks chunks of whole GQA groups; <= 0: 8) Q chunk up ->
+ * attention of those heads -> out chunk down, the uploads, the attention and the downloads
+ * of different chunks overlapping (copies on library-owned streams, ordered after prior work
+ * on `stream`; `stream` completes after the last download).  Results identical to
+ * hack_prefill_attention.  Same errors, plus HACK_ERR_CAPACITY for a small workspace. */
+size_t hack_prefill_host_workspace_size(const hack_config_t* cfg, int32_t batch, int32_t total_tokens);
+hack_status_t hack_prefill_attention_host(const hack_config_t* cfg, const void* q, const void* k,
+                                          const void* v, const int32_t* cu_seqlens, const int32_t* slots,
+                                          int32_t batch, int32_t max_seqlen, const hack_kv_cache_t* cache,
+                                          void* out, void* workspace, size_t workspace_bytes,
+                                          int32_t head_chunks, void* stream);
+
 /* ---- (a8-a9) decode ------------------------------------------------------ */
 /* Append one token per request (a8): quantize k_new into its own partitions,
  * put v_new in the FP16 tail, flush the tail into a V block when it reaches Pi

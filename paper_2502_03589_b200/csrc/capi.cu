@@ -7,7 +7,9 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstdlib>
+#include <algorithm>
 #include <cstring>
+#include <mutex>
 #include <string>
 
 #include "capi_util.h"
@@ -63,6 +65,8 @@ hack_status_t make_kernel_cfg(const hack_config_t* c, KernelCfg* kc) {
   kc->head_base = c->head_base;
   kc->out_fp32 = c->out_dtype == 1;
   kc->pl = page_layout(c->head_dim, c->partition, c->kv_bits);
+  kc->hq_begin = 0;
+  kc->hq_count = c->num_q_heads;
   return HACK_OK;
 }
 
@@ -241,6 +245,63 @@ hack_status_t check_decode(const KernelCfg& kc, const hack_kv_cache_t* cache, co
   return check_debug(kc, dbg, max_seqlen, 1, "decode");
 }
 
+// Library-owned copy streams and events of the host-buffer prefill (one set per device; the
+// enqueue sequence of a call holds the mutex, so concurrent callers do not interleave).
+constexpr int kMaxChunks = 16;
+constexpr int kCompStreams = 4;  // attention chunks in flight at once
+struct HostPipe {
+  bool init = false;
+  cudaStream_t up = nullptr, down = nullptr, comp[kCompStreams] = {};
+  cudaEvent_t start = nullptr, kv = nullptr, ingested = nullptr, done = nullptr, q[kMaxChunks] = {},
+              o[kMaxChunks] = {};
+};
+std::mutex g_pipe_mu;
+HostPipe g_pipe[64];
+
+cudaError_t host_pipe(int dev, HostPipe** out) {
+  if (dev < 0 || dev >= 64) return cudaErrorInvalidDevice;
+  HostPipe& p = g_pipe[dev];
+  if (!p.init) {
+    cudaError_t e;
+    if ((e = cudaStreamCreateWithFlags(&p.up, cudaStreamNonBlocking)) != cudaSuccess) return e;
+    if ((e = cudaStreamCreateWithFlags(&p.down, cudaStreamNonBlocking)) != cudaSuccess) return e;
+    for (int i = 0; i < kCompStreams; ++i)
+      if ((e = cudaStreamCreateWithFlags(&p.comp[i], cudaStreamNonBlocking)) != cudaSuccess) return e;
+    cudaEvent_t* evs[4] = {&p.start, &p.kv, &p.ingested, &p.done};
+    for (cudaEvent_t* ev : evs)
+      if ((e = cudaEventCreateWithFlags(ev, cudaEventDisableTiming)) != cudaSuccess) return e;
+    for (int c = 0; c < kMaxChunks; ++c) {
+      if ((e = cudaEventCreateWithFlags(&p.q[c], cudaEventDisableTiming)) != cudaSuccess) return e;
+      if ((e = cudaEventCreateWithFlags(&p.o[c], cudaEventDisableTiming)) != cudaSuccess) return e;
+    }
+    p.init = true;
+  }
+  *out = &p;
+  return cudaSuccess;
+}
+
+size_t up256(size_t x) { return (x + 255) / 256 * 256; }
+
+// Device staging of the host-buffer prefill: q, k, v, out, cu_seqlens, slots, then the
+// attention workspace.
+struct HostLayout {
+  size_t q, k, v, out, cu, slots, ws, total;
+};
+HostLayout host_layout(const KernelCfg& kc, int batch, int64_t T) {
+  HostLayout l;
+  const size_t qb = up256((size_t)T * kc.Hq * kc.d * 2), kb = up256((size_t)T * kc.Hkv * kc.d * 2);
+  const size_t ob = up256((size_t)T * kc.Hq * kc.d * (kc.out_fp32 ? 4 : 2));
+  l.q = 0;
+  l.k = l.q + qb;
+  l.v = l.k + kb;
+  l.out = l.v + kb;
+  l.cu = l.out + ob;
+  l.slots = l.cu + up256((size_t)(batch + 1) * 4);
+  l.ws = l.slots + up256((size_t)batch * 4);
+  l.total = l.ws + up256(prefill_workspace_bytes(kc, batch, (int)std::min<int64_t>(T, INT32_MAX)));
+  return l;
+}
+
 }  // namespace
 }  // namespace hack
 
@@ -305,6 +366,96 @@ hack_status_t hack_prefill_attention(const hack_config_t* cfg, const void* q, co
   return cuda_status(launch_prefill_attention(kc, q, cu, slots, batch, max_seqlen, cv, out, ws, dbg,
                                               (cudaStream_t)stream, /*pdl=*/true),
                      "prefill_attention");
+}
+
+size_t hack_prefill_host_workspace_size(const hack_config_t* cfg, int32_t batch, int32_t total_tokens) {
+  KernelCfg kc;
+  if (make_kernel_cfg(cfg, &kc) != HACK_OK || batch <= 0 || total_tokens <= 0) return 0;
+  return host_layout(kc, batch, total_tokens).total;
+}
+
+hack_status_t hack_prefill_attention_host(const hack_config_t* cfg, const void* q, const void* k, const void* v,
+                                          const int32_t* cu, const int32_t* slots, int32_t batch, int32_t max_seqlen,
+                                          const hack_kv_cache_t* cache, void* out, void* ws, size_t ws_bytes,
+                                          int32_t head_chunks, void* stream) {
+  KernelCfg kc;
+  CacheView cv;
+  hack_status_t st = make_kernel_cfg(cfg, &kc);
+  if (st != HACK_OK) return st;
+  if ((st = make_cache_view(kc, cache, &cv)) != HACK_OK) return st;
+  // every argument is checked before anything is enqueued (host pointers are only read here
+  // for cu_seqlens, the token count)
+  if ((st = check_ingest(kc, cache, k, v, cu, slots, batch, max_seqlen)) != HACK_OK) return st;
+  if ((st = check_prefill(kc, cache, q, cu, slots, batch, max_seqlen, out, nullptr, 0, nullptr)) != HACK_OK) return st;
+  const int64_t T = cu[batch];
+  if (cu[0] != 0 || T <= 0) return fail(HACK_ERR_INVALID_ARG, "prefill_host: cu_seqlens must start at 0 and grow");
+  for (int b = 0; b < batch; ++b)
+    if (cu[b + 1] < cu[b] || cu[b + 1] - cu[b] > max_seqlen)
+      return fail(HACK_ERR_INVALID_ARG, "prefill_host: cu_seqlens not increasing or a prompt > max_seqlen");
+  const HostLayout lay = host_layout(kc, batch, T);
+  if (!ws || ws_bytes < lay.total) return fail(HACK_ERR_CAPACITY, "prefill_host: workspace %zu < %zu", ws_bytes, lay.total);
+  if ((st = check_device()) != HACK_OK) return st;
+  int dev = 0;
+  if ((st = cuda_status(cudaGetDevice(&dev), "prefill_host")) != HACK_OK) return st;
+  // query-head chunks of whole GQA groups; the CUDA-core baseline kernel has no head range
+  int nch = head_chunks <= 0 ? 8 : head_chunks;  // (C2: 1 / 2 / 4 / 8 chunks 1.97 / 1.52 / 1.42 / 1.37 ms)
+  nch = std::max(1, std::min(std::min(nch, kc.Hkv), kMaxChunks));
+  if (!prefill_head_range_supported(kc)) nch = 1;
+  uint8_t* base = reinterpret_cast<uint8_t*>(ws);
+  uint8_t *qd = base + lay.q, *kd = base + lay.k, *vd = base + lay.v, *od = base + lay.out;
+  int32_t* cud = reinterpret_cast<int32_t*>(base + lay.cu);
+  int32_t* sld = reinterpret_cast<int32_t*>(base + lay.slots);
+  const size_t row_q = (size_t)kc.Hq * kc.d * 2, row_o = (size_t)kc.Hq * kc.d * (kc.out_fp32 ? 4 : 2);
+  const size_t kvb = (size_t)T * kc.Hkv * kc.d * 2;
+  cudaStream_t s0 = (cudaStream_t)stream;
+  std::lock_guard<std::mutex> lock(g_pipe_mu);
+  HostPipe* p = nullptr;
+  if ((st = cuda_status(host_pipe(dev, &p), "prefill_host: streams")) != HACK_OK) return st;
+  auto chk = [](cudaError_t e) { return cuda_status(e, "prefill_host"); };
+  // K, V (and the small index arrays) up, then the ingest on the caller's stream
+  if ((st = chk(cudaEventRecord(p->start, s0))) != HACK_OK) return st;
+  if ((st = chk(cudaStreamWaitEvent(p->up, p->start, 0))) != HACK_OK) return st;
+  if ((st = chk(cudaStreamWaitEvent(p->down, p->start, 0))) != HACK_OK) return st;
+  if ((st = chk(cudaMemcpyAsync(cud, cu, (size_t)(batch + 1) * 4, cudaMemcpyHostToDevice, p->up))) != HACK_OK) return st;
+  if ((st = chk(cudaMemcpyAsync(sld, slots, (size_t)batch * 4, cudaMemcpyHostToDevice, p->up))) != HACK_OK) return st;
+  if ((st = chk(cudaMemcpyAsync(kd, k, kvb, cudaMemcpyHostToDevice, p->up))) != HACK_OK) return st;
+  if ((st = chk(cudaMemcpyAsync(vd, v, kvb, cudaMemcpyHostToDevice, p->up))) != HACK_OK) return st;
+  if ((st = chk(cudaEventRecord(p->kv, p->up))) != HACK_OK) return st;
+  if ((st = chk(cudaStreamWaitEvent(s0, p->kv, 0))) != HACK_OK) return st;
+  if ((st = chk(launch_ingest(kc, kd, vd, cud, sld, batch, max_seqlen, cv, s0))) != HACK_OK) return st;
+  if ((st = chk(cudaEventRecord(p->ingested, s0))) != HACK_OK) return st;
+  // the chunks' attention launches go to kCompStreams streams, so one chunk's CTAs fill the
+  // SMs that the previous chunk's light items free (a head chunk alone cannot fill the GPU:
+  // its longest causal rows set its duration)
+  for (int i = 0; i < std::min(nch, kCompStreams); ++i)
+    if ((st = chk(cudaStreamWaitEvent(p->comp[i], p->ingested, 0))) != HACK_OK) return st;
+  for (int c = 0; c < nch; ++c) {
+    cudaStream_t cs = p->comp[c % kCompStreams];
+    const int h0 = (int)((int64_t)c * kc.Hkv / nch) * kc.G, h1 = (int)((int64_t)(c + 1) * kc.Hkv / nch) * kc.G;
+    const size_t qoff = (size_t)h0 * kc.d * 2, qw = (size_t)(h1 - h0) * kc.d * 2;
+    const size_t ooff = (size_t)h0 * kc.d * (kc.out_fp32 ? 4 : 2), ow = (size_t)(h1 - h0) * kc.d * (kc.out_fp32 ? 4 : 2);
+    // Q of heads [h0, h1) up (strided rows), attention of those heads, their output down
+    if ((st = chk(cudaMemcpy2DAsync(qd + qoff, row_q, reinterpret_cast<const uint8_t*>(q) + qoff, row_q, qw, (size_t)T,
+                                    cudaMemcpyHostToDevice, p->up))) != HACK_OK)
+      return st;
+    if ((st = chk(cudaEventRecord(p->q[c], p->up))) != HACK_OK) return st;
+    if ((st = chk(cudaStreamWaitEvent(cs, p->q[c], 0))) != HACK_OK) return st;
+    KernelCfg kcc = kc;
+    kcc.hq_begin = nch > 1 ? h0 : 0;
+    kcc.hq_count = nch > 1 ? h1 - h0 : kc.Hq;
+    if ((st = chk(launch_prefill_attention(kcc, qd, cud, sld, batch, max_seqlen, cv, od, base + lay.ws, nullptr, cs))) !=
+        HACK_OK)
+      return st;
+    if ((st = chk(cudaEventRecord(p->o[c], cs))) != HACK_OK) return st;
+    if ((st = chk(cudaStreamWaitEvent(p->down, p->o[c], 0))) != HACK_OK) return st;
+    if ((st = chk(cudaMemcpy2DAsync(reinterpret_cast<uint8_t*>(out) + ooff, row_o, od + ooff, row_o, ow, (size_t)T,
+                                    cudaMemcpyDeviceToHost, p->down))) != HACK_OK)
+      return st;
+  }
+  // the caller's stream completes after the last download (which follows every chunk's
+  // attention through the o[c] events)
+  if ((st = chk(cudaEventRecord(p->done, p->down))) != HACK_OK) return st;
+  return chk(cudaStreamWaitEvent(s0, p->done, 0));
 }
 
 hack_status_t hack_decode_append(const hack_config_t* cfg, const void* k_new, const void* v_new,

@@ -60,6 +60,10 @@ cudaError_t launch_prefill_attention(const KernelCfg& kc, const void* q, const i
   return launch_prefill_simt(kc, q, cu_seqlens, slots, batch, max_seqlen, cv, out, dbg, st);
 }
 
+bool prefill_head_range_supported(const KernelCfg& kc) {
+  return prefill_tc_supported(kc) && !env_is("HACK_PREFILL_IMPL", "simt");  // (the CUDA-core kernel: all heads)
+}
+
 static bool use_decode_mma(const KernelCfg& kc) {
   return decode_mma_supported(kc) && !env_is("HACK_DECODE_IMPL", "simt");
 }

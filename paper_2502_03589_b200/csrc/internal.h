@@ -19,6 +19,7 @@ struct KernelCfg {
   int layer, head_base;
   int out_fp32;
   PageLayout pl;
+  int hq_begin, hq_count;  // prefill attention: the query heads this launch computes (all by default)
 };
 
 // Device view of one layer's paged cache (plain POD, passed by value to kernels).
@@ -46,6 +47,9 @@ cudaError_t launch_prefill_attention(const KernelCfg& kc, const void* q, const i
                                      const int32_t* slots, int batch, int max_seqlen, const CacheView& cv,
                                      void* out, void* workspace, const hack_debug_t* dbg, cudaStream_t st,
                                      bool pdl = false);
+
+// whether the prefill kernel serving kc computes a query-head range (kc.hq_begin / hq_count)
+bool prefill_head_range_supported(const KernelCfg& kc);
 
 size_t decode_workspace_bytes(const KernelCfg& kc, int batch, int max_seqlen);
 // hack_acc_form_t of the kernel the next prefill (op 0) / decode (op 1) call dispatches to

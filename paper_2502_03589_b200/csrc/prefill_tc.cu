@@ -270,7 +270,7 @@ __global__ void __launch_bounds__(Geo<PI_, BITS>::THREADS, 1) prefill_tc_kernel(
   // (no per-CTA launch, TMEM allocation and pipeline fill per item).  Otherwise one item per
   // CTA from the grid (head pair fastest, heaviest first).
   const int gp = pack_heads(kc), pbp = BM / gp;
-  const int npk = kc.Hq / gp;
+  const int npk = kc.hq_count / gp;  // head groups of this launch (from kc.hq_begin)
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const PageLayout PL = kc.pl;
   struct Item {
@@ -289,7 +289,7 @@ __global__ void __launch_bounds__(Geo<PI_, BITS>::THREADS, 1) prefill_tc_kernel(
       lin = blockIdx.x + gridDim.x * blockIdx.y;
     }
     const int rank = lin / npk;
-    w.hq0 = (lin % npk) * gp;  // heads hq0 .. hq0 + gp - 1
+    w.hq0 = kc.hq_begin + (lin % npk) * gp;  // heads hq0 .. hq0 + gp - 1
     w.start = cu_seqlens[b];
     w.L = cu_seqlens[b + 1] - w.start;
     const int nqt = (w.L + pbp - 1) / pbp;
@@ -1049,10 +1049,10 @@ cudaError_t launch_t(const KernelCfg& kc, const void* q, const int32_t* cu, cons
     int dev = 0, nsm = 0;
     if ((e = cudaGetDevice(&dev)) != cudaSuccess) return e;
     if ((e = cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev)) != cudaSuccess) return e;
-    nitems = nqt * (kc.Hq / gp);
+    nitems = nqt * (kc.hq_count / gp);
     lc.gridDim = dim3(min(nitems, nsm), 1, 1);
   } else {
-    lc.gridDim = dim3(nqt, kc.Hq / gp, batch);
+    lc.gridDim = dim3(nqt, kc.hq_count / gp, batch);
   }
   lc.blockDim = dim3(Geo<PI_, BITS>::THREADS);
   lc.dynamicSmemBytes = smem;

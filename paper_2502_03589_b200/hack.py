@@ -73,7 +73,8 @@ _lib.hack_decode_workspace_size.restype = C.c_size_t
 _lib.hack_config_default.restype = None
 _lib.hack_debug_acc_form.restype = C.c_int32
 for _name in ("hack_config_validate", "hack_page_layout", "hack_quantize_pack", "hack_cache_ingest",
-              "hack_prefill_attention", "hack_prefill_attention_cached", "hack_decode_append",
+              "hack_prefill_attention", "hack_prefill_attention_cached", "hack_prefill_attention_host",
+              "hack_decode_append",
               "hack_decode_attention", "hack_decode_attention_cached", "hack_homomorphic_matmul",
               "hack_comm_unique_id", "hack_comm_init", "hack_comm_destroy", "hack_kv_pack", "hack_kv_unpack",
               "hack_kv_send", "hack_kv_recv", "hack_kv_send_layer", "hack_kv_recv_layer", "hack_kv_pull",
@@ -90,6 +91,10 @@ _lib.hack_prefill_attention.argtypes = [C.POINTER(Config), _P, _P, _P, _P, _P, C
 _lib.hack_prefill_attention_cached.argtypes = [C.POINTER(Config), _P, _P, _P, C.c_int32, C.c_int32,
                                                C.POINTER(CacheStruct), _P, _P, C.c_size_t,
                                                C.POINTER(DebugStruct), _P]
+_lib.hack_prefill_attention_host.argtypes = [C.POINTER(Config), _P, _P, _P, _P, _P, C.c_int32, C.c_int32,
+                                             C.POINTER(CacheStruct), _P, _P, C.c_size_t, C.c_int32, _P]
+_lib.hack_prefill_host_workspace_size.restype = C.c_size_t
+_lib.hack_prefill_host_workspace_size.argtypes = [C.POINTER(Config), C.c_int32, C.c_int32]
 _lib.hack_decode_append.argtypes = [C.POINTER(Config), _P, _P, _P, C.c_int32, C.POINTER(CacheStruct), _P]
 _lib.hack_decode_attention.argtypes = [C.POINTER(Config), _P, _P, _P, _P, C.c_int32, C.c_int32,
                                        C.POINTER(CacheStruct), _P, _P, C.c_size_t, C.POINTER(DebugStruct), _P]
@@ -307,6 +312,26 @@ def prefill_attention(cfg: Config, q, k, v, cu_seqlens, slots, max_seqlen: int, 
     _check(_lib.hack_prefill_attention(C.byref(cfg), _ptr(q), _ptr(k), _ptr(v), _ptr(cu_seqlens), _ptr(slots),
                                        slots.shape[0], max_seqlen, C.byref(cs), _ptr(out), _ptr(ws), nb,
                                        _dbg(debug_pcodes, debug_qk, debug_pv, debug_head), _stream(stream)), "prefill_attention")
+
+
+def prefill_host_workspace_size(cfg: Config, batch: int, total_tokens: int) -> int:
+    return _lib.hack_prefill_host_workspace_size(C.byref(cfg), batch, total_tokens)
+
+
+def prefill_attention_host(cfg: Config, q, k, v, cu_seqlens, slots, max_seqlen: int, cache: KVCache, out,
+                           workspace=None, head_chunks: int = 0, stream=None):
+    """hack_prefill_attention with HOST q / k / v / cu_seqlens / slots / out (CPU tensors, pinned for
+    copy-compute overlap): the library stages them through `workspace` (device) and pipelines
+    uploads, ingest, per-head-chunk attention and downloads."""
+    for t in (q, k, v, cu_seqlens, slots, out):
+        if t.is_cuda:
+            raise ValueError("prefill_attention_host takes host tensors")
+    cs = cache.struct()
+    T = int(cu_seqlens[-1])
+    ws, nb = _ws(workspace, prefill_host_workspace_size(cfg, slots.shape[0], T), cache.pages.device)
+    _check(_lib.hack_prefill_attention_host(C.byref(cfg), _ptr(q), _ptr(k), _ptr(v), _ptr(cu_seqlens), _ptr(slots),
+                                            slots.shape[0], max_seqlen, C.byref(cs), _ptr(out), _ptr(ws), nb,
+                                            head_chunks, _stream(stream)), "prefill_attention_host")
 
 
 def prefill_attention_cached(cfg: Config, q, cu_seqlens, slots, max_seqlen: int, cache: KVCache, out,

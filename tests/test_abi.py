@@ -130,3 +130,23 @@ def test_debug_acc_form_follows_dispatch(hk, monkeypatch):
     assert hk.debug_acc_form(c, "decode") == hk.ACC_NONE
     monkeypatch.setenv("HACK_PREFILL_IMPL", "simt")
     assert hk.debug_acc_form(c, "prefill") == hk.ACC_NONE
+
+
+def test_prefill_host_rejects_bad_arguments_before_any_work(hk):
+    """hack_prefill_attention_host validates its host index arrays and workspace before it
+    enqueues anything (no GPU needed to reach these errors)."""
+    cfg = hk.config(num_q_heads=4, num_kv_heads=1)
+    assert hk.prefill_host_workspace_size(cfg, 1, 100) > 100 * 4 * 128 * 2 * 2
+    assert hk.prefill_host_workspace_size(cfg, 0, 100) == 0
+    lib = hk.library()
+    cache = hk.CacheStruct(1, 1, 1, 1, 1, 4, 1, 2, hk.page_bytes(cfg))
+    buf = (ctypes.c_uint8 * 64)()
+    cu = (ctypes.c_int32 * 2)(0, 0)          # empty prompt
+    sl = (ctypes.c_int32 * 1)(0)
+    st = lib.hack_prefill_attention_host(ctypes.byref(cfg), buf, buf, buf, cu, sl, 1, 64, ctypes.byref(cache), buf,
+                                         buf, 64, 0, None)
+    assert st == 1, lib.hack_last_error().decode()        # INVALID_ARG
+    cu = (ctypes.c_int32 * 2)(0, 64)
+    st = lib.hack_prefill_attention_host(ctypes.byref(cfg), buf, buf, buf, cu, sl, 1, 64, ctypes.byref(cache), buf,
+                                         buf, 64, 0, None)
+    assert st == 4, lib.hack_last_error().decode()        # CAPACITY: workspace too small

@@ -175,3 +175,35 @@ def test_prefill_p_sr_unsupported_on_the_cuda_core_kernel(monkeypatch):
         h.prefill_attention(cfg, q, k, k, cu, sl, 64, cache, torch.zeros_like(q))
     assert e.value.status == h.ERR_UNSUPPORTED
     assert int(cache.seq_lens[0]) == 0                 # rejected before the ingest launch
+
+
+@pytest.mark.parametrize("chunks", [1, 2, 4, 0])
+def test_prefill_host_buffers_pipelined_equals_device_call(chunks):
+    """hack_prefill_attention_host (host q/k/v/out, the e2e path): per query-head chunk
+    uploads, attention of those heads (kc.hq_begin / hq_count) and downloads overlap on
+    library streams; outputs and cache pages must equal hack_prefill_attention's bit for
+    bit, for a ragged two-request batch and every chunking (0 = the default)."""
+    h = hk()
+    ocfg = att.Config(Hq=16, Hkv=4, Pi=64, bits=2, seed=23)
+    cfg = gpu_cfg(ocfg)
+    lens = [300, 77]
+    T = sum(lens)
+    q, k, v = hack_inputs.qkv(23, T, ocfg.Hq, ocfg.Hkv)
+    cu = torch.tensor([0, lens[0], T], dtype=torch.int32)
+    sl = torch.tensor([1, 0], dtype=torch.int32)
+    caches = [make_cache(cfg, max_reqs=2, max_len=max(lens), seed=3) for _ in range(2)]
+    for c in caches:   # (bytes neither call writes compare equal too)
+        c.pages.zero_()
+        c.v_tail.zero_()
+    ref = torch.zeros((T, ocfg.Hq, 128), dtype=torch.float32, device="cuda")
+    h.prefill_attention(cfg, torch.from_numpy(q).cuda(), torch.from_numpy(k).cuda(), torch.from_numpy(v).cuda(),
+                        cu.cuda(), sl.cuda(), max(lens), caches[0], ref)
+    qh, kh, vh = (torch.from_numpy(x).pin_memory() for x in (q, k, v))
+    outh = torch.full((T, ocfg.Hq, 128), float("nan"), dtype=torch.float32).pin_memory()
+    h.prefill_attention_host(cfg, qh, kh, vh, cu.pin_memory(), sl.pin_memory(), max(lens), caches[1], outh,
+                             head_chunks=chunks)
+    torch.cuda.synchronize()
+    assert torch.equal(outh, ref.cpu())
+    assert torch.equal(caches[0].pages, caches[1].pages)
+    assert torch.equal(caches[0].v_tail, caches[1].v_tail)
+    assert torch.equal(caches[0].seq_lens, caches[1].seq_lens)
