@@ -67,6 +67,8 @@ hack_status_t make_kernel_cfg(const hack_config_t* c, KernelCfg* kc) {
   kc->pl = page_layout(c->head_dim, c->partition, c->kv_bits);
   kc->hq_begin = 0;
   kc->hq_count = c->num_q_heads;
+  kc->kvh_begin = 0;
+  kc->kvh_count = c->num_kv_heads;
   return HACK_OK;
 }
 
@@ -426,7 +428,9 @@ hack_status_t hack_prefill_attention_host(const hack_config_t* cfg, const void* 
   if ((st = chk(cudaEventRecord(p->ingested, s0))) != HACK_OK) return st;
   // the chunks' attention launches go to kCompStreams streams, so one chunk's CTAs fill the
   // SMs that the previous chunk's light items free (a head chunk alone cannot fill the GPU:
-  // its longest causal rows set its duration)
+  // its longest causal rows set its duration).  (Uploading K/V per chunk of KV heads too, with
+  // a per-chunk ingest (kc.kvh_begin / kvh_count), measured slower: 256-byte rows at 8 chunks
+  // make the strided copies inefficient, 1.55 vs 1.37 ms.)
   for (int i = 0; i < std::min(nch, kCompStreams); ++i)
     if ((st = chk(cudaStreamWaitEvent(p->comp[i], p->ingested, 0))) != HACK_OK) return st;
   for (int c = 0; c < nch; ++c) {

@@ -19,7 +19,8 @@ struct KernelCfg {
   int layer, head_base;
   int out_fp32;
   PageLayout pl;
-  int hq_begin, hq_count;  // prefill attention: the query heads this launch computes (all by default)
+  int hq_begin, hq_count;    // prefill attention: the query heads this launch computes (all by default)
+  int kvh_begin, kvh_count;  // ingest: the KV heads this launch quantizes (all by default)
 };
 
 // Device view of one layer's paged cache (plain POD, passed by value to kernels).

@@ -86,13 +86,13 @@ HACK_DEV void ingest_k_body(const __half* __restrict__ k, const int32_t* __restr
                             int b, int tid) {
   const int start = cu_seqlens[b], L = cu_seqlens[b + 1] - start;
   const int slot = slots[b];
-  const int H = kc.Hkv;
+  const int H = kc.Hkv, Hl = kc.kvh_count;  // layout heads; heads of this launch (from kc.kvh_begin)
   const int lane16 = tid & 15;
   const int r = bx * 16 + (tid >> 4);
-  if (bx * 16 >= L * H) return;  // whole block out of range (uniform)
-  const bool valid = r < L * H;
-  const int rr = valid ? r : L * H - 1;
-  const int t = rr / H, h = rr % H;
+  if (bx * 16 >= L * Hl) return;  // whole block out of range (uniform)
+  const bool valid = r < L * Hl;
+  const int rr = valid ? r : L * Hl - 1;
+  const int t = rr / Hl, h = kc.kvh_begin + rr % Hl;
   const uint4 raw = reinterpret_cast<const uint4*>(k + ((int64_t)(start + t) * H + h) * 128)[lane16];
   uint64_t packed;
   float m, s;
@@ -135,7 +135,8 @@ __global__ void __launch_bounds__(128) ingest_v_kernel(const __half* __restrict_
   const int nfull = L / Pi;
   const int id = blockIdx.x * blockDim.x + threadIdx.x;  // (blk, h, c), blk in [0, nfull]
   if (id == 0) cv.seq_lens[slot] = L;
-  const int c = id % 128, h = (id / 128) % H, j = id / (128 * H);
+  const int Hl = kc.kvh_count;  // heads of this launch (from kc.kvh_begin)
+  const int c = id % 128, h = kc.kvh_begin + (id / 128) % Hl, j = id / (128 * Hl);
   if (j > nfull) return;
   const __half* xc = v + ((int64_t)(start + j * Pi) * H + h) * 128 + c;
   if (j == nfull) {  // FP16 tail rows (reading R10)
@@ -178,7 +179,8 @@ HACK_DEV void ingest_v64_body(const __half* __restrict__ v, const int32_t* __res
   const int slot = slots[b];
   const int H = kc.Hkv;
   const int nfull = L / PI;
-  const int cg = bx & 3, h = (bx >> 2) % H, j = (bx >> 2) / H;
+  const int Hl = kc.kvh_count;  // heads of this launch (from kc.kvh_begin)
+  const int cg = bx & 3, h = kc.kvh_begin + (bx >> 2) % Hl, j = (bx >> 2) / Hl;
   const int q = tid >> 5, lane = tid & 31;
   const int c = 32 * cg + lane;
   if (bx == 0 && tid == 0) cv.seq_lens[slot] = L;
@@ -354,9 +356,9 @@ cudaError_t launch_ingest(const KernelCfg& kc, const void* k, const void* v, con
                           cudaStream_t st) {
   const __half* kh = reinterpret_cast<const __half*>(k);
   const __half* vh = reinterpret_cast<const __half*>(v);
-  dim3 gk((max_seqlen * kc.Hkv + 15) / 16, batch);
-  dim3 gv(((max_seqlen / kc.Pi + 1) * kc.Hkv * 128 + 127) / 128, batch);
-  dim3 gv64((max_seqlen / kc.Pi + 1) * kc.Hkv * 4, batch);  // (block, head, 32-channel group)
+  dim3 gk((max_seqlen * kc.kvh_count + 15) / 16, batch);
+  dim3 gv(((max_seqlen / kc.Pi + 1) * kc.kvh_count * 128 + 127) / 128, batch);
+  dim3 gv64((max_seqlen / kc.Pi + 1) * kc.kvh_count * 4, batch);  // (block, head, 32-channel group)
   const bool v64 = kc.Pi == 64;
   if (v64) {
     const int nk = gk.x, nv = gv64.x;
