@@ -427,12 +427,11 @@ HACK_DEV void produce_pages(SMT& sm, SegWalker walk, const CacheView& cv, const 
 // next launch.  A partial covers slot (u + c, warp): CTA c of the unit's CTA span
 // [uoff / R, (uoff + npg - 1) / R].  Writers fence their partial stores before the count;
 // the merging CTA fences after it and reads the partials through L2 (ld.cg).
-// All 4 warps (3 compute + the producer) of the CTA run it: thread = output channel.
+// All warps of the CTA (compute + producer) run it.
 template <int NWp>
 HACK_DEV void merge_units(SegWalker walk, int R, const CacheView& cv, const int32_t* __restrict__ slots,
                           const KernelCfg& kc, int* __restrict__ cnt, const float* __restrict__ part,
                           void* __restrict__ out, int* flag_smem, int tid, int add) {
-  static_assert((NWp + 1) * 32 == 128, "thread = channel");
   __threadfence();  // this thread's partial stores precede the CTA's count below
   __syncthreads();
   const int G = kc.G;
