@@ -36,15 +36,23 @@ hack_status_t cuda_status(cudaError_t e, const char* where) {
   return fail(HACK_ERR_CUDA, "%s: %s", where, cudaGetErrorString(e));
 }
 
+// The compute capability of the current device, queried once per device (every call checks it).
+static std::atomic<int> g_dev_cc[64];  // 0 = not queried, else 10 * major + minor
+
 hack_status_t check_device() {
   int dev = -1;
   cudaError_t e = cudaGetDevice(&dev);
   if (e != cudaSuccess) return fail(HACK_ERR_CUDA, "no CUDA device: %s", cudaGetErrorString(e));
-  int major = 0, minor = 0;
-  cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev);
-  cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, dev);
-  if (major != 10 || minor != 0)
-    return fail(HACK_ERR_CUDA, "libhack is built for sm_100a (B200); device %d is sm_%d%d", dev, major, minor);
+  int cc = dev >= 0 && dev < 64 ? g_dev_cc[dev].load(std::memory_order_relaxed) : 0;
+  if (cc == 0) {
+    int major = 0, minor = 0;
+    cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev);
+    cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, dev);
+    cc = 10 * major + minor;
+    if (dev >= 0 && dev < 64 && major > 0) g_dev_cc[dev].store(cc, std::memory_order_relaxed);
+  }
+  if (cc != 100)
+    return fail(HACK_ERR_CUDA, "libhack is built for sm_100a (B200); device %d is sm_%d", dev, cc);
   return HACK_OK;
 }
 
