@@ -54,17 +54,31 @@ constexpr int PI = 64;
 #ifndef HACK_DEC_CTAS
 #define HACK_DEC_CTAS 4
 #endif
-constexpr int NW = HACK_DEC_NW;        // compute warps per CTA
-constexpr int NSTG = HACK_DEC_NSTG;    // page slots per CTA
-constexpr int kThreads = (NW + 1) * 32;
-constexpr int kCtasPerSm = HACK_DEC_CTAS;
+#ifndef HACK_DEC_PIPES
+#define HACK_DEC_PIPES 1
+#endif
+// decode_pair_kernel runs PIPES independent page pipelines (producer warp + NW compute
+// warps + ring + stream-K range each).  PIPES = 1: one per CTA, HACK_DEC_CTAS CTAs per SM.
+// PIPES = 4: one CTA per SM whose 4 producer warps form warpgroup 0, so setmaxnreg moves
+// their unused registers to the compute warps.
+constexpr int PIPES = HACK_DEC_PIPES;
+constexpr int NW = HACK_DEC_NW;        // compute warps per pipeline
+constexpr int NSTG = HACK_DEC_NSTG;    // page slots per pipeline
+constexpr int kThreads = PIPES * (NW + 1) * 32;
+constexpr int kThreads8 = (NW + 1) * 32;  // decode_g8_kernel: one pipeline per CTA
+constexpr int kCtasPerSm = PIPES == 1 ? HACK_DEC_CTAS : 1;
+static_assert(PIPES == 1 || (PIPES == 4 && NW * PIPES % 4 == 0), "warpgroup roles");
+#ifndef HACK_DEC_REGPROD
+#define HACK_DEC_REGPROD 72
+#endif
+constexpr int kRegProd = HACK_DEC_REGPROD, kRegComp = PIPES == 1 ? 128 : (65536 - 128 * kRegProd) / (32 * NW * PIPES) / 8 * 8;
 constexpr int PB = 5376;    // page bytes at d = 128, Pi = 64, b = 2
 constexpr int kPart = 130;  // floats per partial row: m, l, O[128]
 constexpr uint32_t kMagic = 0x4B400000u;   // bits of 1.5 * 2^23
 constexpr float kMagicF = 12582912.f;      // 1.5 * 2^23
 constexpr int kMetaInts = 16;              // workspace header: R, P, grid, ...
 
-struct PairSmem {
+struct alignas(128) PairSmem {
   uint8_t stage[NSTG][PB];
   struct Warp {
     float4 scr[64][2];      // K coefficients of the page in QK; V coefficients of channels 64..127 in PV
@@ -244,9 +258,8 @@ HACK_DEV void qk_page(const uint8_t* pg, const PageLayout& PL, const float4* kcs
 // CTA 0 also publishes the per-request offsets and page counts for the merge kernel.
 template <class SMT>
 HACK_DEV void locate_range(SMT& sm, const CacheView& cv, const int32_t* __restrict__ slots, int batch, int Hkv,
-                           int* __restrict__ ws_meta, int warp, int lane, int add) {
-  const int c = blockIdx.x;
-  if (warp == 0) {
+                           int* __restrict__ ws_meta, bool leader, int lane, int add, int c, int nvirt) {
+  if (leader) {
     int P = 0;
     for (int b0 = 0; b0 < batch; b0 += 32) {
       const int b = b0 + lane;
@@ -263,7 +276,7 @@ HACK_DEV void locate_range(SMT& sm, const CacheView& cv, const int32_t* __restri
       }
       P += __shfl_sync(0xffffffffu, v, 31);
     }
-    const int R = max(1, (P + (int)gridDim.x - 1) / (int)gridDim.x);
+    const int R = max(1, (P + nvirt - 1) / nvirt);
     const int start = c * R;
     // request holding page `start`
     int base = 0, bsel = batch, basesel = P;
@@ -293,7 +306,7 @@ HACK_DEV void locate_range(SMT& sm, const CacheView& cv, const int32_t* __restri
       if (c == 0) {
         ws_meta[0] = R;
         ws_meta[1] = P;
-        ws_meta[2] = gridDim.x;
+        ws_meta[2] = nvirt;
       }
     }
   }
@@ -428,12 +441,12 @@ HACK_DEV void produce_pages(SMT& sm, SegWalker walk, const CacheView& cv, const 
 // [uoff / R, (uoff + npg - 1) / R].  Writers fence their partial stores before the count;
 // the merging CTA fences after it and reads the partials through L2 (ld.cg).
 // All warps of the CTA (compute + producer) run it.
-template <int NWp>
+template <int NWp, class Sync>
 HACK_DEV void merge_units(SegWalker walk, int R, const CacheView& cv, const int32_t* __restrict__ slots,
                           const KernelCfg& kc, int* __restrict__ cnt, const float* __restrict__ part,
-                          void* __restrict__ out, int* flag_smem, int tid, int add) {
+                          void* __restrict__ out, int* flag_smem, int tid, int add, Sync sync) {
   __threadfence();  // this thread's partial stores precede the CTA's count below
-  __syncthreads();
+  sync();
   const int G = kc.G;
   Seg s;
   while (walk.next(cv, slots, kc.Hkv, s, add)) {
@@ -445,9 +458,9 @@ HACK_DEV void merge_units(SegWalker walk, int R, const CacheView& cv, const int3
       if (last) cnt[u] = 0;  // no other CTA touches it again in this launch
       *flag_smem = last;
     }
-    __syncthreads();
+    sync();
     const bool last = *flag_smem != 0;
-    __syncthreads();  // (flag reused by the next segment)
+    sync();  // (flag reused by the next segment)
     if (!last) continue;
     __threadfence();
     const int np = (cl - cf + 1) * NWp;
@@ -504,17 +517,18 @@ HACK_DEV void merge_units(SegWalker walk, int R, const CacheView& cv, const int3
 
 // seq_lens += 1 for the step's requests, by the last CTA to finish: every CTA has read the old
 // lengths (range geometry, walks, merge) before it counts itself done.
+template <class Sync>
 HACK_DEV void bump_lengths(const StepIO& io, const CacheView& cv, const int32_t* __restrict__ slots, int batch,
-                           int* flag_smem, int tid) {
-  __syncthreads();
+                           int* flag_smem, int tid, int nthreads, int nvirt, Sync sync) {
+  sync();
   if (tid == 0) {
     __threadfence();
-    *flag_smem = atomicAdd(io.done, 1) == (int)gridDim.x - 1;
+    *flag_smem = atomicAdd(io.done, 1) == nvirt - 1;
   }
-  __syncthreads();
+  sync();
   if (*flag_smem == 0) return;
   __threadfence();
-  for (int b = tid; b < batch; b += blockDim.x) {
+  for (int b = tid; b < batch; b += nthreads) {
     const int slot = slots[b];
     const int t = __ldcg(cv.seq_lens + slot);
     if (t / PI < cv.max_pages_per_req) cv.seq_lens[slot] = t + 1;  // capacity guard (append_kernel)
@@ -544,19 +558,28 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
   const int64_t dbg_stride = dbg.pstride;
   constexpr int qkm = 3;
   extern __shared__ __align__(128) uint8_t smem_raw[];
-  PairSmem& sm = *reinterpret_cast<PairSmem*>(smem_raw);
   const int G = kc.G, Hkv = kc.Hkv;
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int tid = threadIdx.x, lane = tid & 31;
   const int g = lane >> 2, tig = lane & 3;
-  const int c = blockIdx.x;
+  // roles: PIPES = 1: warps 0..NW-1 compute, warp NW produces.  PIPES = 4: warps 0-3 are the
+  // 4 pipelines' producers (warpgroup 0), then NW compute warps per pipeline.
+  const int w_ = tid >> 5;
+  const bool producer = PIPES == 1 ? w_ == NW : w_ < PIPES;
+  const int pipe = PIPES == 1 ? 0 : (producer ? w_ : (w_ - PIPES) / NW);
+  const int warp = PIPES == 1 ? w_ : (producer ? NW : (w_ - PIPES) % NW);  // compute warp of the pipeline
+  const int ltid = 32 * warp + lane;  // thread of the pipeline (0 .. 32 (NW + 1) - 1)
+  const int c = blockIdx.x * PIPES + pipe, nvirt = gridDim.x * PIPES;  // page range (virtual CTA)
+  PairSmem& sm = reinterpret_cast<PairSmem*>(smem_raw)[pipe];
+  auto psync = [pipe] { asm volatile("bar.sync %0, %1;" ::"r"(1 + pipe), "n"(32 * (NW + 1)) : "memory"); };
   const PageLayout PL = kc.pl;
 
-  if (tid == 0) {
+  if (tid < PIPES) {
+    PairSmem& sp = reinterpret_cast<PairSmem*>(smem_raw)[tid];
     for (int s = 0; s < NSTG; ++s) {
-      ptx::mbar_init(&sm.full[s], 1);
-      ptx::mbar_init(&sm.fullv[s], 1);
-      sm.tag[s] = -1;
-      ptx::mbar_init(&sm.empty[s], 1);
+      ptx::mbar_init(&sp.full[s], 1);
+      ptx::mbar_init(&sp.fullv[s], 1);
+      sp.tag[s] = -1;
+      ptx::mbar_init(&sp.empty[s], 1);
     }
     ptx::fence_mbar_init();
   }
@@ -565,14 +588,18 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
   // only shared memory; seq_lens, pages and the FP16 tail are read after this wait
   asm volatile("griddepcontrol.wait;" ::: "memory");
 #endif
-  locate_range(sm, cv, slots, batch, Hkv, ws_meta, warp, lane, FUSED);
+  locate_range(sm, cv, slots, batch, Hkv, ws_meta, PIPES == 1 ? w_ == 0 : producer, lane, FUSED, c, nvirt);
   __syncthreads();
   const int R = sm.R, P = sm.P;
   SegWalker walk{sm.range_b0, sm.range_base, min(c * R, P), min(c * R + R, P)};
 
-  if (warp == NW) {
+  // PIPES = 4: the producers' registers go to the compute warps (warpgroup-wide setmaxnreg)
+  if (producer) {
+    if (PIPES > 1) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kRegProd));
     produce_pages<NSTG, FUSED>(sm, walk, cv, slots, Hkv, kc, lane, io);
+    if (PIPES > 1) asm volatile("setmaxnreg.inc.sync.aligned.u32 128;");  // even split for the merge below
   } else {
+  if (PIPES > 1) asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kRegComp));
 
   // -------------------------------------------------------------------- compute warps
   typename PairSmem::Warp& ws = sm.w[warp];
@@ -657,6 +684,16 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
         float sa[4][2], sbv[4][2];
         float mxA, mnA, mxB = -INFINITY, mnB = INFINITY;
         wait_fill<NSTG>(sm, kA);
+#ifdef HACK_DEC_STREAM
+        // timing experiment only (wrong outputs): the page pipeline without any compute
+        if (hasB) wait_fill<NSTG>(sm, kB);
+        __syncwarp();
+        if (lane == 0) {
+          ptx::mbar_arrive(&sm.empty[sA]);
+          if (hasB) ptx::mbar_arrive(&sm.empty[sB]);
+        }
+        continue;
+#endif
         stage_kc<SE>(pgA, PL, &ws.scr[0][0], lane);
         __syncwarp();
         int32_t* dqA = nullptr;
@@ -882,11 +919,13 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
     it_base += nitems;
     k_base += s.p1 - s.p0;
   }
+  if (PIPES > 1) asm volatile("setmaxnreg.dec.sync.aligned.u32 128;");
   }  // compute warps
   if (merge)
     merge_units<NW>(SegWalker{sm.range_b0, sm.range_base, min(c * sm.R, sm.P), min(c * sm.R + sm.R, sm.P)}, sm.R, cv,
-                    slots, kc, cnt, part, out, &sm.mflag, tid, FUSED);
-  if (FUSED && merge) bump_lengths(io, cv, slots, batch, &sm.mflag, tid);  // (else decode_pair_combine)
+                    slots, kc, cnt, part, out, &sm.mflag, ltid, FUSED, psync);
+  if (FUSED && merge)  // (else decode_pair_combine)
+    bump_lengths(io, cv, slots, batch, &sm.mflag, ltid, 32 * (NW + 1), nvirt, psync);
 }
 
 // ============================================================================ G in (4, 8]
@@ -921,7 +960,7 @@ struct G8Smem {
 };
 
 template <bool DBG, bool FUSED>
-__global__ void __launch_bounds__(kThreads, kCtas8)
+__global__ void __launch_bounds__(kThreads8, kCtas8)
     decode_g8_kernel(const __half* __restrict__ q_new, const int32_t* __restrict__ slots, int batch, CacheView cv,
                      KernelCfg kc, int* __restrict__ ws_meta, int* __restrict__ cnt, float* __restrict__ part,
                      void* __restrict__ out, int merge, StepIO io, DecDbg dbg) {
@@ -949,7 +988,7 @@ __global__ void __launch_bounds__(kThreads, kCtas8)
   // only shared memory; seq_lens, pages and the FP16 tail are read after this wait
   asm volatile("griddepcontrol.wait;" ::: "memory");
 #endif
-  locate_range(sm, cv, slots, batch, Hkv, ws_meta, warp, lane, FUSED);
+  locate_range(sm, cv, slots, batch, Hkv, ws_meta, warp == 0, lane, FUSED, c, (int)gridDim.x);
   __syncthreads();
   const int R = sm.R, P = sm.P;
   SegWalker walk{sm.range_b0, sm.range_base, min(c * R, P), min(c * R + R, P)};
@@ -1241,8 +1280,9 @@ __global__ void __launch_bounds__(kThreads, kCtas8)
   }  // compute warps
   if (merge)
     merge_units<NW>(SegWalker{sm.range_b0, sm.range_base, min(c * sm.R, sm.P), min(c * sm.R + sm.R, sm.P)}, sm.R, cv,
-                    slots, kc, cnt, part, out, &sm.mflag, tid, FUSED);
-  if (FUSED && merge) bump_lengths(io, cv, slots, batch, &sm.mflag, tid);  // (else decode_pair_combine)
+                    slots, kc, cnt, part, out, &sm.mflag, tid, FUSED, [] { __syncthreads(); });
+  if (FUSED && merge)  // (else decode_pair_combine)
+    bump_lengths(io, cv, slots, batch, &sm.mflag, tid, (int)blockDim.x, (int)gridDim.x, [] { __syncthreads(); });
 }
 
 // out[b][hk*G + n][c] = sum_parts e^(m - M) O / sum_parts e^(m - M) l over the partials of
@@ -1311,7 +1351,7 @@ int grid_size(bool g8 = false) {
   int dev = 0, sms = 148;
   if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   if (const char* e = getenv("HACK_DECODE_GRID")) return atoi(e);
-  return sms * (g8 ? kCtas8 : kCtasPerSm);
+  return sms * (g8 ? kCtas8 : kCtasPerSm * PIPES);  // page ranges (virtual CTAs)
 }
 
 // Where the split partials are merged: in the main kernel by the CTA completing a unit
@@ -1365,7 +1405,7 @@ cudaError_t launch_decode_pair(const KernelCfg& kc, const void* q_new, const int
   // fused decode step (k_new given): the append runs inside the attention kernel
   const StepIO io = {reinterpret_cast<const __half*>(k_new), reinterpret_cast<const __half*>(v_new), done};
   const bool g8 = kc.G > 4;
-  const size_t smem = g8 ? sizeof(G8Smem) : sizeof(PairSmem);
+  const size_t smem = g8 ? sizeof(G8Smem) : PIPES * sizeof(PairSmem);
   const bool with_dbg = dbg != nullptr && (dbg->pcodes != nullptr || dbg->qk_acc != nullptr ||
                                            dbg->pv_acc != nullptr);  // dumps: parity runs only
   const bool no_se = !g8 && getenv("HACK_DECODE_NO_SE") != nullptr;  // f2 ablation only
@@ -1388,8 +1428,8 @@ cudaError_t launch_decode_pair(const KernelCfg& kc, const void* q_new, const int
     // preceding kernel on the stream (the append) drains; griddepcontrol.wait in the
     // kernel orders its global reads after that kernel's writes
     cudaLaunchConfig_t mc = {};
-    mc.gridDim = dim3(grid);
-    mc.blockDim = dim3(kThreads);
+    mc.gridDim = dim3(g8 ? grid : grid / PIPES);
+    mc.blockDim = dim3(g8 ? kThreads8 : kThreads);
     mc.dynamicSmemBytes = smem;
     mc.stream = st;
     cudaLaunchAttribute ma[1];
