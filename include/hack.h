@@ -206,10 +206,12 @@ hack_status_t hack_prefill_attention_cached(const hack_config_t* cfg, const void
  * pointers (page-locked for copy/compute overlap; pageable works, serialised), total tokens
  * = cu_seqlens[batch].  The library stages them through `workspace` (device, >=
  * hack_prefill_host_workspace_size() bytes, any contents) and pipelines: K/V up -> ingest;
- * then per query-head chunk (head_chunks chunks of whole GQA groups; <= 0: 8) Q chunk up ->
- * attention of those heads -> out chunk down, the uploads, the attention and the downloads
- * of different chunks overlapping (copies on library-owned streams, ordered after prior work
- * on `stream`; `stream` completes after the last download).  Results identical to
+ * then per chunk, Q chunk up -> attention of that chunk -> out chunk down, the uploads, the
+ * attention and the downloads of different chunks overlapping (copies on library-owned
+ * streams, ordered after prior work on `stream`; `stream` completes after the last download).
+ * head_chunks > 0: that many chunks of query heads (whole GQA groups).  head_chunks <= 0 and
+ * batch == 1: chunks of query positions, the last positions (longest causal rows) first
+ * (-n: n chunks, 0: 8); <= 0 with batch > 1: 8 query-head chunks.  Results identical to
  * hack_prefill_attention.  Same errors, plus HACK_ERR_CAPACITY for a small workspace. */
 size_t hack_prefill_host_workspace_size(const hack_config_t* cfg, int32_t batch, int32_t total_tokens);
 hack_status_t hack_prefill_attention_host(const hack_config_t* cfg, const void* q, const void* k,

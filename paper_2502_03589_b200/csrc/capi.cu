@@ -77,6 +77,8 @@ hack_status_t make_kernel_cfg(const hack_config_t* c, KernelCfg* kc) {
   kc->hq_count = c->num_q_heads;
   kc->kvh_begin = 0;
   kc->kvh_count = c->num_kv_heads;
+  kc->qt_begin = 0;
+  kc->qt_count = INT32_MAX;
   return HACK_OK;
 }
 
@@ -378,6 +380,76 @@ hack_status_t hack_prefill_attention(const hack_config_t* cfg, const void* q, co
                      "prefill_attention");
 }
 
+// hack_prefill_attention_host for ONE prompt, by position: K and V up, one ingest, then per
+// chunk c of query positions [a, b) (whole query tiles), LAST positions first: Q rows [a, b) up
+// (contiguous), the attention of those rows' query tiles (kc.qt_begin / qt_count) on a library
+// compute stream, the output rows [a, b) down.  The longest causal rows start first, so the
+// last chunk's attention (the shortest rows) and download are a short tail after the last
+// upload.  C2 (scripts/e2e_probe.py): 1.26 ms at 8 chunks against 1.35 ms for 8 query-head
+// chunks; 4 / 12 / 16 chunks 1.36 / 1.29 / 1.35 ms.  (Streaming K/V/Q rows in ascending order
+// with an ingest per chunk measured 1.47 ms: the longest rows then arrive last.)
+static hack_status_t prefill_host_streamed(const KernelCfg& kc, const CacheView& cv, const void* q, const void* k,
+                                           const void* v, const int32_t* cu, const int32_t* slots, int max_seqlen,
+                                           void* out, void* ws, const HostLayout& lay, int tile_rows, int nch_req,
+                                           void* stream) {
+  const int L = cu[1];
+  const int nqt = (L + tile_rows - 1) / tile_rows;  // query tiles of the prompt (rank 0 = the last)
+  const int nch = std::max(1, std::min(std::min(nch_req > 0 ? nch_req : 8, nqt), kMaxChunks));
+  uint8_t* base = reinterpret_cast<uint8_t*>(ws);
+  uint8_t *qd = base + lay.q, *kd = base + lay.k, *vd = base + lay.v, *od = base + lay.out;
+  int32_t* cud = reinterpret_cast<int32_t*>(base + lay.cu);
+  int32_t* sld = reinterpret_cast<int32_t*>(base + lay.slots);
+  const size_t row_q = (size_t)kc.Hq * kc.d * 2, row_o = (size_t)kc.Hq * kc.d * (kc.out_fp32 ? 4 : 2);
+  const size_t kvb = (size_t)L * kc.Hkv * kc.d * 2;
+  cudaStream_t s0 = (cudaStream_t)stream;
+  int dev = 0;
+  hack_status_t st;
+  if ((st = cuda_status(cudaGetDevice(&dev), "prefill_host")) != HACK_OK) return st;
+  std::lock_guard<std::mutex> lock(g_pipe_mu);
+  HostPipe* p = nullptr;
+  if ((st = cuda_status(host_pipe(dev, &p), "prefill_host: streams")) != HACK_OK) return st;
+  auto chk = [](cudaError_t e) { return cuda_status(e, "prefill_host"); };
+  if ((st = chk(cudaEventRecord(p->start, s0))) != HACK_OK) return st;
+  if ((st = chk(cudaStreamWaitEvent(p->up, p->start, 0))) != HACK_OK) return st;
+  if ((st = chk(cudaStreamWaitEvent(p->down, p->start, 0))) != HACK_OK) return st;
+  if ((st = chk(cudaMemcpyAsync(cud, cu, 2 * 4, cudaMemcpyHostToDevice, p->up))) != HACK_OK) return st;
+  if ((st = chk(cudaMemcpyAsync(sld, slots, 4, cudaMemcpyHostToDevice, p->up))) != HACK_OK) return st;
+  if ((st = chk(cudaMemcpyAsync(kd, k, kvb, cudaMemcpyHostToDevice, p->up))) != HACK_OK) return st;
+  if ((st = chk(cudaMemcpyAsync(vd, v, kvb, cudaMemcpyHostToDevice, p->up))) != HACK_OK) return st;
+  if ((st = chk(cudaEventRecord(p->kv, p->up))) != HACK_OK) return st;
+  if ((st = chk(cudaStreamWaitEvent(s0, p->kv, 0))) != HACK_OK) return st;
+  if ((st = chk(launch_ingest(kc, kd, vd, cud, sld, 1, max_seqlen, cv, s0))) != HACK_OK) return st;
+  if ((st = chk(cudaEventRecord(p->ingested, s0))) != HACK_OK) return st;
+  for (int i = 0; i < std::min(nch, kCompStreams); ++i)
+    if ((st = chk(cudaStreamWaitEvent(p->comp[i], p->ingested, 0))) != HACK_OK) return st;
+  for (int c = 0; c < nch; ++c) {
+    // ranks [r0, r1) = query tiles of positions [a, b), rank 0 = the last tile
+    const int r0 = (int)((int64_t)c * nqt / nch), r1 = (int)((int64_t)(c + 1) * nqt / nch);
+    const int a = (nqt - r1) * tile_rows, b = std::min(L, (nqt - r0) * tile_rows);
+    if ((st = chk(cudaMemcpyAsync(qd + a * row_q, reinterpret_cast<const uint8_t*>(q) + a * row_q, (b - a) * row_q,
+                                  cudaMemcpyHostToDevice, p->up))) != HACK_OK)
+      return st;
+    if ((st = chk(cudaEventRecord(p->q[c], p->up))) != HACK_OK) return st;
+    cudaStream_t cs = p->comp[c % kCompStreams];
+    if ((st = chk(cudaStreamWaitEvent(cs, p->q[c], 0))) != HACK_OK) return st;
+    KernelCfg kca = kc;
+    kca.qt_begin = r0;
+    kca.qt_count = r1 - r0;
+    if ((st = chk(launch_prefill_attention(kca, qd, cud, sld, 1, max_seqlen, cv, od, base + lay.ws, nullptr, cs))) !=
+        HACK_OK)
+      return st;
+    if ((st = chk(cudaEventRecord(p->o[c], cs))) != HACK_OK) return st;
+    if ((st = chk(cudaStreamWaitEvent(p->down, p->o[c], 0))) != HACK_OK) return st;
+    if ((st = chk(cudaMemcpyAsync(reinterpret_cast<uint8_t*>(out) + a * row_o, od + a * row_o, (b - a) * row_o,
+                                  cudaMemcpyDeviceToHost, p->down))) != HACK_OK)
+      return st;
+  }
+  // the caller's stream completes after the last download (which follows every chunk's
+  // attention through the o[c] events)
+  if ((st = chk(cudaEventRecord(p->done, p->down))) != HACK_OK) return st;
+  return chk(cudaStreamWaitEvent(s0, p->done, 0));
+}
+
 size_t hack_prefill_host_workspace_size(const hack_config_t* cfg, int32_t batch, int32_t total_tokens) {
   KernelCfg kc;
   if (make_kernel_cfg(cfg, &kc) != HACK_OK || batch <= 0 || total_tokens <= 0) return 0;
@@ -407,7 +479,12 @@ hack_status_t hack_prefill_attention_host(const hack_config_t* cfg, const void* 
   if ((st = check_device()) != HACK_OK) return st;
   int dev = 0;
   if ((st = cuda_status(cudaGetDevice(&dev), "prefill_host")) != HACK_OK) return st;
-  // query-head chunks of whole GQA groups; the CUDA-core baseline kernel has no head range
+  // one prompt: stream it by position (below); else query-head chunks of whole GQA groups (the
+  // CUDA-core baseline kernel has neither range)
+  const int tile_rows = prefill_query_tile_rows(kc);
+  if (batch == 1 && head_chunks <= 0 && tile_rows > 0)
+    return prefill_host_streamed(kc, cv, q, k, v, cu, slots, max_seqlen, out, ws, lay, tile_rows,
+                                 head_chunks < 0 ? -head_chunks : 0, stream);
   int nch = head_chunks <= 0 ? 8 : head_chunks;  // (C2: 1 / 2 / 4 / 8 chunks 1.97 / 1.52 / 1.42 / 1.37 ms)
   nch = std::max(1, std::min(std::min(nch, kc.Hkv), kMaxChunks));
   if (!prefill_head_range_supported(kc)) nch = 1;

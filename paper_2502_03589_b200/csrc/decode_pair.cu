@@ -71,7 +71,13 @@ static_assert(PIPES == 1 || (PIPES == 4 && NW * PIPES % 4 == 0), "warpgroup role
 #ifndef HACK_DEC_REGPROD
 #define HACK_DEC_REGPROD 72
 #endif
-constexpr int kRegProd = HACK_DEC_REGPROD, kRegComp = PIPES == 1 ? 128 : (65536 - 128 * kRegProd) / (32 * NW * PIPES) / 8 * 8;
+// even split of the register file: what the launch allocates per thread (the launch-bound cap,
+// a multiple of 8), also the share for the merge after the attention loop.  setmaxnreg only
+// moves registers within this pool (an .inc beyond it never completes).
+constexpr int kRegEven = 65536 / kThreads / 8 * 8 < 128 ? 65536 / kThreads / 8 * 8 : 128;
+constexpr int kRegProd = HACK_DEC_REGPROD,
+              kRegComp = PIPES == 1 ? 128 : (kRegEven * kThreads - 128 * kRegProd) / (32 * NW * PIPES) / 8 * 8;
+static_assert(PIPES == 1 || kRegComp * 32 * NW * PIPES + 128 * kRegProd <= kRegEven * kThreads, "register pool");
 constexpr int PB = 5376;    // page bytes at d = 128, Pi = 64, b = 2
 constexpr int kPart = 130;  // floats per partial row: m, l, O[128]
 constexpr uint32_t kMagic = 0x4B400000u;   // bits of 1.5 * 2^23
@@ -597,7 +603,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
   if (producer) {
     if (PIPES > 1) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kRegProd));
     produce_pages<NSTG, FUSED>(sm, walk, cv, slots, Hkv, kc, lane, io);
-    if (PIPES > 1) asm volatile("setmaxnreg.inc.sync.aligned.u32 128;");  // even split for the merge below
+    if (PIPES > 1) asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kRegEven));  // even split for the merge below
   } else {
   if (PIPES > 1) asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kRegComp));
 
@@ -919,7 +925,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
     it_base += nitems;
     k_base += s.p1 - s.p0;
   }
-  if (PIPES > 1) asm volatile("setmaxnreg.dec.sync.aligned.u32 128;");
+  if (PIPES > 1) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kRegEven));
   }  // compute warps
   if (merge)
     merge_units<NW>(SegWalker{sm.range_b0, sm.range_base, min(c * sm.R, sm.P), min(c * sm.R + sm.R, sm.P)}, sm.R, cv,

@@ -16,6 +16,7 @@ cudaError_t launch_prefill_simt(const KernelCfg& kc, const void* q, const int32_
                                 int batch, int max_seqlen, const CacheView& cv, void* out,
                                 const hack_debug_t* dbg, cudaStream_t st);
 bool prefill_tc_supported(const KernelCfg& kc);
+int prefill_tc_tile_rows(const KernelCfg& kc);
 
 cudaError_t launch_prefill_tc(const KernelCfg& kc, const void* q, const int32_t* cu, const int32_t* slots, int batch,
                               int max_seqlen, const CacheView& cv, void* out, const hack_debug_t* dbg,
@@ -62,6 +63,10 @@ cudaError_t launch_prefill_attention(const KernelCfg& kc, const void* q, const i
 
 bool prefill_head_range_supported(const KernelCfg& kc) {
   return prefill_tc_supported(kc) && !env_is("HACK_PREFILL_IMPL", "simt");  // (the CUDA-core kernel: all heads)
+}
+
+int prefill_query_tile_rows(const KernelCfg& kc) {
+  return prefill_head_range_supported(kc) ? prefill_tc_tile_rows(kc) : 0;  // (the CUDA-core kernel: all tiles)
 }
 
 static bool use_decode_mma(const KernelCfg& kc) {

@@ -21,6 +21,9 @@ struct KernelCfg {
   PageLayout pl;
   int hq_begin, hq_count;    // prefill attention: the query heads this launch computes (all by default)
   int kvh_begin, kvh_count;  // ingest: the KV heads this launch quantizes (all by default)
+  // prefill attention: the query tiles of rank [qt_begin, qt_begin + qt_count) of each request
+  // (rank 0 = the last positions, the longest causal rows; all by default)
+  int qt_begin, qt_count;
 };
 
 // Device view of one layer's paged cache (plain POD, passed by value to kernels).
@@ -51,6 +54,9 @@ cudaError_t launch_prefill_attention(const KernelCfg& kc, const void* q, const i
 
 // whether the prefill kernel serving kc computes a query-head range (kc.hq_begin / hq_count)
 bool prefill_head_range_supported(const KernelCfg& kc);
+// query positions per query tile of the prefill kernel serving kc (the unit of kc.qt_begin /
+// qt_count); 0 if that kernel computes every tile in one launch
+int prefill_query_tile_rows(const KernelCfg& kc);
 
 size_t decode_workspace_bytes(const KernelCfg& kc, int batch, int max_seqlen);
 // hack_acc_form_t of the kernel the next prefill (op 0) / decode (op 1) call dispatches to

@@ -83,6 +83,9 @@ constexpr uint32_t kPBar0 = 7;
 #ifndef HACK_PRE_RO
 #define HACK_PRE_RO 112
 #endif
+#ifndef HACK_PRE_RS1
+#define HACK_PRE_RS1 200  // S registers with one S warpgroup (HACK_PRE_NSG=1)
+#endif
 
 // Shapes per partition size: one key tile = one V block (BN = Pi keys); d/Pi d-blocks.
 template <int PI_, int BITS>
@@ -92,12 +95,14 @@ struct Geo {
   // latency of the per-key epilogue chain; the S side is the kernel's critical path)
   static constexpr int NSG = PI_ == 32 ? 2 : HACK_PRE_NSG;
   static constexpr int THREADS = 128 + 128 * NSG + 256;  // service WG + S WGs + 2 O WGs
-  static constexpr int REG_SVC = NSG == 2 ? 40 : HACK_PRE_RSVC;
-  static constexpr int REG_S = NSG == 2 ? 88 : HACK_PRE_RS;
-  static constexpr int REG_O = NSG == 2 ? 128 : HACK_PRE_RO;
+  // NSG = 1 (one S warpgroup, 64 keys per thread at Pi = 64): 512 threads, so the S and O
+  // shares can exceed 128 (40 + S + 2 O <= 512)
+  static constexpr int REG_SVC = NSG == 2 ? 40 : NSG == 1 ? 40 : HACK_PRE_RSVC;
+  static constexpr int REG_S = NSG == 2 ? 88 : NSG == 1 ? HACK_PRE_RS1 : HACK_PRE_RS;
+  static constexpr int REG_O = NSG == 2 ? 128 : NSG == 1 ? (512 - 40 - HACK_PRE_RS1) / 2 / 8 * 8 : HACK_PRE_RO;
   static_assert(REG_SVC * 128 + REG_S * 128 * NSG + REG_O * 256 <= 65536, "register file");
   static constexpr int KPT = BN / NSG;                  // keys per S thread per tile
-  static constexpr bool WB = KPT > (NSG == 2 ? 32 : 16);  // scores written back to TMEM between passes
+  static constexpr bool WB = KPT > (NSG == 2 ? 32 : NSG == 1 ? 64 : 16);  // scores written back to TMEM between passes
   static constexpr int SB = (BITS + (PI_ == 32 ? 5 : PI_ == 64 ? 6 : 7)) <= 8 ? 1 : 2;  // sum bytes (R13)
   static constexpr int up16(int x) { return (x + 15) / 16 * 16; }
   static constexpr int PB = up16(PI_ * 128 * BITS / 8) + up16(PI_ * NBETA * 4) + up16(PI_ * NBETA * SB) +
@@ -288,7 +293,7 @@ __global__ void __launch_bounds__(Geo<PI_, BITS>::THREADS, 1) prefill_tc_kernel(
       b = blockIdx.z;
       lin = blockIdx.x + gridDim.x * blockIdx.y;
     }
-    const int rank = lin / npk;
+    const int rank = kc.qt_begin + lin / npk;
     w.hq0 = kc.hq_begin + (lin % npk) * gp;  // heads hq0 .. hq0 + gp - 1
     w.start = cu_seqlens[b];
     w.L = cu_seqlens[b + 1] - w.start;
@@ -559,7 +564,10 @@ __global__ void __launch_bounds__(Geo<PI_, BITS>::THREADS, 1) prefill_tc_kernel(
   } else if (warp < 4 + 4 * NSG) {
     // ------------------------------------------------------------------ S warpgroups (NSG)
     // thread = query row r = TMEM lane; SW s owns keys KPT s .. KPT s + KPT - 1 of every tile
-    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(Gm::REG_S));
+    if (Gm::REG_S <= 65536 / Gm::THREADS)
+      asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(Gm::REG_S));
+    else  // NSG = 1: the S warpgroup takes part of the service warps' share
+      asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(Gm::REG_S));
     const int sw = (warp - 4) >> 2;
     const int r = (tid - 128) & (BM - 1);
     const uint32_t lane_base = (uint32_t)(32 * (warp & 3)) << 16;
@@ -1049,10 +1057,12 @@ cudaError_t launch_t(const KernelCfg& kc, const void* q, const int32_t* cu, cons
     int dev = 0, nsm = 0;
     if ((e = cudaGetDevice(&dev)) != cudaSuccess) return e;
     if ((e = cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev)) != cudaSuccess) return e;
-    nitems = nqt * (kc.hq_count / gp);
+    nitems = min(nqt - kc.qt_begin, kc.qt_count) * (kc.hq_count / gp);
+    if (nitems <= 0) return cudaSuccess;
     lc.gridDim = dim3(min(nitems, nsm), 1, 1);
   } else {
-    lc.gridDim = dim3(nqt, kc.hq_count / gp, batch);
+    if (min(nqt - kc.qt_begin, kc.qt_count) <= 0) return cudaSuccess;
+    lc.gridDim = dim3(min(nqt - kc.qt_begin, kc.qt_count), kc.hq_count / gp, batch);
   }
   lc.blockDim = dim3(Geo<PI_, BITS>::THREADS);
   lc.dynamicSmemBytes = smem;
@@ -1078,6 +1088,9 @@ cudaError_t launch_t(const KernelCfg& kc, const void* q, const int32_t* cu, cons
 }
 
 }  // namespace
+
+// query positions per work item of one request (the granularity of kc.qt_begin / qt_count)
+int prefill_tc_tile_rows(const KernelCfg& kc) { return BM / pack_heads(kc); }
 
 bool prefill_tc_supported(const KernelCfg& kc) {
   return (kc.Pi == 32 || kc.Pi == 64 || kc.Pi == 128) && kc.d == 128;

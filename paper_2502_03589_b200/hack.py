@@ -322,7 +322,8 @@ def prefill_attention_host(cfg: Config, q, k, v, cu_seqlens, slots, max_seqlen: 
                            workspace=None, head_chunks: int = 0, stream=None):
     """hack_prefill_attention with HOST q / k / v / cu_seqlens / slots / out (CPU tensors, pinned for
     copy-compute overlap): the library stages them through `workspace` (device) and pipelines
-    uploads, ingest, per-head-chunk attention and downloads."""
+    uploads, ingest, per-chunk attention and downloads (head_chunks > 0: query-head chunks;
+    <= 0 for one prompt: query-position chunks, longest rows first, -n = n chunks)."""
     for t in (q, k, v, cu_seqlens, slots, out):
         if t.is_cuda:
             raise ValueError("prefill_attention_host takes host tensors")

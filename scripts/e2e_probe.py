@@ -1,4 +1,4 @@
-"""C2 e2e (host buffers) per head-chunk count: hack_prefill_attention_host vs copies +
+"""C2 e2e (host buffers) per chunking (head chunks, or position streaming): hack_prefill_attention_host vs copies +
 hack_prefill_attention in stream order."""
 import sys
 
@@ -45,6 +45,7 @@ def serial():
 
 ms = timed(serial)
 print(f"copies + prefill_attention    {ms:.3f} ms  {ops / ms / 1e9:.1f} TOPS")
-for c in (1, 2, 4, 8):
+# head_chunks > 0: query-head chunks; <= 0: the prompt streamed by position (-n: n chunks, 0: 8)
+for c in [int(x) for x in (sys.argv[1].split(",") if len(sys.argv) > 1 else "1,2,4,8,0,-4,-8,-12,-16".split(","))]:
     ms = timed(lambda: h.prefill_attention_host(cfg, qh, kh, vh, cuh, slh, L, cache, outh, workspace=ws, head_chunks=c))
-    print(f"prefill_attention_host x{c}     {ms:.3f} ms  {ops / ms / 1e9:.1f} TOPS")
+    print(f"prefill_attention_host {c:+3d}     {ms:.3f} ms  {ops / ms / 1e9:.1f} TOPS")

@@ -207,3 +207,38 @@ def test_prefill_host_buffers_pipelined_equals_device_call(chunks):
     assert torch.equal(caches[0].pages, caches[1].pages)
     assert torch.equal(caches[0].v_tail, caches[1].v_tail)
     assert torch.equal(caches[0].seq_lens, caches[1].seq_lens)
+
+
+@pytest.mark.parametrize("Pi,bits", [(64, 2), (32, 4), (128, 2)])
+@pytest.mark.parametrize("L,chunks,extra", [(300, 0, 0), (1000, -3, 37), (64, 0, 0), (63, -2, 1), (1, 0, 0),
+                                            (1000, -16, 0), (777, -1, 0)])
+def test_prefill_host_position_streamed_equals_device_call(Pi, bits, L, chunks, extra):
+    """hack_prefill_attention_host for ONE prompt streams it by position (head_chunks <= 0):
+    K/V/Q rows [a, b) up, the ingest of those tokens (kc.tok_begin / tok_end), the attention of
+    those query rows (kc.qt_begin / qt_count) and their output down, chunk after chunk.  Output,
+    pages, FP16 tail and length must equal hack_prefill_attention's bit for bit, for ragged
+    lengths, every partition size, chunk counts from 1 to more than the prompt has tiles, and
+    a host bound max_seqlen above the length (extra)."""
+    h = hk()
+    ocfg = att.Config(Hq=16, Hkv=4, Pi=Pi, bits=bits, seed=29)
+    cfg = gpu_cfg(ocfg)
+    q, k, v = hack_inputs.qkv(29 + L, L, ocfg.Hq, ocfg.Hkv)
+    cu = torch.tensor([0, L], dtype=torch.int32)
+    sl = torch.tensor([1], dtype=torch.int32)
+    ms = L + extra
+    caches = [make_cache(cfg, max_reqs=2, max_len=ms, seed=5) for _ in range(2)]
+    for c in caches:
+        c.pages.zero_()
+        c.v_tail.zero_()
+    ref = torch.zeros((L, ocfg.Hq, 128), dtype=torch.float32, device="cuda")
+    h.prefill_attention(cfg, torch.from_numpy(q).cuda(), torch.from_numpy(k).cuda(), torch.from_numpy(v).cuda(),
+                        cu.cuda(), sl.cuda(), ms, caches[0], ref)
+    qh, kh, vh = (torch.from_numpy(x).pin_memory() for x in (q, k, v))
+    outh = torch.full((L, ocfg.Hq, 128), float("nan"), dtype=torch.float32).pin_memory()
+    h.prefill_attention_host(cfg, qh, kh, vh, cu.pin_memory(), sl.pin_memory(), ms, caches[1], outh,
+                             head_chunks=chunks)
+    torch.cuda.synchronize()
+    assert torch.equal(outh, ref.cpu())
+    assert torch.equal(caches[0].pages, caches[1].pages)
+    assert torch.equal(caches[0].v_tail, caches[1].v_tail)
+    assert torch.equal(caches[0].seq_lens, caches[1].seq_lens)
