@@ -215,11 +215,38 @@ HACK_DEV void stage_kc(const uint8_t* pg, const PageLayout& PL, float4* kcs, int
   }
 }
 
+// HACK_DEC_KDIRECT=1: each lane computes the K coefficients of its own 8 tokens from the page
+// (same operations as stage_kc, 4 lanes per token) instead of one staging pass + __syncwarp +
+// shared-memory loads per page (SE only).
+// HACK_DEC_OSUM=1: one O accumulator per (channel, row): pages A and B summed every pair
+// (16 registers fewer, one FADD more per output per pair)
+#ifndef HACK_DEC_OSUM
+#define HACK_DEC_OSUM 0
+#endif
+#ifndef HACK_DEC_KDIRECT
+#define HACK_DEC_KDIRECT 0
+#endif
+HACK_DEV void kcoef(const uint8_t* pg, const PageLayout& PL, int t, float4& c0, float4& c1) {
+  const uint2 mh = *reinterpret_cast<const uint2*>(pg + PL.k_meta + t * 8);
+  const uint32_t sums = *reinterpret_cast<const uint16_t*>(pg + PL.k_sums + t * 2);
+  const float2 m01 = __half22float2(__halves2half2(__ushort_as_half((unsigned short)(mh.x & 0xFFFF)),
+                                                   __ushort_as_half((unsigned short)(mh.y & 0xFFFF))));
+  const float2 s01 = __half22float2(__halves2half2(__ushort_as_half((unsigned short)(mh.x >> 16)),
+                                                   __ushort_as_half((unsigned short)(mh.y >> 16))));
+  const float2 sm23 = asf2(ptx::prmt(sums, 0x4B00u, 0x5440u), ptx::prmt(sums, 0x4B00u, 0x5441u));
+  const float2 sum2 = ptx::fadd2(sm23, f2(-8388608.f, -8388608.f));
+  const float2 mu = ptx::ffma2(s01, f2(1.5f, 1.5f), m01);
+  const float2 yk = ptx::ffma2(s01, ptx::fadd2(sum2, f2(-96.f, -96.f)), ptx::fmul2(f2(64.f, 64.f), mu));
+  const float2 nr = ptx::ffma2(sum2, f2(-510.f, -510.f), f2(-kMagicF, -kMagicF));
+  c0 = make_float4(s01.x, s01.y, mu.x, mu.y);
+  c1 = make_float4(yk.x, yk.y, nr.x, nr.y);
+}
+
 // Homomorphic S^T for one 64-token page: sc[mt][hh] = log2(e)/sqrt(d) * S(token 16mt+g+8hh, row tig).
 // MASK: tokens >= nk (the partial last page) are -inf.  Also the per-lane max/min.
 // dq (debug runs only, else nullptr): this lane's query row's qk_acc at the page's first token;
 // receives the raw block accumulators 4 D_beta + RC (HACK_ACC_CENTERED4), beta 1 at + dstride.
-template <bool MASK>
+template <bool MASK, bool KD = false>
 HACK_DEV void qk_page(const uint8_t* pg, const PageLayout& PL, const float4* kcs, int g, int tig, int nk,
                       const uint32_t (&qb)[4][2], float2 QA, float2 QX, float2 QM, uint32_t rc0, uint32_t rc1,
                       float (&sc)[4][2], float& mx, float& mn, int32_t* dq = nullptr, int64_t dstride = 0) {
@@ -241,7 +268,13 @@ HACK_DEV void qk_page(const uint8_t* pg, const PageLayout& PL, const float4* kcs
 #pragma unroll
     for (int hh = 0; hh < 2; ++hh) {
       const int t = hh ? t1 : t0;
-      const float4 c0 = kcs[2 * t], c1 = kcs[2 * t + 1];
+      float4 c0, c1;
+      if (KD) {
+        kcoef(pg, PL, t, c0, c1);
+      } else {
+        c0 = kcs[2 * t];
+        c1 = kcs[2 * t + 1];
+      }
       const uint32_t e0 = (acc0[2 * hh] << 2) + acc1[2 * hh], e1 = (acc0[2 * hh + 1] << 2) + acc1[2 * hh + 1];
       if (dq != nullptr && t < nk) {
         dq[t] = (int32_t)(e0 - kMagic);
@@ -622,9 +655,15 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
     const int my0 = ((warp - it_base) % NW + NW) % NW;  // first item of this warp in the segment
     const int u = s.b * Hkv + s.hk;
     float m_run = -INFINITY, l_run = 0.f;
+#if HACK_DEC_OSUM
+    float o[8][2];  // [m-tile][channel g / g+8] -> row tig (pages A + B summed every pair)
+#pragma unroll
+    for (int mt = 0; mt < 8; ++mt) o[mt][0] = o[mt][1] = 0.f;
+#else
     float2 o[8][2];  // [m-tile][channel g / g+8] -> (page A, page B) partial sums, row tig
 #pragma unroll
     for (int mt = 0; mt < 8; ++mt) o[mt][0] = o[mt][1] = f2(0.f, 0.f);
+#endif
 
     if (my0 < nitems) {
       const uint32_t rng_id = cv.rng_ids[slot];
@@ -700,26 +739,48 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
         }
         continue;
 #endif
-        stage_kc<SE>(pgA, PL, &ws.scr[0][0], lane);
-        __syncwarp();
+        constexpr bool KD = HACK_DEC_KDIRECT && SE;
         int32_t* dqA = nullptr;
         if (DBG && dbg.qk != nullptr && tig < G && dbg.hsel(s.hk * G + tig) >= 0)
           dqA = dbg.qk + ((int64_t)s.b * dbg.hdim(kc.Hq) + dbg.hsel(s.hk * G + tig)) * 2 * dbg.astride + jpA * PI;
+        if (KD && !tail_item) {
+          // both pages first, then both QKs with no barrier between them (page B = page A
+          // when the pair has one page: computed, then discarded)
+          if (hasB) wait_fill<NSTG>(sm, kB);
+          __syncwarp();
+          qk_page<false, true>(pgA, PL, &ws.scr[0][0], g, tig, PI, qb, QA, QX, QM, rc0, rc1, sa, mxA, mnA, dqA,
+                               dbg.astride);
+          qk_page<false, true>(pgB, PL, &ws.scr[0][0], g, tig, PI, qb, QA, QX, QM, rc0, rc1, sbv, mxB, mnB,
+                               hasB && dqA != nullptr ? dqA + PI : nullptr, dbg.astride);
+          if (!hasB) {
+            mxB = -INFINITY;
+            mnB = INFINITY;
+#pragma unroll
+            for (int mt = 0; mt < 4; ++mt) sbv[mt][0] = sbv[mt][1] = -INFINITY;
+          }
+        } else {
+        if (!KD) {
+          stage_kc<SE>(pgA, PL, &ws.scr[0][0], lane);
+          __syncwarp();
+        }
         if (tail_item)
-          qk_page<true>(pgA, PL, &ws.scr[0][0], g, tig, nkA, qb, QA, QX, QM, rc0, rc1, sa, mxA, mnA, dqA, dbg.astride);
+          qk_page<true, KD>(pgA, PL, &ws.scr[0][0], g, tig, nkA, qb, QA, QX, QM, rc0, rc1, sa, mxA, mnA, dqA, dbg.astride);
         else
-          qk_page<false>(pgA, PL, &ws.scr[0][0], g, tig, PI, qb, QA, QX, QM, rc0, rc1, sa, mxA, mnA, dqA,
+          qk_page<false, KD>(pgA, PL, &ws.scr[0][0], g, tig, PI, qb, QA, QX, QM, rc0, rc1, sa, mxA, mnA, dqA,
                          dbg.astride);
         if (hasB) {
           wait_fill<NSTG>(sm, kB);
           __syncwarp();
-          stage_kc<SE>(pgB, PL, &ws.scr[0][0], lane);
-          __syncwarp();
-          qk_page<false>(pgB, PL, &ws.scr[0][0], g, tig, PI, qb, QA, QX, QM, rc0, rc1, sbv, mxB, mnB,
+          if (!KD) {
+            stage_kc<SE>(pgB, PL, &ws.scr[0][0], lane);
+            __syncwarp();
+          }
+          qk_page<false, KD>(pgB, PL, &ws.scr[0][0], g, tig, PI, qb, QA, QX, QM, rc0, rc1, sbv, mxB, mnB,
                          dqA != nullptr ? dqA + PI : nullptr, dbg.astride);
         } else {
 #pragma unroll
           for (int mt = 0; mt < 4; ++mt) sbv[mt][0] = sbv[mt][1] = -INFINITY;
+        }
         }
         __syncwarp();  // K codes/meta of the pair and the K coefficients are dead from here on
 #if HACK_DEC_SPLIT
@@ -875,15 +936,24 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
               const float2 e = ptx::fadd2(asf2(e0, e1), f2(v1.z, v1.w));
               const float2 t2 = ptx::ffma2(AP, ptx::fmul2(f2(v0.x, v0.y), e),
                                            ptx::ffma2(XP, f2(v0.z, v0.w), ptx::fmul2(MP, f2(v1.x, v1.y))));
+#if HACK_DEC_OSUM
+              o[mt][hh] = __fmaf_rn(o[mt][hh], al, t2.x + t2.y);
+#else
               o[mt][hh] = ptx::ffma2(o[mt][hh], al2, t2);
+#endif
             }
           }
         } else {
           // ---- FP16 last V block (RQE): O^T += V_tail^T p~ in fp32
 #pragma unroll
           for (int mt = 0; mt < 8; ++mt) {
+#if HACK_DEC_OSUM
+            o[mt][0] *= al;
+            o[mt][1] *= al;
+#else
             o[mt][0] = ptx::fmul2(o[mt][0], al2);
             o[mt][1] = ptx::fmul2(o[mt][1], al2);
+#endif
           }
           float* ptl = reinterpret_cast<float*>(pgA + PL.k_codes);  // [row 4][64]
 #pragma unroll
@@ -899,7 +969,11 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
 #pragma unroll
               for (int hh = 0; hh < 2; ++hh) {
                 const float v = __half2float(tail[t * 128 + 16 * mt + g + 8 * hh]);
+#if HACK_DEC_OSUM
+                o[mt][hh] = fmaf(p, v, o[mt][hh]);
+#else
                 o[mt][hh].x = fmaf(p, v, o[mt][hh].x);
+#endif
               }
           }
         }
@@ -920,7 +994,12 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
 #pragma unroll
       for (int mt = 0; mt < 8; ++mt)
 #pragma unroll
-        for (int hh = 0; hh < 2; ++hh) dst[2 + 16 * mt + g + 8 * hh] = o[mt][hh].x + o[mt][hh].y;
+        for (int hh = 0; hh < 2; ++hh)
+#if HACK_DEC_OSUM
+          dst[2 + 16 * mt + g + 8 * hh] = o[mt][hh];
+#else
+          dst[2 + 16 * mt + g + 8 * hh] = o[mt][hh].x + o[mt][hh].y;
+#endif
     }
     it_base += nitems;
     k_base += s.p1 - s.p0;
