@@ -1251,8 +1251,10 @@ __global__ void __launch_bounds__(kThreads8, kCtas8)
               sc[nt][mt][hh] = ex2(sc[nt][mt][hh] - mnew);
               ls[nt] += sc[nt][mt][hh];
             }
+#if !HACK_DEC_LSUM  // (LSUM: l_run stays this lane's partial sum until the flush)
 #pragma unroll
           for (int o2 = 4; o2 < 32; o2 <<= 1) ls[nt] += __shfl_xor_sync(0xffffffffu, ls[nt], o2);
+#endif
           l_run[nt] = __fmaf_rn(l_run[nt], al[nt], ls[nt]);
         }
         uint8_t* pcode = pg + PL.k_meta;                          // [row 8][64] in B-fragment order
@@ -1367,6 +1369,12 @@ __global__ void __launch_bounds__(kThreads8, kCtas8)
       }
     }
     // -- flush: (m, l) from the QK-side rows (tig, 4 + tig), O from the PV-side rows (n0, n1)
+#if HACK_DEC_LSUM
+#pragma unroll
+    for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+      for (int o2 = 4; o2 < 32; o2 <<= 1) l_run[nt] += __shfl_xor_sync(0xffffffffu, l_run[nt], o2);
+#endif
     float* dst = part + (((int64_t)(u + c)) * NW + warp) * G * kPart;
     if (g == 0) {
 #pragma unroll
