@@ -21,6 +21,12 @@
 #include "internal.h"
 #include "tc_ptx.cuh"
 
+// HACK_DMMA_LSUM=1 (default): the row sums stay per lane until the CTA merge (no per-page
+// cross-lane reduction)
+#ifndef HACK_DMMA_LSUM
+#define HACK_DMMA_LSUM 1
+#endif
+
 namespace hack {
 
 namespace {
@@ -349,11 +355,13 @@ __global__ void __launch_bounds__(kThreads, dmma_ctas<BITS, PI_>()) decode_mma_k
           sv2[mt][hh] = make_float2(ex2(a2.x), ex2(a2.y));  // p~; ex2(-inf) = 0
           ls = ptx::fadd2(ls, sv2[mt][hh]);
         }
+#if !HACK_DMMA_LSUM  // (LSUM: l_run stays this lane's partial sum until the merge)
 #pragma unroll
       for (int o2 = 4; o2 < 32; o2 <<= 1) {
         ls.x += __shfl_xor_sync(0xffffffffu, ls.x, o2);
         ls.y += __shfl_xor_sync(0xffffffffu, ls.y, o2);
       }
+#endif
       l_run = ptx::ffma2(l_run, al, ls);
       m_run = mnew;
       // O *= al is fused into the PV update (o = o al + t, one explicit FFMA2): a separate
@@ -518,6 +526,13 @@ __global__ void __launch_bounds__(kThreads, dmma_ctas<BITS, PI_>()) decode_mma_k
   __syncthreads();  // all pages consumed: the stage ring is reused for the merge
   if (warp < NW) {
     // -- publish this warp's partial (m, l, O) for the CTA merge
+#if HACK_DMMA_LSUM
+#pragma unroll
+    for (int o2 = 4; o2 < 32; o2 <<= 1) {
+      l_run.x += __shfl_xor_sync(0xffffffffu, l_run.x, o2);
+      l_run.y += __shfl_xor_sync(0xffffffffu, l_run.y, o2);
+    }
+#endif
     if (g == 0) {
       sm.mrg_m[warp][n0] = m_run.x;
       sm.mrg_m[warp][n1] = m_run.y;
