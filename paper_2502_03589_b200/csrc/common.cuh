@@ -15,6 +15,10 @@ namespace hack {
 
 constexpr int kTagQ = 0, kTagK = 1, kTagV = 2, kTagP = 3;
 
+#ifndef HACK_P_META_IEEE
+#define HACK_P_META_IEEE 0  // 1: decode P' meta by IEEE division (meta_p_fast); measured slower
+#endif
+
 // ---------------------------------------------------------------- Philox4x32-10
 struct Philox4 {
   uint32_t x, y, z, w;
@@ -84,6 +88,22 @@ HACK_DEV QMeta meta_fp16(float lo, float hi, int qmax) {
   q.s = __half2float(__float2half_rn(s32));
   q.inv = q.s > 0.f ? __frcp_rn(q.s) : 0.f;  // scale 0: y = 0, every code 0 (R5)
   return q;
+}
+
+// Transient P' meta (never stored; decode kernels): a multiply and a fast reciprocal instead
+// of the IEEE division and reciprocal.  The codes then agree with meta_fp32's up to near-ties
+// (DESIGN "Parity protocol"); the caller zeroes a scale <= 1e-30 (R5).
+HACK_DEV QMeta meta_p_fast(float lo, float hi) {
+#if HACK_P_META_IEEE
+  QMeta q;
+  q.m = lo;
+  q.s = __fdiv_rn(__fsub_rn(hi, lo), 255.f);
+  q.inv = q.s > 0.f ? __frcp_rn(q.s) : 0.f;
+  return q;
+#else
+  const float r = hi - lo;
+  return {lo, r * (1.f / 255.f), __fdividef(255.f, r)};
+#endif
 }
 
 HACK_DEV QMeta meta_fp32(float lo, float hi, int qmax) {

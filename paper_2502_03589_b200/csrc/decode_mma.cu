@@ -370,7 +370,7 @@ __global__ void __launch_bounds__(kThreads, dmma_ctas<BITS, PI_>()) decode_mma_k
         // -- (a6) P' per (row, V block): lo/hi from the score min/max (ex2 is monotone)
         const float2 lo = make_float2(ex2(mn2.x - mnew.x), ex2(mn2.y - mnew.y));
         const float2 hi = make_float2(ex2(mx2.x - mnew.x), ex2(mx2.y - mnew.y));
-        QMeta pm0 = meta_fp32(lo.x, hi.x, 255), pm1 = meta_fp32(lo.y, hi.y, 255);
+        QMeta pm0 = meta_p_fast(lo.x, hi.x), pm1 = meta_p_fast(lo.y, hi.y);
         if (!(pm0.s > 1e-30f)) { pm0.s = 0.f; pm0.inv = 0.f; }
         if (!(pm1.s > 1e-30f)) { pm1.s = 0.f; pm1.inv = 0.f; }
         const float2 inv2 = make_float2(pm0.inv, pm1.inv), nlo2 = make_float2(-lo.x * pm0.inv, -lo.y * pm1.inv);

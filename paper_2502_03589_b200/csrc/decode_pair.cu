@@ -880,11 +880,11 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
           float2 AP, XP, MP;
           uint32_t rcA, rcB;
           {
-            QMeta pA = meta_fp32(ex2(mnA - mnew), ex2(mxA - mnew), 255);
+            QMeta pA = meta_p_fast(ex2(mnA - mnew), ex2(mxA - mnew));
             if (!(pA.s > 1e-30f)) { pA.s = 0.f; pA.inv = 0.f; }
             QMeta pB = {0.f, 0.f, 0.f};
             if (hasB) {
-              pB = meta_fp32(ex2(mnB - mnew), ex2(mxB - mnew), 255);
+              pB = meta_p_fast(ex2(mnB - mnew), ex2(mxB - mnew));
               if (!(pB.s > 1e-30f)) { pB.s = 0.f; pB.inv = 0.f; }
             }
             const float2 inv = f2(pA.inv, pB.inv), nlo = f2(-pA.m * pA.inv, -pB.m * pB.inv);
@@ -1265,7 +1265,7 @@ __global__ void __launch_bounds__(kThreads8, kCtas8)
 #pragma unroll
           for (int nt = 0; nt < 2; ++nt) {
             const int row = 4 * nt + tig;
-            QMeta pm = meta_fp32(ex2(mn[nt] - m_run[nt]), ex2(mx[nt] - m_run[nt]), 255);
+            QMeta pm = meta_p_fast(ex2(mn[nt] - m_run[nt]), ex2(mx[nt] - m_run[nt]));
             if (!(pm.s > 1e-30f)) { pm.s = 0.f; pm.inv = 0.f; }
             const float nlo = -pm.m * pm.inv;
             uint32_t sp = 0;
