@@ -424,7 +424,8 @@ HACK_DEV void produce_pages(SMT& sm, SegWalker walk, const CacheView& cv, const 
   // time with one coalesced load, so the issuing lane never waits on a dependent global
   // load between two page copies (one such wait per page capped the issue rate).
   Seg s;
-  int k = 0;
+  int k = 0, kslot = 0;  // fill index, its slot k % N
+  uint32_t kpar = 0;     // (k / N) & 1
   while (walk.next(cv, slots, Hkv, s, FUSED)) {
     const int32_t* bt = cv.block_table + (int64_t)slots[s.b] * cv.max_pages_per_req;
     for (int p0 = s.p0; p0 < s.p1; p0 += 32) {
@@ -437,7 +438,11 @@ HACK_DEV void produce_pages(SMT& sm, SegWalker walk, const CacheView& cv, const 
       for (int x = 0; x < n; ++x, ++k) {
         const int pid = __shfl_sync(0xffffffffu, ent, x);
         const int xf = x + HACK_DEC_PF;
-        const int pfa = __shfl_sync(0xffffffffu, ent, xf & 31), pfb = __shfl_sync(0xffffffffu, ent2, xf & 31);
+        int pfa = 0, pfb = 0;
+        if (HACK_DEC_PF > 0) {
+          pfa = __shfl_sync(0xffffffffu, ent, xf & 31);
+          pfb = __shfl_sync(0xffffffffu, ent2, xf & 31);
+        }
         // fused step: the appends of the CTA's units run once the ring is full (the producer
         // would wait for a slot anyway) or before the first page that receives a new token
         if (FUSED && !appended && (k == N || (s.p1 == s.npg && p0 + x == s.p1 - 1))) {
@@ -445,13 +450,13 @@ HACK_DEV void produce_pages(SMT& sm, SegWalker walk, const CacheView& cv, const 
           appended = true;
         }
         if (lane == 0) {
-          const int st = k % N;
+          const int st = kslot;
 #ifdef HACK_DEC_SPIN
-          while (!ptx::mbar_try_wait(&sm.empty[st], ((k / N) & 1) ^ 1)) {
+          while (!ptx::mbar_try_wait(&sm.empty[st], kpar ^ 1)) {
           }
 #else
           // sleep-wait: a spinning producer lane steals issue slots from the compute warps
-          while (!ptx::mbar_try_wait_sleep(&sm.empty[st], ((k / N) & 1) ^ 1)) {
+          while (!ptx::mbar_try_wait_sleep(&sm.empty[st], kpar ^ 1)) {
           }
 #endif
           tag_store(&sm.tag[st], k);  // fill k of slot st is being issued
@@ -474,6 +479,11 @@ HACK_DEV void produce_pages(SMT& sm, SegWalker walk, const CacheView& cv, const 
             const int pidf = xf < 32 ? pfa : pfb;
             ptx::bulk_prefetch_l2(cv.pages + ((int64_t)pidf * cv.num_kv_heads + s.hk) * cv.page_bytes, PB);
           }
+        }
+        // slot and phase of the next fill, kept incrementally (no division per page)
+        if (++kslot == N) {
+          kslot = 0;
+          kpar ^= 1u;
         }
         __syncwarp();
       }
