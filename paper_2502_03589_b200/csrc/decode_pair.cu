@@ -426,8 +426,12 @@ HACK_DEV void produce_pages(SMT& sm, SegWalker walk, const CacheView& cv, const 
   Seg s;
   int k = 0, kslot = 0;  // fill index, its slot k % N
   uint32_t kpar = 0;     // (k / N) & 1
+  // page of block id p, KV head hk: (pages + hk * page_bytes) + p * (heads * page_bytes), the
+  // product one 32 x 32 -> 64-bit multiply per page
+  const uint32_t pg_stride = (uint32_t)cv.num_kv_heads * (uint32_t)cv.page_bytes;
   while (walk.next(cv, slots, Hkv, s, FUSED)) {
     const int32_t* bt = cv.block_table + (int64_t)slots[s.b] * cv.max_pages_per_req;
+    const uint8_t* pg_hk = cv.pages + (int64_t)s.hk * cv.page_bytes;
     for (int p0 = s.p0; p0 < s.p1; p0 += 32) {
       const int n = min(32, s.p1 - p0);
       const int ent = lane < n ? bt[p0 + lane] : 0;
@@ -467,7 +471,7 @@ HACK_DEV void produce_pages(SMT& sm, SegWalker walk, const CacheView& cv, const 
 #else
           ptx::mbar_arrive_expect_tx(&sm.full[st], PB);
 #endif
-          const uint8_t* pg = cv.pages + ((int64_t)pid * cv.num_kv_heads + s.hk) * cv.page_bytes;
+          const uint8_t* pg = pg_hk + (uint64_t)(uint32_t)pid * pg_stride;
 #if HACK_DEC_SPLIT
           ptx::bulk_g2s(sm.stage[st], pg, kb, &sm.full[st]);
           ptx::mbar_arrive_expect_tx(&sm.fullv[st], PB - kb);
