@@ -28,6 +28,7 @@
 //     are both monotone along the flattened order).  The CTA completing a unit merges its
 //     partials (merge_units), no second kernel.
 #include <cstdlib>
+#include <type_traits>
 
 #include "append.cuh"
 #include "common.cuh"
@@ -1210,41 +1211,49 @@ __global__ void __launch_bounds__(kThreads8, kCtas8)
         float sc[2][4][2];
         float mx[2] = {-INFINITY, -INFINITY}, mn[2] = {INFINITY, INFINITY};
         const float4* kcs = &ws.scr[0][0];
-#pragma unroll
-        for (int mt = 0; mt < 4; ++mt) {
-          const int t0 = 16 * mt + g, t1 = t0 + 8;
-          const uint2 w0 = *reinterpret_cast<const uint2*>(pg + PL.k_codes + t0 * 32 + 8 * tig);
-          const uint2 w1 = *reinterpret_cast<const uint2*>(pg + PL.k_codes + t1 * 32 + 8 * tig);
-          const Planes a0 = planes2(w0.x), a1 = planes2(w1.x), a2 = planes2(w0.y), a3 = planes2(w1.y);
-#pragma unroll
-          for (int nt = 0; nt < 2; ++nt) {
-            uint32_t acc0[4], acc1[4];
-            mma16832c(acc0, a0.p0, a1.p0, a2.p0, a3.p0, qb[nt][0][0], qb[nt][0][1], 0u, 0u);
-            mma16832(acc0, a0.p2, a1.p2, a2.p2, a3.p2, qb[nt][1][0], qb[nt][1][1]);
-            mma16832c(acc1, a0.p1, a1.p1, a2.p1, a3.p1, qb[nt][2][0], qb[nt][2][1], rc[nt][0], rc[nt][1]);
-            mma16832(acc1, a0.p3, a1.p3, a2.p3, a3.p3, qb[nt][3][0], qb[nt][3][1]);
-#pragma unroll
-            for (int hh = 0; hh < 2; ++hh) {
-              const int t = hh ? t1 : t0;
-              const float4 c0 = kcs[2 * t], c1 = kcs[2 * t + 1];
-              const uint32_t e0 = (acc0[2 * hh] << 2) + acc1[2 * hh], e1 = (acc0[2 * hh + 1] << 2) + acc1[2 * hh + 1];
-              if (DBG && dbg.qk != nullptr && 4 * nt + tig < G && t < nk && dbg.hsel(s.hk * G + 4 * nt + tig) >= 0) {
-                int32_t* dq = dbg.qk + ((int64_t)s.b * dbg.hdim(kc.Hq) + dbg.hsel(s.hk * G + 4 * nt + tig)) * 2 * dbg.astride +
-                              jp * PI + t;  // raw 4 D_beta + RC
-                dq[0] = (int32_t)(e0 - kMagic);
-                dq[dbg.astride] = (int32_t)(e1 - kMagic);
+        // the partial last page's mask only where it applies (MASK: a compile-time flag)
+        auto qk8 = [&](auto maskc) {
+          constexpr bool MASK = decltype(maskc)::value;
+  #pragma unroll
+          for (int mt = 0; mt < 4; ++mt) {
+            const int t0 = 16 * mt + g, t1 = t0 + 8;
+            const uint2 w0 = *reinterpret_cast<const uint2*>(pg + PL.k_codes + t0 * 32 + 8 * tig);
+            const uint2 w1 = *reinterpret_cast<const uint2*>(pg + PL.k_codes + t1 * 32 + 8 * tig);
+            const Planes a0 = planes2(w0.x), a1 = planes2(w1.x), a2 = planes2(w0.y), a3 = planes2(w1.y);
+  #pragma unroll
+            for (int nt = 0; nt < 2; ++nt) {
+              uint32_t acc0[4], acc1[4];
+              mma16832c(acc0, a0.p0, a1.p0, a2.p0, a3.p0, qb[nt][0][0], qb[nt][0][1], 0u, 0u);
+              mma16832(acc0, a0.p2, a1.p2, a2.p2, a3.p2, qb[nt][1][0], qb[nt][1][1]);
+              mma16832c(acc1, a0.p1, a1.p1, a2.p1, a3.p1, qb[nt][2][0], qb[nt][2][1], rc[nt][0], rc[nt][1]);
+              mma16832(acc1, a0.p3, a1.p3, a2.p3, a3.p3, qb[nt][3][0], qb[nt][3][1]);
+  #pragma unroll
+              for (int hh = 0; hh < 2; ++hh) {
+                const int t = hh ? t1 : t0;
+                const float4 c0 = kcs[2 * t], c1 = kcs[2 * t + 1];
+                const uint32_t e0 = (acc0[2 * hh] << 2) + acc1[2 * hh], e1 = (acc0[2 * hh + 1] << 2) + acc1[2 * hh + 1];
+                if (DBG && dbg.qk != nullptr && 4 * nt + tig < G && t < nk && dbg.hsel(s.hk * G + 4 * nt + tig) >= 0) {
+                  int32_t* dq = dbg.qk + ((int64_t)s.b * dbg.hdim(kc.Hq) + dbg.hsel(s.hk * G + 4 * nt + tig)) * 2 * dbg.astride +
+                                jp * PI + t;  // raw 4 D_beta + RC
+                  dq[0] = (int32_t)(e0 - kMagic);
+                  dq[dbg.astride] = (int32_t)(e1 - kMagic);
+                }
+                const float2 e = ptx::fadd2(asf2(e0, e1), f2(c1.z, c1.w));
+                const float2 s2 = ptx::ffma2(QA[nt], ptx::fmul2(f2(c0.x, c0.y), e),
+                                             ptx::ffma2(QX[nt], f2(c0.z, c0.w), ptx::fmul2(QM[nt], f2(c1.x, c1.y))));
+                float sv = s2.x + s2.y;
+                if (MASK && t >= nk) sv = -INFINITY;
+                sc[nt][mt][hh] = sv;
+                mx[nt] = fmaxf(mx[nt], sv);
+                if (!MASK || t < nk) mn[nt] = fminf(mn[nt], sv);
               }
-              const float2 e = ptx::fadd2(asf2(e0, e1), f2(c1.z, c1.w));
-              const float2 s2 = ptx::ffma2(QA[nt], ptx::fmul2(f2(c0.x, c0.y), e),
-                                           ptx::ffma2(QX[nt], f2(c0.z, c0.w), ptx::fmul2(QM[nt], f2(c1.x, c1.y))));
-              float sv = s2.x + s2.y;
-              if (t >= nk) sv = -INFINITY;
-              sc[nt][mt][hh] = sv;
-              mx[nt] = fmaxf(mx[nt], sv);
-              if (t < nk) mn[nt] = fminf(mn[nt], sv);
             }
           }
-        }
+        };
+        if (nk == PI)
+          qk8(std::false_type{});
+        else
+          qk8(std::true_type{});
         __syncwarp();  // K codes/meta and K coefficients are dead
         // ---- (a5) online softmax, rows tig and 4 + tig
         float al[2], ls[2] = {0.f, 0.f};
