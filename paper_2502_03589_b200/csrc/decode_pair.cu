@@ -820,12 +820,13 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
             const int ch = lane + 32 * x;
             const __half2 hA = reinterpret_cast<const __half2*>(pgA + PL.v_meta)[ch];
             const __half2 hB = reinterpret_cast<const __half2*>(pgB + PL.v_meta)[ch];
-            const float2 mv = f2(__low2float(hA), hasB ? __low2float(hB) : 0.f);
-            const float2 sv = f2(__high2float(hA), hasB ? __high2float(hB) : 0.f);
+            // (a single-page pair has pgB = pgA: finite page-B values, multiplied by its zero P meta)
+            const float2 mv = f2(__low2float(hA), __low2float(hB));
+            const float2 sv = f2(__high2float(hA), __high2float(hB));
             uint32_t sumA, sumB;
             if (SE) {  // cached sums (summation elimination)
               sumA = pgA[PL.v_sums + ch];
-              sumB = hasB ? pgB[PL.v_sums + ch] : 0u;
+              sumB = pgB[PL.v_sums + ch];
             } else {   // HACK/SE ablation: the channel's 64 codes are 4 words of its V row
               const uint4 a = *reinterpret_cast<const uint4*>(pgA + PL.v_codes + ch * 16);
               sumA = codesum2(a.x) + codesum2(a.y) + codesum2(a.z) + codesum2(a.w);
@@ -940,7 +941,8 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
           uint32_t pb[4][2];
           {
             const uint4 Rw = *reinterpret_cast<const uint4*>(pcode + ((g >> 1) * 2 + (g & 1)) * 64 + 16 * tig);
-            const bool onA = (g & 1) == 0, onB = (g & 1) == 1 && hasB;
+            // (a single-page pair's page-B P' row holds zero codes: p~ = 0 and zero meta)
+            const bool onA = (g & 1) == 0, onB = (g & 1) == 1;
             pb[0][0] = onA ? Rw.x : 0u; pb[0][1] = onA ? Rw.z : 0u;
             pb[1][0] = onA ? Rw.y : 0u; pb[1][1] = onA ? Rw.w : 0u;
             pb[2][0] = onB ? Rw.x : 0u; pb[2][1] = onB ? Rw.z : 0u;
