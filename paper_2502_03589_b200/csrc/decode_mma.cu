@@ -17,6 +17,8 @@
 //   * online softmax per warp, P 8-bit RN per (row, committed V block); the
 //     FP16 last V block (RQE) in fp32; warps merged in smem, splits merged by
 //     decode_combine_kernel.
+#include <type_traits>
+
 #include "common.cuh"
 #include "internal.h"
 #include "tc_ptx.cuh"
@@ -263,78 +265,86 @@ __global__ void __launch_bounds__(kThreads, dmma_ctas<BITS, PI_>()) decode_mma_k
       // -- S^T = K' Q'^T per m-tile of 16 tokens; Eq. 4 on (row n0, n1) pairs
       float2 sv2[MT][2];  // [m-tile][token g / g+8]
       float2 mx2 = make_float2(-INFINITY, -INFINITY), mn2 = make_float2(INFINITY, INFINITY);
-#pragma unroll
-      for (int mt = 0; mt < MT; ++mt) {
-        const int t0 = 16 * mt + g, t1 = t0 + 8;
-        const uint4* r0 = reinterpret_cast<const uint4*>(pg + PL.k_codes + t0 * (128 * BITS / 8));
-        const uint4* r1 = reinterpret_cast<const uint4*>(pg + PL.k_codes + t1 * (128 * BITS / 8));
-        uint32_t w0[8 * BITS / 2], w1[8 * BITS / 2];
-#pragma unroll
-        for (int x = 0; x < 2 * BITS / 2; ++x) {
-          const uint4 a = r0[x], c = r1[x];
-          w0[4 * x] = a.x; w0[4 * x + 1] = a.y; w0[4 * x + 2] = a.z; w0[4 * x + 3] = a.w;
-          w1[4 * x] = c.x; w1[4 * x + 1] = c.y; w1[4 * x + 2] = c.z; w1[4 * x + 3] = c.w;
-        }
-        // accumulate on top of 0x4B000000: asfloat(acc) = 2^23 + D exactly (D < 2^22)
-        uint32_t acc[NB][4];
-#pragma unroll
-        for (int beta = 0; beta < NB; ++beta) acc[beta][0] = acc[beta][1] = acc[beta][2] = acc[beta][3] = kMagicI;
-#pragma unroll
-        for (int ks = 0; ks < 4; ++ks) {
-          uint32_t a[4];
-          if (BITS == 2) {
-            a[0] = plane<2>(w0[2 * ks], sh);
-            a[1] = plane<2>(w1[2 * ks], sh);
-            a[2] = plane<2>(w0[2 * ks + 1], sh);
-            a[3] = plane<2>(w1[2 * ks + 1], sh);
-          } else {
-            // 4-bit: 8 codes per word; K-cols 4tig+i of half h <- word 4ks + 2h + (tig >> 1)
-            const bool odd = tig >> 1;  // select, not a dynamic register-array index
-            a[0] = plane<4>(odd ? w0[4 * ks + 1] : w0[4 * ks], sh);
-            a[1] = plane<4>(odd ? w1[4 * ks + 1] : w1[4 * ks], sh);
-            a[2] = plane<4>(odd ? w0[4 * ks + 3] : w0[4 * ks + 2], sh);
-            a[3] = plane<4>(odd ? w1[4 * ks + 3] : w1[4 * ks + 2], sh);
+      // the tail page's mask only where it applies (TAIL: a compile-time flag)
+      auto qk = [&](auto tailc) {
+        constexpr bool TAIL = decltype(tailc)::value;
+  #pragma unroll
+        for (int mt = 0; mt < MT; ++mt) {
+          const int t0 = 16 * mt + g, t1 = t0 + 8;
+          const uint4* r0 = reinterpret_cast<const uint4*>(pg + PL.k_codes + t0 * (128 * BITS / 8));
+          const uint4* r1 = reinterpret_cast<const uint4*>(pg + PL.k_codes + t1 * (128 * BITS / 8));
+          uint32_t w0[8 * BITS / 2], w1[8 * BITS / 2];
+  #pragma unroll
+          for (int x = 0; x < 2 * BITS / 2; ++x) {
+            const uint4 a = r0[x], c = r1[x];
+            w0[4 * x] = a.x; w0[4 * x + 1] = a.y; w0[4 * x + 2] = a.z; w0[4 * x + 3] = a.w;
+            w1[4 * x] = c.x; w1[4 * x + 1] = c.y; w1[4 * x + 2] = c.z; w1[4 * x + 3] = c.w;
           }
-          mma16832(acc[ks * 32 / PI], a, qb[ks][0], qb[ks][1]);  // k-step ks: channels 32ks.. of block beta
-        }
-        if (DBG && dbg_qk != nullptr) {  // rows n0, n1; tokens t0 / t1; every beta
-#pragma unroll
-          for (int hh = 0; hh < 2; ++hh) {
-            const int t = hh ? t1 : t0;
-            if (t < nk) {
-#pragma unroll
-              for (int beta = 0; beta < NB; ++beta) {
-                int32_t* dq = dbg_qk + (int64_t)b * hdim * NB * acc_stride + beta * acc_stride + jp * PI + t;
-                if (n0 < G && hsel(n0) >= 0) dq[(int64_t)hsel(n0) * NB * acc_stride] = (int32_t)(acc[beta][2 * hh] - kMagicI);
-                if (n1 < G && hsel(n1) >= 0)
-                  dq[(int64_t)hsel(n1) * NB * acc_stride] = (int32_t)(acc[beta][2 * hh + 1] - kMagicI);
+          // accumulate on top of 0x4B000000: asfloat(acc) = 2^23 + D exactly (D < 2^22)
+          uint32_t acc[NB][4];
+  #pragma unroll
+          for (int beta = 0; beta < NB; ++beta) acc[beta][0] = acc[beta][1] = acc[beta][2] = acc[beta][3] = kMagicI;
+  #pragma unroll
+          for (int ks = 0; ks < 4; ++ks) {
+            uint32_t a[4];
+            if (BITS == 2) {
+              a[0] = plane<2>(w0[2 * ks], sh);
+              a[1] = plane<2>(w1[2 * ks], sh);
+              a[2] = plane<2>(w0[2 * ks + 1], sh);
+              a[3] = plane<2>(w1[2 * ks + 1], sh);
+            } else {
+              // 4-bit: 8 codes per word; K-cols 4tig+i of half h <- word 4ks + 2h + (tig >> 1)
+              const bool odd = tig >> 1;  // select, not a dynamic register-array index
+              a[0] = plane<4>(odd ? w0[4 * ks + 1] : w0[4 * ks], sh);
+              a[1] = plane<4>(odd ? w1[4 * ks + 1] : w1[4 * ks], sh);
+              a[2] = plane<4>(odd ? w0[4 * ks + 3] : w0[4 * ks + 2], sh);
+              a[3] = plane<4>(odd ? w1[4 * ks + 3] : w1[4 * ks + 2], sh);
+            }
+            mma16832(acc[ks * 32 / PI], a, qb[ks][0], qb[ks][1]);  // k-step ks: channels 32ks.. of block beta
+          }
+          if (DBG && dbg_qk != nullptr) {  // rows n0, n1; tokens t0 / t1; every beta
+  #pragma unroll
+            for (int hh = 0; hh < 2; ++hh) {
+              const int t = hh ? t1 : t0;
+              if (t < nk) {
+  #pragma unroll
+                for (int beta = 0; beta < NB; ++beta) {
+                  int32_t* dq = dbg_qk + (int64_t)b * hdim * NB * acc_stride + beta * acc_stride + jp * PI + t;
+                  if (n0 < G && hsel(n0) >= 0) dq[(int64_t)hsel(n0) * NB * acc_stride] = (int32_t)(acc[beta][2 * hh] - kMagicI);
+                  if (n1 < G && hsel(n1) >= 0)
+                    dq[(int64_t)hsel(n1) * NB * acc_stride] = (int32_t)(acc[beta][2 * hh + 1] - kMagicI);
+                }
               }
             }
           }
-        }
-        float2 st[2];
-#pragma unroll
-        for (int hh = 0; hh < 2; ++hh) {  // token t0 (c0, c1) / t1 (c2, c3)
-          const int t = hh ? t1 : t0;
-          float2 accf = make_float2(0.f, 0.f);
-#pragma unroll
-          for (int beta = 0; beta < NB; ++beta) {
-            const float4 k4 = ws.kc[beta][t];
-            const float sk = k4.x, mu = k4.y, yk = k4.z, nr = k4.w;
-            const float2 df = ptx::fadd2(make_float2(__uint_as_float(acc[beta][2 * hh]), __uint_as_float(acc[beta][2 * hh + 1])),
-                                         make_float2(-8388608.f, -8388608.f));
-            const float2 e = ptx::ffma2(make_float2(4.f, 4.f), df, ptx::fadd2(QN[beta], make_float2(nr, nr)));
-            const float2 base = ptx::ffma2(QM[beta], make_float2(yk, yk), accf);
-            accf = ptx::ffma2(QA[beta], ptx::fmul2(make_float2(sk, sk), e), ptx::ffma2(QX[beta], make_float2(mu, mu), base));
+          float2 st[2];
+  #pragma unroll
+          for (int hh = 0; hh < 2; ++hh) {  // token t0 (c0, c1) / t1 (c2, c3)
+            const int t = hh ? t1 : t0;
+            float2 accf = make_float2(0.f, 0.f);
+  #pragma unroll
+            for (int beta = 0; beta < NB; ++beta) {
+              const float4 k4 = ws.kc[beta][t];
+              const float sk = k4.x, mu = k4.y, yk = k4.z, nr = k4.w;
+              const float2 df = ptx::fadd2(make_float2(__uint_as_float(acc[beta][2 * hh]), __uint_as_float(acc[beta][2 * hh + 1])),
+                                           make_float2(-8388608.f, -8388608.f));
+              const float2 e = ptx::ffma2(make_float2(4.f, 4.f), df, ptx::fadd2(QN[beta], make_float2(nr, nr)));
+              const float2 base = ptx::ffma2(QM[beta], make_float2(yk, yk), accf);
+              accf = ptx::ffma2(QA[beta], ptx::fmul2(make_float2(sk, sk), e), ptx::ffma2(QX[beta], make_float2(mu, mu), base));
+            }
+            if (TAIL && t >= nk) accf = make_float2(-INFINITY, -INFINITY);  // beyond the cache (tail page)
+            st[hh] = accf;
+            mx2 = make_float2(fmaxf(mx2.x, accf.x), fmaxf(mx2.y, accf.y));
+            if (!TAIL || t < nk) mn2 = make_float2(fminf(mn2.x, accf.x), fminf(mn2.y, accf.y));
           }
-          if (!committed && t >= nk) accf = make_float2(-INFINITY, -INFINITY);  // beyond the cache (tail page)
-          st[hh] = accf;
-          mx2 = make_float2(fmaxf(mx2.x, accf.x), fmaxf(mx2.y, accf.y));
-          if (committed || t < nk) mn2 = make_float2(fminf(mn2.x, accf.x), fminf(mn2.y, accf.y));
+          sv2[mt][0] = st[0];
+          sv2[mt][1] = st[1];
         }
-        sv2[mt][0] = st[0];
-        sv2[mt][1] = st[1];
-      }
+      };
+      if (committed)
+        qk(std::false_type{});
+      else
+        qk(std::true_type{});
       // row reductions over the 8 lanes sharing tig
 #pragma unroll
       for (int o2 = 4; o2 < 32; o2 <<= 1) {
