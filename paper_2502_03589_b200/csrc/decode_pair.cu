@@ -680,9 +680,9 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
     const int u = s.b * Hkv + s.hk;
     float m_run = -INFINITY, l_run = 0.f;
 #if HACK_DEC_OSUM
-    float o[8][2];  // [m-tile][channel g / g+8] -> row tig (pages A + B summed every pair)
+    float2 o[8];  // [m-tile] -> (channel g, channel g + 8), row tig (pages A + B summed every pair)
 #pragma unroll
-    for (int mt = 0; mt < 8; ++mt) o[mt][0] = o[mt][1] = 0.f;
+    for (int mt = 0; mt < 8; ++mt) o[mt] = f2(0.f, 0.f);
 #else
     float2 o[8][2];  // [m-tile][channel g / g+8] -> (page A, page B) partial sums, row tig
 #pragma unroll
@@ -961,6 +961,9 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
             mma16832c(acc1, vaA.p1, vbA.p1, vaA.p3, vbA.p3, pb[1][0], pb[1][1], rcA, rcB);
             mma16832(acc0, vaB.p0, vbB.p0, vaB.p2, vbB.p2, pb[2][0], pb[2][1]);
             mma16832(acc1, vaB.p1, vbB.p1, vaB.p3, vbB.p3, pb[3][0], pb[3][1]);
+#if HACK_DEC_OSUM
+            float2 tq[2];  // t2 of channels g, g + 8: (page A, page B)
+#endif
 #pragma unroll
             for (int hh = 0; hh < 2; ++hh) {
               const int ch = hh ? c1 : c0;
@@ -977,19 +980,23 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
               const float2 t2 = ptx::ffma2(AP, ptx::fmul2(f2(v0.x, v0.y), e),
                                            ptx::ffma2(XP, f2(v0.z, v0.w), ptx::fmul2(MP, f2(v1.x, v1.y))));
 #if HACK_DEC_OSUM
-              o[mt][hh] = __fmaf_rn(o[mt][hh], al, t2.x + t2.y);
+              tq[hh] = t2;
 #else
               o[mt][hh] = ptx::ffma2(o[mt][hh], al2, t2);
 #endif
             }
+#if HACK_DEC_OSUM
+            // o = o al + (page A + page B) for both channels on paired ops (same values as the
+            // scalar fma(o, al, a + b) per channel)
+            o[mt] = ptx::ffma2(o[mt], al2, ptx::fadd2(f2(tq[0].x, tq[1].x), f2(tq[0].y, tq[1].y)));
+#endif
           }
         } else {
           // ---- FP16 last V block (RQE): O^T += V_tail^T p~ in fp32
 #pragma unroll
           for (int mt = 0; mt < 8; ++mt) {
 #if HACK_DEC_OSUM
-            o[mt][0] *= al;
-            o[mt][1] *= al;
+            o[mt] = ptx::fmul2(o[mt], al2);
 #else
             o[mt][0] = ptx::fmul2(o[mt][0], al2);
             o[mt][1] = ptx::fmul2(o[mt][1], al2);
@@ -1010,7 +1017,10 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
               for (int hh = 0; hh < 2; ++hh) {
                 const float v = __half2float(tail[t * 128 + 16 * mt + g + 8 * hh]);
 #if HACK_DEC_OSUM
-                o[mt][hh] = fmaf(p, v, o[mt][hh]);
+                if (hh)
+                  o[mt].y = fmaf(p, v, o[mt].y);
+                else
+                  o[mt].x = fmaf(p, v, o[mt].x);
 #else
                 o[mt][hh].x = fmaf(p, v, o[mt][hh].x);
 #endif
@@ -1040,7 +1050,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
 #pragma unroll
         for (int hh = 0; hh < 2; ++hh)
 #if HACK_DEC_OSUM
-          dst[2 + 16 * mt + g + 8 * hh] = o[mt][hh];
+          dst[2 + 16 * mt + g + 8 * hh] = hh ? o[mt].y : o[mt].x;
 #else
           dst[2 + 16 * mt + g + 8 * hh] = o[mt][hh].x + o[mt][hh].y;
 #endif
