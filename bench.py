@@ -302,7 +302,8 @@ def run_hack(args, rank, local_rank, world):
 
     # ---------------- e2e through the C ABI with host buffers: hack_prefill_attention_host
     # stages pinned host q/k/v through device memory and pipelines the uploads, the ingest,
-    # the attention per query-head chunk and the downloads of the output (library streams)
+    # the attention per chunk of query positions (longest rows first) and the downloads of
+    # the output (library streams)
     qh = q.cpu().pin_memory(); kh = k.cpu().pin_memory(); vh = v.cpu().pin_memory()
     outh = torch.empty(out.shape, dtype=out.dtype).pin_memory()
     cuh, slh = cu.cpu().pin_memory(), slots.cpu().pin_memory()
@@ -359,8 +360,9 @@ def run_hack(args, rank, local_rank, world):
             "e2e": {"value": e2e_val, "unit": "TOPS",
                     "h2d_bytes_per_step": q.nbytes + k.nbytes + v.nbytes + cuh.nbytes + slh.nbytes,
                     "d2h_bytes_per_step": out.nbytes, "ms_per_step": e2e_ms,
-                    "path": "pinned host q/k/v -> hack_prefill_attention_host (uploads, ingest, attention per "
-                            "query-head chunk and output downloads pipelined) -> pinned host out"},
+                    "path": "pinned host q/k/v -> hack_prefill_attention_host (K/V up + ingest, then Q up, "
+                            "attention and output down per chunk of query positions, longest rows first, "
+                            "pipelined) -> pinned host out"},
             "gpu_launches": launches,
             "clocks": clk.summary(),
             "decode": dec,
